@@ -1,0 +1,365 @@
+"""Benchmark: one optimisation step of the DiffTrans refine-stage tracer on B200.
+
+A step = LBVH rebuild (dt_build_bvh) + recursive forward trace of every ray of the
+workload (dt_trace_forward) + fused L_color loss/gradient (dt_loss_color) + backward
+replay (dt_trace_backward) [+ NCCL all-reduce of the gradients when N > 1].
+Metric (BASELINE.json): Mray.bounce/s fwd+bwd = traced segments / step time.
+
+  python bench.py [--gpus N --steps K --warmup W --config C3 --impl ours|reference]
+
+N > 1: launched by torchrun, one rank per GPU; rays shard by (view, 32x32 tile) across
+ranks (strong scaling: the C3 step's total work is fixed), and rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "Mray*bounce/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(PEAKS))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def target_scene(sc):
+    """Ground truth for the loss: the same scene rendered with IoR 1.45, sigma x 1.2 and the
+    vertices jittered by 0.5% of the radius."""
+    from paper_2603_00413_b200 import scenes as S
+    g = S.rng(777, 81)
+    r = float(np.linalg.norm(sc.V, axis=1).max())
+    V = (sc.V + g.normal(size=sc.V.shape) * 0.005 * r / np.sqrt(3)).astype(np.float32)
+    ab = dataclasses.replace(sc.absorption, sigma=(sc.absorption.sigma * 1.2).astype(np.float32))
+    return dataclasses.replace(sc, V=V, ior=1.45, absorption=ab)
+
+
+def oracle_sample(sc, n_pix: int, seed: int = 9):
+    """Bounded oracle run (forward + backward) on n_pix object pixels: (seconds, segments, threads)."""
+    import oracle as O
+    from paper_2603_00413_b200 import scenes as S
+    osc = O.OracleScene(sc)
+    pid = S.central_pixels(sc.cams, n_pix, seed)
+    g = S.upstream_grad(len(pid), seed)
+    t0 = time.perf_counter()
+    out = O.render(osc, pid)
+    O.backward(osc, g, pid)
+    dt = time.perf_counter() - t0
+    return dt, int(out["segments"].sum()), os.cpu_count()
+
+
+def algorithmic_bytes(stats, nf: int):
+    """Compulsory bytes per launch class: record streams, shading gathers,
+    children writes, and the LBVH read once per launch (served from L2 afterwards)."""
+    seg = stats["segments_per_depth"]
+    D = len(seg) - 1
+    bvh = 64 * max(nf - 1, 0) + 48 * nf
+    trace = 0
+    for k in range(1, D + 1):
+        nxt = seg[k + 1] if k + 1 <= D else 0
+        trace += seg[k] * (48 + 48 + 108) + nxt * 48 + bvh
+    bwd = 0
+    for k in range(0, D + 1):
+        nxt = seg[k + 1] if k + 1 <= D else 0
+        bwd += seg[k] * (96 + 12 + 32 + 108 + 192) + nxt * 48
+    return {"trace": trace, "bwd": bwd, "trace_launches": D, "bwd_launches": D + 1}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_00413_b200 import dist as DD
+    from paper_2603_00413_b200 import scenes as S
+    from paper_2603_00413_b200.tracer import DeviceScene, Tracer
+
+    dev = torch.device(f"cuda:{local_rank}")
+    torch.cuda.set_device(dev)
+    sc = S.CONFIGS[args.config]()
+    ds = DeviceScene(sc, dev)
+    tr = Tracer(dev)
+    pid = None
+    if world > 1:
+        pid = torch.as_tensor(DD.tile_pixel_ids(sc.cams.n_views, sc.cams.width, sc.cams.height, rank, world), device=dev)
+    n_rays = ds.n_pixels if pid is None else pid.numel()
+    # ground-truth colours for the loss (not timed)
+    tgt_sc = target_scene(sc)
+    dt_ = DeviceScene(tgt_sc, dev)
+    tr.build_bvh(dt_.V, dt_.F)
+    target = tr.trace_forward(dt_, pid).rgb.clone()
+    del dt_
+    rgb = torch.empty((n_rays, 3), dtype=torch.float32, device=dev)
+    grad = torch.empty_like(rgb)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    gV = torch.empty((sc.V.shape[0], 3), dtype=torch.float32, device=dev)
+    gi = torch.empty(1, dtype=torch.float32, device=dev)
+    gs = torch.empty(tuple(ds.sigma.shape), dtype=torch.float32, device=dev)
+    flat = None
+
+    def step():
+        nonlocal flat
+        tr.build_bvh(ds.V, ds.F)
+        out = tr.trace_forward(ds, pid, rgb=rgb, stats=True)
+        tr.loss_color(rgb, target, grad, loss)
+        tr.trace_backward(grad, gV, gi, gs)
+        if world > 1:
+            flat = DD.allreduce_grads(gV, gi, gs, flat)
+        return out.stats
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    tr.profile(reset=True)
+    tr.set_profiling(True)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    segs = 0
+    last = None
+    e0.record()
+    for _ in range(args.steps):
+        last = step()
+        segs += last["segments"]
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    tr.set_profiling(False)
+    prof = tr.profile(reset=True)
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms, float(segs)], dtype=torch.float64, device=dev)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms, segs = float(mx[0]), float(t[1])
+    value = segs / (ms / 1e3) / 1e6
+
+    # ---- end-to-end through the public API with host buffers (pinned), same metric
+    e2e = None
+    if not args.no_e2e:
+        hV = torch.empty((sc.V.shape[0], 3), dtype=torch.float32, pin_memory=True)
+        hV.copy_(torch.as_tensor(sc.V))
+        hsig = torch.as_tensor(sc.absorption.sigma).clone().pin_memory()
+        htgt = torch.empty((n_rays, 3), dtype=torch.float32, pin_memory=True)
+        htgt.copy_(target.cpu())
+        hgV = torch.empty_like(hV, pin_memory=True)
+        hgi = torch.empty(1, pin_memory=True)
+        hgs = torch.empty_like(hsig, pin_memory=True)
+        hloss = torch.empty(1, pin_memory=True)
+        dV = ds.V
+        dsig = ds.sigma
+        tgt_d = target
+
+        def e2e_step():
+            nonlocal flat
+            dV.copy_(hV, non_blocking=True)
+            dsig.copy_(hsig, non_blocking=True)
+            tgt_d.copy_(htgt, non_blocking=True)
+            tr.build_bvh(dV, ds.F)
+            out = tr.trace_forward(ds, pid, rgb=rgb, stats=True)
+            tr.loss_color(rgb, tgt_d, grad, loss)
+            tr.trace_backward(grad, gV, gi, gs)
+            if world > 1:
+                flat = DD.allreduce_grads(gV, gi, gs, flat)
+            hgV.copy_(gV, non_blocking=True)
+            hgi.copy_(gi, non_blocking=True)
+            hgs.copy_(gs, non_blocking=True)
+            hloss.copy_(loss, non_blocking=True)
+            return out.stats["segments"]
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s2 = 0
+        e0.record()
+        for _ in range(args.steps):
+            s2 += e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms2 = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms2, float(s2)], dtype=torch.float64, device=dev)
+            mx = t.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            ms2, s2 = float(mx[0]), float(t[1])
+        h2d = hV.numel() * 4 + hsig.numel() * 4 + htgt.numel() * 4
+        d2h = hgV.numel() * 4 + hgi.numel() * 4 + hgs.numel() * 4 + 4
+        e2e = {"value": s2 / (ms2 / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms2 / args.steps}
+
+    if rank != 0:
+        return None
+    # ---- roofline of the dominant launch class, device time measured live (CUDA events)
+    peak, peak_src = hbm_peak()
+    ab = algorithmic_bytes(last, sc.F.shape[0])
+    ph = prof["ms"]
+    cls = "trace" if ph["trace"] >= ph["bwd"] else "bwd"
+    launches = prof["launches"][cls]
+    ms_per_launch = ph[cls] / max(launches, 1)
+    bytes_per_launch = ab[cls] / max(ab[f"{cls}_launches"], 1)
+    achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_trace_level" if cls == "trace" else "k_backward_level",
+                "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "note": "algorithmic = compulsory record/gather bytes + LBVH once per launch; node/tri re-reads "
+                        "are cache traffic (l2_bytes_per_launch)",
+                "l2_bytes_per_launch": int((prof["node_visits"] * 64 + prof["tri_tests"] * 48) /
+                                           max(prof["launches"]["trace0"] + prof["launches"]["trace"], 1)),
+                "share_of_step": round(ph[cls] / ms, 4)}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        dt, osegs, cores = oracle_sample(sc, args.cpu_pixels)
+        cpu = {"value": osegs / dt / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{args.cpu_pixels} object pixels of {args.config}, fwd+bwd, fp64 brute force, "
+                         f"{osegs} segments in {dt:.1f}s"}
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {sc.F.shape[0]} tris, {sc.cams.n_views} views "
+                               f"{sc.cams.width}x{sc.cams.height}, depth {sc.max_depth}, "
+                               f"{'const' if sc.absorption.kind == 0 else 'grid'} sigma, "
+                               f"{'analytic' if sc.env.kind == 0 else 'voxel+triplane'} env",
+                   "rays_per_step": int(n_rays) * world, "segments_per_step": int(segs / args.steps),
+                   "segments_per_depth": last["segments_per_depth"], "parallelism": f"rays{world}",
+                   "l2": "working set > L2: path-record arena "
+                         f"{last['arena_capacity'] * 128 / 1e9:.1f} GB streamed every step; LBVH rebuilt in-step"},
+        "clocks": clk, "e2e": e2e, "gpu_launches": int(prof["kernel_launches"]), "roofline": roofline,
+        "cpu_baseline": cpu,
+        "phase_ms_per_step": {k: round(v / args.steps, 3) for k, v in ph.items()},
+        "counters_per_step": {"node_visits": prof["node_visits"] // args.steps,
+                              "tri_tests": prof["tri_tests"] // args.steps},
+    }
+    return line
+
+
+def run_reference(args, rank, world):
+    """The oracle (fp64 CPU, brute force) as it stands, on a bounded sample of the workload."""
+    if rank != 0:
+        return None
+    from paper_2603_00413_b200 import scenes as S
+    sc = S.CONFIGS[args.config]()
+    for _ in range(args.warmup):
+        oracle_sample(sc, max(args.cpu_pixels // 4, 1), seed=100)
+    tot_t, tot_s = 0.0, 0
+    for k in range(args.steps):
+        dt, segs, cores = oracle_sample(sc, args.cpu_pixels, seed=200 + k)
+        tot_t += dt
+        tot_s += segs
+    v = tot_s / tot_t / 1e6
+    sample = (f"each step: {args.cpu_pixels} object pixels of {args.config} (fp64 brute force fwd+bwd); "
+              f"{tot_s} segments in {tot_t:.1f}s")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-pixels", type=int, default=24)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        line = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/* libdifftrans — B200 (sm_100a) differentiable recursive mesh ray tracer.  C ABI.
+ *
+ * The hot path of DiffTrans' refine stage (arXiv 2603.00413):
+ * for every pixel ray, closest mesh hit; at each hit a Fresnel-weighted reflection and a
+ * Snell refraction (total internal reflection drops the refraction); interior segments
+ * attenuated by Beer-Lambert absorption; escaping rays end in a lookup of the frozen
+ * environment field.  The backward pass returns d/dV, d/dIOR and d/dsigma.
+ *
+ * Citations: P:n = PAPER.md line n; R# = reading n of DESIGN.md §3 (where the paper is
+ * silent or garbled).  All arithmetic is float32 on the device.
+ *
+ * Conventions shared by every entry point
+ *  - Array arguments are caller-owned, contiguous DEVICE memory unless marked "host".
+ *    Nothing here allocates caller-visible memory; the context owns its own buffers.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All work
+ *    is enqueued on it.  dt_trace_forward synchronises the stream once at its end (it
+ *    reads back the wavefront sizes to validate the record arena); nothing else blocks.
+ *  - Errors are return codes; nothing throws across the ABI.  dt_last_error(ctx) holds a
+ *    one-line message naming the offending argument.  A CUDA fault surfaces as DT_ERR_CUDA.
+ *  - A context is bound to one device and is not thread-safe; use one per GPU / thread.
+ */
+#ifndef DIFFTRANS_H
+#define DIFFTRANS_H
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DT_API __attribute__((visibility("default")))
+#else
+#define DT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dt_ctx dt_ctx;
+
+typedef enum {
+  DT_OK = 0,
+  DT_ERR_INVALID_ARG = 1,    /* a NULL / out-of-range argument; dt_last_error names it       */
+  DT_ERR_EMPTY_GEOMETRY = 2, /* nf == 0 or nv == 0                                            */
+  DT_ERR_CUDA = 3,           /* a CUDA runtime error (possibly from earlier async work)      */
+  DT_ERR_OOM = 4,            /* device allocation failed (record arena larger than free HBM) */
+  DT_ERR_NOT_BUILT = 5,      /* dt_trace_forward before dt_build_bvh                          */
+  DT_ERR_NO_FORWARD = 6,     /* dt_trace_backward without a preceding dt_trace_forward        */
+  DT_ERR_NONFINITE = 7,      /* opts.check_finite and a NaN/Inf output; message names it     */
+  DT_ERR_STACK = 8           /* BVH deeper than the traversal stack (never for LBVH < 2^30)   */
+} dt_status;
+
+enum { DT_ABS_CONST = 0, DT_ABS_GRID = 1 };
+enum { DT_ENV_ANALYTIC = 0, DT_ENV_GRID = 1 };
+enum { DT_CAP_ZERO = 0, DT_CAP_ENV = 1 };
+#define DT_MAX_DEPTH 15
+
+/* Absorption rate mu_t(x), P:124-138 ("differentiable 3D texture").  Per-channel RGB (R11).
+ *  CONST: sigma -> float[3].
+ *  GRID:  sigma -> float[res][res][res][3] = [z][y][x][c], vertex-centred nodes spanning the
+ *         fixed box [box_lo, box_hi]; trilinear; zero outside the box (R11).  Interior
+ *         segments integrate it with n_samples midpoint samples (R10). */
+typedef struct {
+  int32_t kind;
+  const float* sigma;
+  int32_t res;
+  float box_lo[3], box_hi[3];
+  int32_t n_samples;
+} dt_absorption;
+
+/* Frozen environment radiance, P:91 and P:160 step 3 (R14).
+ *  ANALYTIC: L(d) = ambient + sum_j w_j exp(kappa_j (mu_j . d/|d| - 1)); lobes -> float
+ *            [n_lobes][7] = mu(3), kappa, w(3).  Direction only.
+ *  GRID:     escaping ray looked up once at the shell point p (|p| = radius, or p =
+ *            radius * d/|d| if far_field): trilinear(voxel, p) + bilinear(P_xy, p.x, p.y)
+ *            + bilinear(P_xz, p.x, p.z) + bilinear(P_yz, p.y, p.z).  voxel -> float
+ *            [vres][vres][vres][4] = [z][y][x][rgb_]; planes -> float [3][pres][pres][4]
+ *            (P_xy[y][x], P_xz[z][x], P_yz[z][y]); both span [-radius, radius].
+ *  The env is not differentiated (R22).  It must stay alive and unchanged until the
+ *  matching dt_trace_backward returns (the backward replays the lookups). */
+typedef struct {
+  int32_t kind;
+  float ambient[3];
+  const float* lobes;
+  int32_t n_lobes;
+  const float* voxel;
+  int32_t vres;
+  const float* planes;
+  int32_t pres;
+  float radius;
+  int32_t far_field;
+} dt_env;
+
+/* Pinhole cameras, OpenCV axes (R19): d_cam = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1),
+ * d = normalize(R d_cam), o = camera centre.  K -> float [n_views][4] = fx, fy, cx, cy;
+ * c2w -> float [n_views][3][4] row-major.
+ * Rays: if pixel_ids != NULL, ray r is pixel pixel_ids[r] (= view*H*W + y*W + x) for
+ * r < n_rays; else every pixel of every view, ray r = pixel id r, n_rays ignored.
+ * K, c2w and pixel_ids are read during dt_trace_forward only. */
+typedef struct {
+  int32_t n_views, width, height;
+  const float* K;
+  const float* c2w;
+  const int64_t* pixel_ids;
+  int64_t n_rays;
+} dt_cameras;
+
+/* max_depth = D_max (R12): segments at depth 0..D_max are intersection-tested; a
+ * hit on a depth-D_max segment is capped.  cap_policy: DT_CAP_ZERO returns 0 for a capped
+ * branch ("discarded", R13); DT_CAP_ENV returns tau * Env(o, d).  t_eps: secondary
+ * rays start at the hit point with t > t_eps * bbox diagonal (R17); default 1e-4. */
+typedef struct {
+  int32_t max_depth;
+  int32_t cap_policy;
+  float t_eps;
+  int32_t check_finite;      /* nonzero: verify rgb is finite (extra pass + sync)  */
+} dt_trace_opts;
+
+/* Host-side statistics filled by dt_trace_forward when requested. */
+typedef struct {
+  int64_t segments_per_depth[DT_MAX_DEPTH + 1]; /* records traced at each depth (level 0 = hits) */
+  int64_t primaries;          /* camera rays                                                     */
+  int64_t primaries_traced;   /* camera rays that passed the root-AABB test and were traversed   */
+  int64_t segments;           /* traced segments = primaries_traced + sum_{k>=1} depth k        */
+  int64_t arena_capacity;     /* path-record capacity (records)                                 */
+  int32_t arena_retries;      /* forward re-runs after growing the arena (0 in steady state)    */
+  int32_t bvh_depth;          /* 0 unless dt_debug_bvh_check ran                                */
+} dt_stats;
+
+DT_API dt_status dt_create(int32_t device, dt_ctx** out);
+DT_API void dt_destroy(dt_ctx* ctx);
+DT_API const char* dt_last_error(const dt_ctx* ctx);
+DT_API const char* dt_status_string(dt_status s);
+
+/* Snapshot the mesh and rebuild the acceleration structure (rebuilt every step
+ * because the mesh moves): vertex normals n_v = normalize(sum of incident unit face
+ * normals) (R6), then an LBVH (Morton codes, radix sort, Karras hierarchy,
+ * bottom-up AABB refit).  V -> float [nv][3]; F -> int32 [nf][3], CCW = outward (R8).
+ * The context copies V and F: the caller may modify V right after this returns (on the
+ * stream).  Errors: DT_ERR_EMPTY_GEOMETRY if nv or nf is 0; DT_ERR_INVALID_ARG for NULL. */
+DT_API dt_status dt_build_bvh(dt_ctx* ctx, const float* V, int32_t nv, const int32_t* F, int32_t nf, void* stream);
+
+/* Forward recursive trace (P:154-163 steps 1-5) of every ray of `cams`.
+ *  ior:       eta_o of the object (R1).
+ *  rgb:       out float [n_rays][3], radiance.
+ *  capped_w:  out float [n_rays] or NULL: sum over capped branches of the R/T path weight.
+ *  sig_topo:  out uint64 [n_rays] or NULL: order-independent signature of the ray tree
+ *             (tree position + event per node), sig_face likewise including face ids
+ *             (parity protocol).
+ *  stats:     host dt_stats or NULL.
+ * Path records stay in the context until the next forward; the absorption field is
+ * snapshotted for the backward.  Synchronises `stream` once. */
+DT_API dt_status dt_trace_forward(dt_ctx* ctx, float ior, const dt_absorption* absorption, const dt_env* env,
+                           const dt_cameras* cams, const dt_trace_opts* opts, float* rgb, float* capped_w,
+                           uint64_t* sig_topo, uint64_t* sig_face, dt_stats* stats, void* stream);
+
+/* Reverse mode of the last forward ("The IoR ... is differentiable"):
+ * the VJP of sum(grad_rgb * rgb) at fixed path topology (R22).
+ *  grad_rgb:   in  float [n_rays][3].
+ *  grad_V:     out float [nv][3]; grad_ior: out float [1]; grad_sigma: out float [3] or
+ *              [res^3][3] matching the forward's absorption.  Any may be NULL (skipped).
+ *  accumulate: 0 overwrites the outputs, nonzero adds to them.
+ * Gradients are w.r.t. sigma itself; any activation is the caller's chain rule.
+ * Float atomics make the result nondeterministic at the ulp level. */
+DT_API dt_status dt_trace_backward(dt_ctx* ctx, const float* grad_rgb, float* grad_V, float* grad_ior, float* grad_sigma,
+                            int32_t accumulate, void* stream);
+
+/* L_color of P:177-180, its gradient fused: loss = (1/B) sum_i ||(rgb_i - target_i) * target_i||^2
+ * (elementwise *), grad_rgb = 2 (rgb - target) * target^2 / B with B = n_rays.
+ * rgb, target -> float [n][3]; grad_rgb out [n][3]; loss out float [1] (device). */
+DT_API dt_status dt_loss_color(dt_ctx* ctx, const float* rgb, const float* target, int64_t n, float* grad_rgb, float* loss,
+                        void* stream);
+
+/* Profiling.  With profiling enabled the library brackets each phase's launches with CUDA
+ * events on the caller's stream (no extra synchronisation) and accumulates their device
+ * time; dt_get_profile resolves pending events (synchronising on them) and returns the
+ * totals since the last reset.  Traversal counters and the kernel-launch count are always
+ * maintained.  Phases: */
+enum { DT_PH_BUILD = 0, DT_PH_TRACE0 = 1, DT_PH_SHADE0 = 2, DT_PH_TRACE = 3, DT_PH_GATHER = 4, DT_PH_BWD = 5,
+       DT_PH_NORMALS_BWD = 6, DT_PH_LOSS = 7, DT_PH_COUNT = 8 };
+typedef struct {
+  double ms[DT_PH_COUNT];          /* summed device time per phase                           */
+  int64_t launches[DT_PH_COUNT];   /* kernel launches per phase                              */
+  int64_t kernel_launches;         /* all kernels this context launched since the reset     */
+  int64_t node_visits;             /* LBVH inner nodes fetched by the trace kernels          */
+  int64_t tri_tests;               /* ray-triangle tests by the trace kernels                */
+} dt_profile;
+DT_API dt_status dt_set_profiling(dt_ctx* ctx, int32_t enable);
+DT_API dt_status dt_get_profile(dt_ctx* ctx, dt_profile* out, int32_t reset);
+
+/* Test-only: closest hit of n rays (rays -> float [n][6] = o.xyz, d.xyz) with t > t_lo via the
+ * LBVH (brute_force = 0) or by testing every face with the same routine (brute_force = 1).
+ * face out int32 [n] (original face id, -1 = miss); tuv out float [n][3]. */
+DT_API dt_status dt_debug_closest_hit(dt_ctx* ctx, const float* rays, int64_t n, float t_lo, int32_t brute_force,
+                               int32_t* face, float* tuv, void* stream);
+
+/* Test-only: validate the LBVH (host out int64[4]): [0] boxes not containing their child's
+ * box, [1] leaves reached from the root, [2] distinct faces reached, [3] tree depth. */
+DT_API dt_status dt_debug_bvh_check(dt_ctx* ctx, int64_t* out, void* stream);
+
+/* Test-only: copy the vertex normals of the last build to out (device float [nv][3]). */
+DT_API dt_status dt_debug_vertex_normals(dt_ctx* ctx, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -54,7 +54,7 @@ def lib():
     global _lib
     if _lib is None:
         _lib = C.CDLL(build())
-        for name in ("dto_render", "dto_backward", "dto_jvp", "dto_closest_hit", "dto_vertex_normals",
+        for name in ("dto_render", "dto_backward", "dto_jvp", "dto_closest_hit", "dto_vertex_normals", "dto_camera_rays",
                      "dto_interface", "dto_env", "dto_transmittance"):
             getattr(_lib, name).restype = C.c_int
     return _lib
@@ -169,6 +169,43 @@ def closest_hit(osc: OracleScene, rays, t_lo: float = 0.0, nthreads: int = 0):
                                C.c_int(nthreads))
     assert rc == 0, rc
     return face, tuv, flags
+
+
+def camera_rays(osc: OracleScene, pixel_ids):
+    pid = np.ascontiguousarray(pixel_ids, np.int64)
+    out = np.zeros((pid.shape[0], 6))
+    assert lib().dto_camera_rays(osc.ref, _p(pid), C.c_int64(pid.shape[0]), _p(out)) == 0
+    return out
+
+
+FLAG_ILLCOND = 8
+F32_DIR_ERR = 1.2e-7     # ~2 ulp of a float32 unit direction component
+
+
+def ill_conditioned(osc: OracleScene, pixel_ids, tol: float = 5e-5, n_dirs: int = 2, nthreads: int = 0):
+    """Pixels whose radiance moves by more than `tol` when the camera ray direction moves by
+    the float32 rounding of its components (F32_DIR_ERR): float32 arithmetic cannot hold them
+    to 1e-4 whatever the implementation.  Estimated with float64 central
+    differences along random tangents (eps = 1e-7, far inside the smooth region)."""
+    rays = camera_rays(osc, pixel_ids)
+    n = rays.shape[0]
+    g = np.random.default_rng(1234)
+    sens = np.zeros(n)
+    eps = 1e-7
+    base_sig = None
+    for k in range(n_dirs):
+        u = g.normal(size=(n, 3))
+        d = rays[:, 3:]
+        u -= d * (u * d).sum(1, keepdims=True)
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        rp = rays.copy(); rp[:, 3:] += eps * u
+        rm = rays.copy(); rm[:, 3:] -= eps * u
+        a = render(osc, rays=rp, nthreads=nthreads)
+        b = render(osc, rays=rm, nthreads=nthreads)
+        s = np.abs(a["rgb"] - b["rgb"]).max(1) / (2 * eps)
+        s[a["sig_topo"] != b["sig_topo"]] = np.inf
+        sens = np.maximum(sens, s)
+    return sens * F32_DIR_ERR > tol
 
 
 def vertex_normals(osc: OracleScene):

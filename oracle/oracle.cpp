@@ -879,6 +879,16 @@ int dto_closest_hit(const dto_scene* s, const double* rays, int64_t n, double t_
   return 0;
 }
 
+int dto_camera_rays(const dto_scene* s, const int64_t* pixel_ids, int64_t n, double* rays) {
+  for (int64_t i = 0; i < n; ++i) {
+    V3d o, d;
+    camera_ray(s, pixel_ids ? pixel_ids[i] : i, o, d);
+    rays[6 * i] = o.x; rays[6 * i + 1] = o.y; rays[6 * i + 2] = o.z;
+    rays[6 * i + 3] = d.x; rays[6 * i + 4] = d.y; rays[6 * i + 5] = d.z;
+  }
+  return 0;
+}
+
 int dto_vertex_normals(const dto_scene* s, double* out) {
   if (check_scene(s)) return 1;
   Model<double> m = make_model<double>(s, nullptr, 0.0, nullptr);

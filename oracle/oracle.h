@@ -82,6 +82,9 @@ int dto_jvp(const dto_scene* s, const int64_t* pixel_ids, const double* rays, in
 int dto_closest_hit(const dto_scene* s, const double* rays, int64_t n, double t_lo,
                     int32_t* face, double* tuv, int32_t* flags, int nthreads);
 
+/* Camera rays (R19) of the given pixels: rays [n][6] = o.xyz, d.xyz (float64). */
+int dto_camera_rays(const dto_scene* s, const int64_t* pixel_ids, int64_t n, double* rays);
+
 /* Pieces, exposed for the closed-form pins. */
 int dto_vertex_normals(const dto_scene* s, double* out /* [nv][3] */);
 /* d: incoming ray direction, n: unit normal oriented against d.  out[12] =

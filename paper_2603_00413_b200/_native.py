@@ -1,0 +1,104 @@
+"""ctypes declarations of libdifftrans (include/difftrans.h).  Argument marshalling only.
+
+The product path has no fallback: if the shared library is missing or cannot be loaded,
+importing the tracer raises.  It never loads or calls anything under oracle/.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdifftrans.so")
+
+DT_OK = 0
+STATUS = {0: "DT_OK", 1: "DT_ERR_INVALID_ARG", 2: "DT_ERR_EMPTY_GEOMETRY", 3: "DT_ERR_CUDA", 4: "DT_ERR_OOM",
+          5: "DT_ERR_NOT_BUILT", 6: "DT_ERR_NO_FORWARD", 7: "DT_ERR_NONFINITE", 8: "DT_ERR_STACK"}
+DT_MAX_DEPTH = 15
+
+
+class Absorption(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("sigma", C.c_void_p), ("res", C.c_int32), ("box_lo", C.c_float * 3),
+                ("box_hi", C.c_float * 3), ("n_samples", C.c_int32)]
+
+
+class Env(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("ambient", C.c_float * 3), ("lobes", C.c_void_p), ("n_lobes", C.c_int32),
+                ("voxel", C.c_void_p), ("vres", C.c_int32), ("planes", C.c_void_p), ("pres", C.c_int32),
+                ("radius", C.c_float), ("far_field", C.c_int32)]
+
+
+class Cameras(C.Structure):
+    _fields_ = [("n_views", C.c_int32), ("width", C.c_int32), ("height", C.c_int32), ("K", C.c_void_p),
+                ("c2w", C.c_void_p), ("pixel_ids", C.c_void_p), ("n_rays", C.c_int64)]
+
+
+class TraceOpts(C.Structure):
+    _fields_ = [("max_depth", C.c_int32), ("cap_policy", C.c_int32), ("t_eps", C.c_float),
+                ("check_finite", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("segments_per_depth", C.c_int64 * (DT_MAX_DEPTH + 1)), ("primaries", C.c_int64),
+                ("primaries_traced", C.c_int64), ("segments", C.c_int64), ("arena_capacity", C.c_int64),
+                ("arena_retries", C.c_int32), ("bvh_depth", C.c_int32)]
+
+    def as_dict(self, max_depth: int):
+        return dict(segments_per_depth=[int(self.segments_per_depth[k]) for k in range(max_depth + 1)],
+                    primaries=int(self.primaries), primaries_traced=int(self.primaries_traced),
+                    segments=int(self.segments), arena_capacity=int(self.arena_capacity),
+                    arena_retries=int(self.arena_retries))
+
+
+PHASES = ["build", "trace0", "shade0", "trace", "gather", "bwd", "normals_bwd", "loss"]
+
+
+class Profile(C.Structure):
+    _fields_ = [("ms", C.c_double * len(PHASES)), ("launches", C.c_int64 * len(PHASES)),
+                ("kernel_launches", C.c_int64), ("node_visits", C.c_int64), ("tri_tests", C.c_int64)]
+
+    def as_dict(self):
+        return dict(ms={p: float(self.ms[i]) for i, p in enumerate(PHASES)},
+                    launches={p: int(self.launches[i]) for i, p in enumerate(PHASES)},
+                    kernel_launches=int(self.kernel_launches), node_visits=int(self.node_visits),
+                    tri_tests=int(self.tri_tests))
+
+
+_P = C.c_void_p
+SIGNATURES = {
+    "dt_set_profiling": (C.c_int, [_P, C.c_int32]),
+    "dt_get_profile": (C.c_int, [_P, C.POINTER(Profile), C.c_int32]),
+    "dt_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "dt_destroy": (None, [_P]),
+    "dt_last_error": (C.c_char_p, [_P]),
+    "dt_status_string": (C.c_char_p, [C.c_int]),
+    "dt_build_bvh": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int32, _P]),
+    "dt_trace_forward": (C.c_int, [_P, C.c_float, C.POINTER(Absorption), C.POINTER(Env), C.POINTER(Cameras),
+                                   C.POINTER(TraceOpts), _P, _P, _P, _P, C.POINTER(Stats), _P]),
+    "dt_trace_backward": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, _P]),
+    "dt_loss_color": (C.c_int, [_P, _P, _P, C.c_int64, _P, _P, _P]),
+    "dt_debug_closest_hit": (C.c_int, [_P, _P, C.c_int64, C.c_float, C.c_int32, _P, _P, _P]),
+    "dt_debug_bvh_check": (C.c_int, [_P, C.POINTER(C.c_int64), _P]),
+    "dt_debug_vertex_normals": (C.c_int, [_P, _P, _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libdifftrans.so (building it with nvcc first if it is absent)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            from . import build as _build
+            _build.build()
+        _lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(_lib, name)
+            fn.restype = res
+            fn.argtypes = args
+    return _lib
+
+
+class DiffTransError(RuntimeError):
+    pass

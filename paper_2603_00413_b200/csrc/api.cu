@@ -1,0 +1,459 @@
+// C ABI of libdifftrans (include/difftrans.h): argument checking, context-owned memory,
+// the record-arena policy and the per-depth launch sequence.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "dt_internal.h"
+
+using namespace dt;
+
+namespace {
+
+dt_status fail(dt_ctx* c, dt_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define DT_CU(call)                                                                              \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess) {                                                                     \
+      dt_status s_ = e_ == cudaErrorMemoryAllocation ? DT_ERR_OOM : DT_ERR_CUDA;                 \
+      return fail(c, s_, "%s failed: %s", #call, cudaGetErrorString(e_));                        \
+    }                                                                                            \
+  } while (0)
+
+#define DT_ARG(cond, ...) \
+  do {                    \
+    if (!(cond)) return fail(c, DT_ERR_INVALID_ARG, __VA_ARGS__); \
+  } while (0)
+
+cudaError_t alloc_arena(dt_ctx* c, int64_t cap) {
+  if (c->rec.o) cudaFree(c->rec.o);
+  c->rec = Records{};
+  c->arena_cap = 0;
+  float4* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, (size_t)cap * kRecordBytes);
+  if (e != cudaSuccess) return e;
+  c->rec.o = base;
+  c->rec.d = base + cap;
+  c->rec.thr = base + 2 * cap;
+  c->rec.hit = base + 3 * cap;
+  c->rec.tau = base + 4 * cap;
+  c->rec.lsub = base + 5 * cap;
+  c->rec.go = base + 6 * cap;
+  c->rec.gd = base + 7 * cap;
+  c->arena_cap = cap;
+  return cudaSuccess;
+}
+
+int64_t arena_limit() {
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  return (int64_t)((double)fr * 0.70 / kRecordBytes);
+}
+
+cudaEvent_t get_event(dt_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Fold completed phase timings into the totals (waits on the pending events).
+void resolve_profile(dt_ctx* c) {
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(p.b);
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) c->ph_ms[p.ph] += ms;
+    c->event_pool.push_back(p.a);
+    c->event_pool.push_back(p.b);
+  }
+  c->pending.clear();
+}
+
+}  // namespace
+
+PhaseTimer::PhaseTimer(dt_ctx* c_, int ph_, cudaStream_t st_) : c(c_), ph(ph_), st(st_) {
+  if (c->prof) {
+    a = get_event(c);
+    cudaEventRecord(a, st);
+  }
+}
+
+void PhaseTimer::end(int n_launches) {
+  c->ph_launches[ph] += n_launches;
+  c->kernel_launches += n_launches;
+  if (c->prof) {
+    cudaEvent_t b = get_event(c);
+    cudaEventRecord(b, st);
+    c->pending.push_back({ph, a, b});
+  }
+}
+
+extern "C" {
+
+const char* dt_status_string(dt_status s) {
+  switch (s) {
+    case DT_OK: return "DT_OK";
+    case DT_ERR_INVALID_ARG: return "DT_ERR_INVALID_ARG";
+    case DT_ERR_EMPTY_GEOMETRY: return "DT_ERR_EMPTY_GEOMETRY";
+    case DT_ERR_CUDA: return "DT_ERR_CUDA";
+    case DT_ERR_OOM: return "DT_ERR_OOM";
+    case DT_ERR_NOT_BUILT: return "DT_ERR_NOT_BUILT";
+    case DT_ERR_NO_FORWARD: return "DT_ERR_NO_FORWARD";
+    case DT_ERR_NONFINITE: return "DT_ERR_NONFINITE";
+    case DT_ERR_STACK: return "DT_ERR_STACK";
+  }
+  return "DT_ERR_UNKNOWN";
+}
+
+dt_status dt_create(int32_t device, dt_ctx** out) {
+  dt_ctx* c = nullptr;
+  if (!out) return DT_ERR_INVALID_ARG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return DT_ERR_CUDA;
+  if (device < 0 || device >= n) return DT_ERR_INVALID_ARG;
+  c = new dt_ctx();
+  c->device = device;
+  cudaSetDevice(device);
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->lvl, LV_INTS * sizeof(int))) || (e = cudaMallocHost(&c->host_lvl, LV_INTS * sizeof(int))) ||
+      (e = cudaMalloc(&c->gior, 4 * sizeof(float))) || (e = cudaMalloc(&c->counters, 2 * sizeof(unsigned long long))) ||
+      (e = cudaMemset(c->counters, 0, 2 * sizeof(unsigned long long)))) {
+    dt_destroy(c);
+    return DT_ERR_CUDA;
+  }
+  *out = c;
+  return DT_OK;
+}
+
+void dt_destroy(dt_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  void* ptrs[] = {c->V, c->F, c->nrm, c->fnrm, c->nodes, c->tris, c->keys, c->vals, c->hist, c->children,
+                  c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, c->vstart, c->vcorner, c->scal,
+                  c->iscal, c->rec.o, c->lvl, c->sigma_snap, c->gV, c->gN, c->gVn, c->gS, c->fe, c->gsig, c->gior,
+                  c->counters};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->host_lvl) cudaFreeHost(c->host_lvl);
+  delete c;
+}
+
+const char* dt_last_error(const dt_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+dt_status dt_build_bvh(dt_ctx* c, const float* V, int32_t nv, const int32_t* F, int32_t nf, void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  DT_ARG(V && F, "dt_build_bvh: V and F must be non-NULL device pointers");
+  if (nv <= 0 || nf <= 0) return fail(c, DT_ERR_EMPTY_GEOMETRY, "dt_build_bvh: empty geometry (nv=%d, nf=%d)", nv, nf);
+  DT_ARG(nf < (1 << 29) && nv < (1 << 29), "dt_build_bvh: nv/nf too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  PhaseTimer pt(c, DT_PH_BUILD, st);
+  int nl = 0;
+  DT_CU(build_bvh(c, V, nv, F, nf, st, &nl));
+  pt.end(nl);
+  c->built = true;
+  c->have_fwd = false;
+  return DT_OK;
+}
+
+dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const dt_env* env, const dt_cameras* cams,
+                           const dt_trace_opts* opts, float* rgb, float* capped_w, uint64_t* sig_topo,
+                           uint64_t* sig_face, dt_stats* stats, void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_trace_forward: call dt_build_bvh first");
+  DT_ARG(ab && env && cams && opts, "dt_trace_forward: absorption/env/cams/opts must be non-NULL");
+  DT_ARG(rgb, "dt_trace_forward: rgb must be a device pointer");
+  DT_ARG(opts->max_depth >= 0 && opts->max_depth <= DT_MAX_DEPTH, "dt_trace_forward: opts.max_depth=%d not in [0,%d]",
+         opts->max_depth, DT_MAX_DEPTH);
+  DT_ARG(opts->cap_policy == DT_CAP_ZERO || opts->cap_policy == DT_CAP_ENV, "dt_trace_forward: bad opts.cap_policy");
+  DT_ARG(opts->t_eps >= 0.0f, "dt_trace_forward: opts.t_eps must be >= 0");
+  DT_ARG(ior > 0.0f, "dt_trace_forward: ior must be > 0");
+  DT_ARG(cams->K && cams->c2w && cams->n_views > 0 && cams->width > 0 && cams->height > 0,
+         "dt_trace_forward: cams (K, c2w, n_views, width, height) invalid");
+  DT_ARG(ab->sigma, "dt_trace_forward: absorption.sigma is NULL");
+  DT_ARG(ab->kind == DT_ABS_CONST || (ab->kind == DT_ABS_GRID && ab->res >= 2 && ab->n_samples >= 1),
+         "dt_trace_forward: absorption (kind=%d res=%d n_samples=%d) invalid", ab->kind, ab->res, ab->n_samples);
+  DT_ARG((env->kind == DT_ENV_ANALYTIC && (env->n_lobes == 0 || env->lobes)) ||
+             (env->kind == DT_ENV_GRID && env->voxel && env->planes && env->vres >= 2 && env->pres >= 2 && env->radius > 0),
+         "dt_trace_forward: env (kind=%d) invalid", env->kind);
+  int64_t npix = (int64_t)cams->n_views * cams->width * cams->height;
+  int64_t n_rays = cams->pixel_ids ? cams->n_rays : npix;
+  DT_ARG(n_rays >= 0 && n_rays < (1ll << 31), "dt_trace_forward: n_rays=%lld out of range", (long long)n_rays);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int D = opts->max_depth;
+
+  // absorption snapshot (the backward differentiates w.r.t. these values)
+  size_t slen = ab->kind == DT_ABS_CONST ? 3 : (size_t)ab->res * ab->res * ab->res * 3;
+  if (slen > c->sigma_cap) {
+    if (c->sigma_snap) cudaFree(c->sigma_snap);
+    if (c->gsig) cudaFree(c->gsig);
+    c->sigma_snap = c->gsig = nullptr;
+    c->sigma_cap = 0;
+    DT_CU(cudaMalloc(&c->sigma_snap, slen * sizeof(float)));
+    DT_CU(cudaMalloc(&c->gsig, slen * sizeof(float)));
+    c->sigma_cap = slen;
+  }
+  c->sigma_len = slen;
+  DT_CU(cudaMemcpyAsync(c->sigma_snap, ab->sigma, slen * sizeof(float), cudaMemcpyDeviceToDevice, st));
+
+  DevScene s = scene_from_ctx(c);
+  s.ior = ior;
+  s.abs_kind = ab->kind;
+  s.sigma = c->sigma_snap;
+  s.sres = ab->res;
+  s.nsamp = std::max(1, ab->n_samples);
+  s.slo = f3(ab->box_lo[0], ab->box_lo[1], ab->box_lo[2]);
+  s.shi = f3(ab->box_hi[0], ab->box_hi[1], ab->box_hi[2]);
+  s.env_kind = env->kind;
+  s.ambient = f3(env->ambient[0], env->ambient[1], env->ambient[2]);
+  s.lobes = env->lobes;
+  s.nlobes = env->n_lobes;
+  s.voxel = (const float4*)env->voxel;
+  s.vres = env->vres;
+  s.planes = (const float4*)env->planes;
+  s.pres = env->pres;
+  s.radius = env->radius;
+  s.far_field = env->far_field;
+  s.max_depth = D;
+  s.cap_policy = opts->cap_policy;
+
+  FwdLaunch a{};
+  a.s = s;
+  a.lvl = c->lvl;
+  a.t_eps = opts->t_eps;
+  a.K = cams->K;
+  a.c2w = cams->c2w;
+  a.W = cams->width;
+  a.H = cams->height;
+  a.n_views = cams->n_views;
+  a.pids = cams->pixel_ids;
+  a.tiles_x = (cams->width + 7) / 8;
+  a.tiles_per_view = a.tiles_x * ((cams->height + 3) / 4);
+  a.n_items = cams->pixel_ids ? n_rays : (int64_t)a.tiles_per_view * cams->n_views * 32;
+  a.rgb = rgb;
+  a.capw = capped_w;
+  a.sig_t = (unsigned long long*)sig_topo;
+  a.sig_f = (unsigned long long*)sig_face;
+  a.counters = c->counters;
+
+  int64_t limit = arena_limit() + c->arena_cap;
+  if (c->arena_cap == 0) {
+    int64_t want = std::min<int64_t>(std::max<int64_t>(n_rays * 3, 1 << 16), limit);
+    DT_CU(alloc_arena(c, want));
+  }
+  int retries = 0;
+  while (true) {
+    a.r = c->rec;
+    a.cap = c->arena_cap;
+    DT_CU(cudaMemsetAsync(c->lvl, 0, LV_INTS * sizeof(int), st));
+    if (capped_w) DT_CU(cudaMemsetAsync(capped_w, 0, (size_t)n_rays * sizeof(float), st));
+    if (sig_topo) DT_CU(cudaMemsetAsync(sig_topo, 0, (size_t)n_rays * sizeof(uint64_t), st));
+    if (sig_face) DT_CU(cudaMemsetAsync(sig_face, 0, (size_t)n_rays * sizeof(uint64_t), st));
+    if (n_rays > 0) {
+      {
+        PhaseTimer p(c, DT_PH_TRACE0, st);
+        DT_CU(launch_trace_primary(a, D, c->sm_count, st));
+        p.end(1);
+      }
+      {
+        PhaseTimer p(c, DT_PH_SHADE0, st);
+        DT_CU(launch_shade_level0(a, D, c->sm_count, st));
+        p.end(1);
+      }
+      for (int k = 1; k <= D; ++k) {
+        PhaseTimer p(c, DT_PH_TRACE, st);
+        DT_CU(launch_forward_level(a, k, D, c->sm_count, st));
+        p.end(1);
+      }
+      for (int k = std::max(D - 1, 0); k >= 0; --k) {
+        PhaseTimer p(c, DT_PH_GATHER, st);
+        DT_CU(launch_gather_level(a, k, c->sm_count, st));
+        p.end(1);
+      }
+    }
+    DT_CU(cudaMemcpyAsync(c->host_lvl, c->lvl, LV_INTS * sizeof(int), cudaMemcpyDeviceToHost, st));
+    DT_CU(cudaStreamSynchronize(st));
+    if (!c->host_lvl[LV_OVERFLOW]) break;
+    int64_t need = 0;
+    for (int k = 0; k <= D; ++k) need += (unsigned)c->host_lvl[LV_CNT + k];
+    int64_t next = std::max<int64_t>(2 * c->arena_cap, need + need / 4 + 1024);
+    limit = arena_limit() + c->arena_cap;
+    if (c->arena_cap >= limit || ++retries > 8)
+      return fail(c, DT_ERR_OOM, "dt_trace_forward: record arena needs > %lld records (HBM budget %lld)",
+                  (long long)next, (long long)limit);
+    next = std::min(next, limit);
+    cudaFree(c->rec.o);
+    c->rec = Records{};
+    c->arena_cap = 0;
+    DT_CU(alloc_arena(c, next));
+  }
+  if (c->prof) resolve_profile(c);   // all recorded events are complete after the sync
+  if (c->host_lvl[LV_STACKERR]) return fail(c, DT_ERR_STACK, "dt_trace_forward: BVH deeper than the traversal stack");
+  if (opts->check_finite && n_rays > 0) {
+    DT_CU(cudaMemsetAsync(c->lvl + LV_NONFINITE, 0, sizeof(int), st));
+    DT_CU(launch_check_finite(rgb, 3 * n_rays, c->lvl + LV_NONFINITE, st));
+    int flag = 0;
+    DT_CU(cudaMemcpyAsync(&flag, c->lvl + LV_NONFINITE, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DT_CU(cudaStreamSynchronize(st));
+    if (flag) return fail(c, DT_ERR_NONFINITE, "dt_trace_forward: rgb has non-finite values");
+  }
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    int64_t seg = c->host_lvl[LV_TRACED];
+    for (int k = 0; k <= D; ++k) {
+      stats->segments_per_depth[k] = c->host_lvl[LV_CNT + k];
+      if (k > 0) seg += c->host_lvl[LV_CNT + k];
+    }
+    stats->primaries = n_rays;
+    stats->primaries_traced = c->host_lvl[LV_TRACED];
+    stats->segments = seg;
+    stats->arena_capacity = c->arena_cap;
+    stats->arena_retries = retries;
+  }
+  c->have_fwd = true;
+  c->n_rays = n_rays;
+  c->fwd_scene = s;
+  c->fwd_t_eps = opts->t_eps;
+  return DT_OK;
+}
+
+dt_status dt_trace_backward(dt_ctx* c, const float* grad_rgb, float* grad_V, float* grad_ior, float* grad_sigma,
+                            int32_t accumulate, void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (!c->have_fwd) return fail(c, DT_ERR_NO_FORWARD, "dt_trace_backward: no forward on this context");
+  DT_ARG(grad_rgb || c->n_rays == 0, "dt_trace_backward: grad_rgb is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  DT_CU(cudaMemsetAsync(c->gV, 0, (size_t)c->nv * 16, st));
+  DT_CU(cudaMemsetAsync(c->gN, 0, (size_t)c->nv * 16, st));
+  DT_CU(cudaMemsetAsync(c->gsig, 0, c->sigma_len * sizeof(float), st));
+  DT_CU(cudaMemsetAsync(c->gior, 0, sizeof(float), st));
+  BwdLaunch b{};
+  b.s = c->fwd_scene;
+  b.r = c->rec;
+  b.lvl = c->lvl;
+  b.cap = c->arena_cap;
+  b.t_eps = c->fwd_t_eps;
+  b.grad_rgb = grad_rgb;
+  b.dV = c->gV;
+  b.dN = c->gN;
+  b.dsig = c->gsig;
+  b.dior = c->gior;
+  if (c->n_rays > 0)
+    for (int k = b.s.max_depth; k >= 0; --k) {
+      PhaseTimer p(c, DT_PH_BWD, st);
+      DT_CU(launch_backward_level(b, k, c->sm_count, st));
+      p.end(1);
+    }
+  PhaseTimer p(c, DT_PH_NORMALS_BWD, st);
+  DT_CU(launch_vertex_normal_backward(c, st));
+  DT_CU(launch_finalize(c, grad_V, grad_ior, grad_sigma, accumulate, st));
+  p.end(3 + (grad_V ? 1 : 0) + (grad_ior ? 1 : 0) + (grad_sigma ? 1 : 0));
+  return DT_OK;
+}
+
+dt_status dt_set_profiling(dt_ctx* c, int32_t enable) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (!enable) resolve_profile(c);
+  c->prof = enable != 0;
+  return DT_OK;
+}
+
+dt_status dt_get_profile(dt_ctx* c, dt_profile* out, int32_t reset) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  DT_ARG(out, "dt_get_profile: out is NULL");
+  resolve_profile(c);
+  unsigned long long cnt[2] = {0, 0};
+  DT_CU(cudaMemcpy(cnt, c->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < DT_PH_COUNT; ++i) {
+    out->ms[i] = c->ph_ms[i];
+    out->launches[i] = c->ph_launches[i];
+  }
+  out->kernel_launches = c->kernel_launches;
+  out->node_visits = (int64_t)cnt[0];
+  out->tri_tests = (int64_t)cnt[1];
+  if (reset) {
+    for (int i = 0; i < DT_PH_COUNT; ++i) { c->ph_ms[i] = 0.0; c->ph_launches[i] = 0; }
+    c->kernel_launches = 0;
+    DT_CU(cudaMemset(c->counters, 0, sizeof(cnt)));
+  }
+  return DT_OK;
+}
+
+dt_status dt_loss_color(dt_ctx* c, const float* rgb, const float* target, int64_t n, float* grad_rgb, float* loss,
+                        void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  DT_ARG(rgb && target && grad_rgb && loss, "dt_loss_color: NULL argument");
+  DT_ARG(n >= 0, "dt_loss_color: n < 0");
+  PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
+  DT_CU(launch_loss_color(rgb, target, n, grad_rgb, loss, (cudaStream_t)stream));
+  p.end(1);
+  return DT_OK;
+}
+
+dt_status dt_debug_closest_hit(dt_ctx* c, const float* rays, int64_t n, float t_lo, int32_t brute_force, int32_t* face,
+                               float* tuv, void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_debug_closest_hit: call dt_build_bvh first");
+  DT_ARG(rays && face && tuv, "dt_debug_closest_hit: NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  DevScene s = scene_from_ctx(c);
+  DT_CU(cudaMemsetAsync(c->lvl + LV_STACKERR, 0, sizeof(int), st));
+  if (n > 0) DT_CU(launch_debug_closest_hit(s, rays, n, t_lo, brute_force, face, tuv, c->lvl + LV_STACKERR, st));
+  int err = 0;
+  DT_CU(cudaMemcpyAsync(&err, c->lvl + LV_STACKERR, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DT_CU(cudaStreamSynchronize(st));
+  if (err) return fail(c, DT_ERR_STACK, "dt_debug_closest_hit: traversal stack overflow");
+  return DT_OK;
+}
+
+dt_status dt_debug_bvh_check(dt_ctx* c, int64_t* out, void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_debug_bvh_check: call dt_build_bvh first");
+  DT_ARG(out, "dt_debug_bvh_check: out is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  long long* dev = nullptr;
+  DT_CU(cudaMallocAsync(&dev, 4 * sizeof(long long), st));
+  DT_CU(launch_bvh_check(c, dev, st));
+  DT_CU(cudaMemcpyAsync(out, dev, 4 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  DT_CU(cudaFreeAsync(dev, st));
+  DT_CU(cudaStreamSynchronize(st));
+  return DT_OK;
+}
+
+dt_status dt_debug_vertex_normals(dt_ctx* c, float* out, void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_debug_vertex_normals: call dt_build_bvh first");
+  DT_ARG(out, "dt_debug_vertex_normals: out is NULL");
+  DT_CU(cudaMemcpy2DAsync(out, 12, c->nrm, 16, 12, c->nv, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return DT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,501 @@
+// Device-side building blocks of the tracer: camera rays, ray/box and ray/triangle tests,
+// the specular interface, Beer-Lambert transmittance, the frozen
+// environment lookup (R14) and the local reverse-mode rules (DESIGN.md Appendix B).
+// Float32 throughout.  Written independently of oracle/ (no shared code).
+#pragma once
+#include "dt_math.cuh"
+
+namespace dt {
+
+constexpr float kInf = __builtin_huge_valf();
+constexpr int kStackShared = 16;   // short stack entries per thread in shared memory
+constexpr int kStackLocal = 112;   // spill entries per thread (local memory, L1-cached)
+
+// per-record event codes (the protocol numbering, shared only as a spec)
+enum { EV_MISS = 0, EV_HIT_OUT = 1, EV_HIT_IN = 2, EV_HIT_OUT_TIR = 3, EV_HIT_IN_TIR = 4, EV_CAP_OUT = 5, EV_CAP_IN = 6 };
+// record flag bits (hit.w)
+enum { RF_MISS = 1, RF_CAPPED = 2, RF_INSIDE = 4, RF_TIR = 8, RF_DEGEN = 16, RF_CULLED = 32 };
+
+DT_D uint64_t topo_key(uint32_t pos, int ev) { return (uint64_t)pos | ((uint64_t)ev << 32); }
+DT_D uint64_t face_key(uint32_t pos, int ev, int face) {
+  return (uint64_t)pos | ((uint64_t)(uint32_t)(face + 1) << 20) | ((uint64_t)ev << 52);
+}
+
+struct DevScene {
+  // mesh snapshot (dt_build_bvh)
+  const float4* V;      // [nv] xyz
+  const int* F;         // [nf*3]
+  const float4* nrm;    // [nv] vertex normal xyz, |sum of unit face normals| in w
+  int nv, nf;
+  // LBVH
+  const float4* nodes;  // [(nf-1)*4] 64-B nodes: two child AABBs + child refs
+  const float4* tris;   // [nf*3] 48-B triangles in leaf order: (v0, id), (e1, -), (e2, -)
+  int root;             // internal node 0, or ~0 when nf == 1
+  const float* scal;    // device scalars: [0..5] root box lo/hi, [6] t_min
+  // material
+  float ior;
+  int abs_kind;
+  const float* sigma;
+  int sres, nsamp;
+  float3 slo, shi;
+  // environment
+  int env_kind;
+  float3 ambient;
+  const float* lobes;
+  int nlobes;
+  const float4* voxel;
+  int vres;
+  const float4* planes;
+  int pres;
+  float radius;
+  int far_field;
+  // options
+  int max_depth, cap_policy;
+};
+
+// ----------------------------------------------------------------------------- camera (R19)
+DT_D void camera_ray(const float* K, const float* c2w, int W, int H, int64_t pid, float3& o, float3& d) {
+  int64_t hw = (int64_t)W * H;
+  int view = (int)(pid / hw);
+  int64_t rem = pid - (int64_t)view * hw;
+  int y = (int)(rem / W), x = (int)(rem - (int64_t)y * W);
+  const float* k = K + 4 * view;
+  const float* m = c2w + 12 * view;
+  float dx = ((float)x + 0.5f - k[2]) / k[0];
+  float dy = ((float)y + 0.5f - k[3]) / k[1];
+  float3 w = f3(m[0] * dx + m[1] * dy + m[2], m[4] * dx + m[5] * dy + m[6], m[8] * dx + m[9] * dy + m[10]);
+  d = w * (1.0f / sqrtf(dot(w, w)));
+  o = f3(m[3], m[7], m[11]);
+}
+
+// ----------------------------------------------------------------------------- intersection
+// Explicit round-to-nearest intrinsics: no FMA contraction, so the LBVH traversal, the
+// brute-force test and the backward replay produce bit-identical (t, u, v).
+DT_D float3 sub_rn(float3 a, float3 b) { return f3(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z)); }
+DT_D float dot_rn(float3 a, float3 b) {
+  return __fadd_rn(__fadd_rn(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)), __fmul_rn(a.z, b.z));
+}
+DT_D float3 cross_rn(float3 a, float3 b) {
+  return f3(__fsub_rn(__fmul_rn(a.y, b.z), __fmul_rn(a.z, b.y)), __fsub_rn(__fmul_rn(a.z, b.x), __fmul_rn(a.x, b.z)),
+            __fsub_rn(__fmul_rn(a.x, b.y), __fmul_rn(a.y, b.x)));
+}
+
+// Moller-Trumbore (R15/R16): hit iff det != 0, u >= 0, v >= 0, u + v <= 1, t > t_lo.
+DT_D bool intersect_tri(float3 o, float3 d, float3 v0, float3 e1, float3 e2, float t_lo, float& t, float& u,
+                        float& v) {
+  float3 p = cross_rn(d, e2);
+  float det = dot_rn(e1, p);
+  if (det == 0.0f) return false;
+  float inv = __frcp_rn(det);
+  float3 s = sub_rn(o, v0);
+  u = __fmul_rn(dot_rn(s, p), inv);
+  if (!(u >= 0.0f)) return false;
+  float3 q = cross_rn(s, e1);
+  v = __fmul_rn(dot_rn(d, q), inv);
+  if (!(v >= 0.0f) || !(__fadd_rn(u, v) <= 1.0f)) return false;
+  t = __fmul_rn(dot_rn(e2, q), inv);
+  return t > t_lo;
+}
+
+DT_D float3 safe_inv(float3 d) {
+  const float e = 1e-20f;
+  return f3(1.0f / (fabsf(d.x) < e ? copysignf(e, d.x) : d.x), 1.0f / (fabsf(d.y) < e ? copysignf(e, d.y) : d.y),
+            1.0f / (fabsf(d.z) < e ? copysignf(e, d.z) : d.z));
+}
+
+// Conservative slab test: padded so that no box whose triangle the exact-rounding test
+// above would accept is culled (boxes are also inflated at build time).
+DT_D bool slab(float lx, float hx, float ly, float hy, float lz, float hz, float3 o, float3 inv, float tbest,
+               float& tnear) {
+  float tx0 = (lx - o.x) * inv.x, tx1 = (hx - o.x) * inv.x;
+  float ty0 = (ly - o.y) * inv.y, ty1 = (hy - o.y) * inv.y;
+  float tz0 = (lz - o.z) * inv.z, tz1 = (hz - o.z) * inv.z;
+  float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+  float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tbest));
+  tnear = tmin;
+  return tmin * 0.99999f <= tmax * 1.00001f;
+}
+
+// Closest hit through the LBVH.  Ties in t resolve to the lowest ORIGINAL face id (R18), so
+// the answer does not depend on the visiting order.  Returns the original face id or -1.
+// sstack: this thread's column of the block's shared short stack (stride = blockDim.x).
+DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, float& bu, float& bv, int* sstack,
+                  int stride, int& err, int& visits, int& tests) {
+  float3 inv = safe_inv(d);
+  int lstack[kStackLocal];
+  int sp = 0;
+  int best = -1;
+  bt = kInf;
+  bu = bv = 0.0f;
+  int cur = s.root;
+  while (true) {
+    if (cur >= 0) {
+      const float4* n = s.nodes + 4 * (size_t)cur;
+      float4 a = __ldg(n), b = __ldg(n + 1), c = __ldg(n + 2), e = __ldg(n + 3);
+      ++visits;
+      float t0, t1;
+      bool h0 = slab(a.x, a.y, a.z, a.w, b.x, b.y, o, inv, bt, t0);
+      bool h1 = slab(b.z, b.w, c.x, c.y, c.z, c.w, o, inv, bt, t1);
+      int c0 = __float_as_int(e.x), c1 = __float_as_int(e.y);
+      if (h0 && h1) {
+        int nr = t0 <= t1 ? c0 : c1, fr = t0 <= t1 ? c1 : c0;
+        if (sp < kStackShared) sstack[sp * stride] = fr;
+        else if (sp < kStackShared + kStackLocal) lstack[sp - kStackShared] = fr;
+        else { err = 1; break; }
+        ++sp;
+        cur = nr;
+        continue;
+      }
+      if (h0) { cur = c0; continue; }
+      if (h1) { cur = c1; continue; }
+    } else {
+      const float4* tr = s.tris + 3 * (size_t)(~cur);
+      float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
+      float t, u, v;
+      ++tests;
+      if (intersect_tri(o, d, f3(a), f3(b), f3(c), t_lo, t, u, v)) {
+        int id = __float_as_int(a.w);
+        if (t < bt || (t == bt && id < best)) { bt = t; bu = u; bv = v; best = id; }
+      }
+    }
+    if (sp == 0) break;
+    --sp;
+    cur = sp < kStackShared ? sstack[sp * stride] : lstack[sp - kStackShared];
+  }
+  return best;
+}
+
+// triangle of ORIGINAL face f from the snapshot, with the same e1/e2 rounding as the leaves
+DT_D void face_tri(const DevScene& s, int f, int& i0, int& i1, int& i2, float3& v0, float3& e1, float3& e2) {
+  i0 = __ldg(s.F + 3 * f); i1 = __ldg(s.F + 3 * f + 1); i2 = __ldg(s.F + 3 * f + 2);
+  v0 = f3(__ldg(s.V + i0));
+  e1 = sub_rn(f3(__ldg(s.V + i1)), v0);
+  e2 = sub_rn(f3(__ldg(s.V + i2)), v0);
+}
+
+// ----------------------------------------------------------------------------- interface
+// One specular event (R1-R5, R7, R8).  Everything the reverse pass needs.
+struct Shade {
+  float3 n, ns, m, wi, wr, wt;
+  float Lm, sg, c_raw, ci, eta, eta_i, eta_t, q, ct, R, T;
+  float b0, b1, b2;
+  bool inside, tir, clamped, degen, fb;
+};
+
+DT_D void shade_forward(const DevScene& s, int i0, int i1, int i2, float3 e1, float3 e2, float3 d, float u, float v,
+                        bool inside, Shade& S) {
+  S.inside = inside;
+  S.b0 = 1.0f - u - v; S.b1 = u; S.b2 = v;
+  float3 n0 = f3(__ldg(s.nrm + i0)), n1 = f3(__ldg(s.nrm + i1)), n2 = f3(__ldg(s.nrm + i2));
+  S.m = n0 * S.b0 + n1 * S.b1 + n2 * S.b2;                 // n(x) = sum beta_i n_vi
+  S.Lm = length(S.m);
+  S.fb = !(S.Lm >= 1e-12f);
+  if (!S.fb) S.ns = S.m * (1.0f / S.Lm);
+  else { float3 c = cross(e1, e2); S.ns = c * (1.0f / length(c)); }
+  S.sg = inside ? -1.0f : 1.0f;
+  S.n = S.ns * S.sg;
+  S.eta_i = inside ? s.ior : 1.0f;
+  S.eta_t = inside ? 1.0f : s.ior;
+  S.wi = -d;
+  S.c_raw = dot(S.wi, S.n);
+  S.clamped = !(S.c_raw > 0.0f);
+  S.ci = S.clamped ? 0.0f : fminf(S.c_raw, 1.0f);
+  S.eta = S.eta_t / S.eta_i;
+  S.q = S.eta * S.eta - 1.0f + S.ci * S.ci;
+  S.wr = S.n * (2.0f * S.ci) - S.wi;
+  S.tir = S.q < 0.0f;
+  S.degen = false;
+  if (S.tir) { S.ct = 0.0f; S.R = 1.0f; S.T = 0.0f; S.wt = f3(0, 0, 0); return; }
+  S.ct = sqrtf(S.q) / S.eta;
+  S.wt = (S.wi - S.n * S.ci) * (-1.0f / S.eta) - S.n * S.ct;  // P:106-108 (R4)
+  if (S.ci == 0.0f && S.ct == 0.0f) { S.degen = true; S.R = 1.0f; S.T = 0.0f; return; }
+  float A = S.eta_i * S.ci, B = S.eta_t * S.ct, C = S.eta_i * S.ct, D = S.eta_t * S.ci;
+  float rs = (A - B) / (A + B), rp = (C - D) / (C + D);
+  S.R = 0.5f * (rs * rs + rp * rp);
+  S.T = 1.0f - S.R;
+}
+
+// Reverse of shade_forward: given dL/dR (T = 1 - R folded in), dL/dwr, dL/dwt, returns
+// dL/dd (through omega_i = -d), dL/d(u, v) (through the shading normal), d/dn_vk and d/dior.
+DT_D void shade_backward(const Shade& S, float gR, float3 gwr, float3 gwt, float3 nv0, float3 nv1, float3 nv2,
+                         float3& gd, float& gu, float& gv, float3 gN[3], float& gior) {
+  float gci = 0.0f, geta = 0.0f, geta_i = 0.0f, geta_t = 0.0f;
+  float3 gn = f3(0, 0, 0), gwi = f3(0, 0, 0);
+  if (!S.tir) {
+    if (!S.degen) {
+      float A = S.eta_i * S.ci, B = S.eta_t * S.ct, C = S.eta_i * S.ct, D = S.eta_t * S.ci;
+      float rs = (A - B) / (A + B), rp = (C - D) / (C + D);
+      float grs = gR * rs, grp = gR * rp;
+      float iab = 1.0f / ((A + B) * (A + B)), icd = 1.0f / ((C + D) * (C + D));
+      float gA = grs * 2.0f * B * iab, gB = -grs * 2.0f * A * iab;
+      float gC = grp * 2.0f * D * icd, gD = -grp * 2.0f * C * icd;
+      float gct = gB * S.eta_t + gC * S.eta_i;
+      gci += gA * S.eta_i + gD * S.eta_t;
+      geta_i += gA * S.ci + gC * S.ct;
+      geta_t += gB * S.ct + gD * S.ci;
+      // hand the gct through the transmitted direction and cos(theta_t) below
+      float ie = 1.0f / S.eta;
+      gwi -= gwt * ie;
+      gci += dot(gwt, S.n) * ie;
+      gn += gwt * (S.ci * ie) - gwt * S.ct;
+      geta += dot(gwt, S.wi - S.n * S.ci) * ie * ie;
+      gct -= dot(gwt, S.n);
+      float sq = sqrtf(S.q);
+      float gq = sq > 0.0f ? gct / (2.0f * S.eta * sq) : 0.0f;
+      geta += -gct * sq * ie * ie + gq * 2.0f * S.eta;
+      gci += gq * 2.0f * S.ci;
+    }
+    // degen (both cosines 0): R = 1, T = 0 constant; the refracted child carries zero
+    // adjoint, so gwt = 0 and nothing flows.
+  }
+  // omega_r = 2 ci n - omega_i
+  gci += 2.0f * dot(gwr, S.n);
+  gn += gwr * (2.0f * S.ci);
+  gwi -= gwr;
+  // eta = eta_t / eta_i
+  geta_t += geta / S.eta_i;
+  geta_i -= geta * S.eta_t / (S.eta_i * S.eta_i);
+  gior = S.inside ? geta_i : geta_t;
+  // ci = clamp(omega_i . n): the lower clamp stops the gradient (R3)
+  if (!S.clamped) { gwi += S.n * gci; gn += S.wi * gci; }
+  gd = -gwi;
+  gu = gv = 0.0f;
+  gN[0] = gN[1] = gN[2] = f3(0, 0, 0);
+  if (!S.fb) {
+    float3 gns = gn * S.sg;
+    float3 gm = (gns - S.ns * dot(S.ns, gns)) * (1.0f / S.Lm);
+    gN[0] = gm * S.b0; gN[1] = gm * S.b1; gN[2] = gm * S.b2;
+    float g0 = dot(gm, nv0), g1 = dot(gm, nv1), g2 = dot(gm, nv2);
+    gu = g1 - g0;
+    gv = g2 - g0;
+  }
+}
+
+// Reverse of the Moller-Trumbore solve M [u v t]^T = o - v0 with M = [e1 e2 -d]:
+// lambda = M^-T (gu, gv, gt); go += lambda, gd += t lambda, gV_k = -beta_k lambda.
+DT_D void mt_backward(float3 d, float3 e1, float3 e2, float t, float u, float v, float gu, float gv, float gt,
+                      float3& go, float3& gd, float3 gV[3]) {
+  float3 de2 = cross(d, e2), e1d = cross(e1, d), e12 = cross(e1, e2);
+  float det = dot(e1, de2);
+  float3 lam = (de2 * gu + e1d * gv + e12 * gt) * (1.0f / det);
+  go += lam;
+  gd += lam * t;
+  gV[0] = lam * -(1.0f - u - v);
+  gV[1] = lam * -u;
+  gV[2] = lam * -v;
+}
+
+// ----------------------------------------------------------------------------- absorption
+DT_D bool sigma_cell(const DevScene& s, float3 p, int i0[3], float f[3], float scale[3]) {
+  const float lo[3] = {s.slo.x, s.slo.y, s.slo.z}, hi[3] = {s.shi.x, s.shi.y, s.shi.z};
+  const float pp[3] = {p.x, p.y, p.z};
+  int R = s.sres;
+  for (int a = 0; a < 3; ++a) {
+    float g = (pp[a] - lo[a]) / (hi[a] - lo[a]) * (float)(R - 1);
+    if (g < 0.0f || g > (float)(R - 1)) return false;     // zero outside the box (R11)
+    i0[a] = min((int)floorf(g), R - 2);
+    f[a] = g - (float)i0[a];
+    scale[a] = (float)(R - 1) / (hi[a] - lo[a]);
+  }
+  return true;
+}
+
+DT_D float3 sigma_at(const DevScene& s, float3 p) {
+  int i0[3];
+  float f[3], sc[3];
+  if (!sigma_cell(s, p, i0, f, sc)) return f3(0, 0, 0);
+  int R = s.sres;
+  float3 out = f3(0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
+    float w = (dx ? f[0] : 1 - f[0]) * (dy ? f[1] : 1 - f[1]) * (dz ? f[2] : 1 - f[2]);
+    const float* t = s.sigma + (((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx)) * 3;
+    out += f3(__ldg(t), __ldg(t + 1), __ldg(t + 2)) * w;
+  }
+  return out;
+}
+
+// tau = exp(-sum_j mu(x_j) dx) over o -> x, midpoint rule with N samples (R10)
+DT_D float3 transmittance(const DevScene& s, float3 o, float3 x) {
+  float3 dx = x - o;
+  float l = length(dx);
+  float3 S;
+  if (s.abs_kind == 0) {
+    S = f3(__ldg(s.sigma), __ldg(s.sigma + 1), __ldg(s.sigma + 2)) * l;
+  } else {
+    int N = s.nsamp;
+    S = f3(0, 0, 0);
+    for (int j = 0; j < N; ++j) S += sigma_at(s, o + dx * (((float)j + 0.5f) / (float)N));
+    S = S * (l / (float)N);
+  }
+  return f3(expf(-S.x), expf(-S.y), expf(-S.z));
+}
+
+// reverse of transmittance given gS = dL/d(optical depth); gsig: device dsigma buffer
+// (const: partial sums returned in gsc[3]; grid: atomics).
+DT_D void transmittance_backward(const DevScene& s, float3 o, float3 x, float3 gS, float3& gx, float3& go, float* gsig,
+                                 float3& gsc) {
+  float3 dx = x - o;
+  float l = length(dx);
+  float gl = 0.0f;
+  if (s.abs_kind == 0) {
+    gsc += gS * l;
+    gl = dot(gS, f3(__ldg(s.sigma), __ldg(s.sigma + 1), __ldg(s.sigma + 2)));
+  } else {
+    int N = s.nsamp, R = s.sres;
+    float sc = l / (float)N;
+    float3 gSs = gS * sc;
+    for (int j = 0; j < N; ++j) {
+      float w = ((float)j + 0.5f) / (float)N;
+      float3 p = o + dx * w;
+      int i0[3];
+      float f[3], scl[3];
+      if (!sigma_cell(s, p, i0, f, scl)) continue;
+      float3 gp = f3(0, 0, 0), val = f3(0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        int ix = k & 1, iy = (k >> 1) & 1, iz = k >> 2;
+        float wx = ix ? f[0] : 1 - f[0], wy = iy ? f[1] : 1 - f[1], wz = iz ? f[2] : 1 - f[2];
+        float ww = wx * wy * wz;
+        size_t node = ((size_t)(i0[2] + iz) * R + (i0[1] + iy)) * R + (i0[0] + ix);
+        const float* t = s.sigma + node * 3;
+        float3 sv = f3(__ldg(t), __ldg(t + 1), __ldg(t + 2));
+        val += sv * ww;
+        atomicAdd(gsig + node * 3 + 0, gSs.x * ww);
+        atomicAdd(gsig + node * 3 + 1, gSs.y * ww);
+        atomicAdd(gsig + node * 3 + 2, gSs.z * ww);
+        float sd = dot(gSs, sv);
+        gp += f3((ix ? 1.f : -1.f) * wy * wz * scl[0], wx * (iy ? 1.f : -1.f) * wz * scl[1],
+                 wx * wy * (iz ? 1.f : -1.f) * scl[2]) * sd;
+      }
+      gl += dot(gS, val) / (float)N;
+      go += gp * (1.0f - w);
+      gx += gp * w;
+    }
+  }
+  if (l > 0.0f) {
+    float3 u = dx * (1.0f / l);
+    gx += u * gl;
+    go -= u * gl;
+  }
+}
+
+// ----------------------------------------------------------------------------- environment
+DT_D float grid_coord(float p, float Re, int res, bool& clamped) {
+  float g = (p + Re) / (2.0f * Re) * (float)(res - 1);
+  clamped = false;
+  if (g < 0.0f) { clamped = true; return 0.0f; }
+  if (g > (float)(res - 1)) { clamped = true; return (float)(res - 1); }
+  return g;
+}
+
+DT_D float3 shell_point(const DevScene& s, float3 o, float3 dh, float& ts, float& sq) {
+  if (s.far_field) { ts = s.radius; sq = 0.0f; return dh * s.radius; }
+  float b = dot(o, dh);
+  sq = sqrtf(fmaxf(b * b - dot(o, o) + s.radius * s.radius, 0.0f));
+  ts = -b + sq;
+  return o + dh * ts;
+}
+
+DT_D float3 env_voxel(const DevScene& s, float3 p, float3 a, float3* gp) {
+  bool c[3];
+  float g[3] = {grid_coord(p.x, s.radius, s.vres, c[0]), grid_coord(p.y, s.radius, s.vres, c[1]),
+                grid_coord(p.z, s.radius, s.vres, c[2])};
+  int R = s.vres, i0[3];
+  float f[3];
+  for (int k = 0; k < 3; ++k) { i0[k] = min((int)floorf(g[k]), R - 2); f[k] = g[k] - (float)i0[k]; }
+  float3 out = f3(0, 0, 0), gg = f3(0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
+    float wx = dx ? f[0] : 1 - f[0], wy = dy ? f[1] : 1 - f[1], wz = dz ? f[2] : 1 - f[2];
+    float4 t = __ldg(s.voxel + ((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx));
+    out += f3(t) * (wx * wy * wz);
+    if (gp) {
+      float sd = a.x * t.x + a.y * t.y + a.z * t.z;
+      gg += f3((dx ? 1.f : -1.f) * wy * wz, wx * (dy ? 1.f : -1.f) * wz, wx * wy * (dz ? 1.f : -1.f)) * sd;
+    }
+  }
+  if (gp) {
+    float sc = (float)(R - 1) / (2.0f * s.radius);
+    *gp += f3(c[0] ? 0.f : gg.x * sc, c[1] ? 0.f : gg.y * sc, c[2] ? 0.f : gg.z * sc);
+  }
+  return out;
+}
+
+DT_D float3 env_plane(const DevScene& s, int k, float a_, float b_, float3 adj, float* ga, float* gb) {
+  bool ca, cb;
+  int R = s.pres;
+  float g_a = grid_coord(a_, s.radius, R, ca), g_b = grid_coord(b_, s.radius, R, cb);
+  int ia = min((int)floorf(g_a), R - 2), ib = min((int)floorf(g_b), R - 2);
+  float fa = g_a - (float)ia, fb = g_b - (float)ib;
+  const float4* P = s.planes + (size_t)k * R * R;
+  float4 t00 = __ldg(P + (size_t)ib * R + ia), t01 = __ldg(P + (size_t)ib * R + ia + 1);
+  float4 t10 = __ldg(P + (size_t)(ib + 1) * R + ia), t11 = __ldg(P + (size_t)(ib + 1) * R + ia + 1);
+  float3 out = f3(t00) * ((1 - fa) * (1 - fb)) + f3(t01) * (fa * (1 - fb)) + f3(t10) * ((1 - fa) * fb) +
+               f3(t11) * (fa * fb);
+  if (ga) {
+    float s00 = dot(adj, f3(t00)), s01 = dot(adj, f3(t01)), s10 = dot(adj, f3(t10)), s11 = dot(adj, f3(t11));
+    float sc = (float)(R - 1) / (2.0f * s.radius);
+    float da = (s01 - s00) * (1 - fb) + (s11 - s10) * fb;
+    float db = (s10 - s00) * (1 - fa) + (s11 - s01) * fa;
+    *ga = ca ? 0.f : da * sc;
+    *gb = cb ? 0.f : db * sc;
+  }
+  return out;
+}
+
+// Env(o, d) (P:160 step 3).  If go/gd are non-null, also the reverse for adjoint a.
+DT_D float3 env_eval(const DevScene& s, float3 o, float3 d, float3 a, float3* go, float3* gd) {
+  float dn = length(d);
+  float3 dh = d * (1.0f / dn);
+  float3 L, gdh = f3(0, 0, 0);
+  if (s.env_kind == 0) {
+    L = s.ambient;
+    for (int j = 0; j < s.nlobes; ++j) {
+      const float* lb = s.lobes + 7 * j;
+      float3 mu = f3(__ldg(lb), __ldg(lb + 1), __ldg(lb + 2));
+      float kap = __ldg(lb + 3);
+      float3 w = f3(__ldg(lb + 4), __ldg(lb + 5), __ldg(lb + 6));
+      float e = expf(kap * (dot(mu, dh) - 1.0f));
+      L += w * e;
+      if (gd) gdh += mu * (dot(a, w) * e * kap);
+    }
+    if (go) *go = f3(0, 0, 0);
+  } else {
+    float ts, sq;
+    float3 p = shell_point(s, o, dh, ts, sq);
+    float3 gp = f3(0, 0, 0);
+    float3* gpp = gd ? &gp : nullptr;
+    L = env_voxel(s, p, a, gpp);
+    float g1 = 0, g2 = 0;
+    L += env_plane(s, 0, p.x, p.y, a, gd ? &g1 : nullptr, &g2);
+    if (gd) { gp.x += g1; gp.y += g2; }
+    L += env_plane(s, 1, p.x, p.z, a, gd ? &g1 : nullptr, &g2);
+    if (gd) { gp.x += g1; gp.z += g2; }
+    L += env_plane(s, 2, p.y, p.z, a, gd ? &g1 : nullptr, &g2);
+    if (gd) { gp.y += g1; gp.z += g2; }
+    if (gd) {
+      if (s.far_field) {
+        gdh = gp * s.radius;
+        *go = f3(0, 0, 0);
+      } else {
+        float b = dot(o, dh);
+        float3 g_o = gp;
+        gdh = gp * ts;
+        float gts = dot(gp, dh);
+        float gdisc = sq > 0.0f ? gts / (2.0f * sq) : 0.0f;
+        float gb = -gts + gdisc * 2.0f * b;
+        g_o -= o * (2.0f * gdisc);
+        g_o += dh * gb;
+        gdh += o * gb;
+        *go = g_o;
+      }
+    }
+  }
+  if (gd) *gd = (gdh - dh * dot(dh, gdh)) * (1.0f / dn);
+  return L;
+}
+
+}  // namespace dt

@@ -1,0 +1,167 @@
+// Host-side context and kernel-launcher declarations of libdifftrans.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/difftrans.h"
+#include "dt_device.cuh"
+
+namespace dt {
+
+// Path-record arena: one entry per traced segment, structure-of-arrays of 16-B lanes so
+// every kernel's loads/stores are coalesced float4 accesses.  Levels (depths) are
+// contiguous: level k occupies [off_k, off_k + cnt_k).
+struct Records {
+  float4* o;     // origin.xyz, ray index (int bits)
+  float4* d;     // direction.xyz, tree position (uint bits: root 1, reflect 2p, refract 2p+1)
+  float4* thr;   // throughput into the node (product of ancestors' R/T and tau), scalar R/T weight
+  float4* hit;   // face (int bits), t, R, flags (int bits, RF_*)
+  float4* tau;   // interior transmittance of this segment (rgb), refract child index (int bits)
+  float4* lsub;  // radiance returned by the subtree (rgb), reflect child index (int bits)
+  float4* go;    // backward: dL/d(origin) of this segment, for the parent
+  float4* gd;    // backward: dL/d(direction)
+};
+constexpr int kRecordBytes = 8 * 16;
+
+// device int block: per-level counts and work counters
+enum {
+  LV_CNT = 0,            // [16] records per level
+  LV_WORK_TRACE = 16,    // [16]
+  LV_WORK_GATHER = 32,   // [16]
+  LV_WORK_BWD = 48,      // [16]
+  LV_OVERFLOW = 64,
+  LV_STACKERR = 65,
+  LV_TRACED = 66,        // primaries traversed (passed the root-box test)
+  LV_NONFINITE = 67,
+  LV_WORK_PRIMARY = 68,
+  LV_INTS = 80
+};
+
+struct FwdLaunch {
+  DevScene s;
+  Records r;
+  int* lvl;
+  int64_t cap;
+  float t_eps;
+  // cameras
+  const float* K;
+  const float* c2w;
+  int W, H, n_views;
+  const int64_t* pids;
+  int64_t n_items;      // work items for level 0
+  int tiles_x, tiles_per_view;
+  // outputs
+  float* rgb;
+  float* capw;
+  unsigned long long* sig_t;
+  unsigned long long* sig_f;
+  unsigned long long* counters;   // [0] node visits, [1] triangle tests
+};
+
+struct BwdLaunch {
+  DevScene s;
+  Records r;
+  int* lvl;
+  int64_t cap;
+  float t_eps;
+  const float* grad_rgb;
+  float4* dV;       // [nv] vertex-position adjoints (atomics)
+  float4* dN;       // [nv] vertex-normal adjoints (atomics)
+  float* dsig;      // [3] or [R^3*3]
+  float* dior;      // [1]
+};
+
+}  // namespace dt
+
+struct dt_ctx {
+  int device = 0;
+  int sm_count = 148;
+  std::string err;
+  // mesh snapshot
+  int nv = 0, nf = 0;
+  bool built = false;
+  size_t cap_nv = 0, cap_nf = 0;
+  float4* V = nullptr;        // [nv]
+  int* F = nullptr;           // [nf*3]
+  float4* nrm = nullptr;      // [nv]
+  float4* fnrm = nullptr;     // [nf] unit face normals
+  // LBVH
+  float4* nodes = nullptr;    // [(nf-1)*4]
+  float4* tris = nullptr;     // [nf*3]
+  unsigned* keys = nullptr;   // [2 * max(nf, 3nf)] radix sort ping-pong
+  unsigned* vals = nullptr;
+  unsigned* hist = nullptr;
+  int2* children = nullptr;   // [nf-1]
+  int* parent_int = nullptr;  // [nf-1]
+  int* parent_leaf = nullptr; // [nf]
+  int* rflags = nullptr;      // [nf-1]
+  float4* nodebox = nullptr;  // [2*(nf-1)]
+  float4* leafbox = nullptr;  // [2*nf]
+  int* vstart = nullptr;      // [nv+1] CSR of (vertex -> incident corners)
+  unsigned* vcorner = nullptr;// [3nf] sorted corner ids (face*3 + k)
+  float* scal = nullptr;      // device scalars: [0..5] root box, [6] bbox diagonal
+  int* iscal = nullptr;       // device ints: ordered-int bounds
+  size_t hist_cap = 0;
+  // record arena
+  int64_t arena_cap = 0;
+  dt::Records rec{};
+  int* lvl = nullptr;
+  int* host_lvl = nullptr;    // pinned
+  // last forward
+  bool have_fwd = false;
+  int64_t n_rays = 0;
+  dt::DevScene fwd_scene{};
+  float fwd_t_eps = 1e-4f;
+  float* sigma_snap = nullptr;
+  size_t sigma_cap = 0, sigma_len = 0;
+  // gradients
+  float4* gV = nullptr;       // [nv]
+  float4* gN = nullptr;       // [nv]
+  float4* gVn = nullptr;      // [nv]  vertex-normal chain, gathered per vertex
+  float4* gS = nullptr;       // [nv]  d/d(sum of face normals)
+  float4* fe = nullptr;       // [2nf] per-face d/de1, d/de2
+  float* gsig = nullptr;
+  float* gior = nullptr;
+  size_t gsig_cap = 0;
+  // profiling (dt_set_profiling / dt_get_profile)
+  bool prof = false;
+  double ph_ms[DT_PH_COUNT] = {};
+  long long ph_launches[DT_PH_COUNT] = {};
+  long long kernel_launches = 0;
+  unsigned long long* counters = nullptr;       // device [2]: node visits, triangle tests
+  struct Pending { int ph; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+};
+
+// Brackets one phase's launches with CUDA events on `st` when profiling is on.
+struct PhaseTimer {
+  dt_ctx* c;
+  int ph;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  PhaseTimer(dt_ctx* c_, int ph_, cudaStream_t st_);
+  void end(int n_launches);
+};
+
+// kernel launchers (bvh.cu, trace.cu)
+namespace dt {
+// each launcher returns the CUDA error and adds the number of kernels it launched to *nl
+cudaError_t build_bvh(dt_ctx* c, const float* V, int nv, const int* F, int nf, cudaStream_t st, int* nl);
+cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count, cudaStream_t st);
+cudaError_t launch_shade_level0(const FwdLaunch& a, int max_depth, int sm_count, cudaStream_t st);
+cudaError_t launch_forward_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st);
+cudaError_t launch_gather_level(const FwdLaunch& a, int level, int sm_count, cudaStream_t st);
+cudaError_t launch_backward_level(const BwdLaunch& a, int level, int sm_count, cudaStream_t st);
+cudaError_t launch_vertex_normal_backward(dt_ctx* c, cudaStream_t st);
+cudaError_t launch_finalize(dt_ctx* c, float* grad_V, float* grad_ior, float* grad_sigma, int accumulate,
+                            cudaStream_t st);
+cudaError_t launch_loss_color(const float* rgb, const float* tgt, int64_t n, float* grad, float* loss, cudaStream_t st);
+cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64_t n, float t_lo, int brute, int* face,
+                                     float* tuv, int* err_flag, cudaStream_t st);
+cudaError_t launch_bvh_check(dt_ctx* c, long long* out_dev, cudaStream_t st);
+cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
+DevScene scene_from_ctx(const dt_ctx* c);
+}  // namespace dt

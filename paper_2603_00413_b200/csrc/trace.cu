@@ -1,0 +1,595 @@
+// Wavefront forward trace, radiance gather and backward replay (K8-K14).
+//
+// Forward, level k = 0..D_max (one launch per depth, persistent warps, dynamic fetch):
+//   traverse the level's rays through the LBVH (shared-memory short stack), then for each
+//   hit evaluate the interface (Fresnel/Snell/TIR), the interior transmittance and append
+//   the reflect/refract children to level k+1 with one warp-ballot compaction per warp.
+//   Misses end in the environment lookup; hits at depth D_max are capped (R12, R13).
+// Gather, level k = D_max-1..0: L_sub = tau * (R L_r + T L_t) bottom-up; level 0 writes
+//   the pixel radiance (deterministic, no atomics).
+// Backward, level k = D_max..0: local VJP per record at fixed topology; children pass
+//   dL/d(origin, direction) up through their own record slots; vertex-position and
+//   vertex-normal adjoints scatter with float4 atomics, IOR / constant-sigma adjoints are
+//   reduced per warp.
+//
+// Arena layout: level 0 (camera-ray hits) grows DOWN from the top of the arena
+// (record cap-1-i), levels 1..D_max are contiguous from the bottom (level k starts at
+// sum_{1<=j<k} cnt_j).  So every level's start is known once the previous level is done.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "dt_internal.h"
+
+namespace dt {
+namespace {
+
+constexpr int kTraceThreads = 128;
+constexpr int kBwdThreads = 128;
+
+DT_D int fetch_work(int* counter) {
+  int base = 0;
+  if (lane_id() == 0) base = atomicAdd(counter, 32);
+  return __shfl_sync(~0u, base, 0);
+}
+
+// first record index of level k >= 1
+DT_D int64_t level_base(const int* lvl, int k) {
+  int64_t off = 0;
+  for (int j = 1; j < k; ++j) off += lvl[LV_CNT + j];
+  return off;
+}
+DT_D int64_t rec_index(const int* lvl, int64_t cap, int k, int64_t item) {
+  return k == 0 ? cap - 1 - item : level_base(lvl, k) + item;
+}
+
+DT_D void sig_add(unsigned long long* sig, int64_t r, uint64_t key) {
+  if (sig) atomicAdd(sig + r, (unsigned long long)dt_mix64(key));
+}
+
+// per-warp sum of the traversal counters, one 64-bit atomic per warp
+DT_D void flush_counters(unsigned long long* c, int visits, int tests) {
+  unsigned long long v = (unsigned long long)visits, t = (unsigned long long)tests;
+  for (int o = 16; o > 0; o >>= 1) {
+    v += __shfl_xor_sync(~0u, v, o);
+    t += __shfl_xor_sync(~0u, t, o);
+  }
+  if (lane_id() == 0 && c) {
+    atomicAdd(c, v);
+    atomicAdd(c + 1, t);
+  }
+}
+
+// Shade one traced segment (record idx at level k) and spawn its children into level k+1.
+// All 32 lanes of the warp must call this (the compaction is a warp collective).
+DT_D void shade_and_spawn(const FwdLaunch& a, int k, int max_depth, bool valid, int64_t idx, float3 o, float3 d,
+                          int64_t ray, uint32_t pos, float3 thr, float w, int face, float t, float u, float v) {
+  const DevScene& s = a.s;
+  bool is_hit = valid && face >= 0;
+  bool spawn_r = false, spawn_t = false;
+  float3 x = f3(0, 0, 0), wr = x, wt = x, tau = f3(1, 1, 1);
+  float R = 0.f, T = 0.f;
+  if (valid) {
+    if (!is_hit) {
+      float3 L = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);          // P:160 step 3
+      a.r.hit[idx] = make_float4(__int_as_float(-1), 0.f, 0.f, __int_as_float(RF_MISS));
+      a.r.lsub[idx] = f4(L, __int_as_float(-1));
+      a.r.tau[idx] = make_float4(1.f, 1.f, 1.f, __int_as_float(-1));
+      sig_add(a.sig_t, ray, topo_key(pos, EV_MISS));
+      sig_add(a.sig_f, ray, face_key(pos, EV_MISS, -1));
+    } else {
+      int i0, i1, i2;
+      float3 v0, e1, e2;
+      face_tri(s, face, i0, i1, i2, v0, e1, e2);
+      bool inside = dot(d, cross(e1, e2)) > 0.0f;                             // R8
+      x = o + d * t;
+      if (k == max_depth) {                                                   // capped (R12, R13)
+        float3 L = f3(0, 0, 0);
+        if (inside) tau = transmittance(s, o, x);
+        if (s.cap_policy == 1) L = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr) * tau;
+        int fl = RF_CAPPED | (inside ? RF_INSIDE : 0);
+        a.r.hit[idx] = make_float4(__int_as_float(face), t, 0.f, __int_as_float(fl));
+        a.r.lsub[idx] = f4(L, __int_as_float(-1));
+        a.r.tau[idx] = f4(tau, __int_as_float(-1));
+        int ev = inside ? EV_CAP_IN : EV_CAP_OUT;
+        sig_add(a.sig_t, ray, topo_key(pos, ev));
+        sig_add(a.sig_f, ray, face_key(pos, ev, face));
+        if (a.capw) atomicAdd(a.capw + ray, w);
+      } else {
+        Shade S;
+        shade_forward(s, i0, i1, i2, e1, e2, d, u, v, inside, S);
+        if (inside) tau = transmittance(s, o, x);                             // P:162 (R9)
+        R = S.R;
+        T = S.T;
+        wr = S.wr;
+        wt = S.wt;
+        spawn_r = true;                                                       // P:161 (R5)
+        spawn_t = !S.tir;
+        int fl = (inside ? RF_INSIDE : 0) | (S.tir ? RF_TIR : 0) | (S.degen ? RF_DEGEN : 0);
+        a.r.hit[idx] = make_float4(__int_as_float(face), t, R, __int_as_float(fl));
+        int ev = inside ? (S.tir ? EV_HIT_IN_TIR : EV_HIT_IN) : (S.tir ? EV_HIT_OUT_TIR : EV_HIT_OUT);
+        sig_add(a.sig_t, ray, topo_key(pos, ev));
+        sig_add(a.sig_f, ray, face_key(pos, ev, face));
+      }
+    }
+  }
+  // warp-ballot compaction of the children: the warp's reflect children first, then its
+  // refract children, each group contiguous in level k+1
+  unsigned mr = __ballot_sync(~0u, spawn_r), mt = __ballot_sync(~0u, spawn_t);
+  int nr = __popc(mr), nt = __popc(mt);
+  int base = 0;
+  if (nr + nt > 0) {
+    if (lane_id() == 0) base = atomicAdd(a.lvl + LV_CNT + k + 1, nr + nt);
+    base = __shfl_sync(~0u, base, 0);
+  }
+  if (spawn_r) {
+    int64_t off = level_base(a.lvl, k + 1);
+    int64_t lim = a.cap - a.lvl[LV_CNT + 0];
+    int64_t cr = -1, ct = -1;
+    int64_t j = off + base + __popc(mr & lanemask_lt());
+    if (j < lim) {
+      cr = j;
+      a.r.o[j] = f4(x, __int_as_float((int)ray));
+      a.r.d[j] = f4(wr, __uint_as_float(pos * 2u));
+      a.r.thr[j] = f4(thr * tau * R, w * R);
+    } else {
+      a.lvl[LV_OVERFLOW] = 1;
+    }
+    if (spawn_t) {
+      j = off + base + nr + __popc(mt & lanemask_lt());
+      if (j < lim) {
+        ct = j;
+        a.r.o[j] = f4(x, __int_as_float((int)ray));
+        a.r.d[j] = f4(wt, __uint_as_float(pos * 2u + 1u));
+        a.r.thr[j] = f4(thr * tau * T, w * T);
+      } else {
+        a.lvl[LV_OVERFLOW] = 1;
+      }
+    }
+    a.r.tau[idx] = f4(tau, __int_as_float((int)ct));
+    a.r.lsub[idx] = make_float4(0.f, 0.f, 0.f, __int_as_float((int)cr));
+  }
+}
+
+// Level 0: camera rays.  Each warp takes 32 pixels of an 8x4 tile (or 32 consecutive
+// entries of the caller's pixel list), culls against the root box, traverses, and records
+// only the hitting rays (misses write their env radiance straight to rgb).
+__global__ void __launch_bounds__(kTraceThreads) k_trace_primary(FwdLaunch a, int max_depth) {
+  __shared__ int sstack[kStackShared * kTraceThreads];
+  const DevScene& s = a.s;
+  float3 blo = f3(s.scal[0], s.scal[1], s.scal[2]), bhi = f3(s.scal[3], s.scal[4], s.scal[5]);
+  int err = 0, visits = 0, tests = 0, traced = 0;
+  while (true) {
+    int base = fetch_work(a.lvl + LV_WORK_PRIMARY);
+    if (base >= a.n_items) break;
+    int64_t item = (int64_t)base + lane_id();
+    bool valid = item < a.n_items;
+    int64_t pid = 0;
+    if (valid) {
+      if (a.pids) {
+        pid = a.pids[item];
+      } else {
+        int64_t tile = item >> 5;
+        int l = (int)(item & 31);
+        int view = (int)(tile / a.tiles_per_view);
+        int tv = (int)(tile - (int64_t)view * a.tiles_per_view);
+        int ty = tv / a.tiles_x, tx = tv - ty * a.tiles_x;
+        int px = tx * 8 + (l & 7), py = ty * 4 + (l >> 3);
+        valid = px < a.W && py < a.H;
+        pid = ((int64_t)view * a.H + py) * a.W + px;
+      }
+    }
+    int64_t ray = a.pids ? item : pid;
+    float3 o = f3(0, 0, 0), d = f3(0, 0, 1);
+    int face = -1;
+    float t = 0.f, u = 0.f, v = 0.f;
+    if (valid) {
+      camera_ray(a.K, a.c2w, a.W, a.H, pid, o, d);
+      float tn;
+      bool inbox = slab(blo.x, bhi.x, blo.y, bhi.y, blo.z, bhi.z, o, safe_inv(d), kInf, tn);
+      if (inbox) {
+        ++traced;
+        face = traverse(s, o, d, 0.0f, t, u, v, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
+      }
+      if (face < 0) {
+        float3 L = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);
+        a.rgb[3 * ray] = L.x; a.rgb[3 * ray + 1] = L.y; a.rgb[3 * ray + 2] = L.z;
+        sig_add(a.sig_t, ray, topo_key(1u, EV_MISS));
+        sig_add(a.sig_f, ray, face_key(1u, EV_MISS, -1));
+      }
+    }
+    bool rec = valid && face >= 0;
+    unsigned m = __ballot_sync(~0u, rec);
+    int rb = 0;
+    if (m) {
+      if (lane_id() == 0) rb = atomicAdd(a.lvl + LV_CNT + 0, __popc(m));
+      rb = __shfl_sync(~0u, rb, 0);
+    }
+    int64_t idx = a.cap - 1 - (rb + __popc(m & lanemask_lt()));
+    if (rec && idx < 0) { a.lvl[LV_OVERFLOW] = 1; rec = false; }
+    if (rec) {
+      a.r.o[idx] = f4(o, __int_as_float((int)ray));
+      a.r.d[idx] = f4(d, __uint_as_float(1u));
+      a.r.thr[idx] = make_float4(1.f, 1.f, 1.f, 1.f);
+      a.r.hit[idx] = make_float4(__int_as_float(face), t, u, v);   // shaded by k_shade_level0
+    }
+  }
+  if (err) a.lvl[LV_STACKERR] = 1;
+  for (int o = 16; o > 0; o >>= 1) traced += __shfl_xor_sync(~0u, traced, o);
+  if (lane_id() == 0 && traced) atomicAdd(a.lvl + LV_TRACED, traced);
+  flush_counters(a.counters, visits, tests);
+}
+
+// Level 0 shading (needs the final level-0 count, so it is a second pass over the hits).
+__global__ void __launch_bounds__(kTraceThreads) k_shade_level0(FwdLaunch a, int max_depth) {
+  if (a.lvl[LV_OVERFLOW]) return;   // arena too small: the host grows it and re-runs
+  int n = a.lvl[LV_CNT + 0];
+  while (true) {
+    int base = fetch_work(a.lvl + LV_WORK_TRACE + 0);
+    if (base >= n) break;
+    int64_t item = (int64_t)base + lane_id();
+    bool valid = item < n;
+    int64_t idx = a.cap - 1 - item;
+    float3 o = f3(0, 0, 0), d = f3(0, 0, 1);
+    int64_t ray = 0;
+    int face = -1;
+    float t = 0, u = 0, v = 0;
+    if (valid) {
+      float4 ro = a.r.o[idx], rd = a.r.d[idx], h = a.r.hit[idx];
+      o = f3(ro); d = f3(rd);
+      ray = __float_as_int(ro.w);
+      face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
+    }
+    shade_and_spawn(a, 0, max_depth, valid, idx, o, d, ray, 1u, f3(1, 1, 1), 1.f, face, t, u, v);
+  }
+}
+
+// Levels 1..D_max: traverse + shade + spawn.
+__global__ void __launch_bounds__(kTraceThreads) k_trace_level(FwdLaunch a, int k, int max_depth) {
+  __shared__ int sstack[kStackShared * kTraceThreads];
+  const DevScene& s = a.s;
+  if (a.lvl[LV_OVERFLOW]) return;
+  float t_lo = a.t_eps * s.scal[6];                                            // R17
+  int n = a.lvl[LV_CNT + k];
+  int64_t off = level_base(a.lvl, k);
+  int err = 0, visits = 0, tests = 0;
+  while (true) {
+    int base = fetch_work(a.lvl + LV_WORK_TRACE + k);
+    if (base >= n) break;
+    int64_t item = (int64_t)base + lane_id();
+    bool valid = item < n;
+    int64_t idx = off + item;
+    float3 o = f3(0, 0, 0), d = f3(0, 0, 1), thr = f3(0, 0, 0);
+    float w = 0.f;
+    int64_t ray = 0;
+    uint32_t pos = 0;
+    int face = -1;
+    float t = 0, u = 0, v = 0;
+    if (valid) {
+      float4 ro = a.r.o[idx], rd = a.r.d[idx], rt = a.r.thr[idx];
+      o = f3(ro); d = f3(rd); thr = f3(rt); w = rt.w;
+      ray = __float_as_int(ro.w);
+      pos = __float_as_uint(rd.w);
+      face = traverse(s, o, d, t_lo, t, u, v, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
+    }
+    shade_and_spawn(a, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
+  }
+  if (err) a.lvl[LV_STACKERR] = 1;
+  flush_counters(a.counters, visits, tests);
+}
+
+// Bottom-up radiance: L = tau * (R L_r + T L_t); level 0 writes the pixel.
+__global__ void k_gather(FwdLaunch a, int k) {
+  if (a.lvl[LV_OVERFLOW]) return;
+  int n = a.lvl[LV_CNT + k];
+  for (int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; item < n; item += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx = rec_index(a.lvl, a.cap, k, item);
+    float4 h = a.r.hit[idx];
+    int fl = __float_as_int(h.w);
+    float4 ls = a.r.lsub[idx];
+    float3 L;
+    if (fl & (RF_MISS | RF_CAPPED)) {
+      L = f3(ls);
+    } else {
+      float4 tu = a.r.tau[idx];
+      int cr = __float_as_int(ls.w), ct = __float_as_int(tu.w);
+      float R = h.z;
+      float3 Lr = cr >= 0 ? f3(a.r.lsub[cr]) : f3(0, 0, 0);
+      float3 Lt = ct >= 0 ? f3(a.r.lsub[ct]) : f3(0, 0, 0);
+      L = f3(tu) * (Lr * R + Lt * (1.0f - R));
+      a.r.lsub[idx] = f4(L, ls.w);
+    }
+    if (k == 0) {
+      int64_t ray = __float_as_int(a.r.o[idx].w);
+      a.rgb[3 * ray] = L.x; a.rgb[3 * ray + 1] = L.y; a.rgb[3 * ray + 2] = L.z;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- backward
+DT_D void atomic_add3(float4* p, float3 v) {
+  atomicAdd(p, make_float4(v.x, v.y, v.z, 0.0f));
+}
+
+__global__ void __launch_bounds__(kBwdThreads) k_backward_level(BwdLaunch a, int k, int max_depth, int64_t cap) {
+  const DevScene& s = a.s;
+  int n = a.lvl[LV_CNT + k];
+  float gior = 0.0f;
+  float3 gsc = f3(0, 0, 0);
+  for (int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; item < n; item += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx = rec_index(a.lvl, cap, k, item);
+    float4 ro = a.r.o[idx], rd = a.r.d[idx], rt = a.r.thr[idx], h = a.r.hit[idx];
+    float3 o = f3(ro), d = f3(rd);
+    int64_t ray = __float_as_int(ro.w);
+    int fl = __float_as_int(h.w);
+    const float* g = a.grad_rgb + 3 * ray;
+    float3 adj = f3(__ldg(g), __ldg(g + 1), __ldg(g + 2)) * f3(rt);            // a_n = grad * throughput
+    float3 go = f3(0, 0, 0), gd = f3(0, 0, 0);
+    if (fl & RF_MISS) {
+      env_eval(s, o, d, adj, &go, &gd);
+    } else if ((fl & RF_CAPPED) && s.cap_policy == 0) {
+      // capped branches return 0: no dependence
+    } else {
+      int face = __float_as_int(h.x);
+      int i0, i1, i2;
+      float3 v0, e1, e2;
+      face_tri(s, face, i0, i1, i2, v0, e1, e2);
+      float t, u, v;
+      intersect_tri(o, d, v0, e1, e2, -kInf, t, u, v);                      // replay (bit-identical)
+      float3 x = o + d * t;
+      bool inside = (fl & RF_INSIDE) != 0;
+      float3 tau = f3(a.r.tau[idx]);
+      float3 gx = f3(0, 0, 0);
+      float gu = 0.f, gv = 0.f;
+      float3 gVk[3], gNk[3];
+      if (fl & RF_CAPPED) {                                                   // CAP_ENV leaf
+        float3 E = env_eval(s, o, d, adj * tau, &go, &gd);
+        if (inside) {
+          float3 gS = -(adj * E * tau);
+          transmittance_backward(s, o, x, gS, gx, go, a.dsig, gsc);
+        }
+        gNk[0] = gNk[1] = gNk[2] = f3(0, 0, 0);
+      } else {
+        Shade S;
+        shade_forward(s, i0, i1, i2, e1, e2, d, u, v, inside, S);
+        float4 ls = a.r.lsub[idx], tu = a.r.tau[idx];
+        int cr = __float_as_int(ls.w), ct = __float_as_int(tu.w);
+        float3 Lr = f3(0, 0, 0), Lt = f3(0, 0, 0), gwr = f3(0, 0, 0), gwt = f3(0, 0, 0);
+        if (cr >= 0) { Lr = f3(a.r.lsub[cr]); gx += f3(a.r.go[cr]); gwr = f3(a.r.gd[cr]); }
+        if (ct >= 0) { Lt = f3(a.r.lsub[ct]); gx += f3(a.r.go[ct]); gwt = f3(a.r.gd[ct]); }
+        float3 ap = adj * tau;
+        float3 Lc = Lr * S.R + Lt * S.T;
+        float gR = S.tir ? 0.0f : dot(ap, Lr - Lt);
+        if (inside) {
+          float3 gS = -(adj * Lc * tau);
+          transmittance_backward(s, o, x, gS, gx, go, a.dsig, gsc);
+        }
+        float3 gd_s;
+        float gi;
+        float3 n0 = f3(__ldg(s.nrm + i0)), n1 = f3(__ldg(s.nrm + i1)), n2 = f3(__ldg(s.nrm + i2));
+        shade_backward(S, gR, gwr, gwt, n0, n1, n2, gd_s, gu, gv, gNk, gi);
+        gd += gd_s;
+        gior += gi;
+      }
+      // x = o + t d, then the Moller-Trumbore solve
+      go += gx;
+      gd += gx * t;
+      float gt = dot(gx, d);
+      mt_backward(d, e1, e2, t, u, v, gu, gv, gt, go, gd, gVk);
+      atomic_add3(a.dV + i0, gVk[0]);
+      atomic_add3(a.dV + i1, gVk[1]);
+      atomic_add3(a.dV + i2, gVk[2]);
+      if (!(fl & RF_CAPPED)) {
+        atomic_add3(a.dN + i0, gNk[0]);
+        atomic_add3(a.dN + i1, gNk[1]);
+        atomic_add3(a.dN + i2, gNk[2]);
+      }
+    }
+    if (k > 0) {                                                              // camera rays: dropped (R22)
+      a.r.go[idx] = f4(go, 0.f);
+      a.r.gd[idx] = f4(gd, 0.f);
+    }
+  }
+  // warp reductions of the scalar adjoints
+  for (int o = 16; o > 0; o >>= 1) {
+    gior += __shfl_xor_sync(~0u, gior, o);
+    gsc.x += __shfl_xor_sync(~0u, gsc.x, o);
+    gsc.y += __shfl_xor_sync(~0u, gsc.y, o);
+    gsc.z += __shfl_xor_sync(~0u, gsc.z, o);
+  }
+  if (lane_id() == 0) {
+    if (gior != 0.0f) atomicAdd(a.dior, gior);
+    if (s.abs_kind == 0 && (gsc.x != 0.0f || gsc.y != 0.0f || gsc.z != 0.0f)) {
+      atomicAdd(a.dsig, gsc.x);
+      atomicAdd(a.dsig + 1, gsc.y);
+      atomicAdd(a.dsig + 2, gsc.z);
+    }
+  }
+}
+
+// Vertex-normal chain (reverse of P:170-173): dN -> d(sum of unit face normals) per vertex,
+// -> per face d/de1, d/de2 -> gathered back per vertex through the corner CSR.
+__global__ void k_vn_bwd_vertex(const float4* __restrict__ dN, const float4* __restrict__ nrm, int nv, float4* __restrict__ gS) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    float4 n = nrm[v];
+    float3 g = f3(dN[v]), nn = f3(n);
+    gS[v] = n.w > 0.0f ? f4((g - nn * dot(nn, g)) * (1.0f / n.w), 0.f) : make_float4(0, 0, 0, 0);
+  }
+}
+
+__global__ void k_vn_bwd_face(const float4* __restrict__ V, const int* __restrict__ F, const float4* __restrict__ fn,
+                              const float4* __restrict__ gS, int nf, float4* __restrict__ fe) {
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x) {
+    float4 h4 = fn[f];
+    if (!(h4.w > 0.0f)) { fe[2 * f] = make_float4(0, 0, 0, 0); fe[2 * f + 1] = make_float4(0, 0, 0, 0); continue; }
+    int i0 = F[3 * f], i1 = F[3 * f + 1], i2 = F[3 * f + 2];
+    float3 gh = f3(gS[i0]) + f3(gS[i1]) + f3(gS[i2]);
+    float3 h = f3(h4);
+    float3 gc = (gh - h * dot(h, gh)) * (1.0f / h4.w);
+    float3 a = f3(V[i0]);
+    float3 e1 = f3(V[i1]) - a, e2 = f3(V[i2]) - a;
+    fe[2 * f] = f4(cross(e2, gc), 0.f);      // d/de1 of c = e1 x e2
+    fe[2 * f + 1] = f4(cross(gc, e1), 0.f);  // d/de2
+  }
+}
+
+__global__ void k_vn_bwd_gather(const int* __restrict__ vstart, const unsigned* __restrict__ corner,
+                                const float4* __restrict__ fe, int nv, float4* __restrict__ gVn) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    float3 acc = f3(0, 0, 0);
+    for (int j = vstart[v]; j < vstart[v + 1]; ++j) {
+      unsigned c = corner[j];
+      unsigned f = c / 3, kk = c - 3 * f;
+      float3 g1 = f3(fe[2 * f]), g2 = f3(fe[2 * f + 1]);
+      acc += kk == 0 ? -(g1 + g2) : (kk == 1 ? g1 : g2);
+    }
+    gVn[v] = f4(acc, 0.f);
+  }
+}
+
+__global__ void k_finalize(const float4* __restrict__ gV, const float4* __restrict__ gVn, int nv, float* __restrict__ out,
+                           int acc) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    float3 g = f3(gV[v]) + f3(gVn[v]);
+    if (acc) { out[3 * v] += g.x; out[3 * v + 1] += g.y; out[3 * v + 2] += g.z; }
+    else { out[3 * v] = g.x; out[3 * v + 1] = g.y; out[3 * v + 2] = g.z; }
+  }
+}
+
+__global__ void k_copy_add(const float* __restrict__ src, float* __restrict__ dst, int64_t n, int acc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = acc ? dst[i] + src[i] : src[i];
+}
+
+// L_color and its gradient, fused
+__global__ void k_loss_color(const float* __restrict__ rgb, const float* __restrict__ tgt, int64_t n, float inv_b,
+                             float* __restrict__ grad, float* __restrict__ loss) {
+  float acc = 0.0f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * n; i += (int64_t)gridDim.x * blockDim.x) {
+    float c = tgt[i], e = rgb[i] - c;
+    float we = e * c;
+    acc += we * we;
+    grad[i] = 2.0f * we * c * inv_b;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(~0u, acc, o);
+  if (lane_id() == 0) atomicAdd(loss, acc * inv_b);
+}
+
+__global__ void k_check_finite(const float* __restrict__ x, int64_t n, int* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) *flag = 1;
+}
+
+__global__ void __launch_bounds__(kTraceThreads) k_debug_hit(DevScene s, const float* __restrict__ rays, int64_t n,
+                                                             float t_lo, int brute, int* __restrict__ face,
+                                                             float* __restrict__ tuv, int* err_flag) {
+  __shared__ int sstack[kStackShared * kTraceThreads];
+  int err = 0, visits = 0, tests = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float3 o = f3(rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]), d = f3(rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]);
+    float bt = kInf, bu = 0.f, bv = 0.f;
+    int best = -1;
+    if (brute) {
+      for (int j = 0; j < s.nf; ++j) {
+        const float4* tr = s.tris + 3 * (size_t)j;
+        float4 a = tr[0], b = tr[1], c = tr[2];
+        float t, u, v;
+        if (intersect_tri(o, d, f3(a), f3(b), f3(c), t_lo, t, u, v)) {
+          int id = __float_as_int(a.w);
+          if (t < bt || (t == bt && id < best)) { bt = t; bu = u; bv = v; best = id; }
+        }
+      }
+    } else {
+      best = traverse(s, o, d, t_lo, bt, bu, bv, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
+    }
+    face[i] = best;
+    tuv[3 * i] = best >= 0 ? bt : 0.f;
+    tuv[3 * i + 1] = bu;
+    tuv[3 * i + 2] = bv;
+  }
+  if (err) *err_flag = 1;
+}
+
+int persistent_blocks(const void* fn, int threads, int sm_count) {
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  return std::max(1, per_sm) * sm_count;
+}
+
+}  // namespace
+
+cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count, cudaStream_t st) {
+  static int gp = 0;
+  if (!gp) gp = persistent_blocks((const void*)k_trace_primary, kTraceThreads, sm_count);
+  k_trace_primary<<<gp, kTraceThreads, 0, st>>>(a, max_depth);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shade_level0(const FwdLaunch& a, int max_depth, int sm_count, cudaStream_t st) {
+  static int gs = 0;
+  if (!gs) gs = persistent_blocks((const void*)k_shade_level0, kTraceThreads, sm_count);
+  k_shade_level0<<<gs, kTraceThreads, 0, st>>>(a, max_depth);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_forward_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
+  static int gl = 0;
+  if (!gl) gl = persistent_blocks((const void*)k_trace_level, kTraceThreads, sm_count);
+  k_trace_level<<<gl, kTraceThreads, 0, st>>>(a, level, max_depth);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_level(const FwdLaunch& a, int level, int sm_count, cudaStream_t st) {
+  k_gather<<<sm_count * 8, 256, 0, st>>>(a, level);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_backward_level(const BwdLaunch& a, int level, int sm_count, cudaStream_t st) {
+  static int gb = 0;
+  if (!gb) gb = persistent_blocks((const void*)k_backward_level, kBwdThreads, sm_count);
+  k_backward_level<<<gb, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vertex_normal_backward(dt_ctx* c, cudaStream_t st) {
+  int gv = std::min((c->nv + 255) / 256, c->sm_count * 8), gf = std::min((c->nf + 255) / 256, c->sm_count * 8);
+  k_vn_bwd_vertex<<<gv, 256, 0, st>>>(c->gN, c->nrm, c->nv, c->gS);
+  k_vn_bwd_face<<<gf, 256, 0, st>>>(c->V, c->F, c->fnrm, c->gS, c->nf, c->fe);
+  k_vn_bwd_gather<<<gv, 256, 0, st>>>(c->vstart, c->vcorner, c->fe, c->nv, c->gVn);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(dt_ctx* c, float* grad_V, float* grad_ior, float* grad_sigma, int accumulate,
+                            cudaStream_t st) {
+  int gv = std::min((c->nv + 255) / 256, c->sm_count * 8);
+  if (grad_V) k_finalize<<<gv, 256, 0, st>>>(c->gV, c->gVn, c->nv, grad_V, accumulate);
+  if (grad_ior) k_copy_add<<<1, 32, 0, st>>>(c->gior, grad_ior, 1, accumulate);
+  if (grad_sigma) {
+    int64_t n = (int64_t)c->sigma_len;
+    k_copy_add<<<(int)std::min<int64_t>((n + 255) / 256, c->sm_count * 8), 256, 0, st>>>(c->gsig, grad_sigma, n,
+                                                                                         accumulate);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loss_color(const float* rgb, const float* tgt, int64_t n, float* grad, float* loss, cudaStream_t st) {
+  cudaMemsetAsync(loss, 0, sizeof(float), st);
+  int g = (int)std::min<int64_t>((3 * n + 255) / 256, 148 * 16);
+  k_loss_color<<<std::max(g, 1), 256, 0, st>>>(rgb, tgt, n, 1.0f / (float)std::max<int64_t>(n, 1), grad, loss);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64_t n, float t_lo, int brute, int* face,
+                                     float* tuv, int* err_flag, cudaStream_t st) {
+  int g = (int)std::min<int64_t>((n + kTraceThreads - 1) / kTraceThreads, 148 * 32);
+  k_debug_hit<<<std::max(g, 1), kTraceThreads, 0, st>>>(s, rays, n, t_lo, brute, face, tuv, err_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st) {
+  int g = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_check_finite<<<std::max(g, 1), 256, 0, st>>>(x, n, flag);
+  return cudaGetLastError();
+}
+
+}  // namespace dt

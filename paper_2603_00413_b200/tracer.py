@@ -1,0 +1,241 @@
+"""Python front-end of libdifftrans: the same calls as include/difftrans.h, taking torch
+CUDA tensors.  Every step of the path runs in the library's kernels; this module only
+marshals pointers, shapes and the current CUDA stream.  PyTorch supplies device memory,
+streams and (in dist.py) process groups.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import scenes as S
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev(a, dtype, device):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device).contiguous()
+
+
+class DeviceScene:
+    """Device copies of a scenes.Scene's inputs plus the ABI parameter blocks.
+
+    The mesh (V, F), IOR and sigma are the differentiable parameters; they can be
+    replaced between steps (set_vertices / ior / set_sigma).  Env and cameras are frozen."""
+
+    def __init__(self, sc: S.Scene, device: torch.device):
+        self.device = device
+        self.name = sc.name
+        self.V = _dev(sc.V, torch.float32, device)
+        self.F = _dev(sc.F, torch.int32, device)
+        self.ior = float(sc.ior)
+        ab = sc.absorption
+        self.sigma = _dev(ab.sigma, torch.float32, device)
+        self.absorption = N.Absorption()
+        self.absorption.kind = ab.kind
+        self.absorption.res = ab.res
+        if ab.box_lo is not None:
+            self.absorption.box_lo = (C.c_float * 3)(*map(float, ab.box_lo))
+            self.absorption.box_hi = (C.c_float * 3)(*map(float, ab.box_hi))
+        self.absorption.n_samples = ab.n_samples
+        env = sc.env
+        self.env = N.Env()
+        self.env.kind = env.kind
+        self.env.ambient = (C.c_float * 3)(*map(float, env.ambient if env.ambient is not None else (0, 0, 0)))
+        self.lobes = _dev(env.lobes if env.lobes is not None else np.zeros((0, 7)), torch.float32, device)
+        self.voxel = None if env.voxel is None else _dev(env.voxel, torch.float32, device)
+        self.planes = None if env.planes is None else _dev(env.planes, torch.float32, device)
+        self.env.lobes = _ptr(self.lobes) if self.lobes.numel() else None
+        self.env.n_lobes = self.lobes.shape[0]
+        self.env.voxel = _ptr(self.voxel)
+        self.env.vres = 0 if self.voxel is None else self.voxel.shape[0]
+        self.env.planes = _ptr(self.planes)
+        self.env.pres = 0 if self.planes is None else self.planes.shape[1]
+        self.env.radius = float(env.radius)
+        self.env.far_field = int(env.far_field)
+        cams = sc.cams
+        self.K = _dev(cams.K, torch.float32, device)
+        self.c2w = _dev(cams.c2w, torch.float32, device)
+        self.width, self.height, self.n_views = cams.width, cams.height, cams.n_views
+        self.max_depth = sc.max_depth
+        self.cap_policy = sc.cap_policy
+        self.t_eps = sc.t_eps
+
+    @property
+    def n_pixels(self):
+        return self.n_views * self.width * self.height
+
+    def set_vertices(self, V: torch.Tensor):
+        self.V = V.to(self.device, torch.float32).contiguous()
+
+    def set_sigma(self, sigma: torch.Tensor):
+        assert sigma.numel() == self.sigma.numel()
+        self.sigma = sigma.to(self.device, torch.float32).contiguous()
+
+    def cameras(self, pixel_ids: Optional[torch.Tensor] = None) -> N.Cameras:
+        c = N.Cameras()
+        c.n_views, c.width, c.height = self.n_views, self.width, self.height
+        c.K, c.c2w = _ptr(self.K), _ptr(self.c2w)
+        if pixel_ids is not None:
+            assert pixel_ids.dtype == torch.int64 and pixel_ids.is_cuda and pixel_ids.is_contiguous()
+            c.pixel_ids, c.n_rays = _ptr(pixel_ids), pixel_ids.numel()
+        else:
+            c.pixel_ids, c.n_rays = None, self.n_pixels
+        return c
+
+
+@dataclass
+class ForwardOut:
+    rgb: torch.Tensor
+    capped_w: Optional[torch.Tensor] = None
+    sig_topo: Optional[torch.Tensor] = None
+    sig_face: Optional[torch.Tensor] = None
+    stats: Optional[dict] = None
+
+
+class Tracer:
+    """One libdifftrans context (one per GPU)."""
+
+    def __init__(self, device=None):
+        self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+        self._lib = N.lib()
+        h = C.c_void_p()
+        self._check(self._lib.dt_create(self.device.index or 0, C.byref(h)), None)
+        self.h = h
+        self.n_rays = 0
+        self._keep = []
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self._lib.dt_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def _check(self, rc, h):
+        if rc != N.DT_OK:
+            msg = self._lib.dt_last_error(h).decode() if h else ""
+            raise N.DiffTransError(f"{N.STATUS.get(rc, rc)}: {msg}")
+
+    # ------------------------------------------------------------------ path
+    def build_bvh(self, V: torch.Tensor, F: torch.Tensor, stream=None):
+        assert V.is_cuda and V.dtype == torch.float32 and V.is_contiguous() and V.shape[-1] == 3
+        assert F.is_cuda and F.dtype == torch.int32 and F.is_contiguous() and F.shape[-1] == 3
+        self._check(self._lib.dt_build_bvh(self.h, _ptr(V), V.shape[0], _ptr(F), F.shape[0], _stream(stream)), self.h)
+
+    def trace_forward(self, ds: DeviceScene, pixel_ids: Optional[torch.Tensor] = None, ior: Optional[float] = None,
+                      max_depth: Optional[int] = None, cap_policy: Optional[int] = None, want_capped=False,
+                      want_sig=False, stats=False, check_finite=False, rgb: Optional[torch.Tensor] = None,
+                      stream=None) -> ForwardOut:
+        cams = ds.cameras(pixel_ids)
+        n = cams.n_rays
+        dev = self.device
+        if rgb is None:
+            rgb = torch.empty((n, 3), dtype=torch.float32, device=dev)
+        capw = torch.empty(n, dtype=torch.float32, device=dev) if want_capped else None
+        st = torch.empty(n, dtype=torch.int64, device=dev) if want_sig else None
+        sf = torch.empty(n, dtype=torch.int64, device=dev) if want_sig else None
+        opts = N.TraceOpts()
+        opts.max_depth = ds.max_depth if max_depth is None else max_depth
+        opts.cap_policy = ds.cap_policy if cap_policy is None else cap_policy
+        opts.t_eps = ds.t_eps
+        opts.check_finite = int(check_finite)
+        ds.absorption.sigma = _ptr(ds.sigma)
+        st_out = N.Stats() if stats else None
+        rc = self._lib.dt_trace_forward(self.h, float(ds.ior if ior is None else ior), C.byref(ds.absorption),
+                                        C.byref(ds.env), C.byref(cams), C.byref(opts), _ptr(rgb), _ptr(capw),
+                                        _ptr(st), _ptr(sf), C.byref(st_out) if stats else None, _stream(stream))
+        self._check(rc, self.h)
+        self.n_rays = n
+        self._sigma_shape = tuple(ds.sigma.shape)
+        self._nv = ds.V.shape[0]
+        self._keep = [ds]          # env buffers must outlive the backward
+        return ForwardOut(rgb, capw, st, sf, st_out.as_dict(opts.max_depth) if stats else None)
+
+    def trace_backward(self, grad_rgb: torch.Tensor, grad_V=None, grad_ior=None, grad_sigma=None,
+                       accumulate: bool = False, stream=None):
+        assert grad_rgb.is_cuda and grad_rgb.dtype == torch.float32 and grad_rgb.is_contiguous()
+        assert grad_rgb.numel() == 3 * self.n_rays
+        dev = self.device
+        if grad_V is None:
+            grad_V = torch.empty((self._nv, 3), dtype=torch.float32, device=dev)
+        if grad_ior is None:
+            grad_ior = torch.empty(1, dtype=torch.float32, device=dev)
+        if grad_sigma is None:
+            grad_sigma = torch.empty(self._sigma_shape, dtype=torch.float32, device=dev)
+        rc = self._lib.dt_trace_backward(self.h, _ptr(grad_rgb), _ptr(grad_V), _ptr(grad_ior), _ptr(grad_sigma),
+                                         int(accumulate), _stream(stream))
+        self._check(rc, self.h)
+        return grad_V, grad_ior, grad_sigma
+
+    def loss_color(self, rgb: torch.Tensor, target: torch.Tensor, grad_rgb: Optional[torch.Tensor] = None,
+                   loss: Optional[torch.Tensor] = None, stream=None):
+        n = rgb.shape[0]
+        if grad_rgb is None:
+            grad_rgb = torch.empty_like(rgb)
+        if loss is None:
+            loss = torch.empty(1, dtype=torch.float32, device=rgb.device)
+        self._check(self._lib.dt_loss_color(self.h, _ptr(rgb), _ptr(target), n, _ptr(grad_rgb), _ptr(loss),
+                                            _stream(stream)), self.h)
+        return loss, grad_rgb
+
+    # ------------------------------------------------------------------ profiling
+    def set_profiling(self, enable: bool):
+        self._check(self._lib.dt_set_profiling(self.h, int(enable)), self.h)
+
+    def profile(self, reset: bool = False) -> dict:
+        p = N.Profile()
+        self._check(self._lib.dt_get_profile(self.h, C.byref(p), int(reset)), self.h)
+        return p.as_dict()
+
+    # ------------------------------------------------------------------ test hooks
+    def closest_hit(self, rays: torch.Tensor, t_lo: float = 0.0, brute_force: bool = False, stream=None):
+        rays = rays.to(self.device, torch.float32).contiguous()
+        n = rays.shape[0]
+        face = torch.empty(n, dtype=torch.int32, device=self.device)
+        tuv = torch.empty((n, 3), dtype=torch.float32, device=self.device)
+        self._check(self._lib.dt_debug_closest_hit(self.h, _ptr(rays), n, float(t_lo), int(brute_force), _ptr(face),
+                                                   _ptr(tuv), _stream(stream)), self.h)
+        return face, tuv
+
+    def bvh_check(self, stream=None):
+        out = (C.c_int64 * 4)()
+        self._check(self._lib.dt_debug_bvh_check(self.h, out, _stream(stream)), self.h)
+        return dict(bad_boxes=out[0], leaves=out[1], distinct_faces=out[2], depth=out[3])
+
+    def vertex_normals(self, nv: int, stream=None):
+        out = torch.empty((nv, 3), dtype=torch.float32, device=self.device)
+        self._check(self._lib.dt_debug_vertex_normals(self.h, _ptr(out), _stream(stream)), self.h)
+        return out
+
+
+class DiffTraceFunction(torch.autograd.Function):
+    """autograd wrapper: rgb = trace(V, ior, sigma); backward through dt_trace_backward."""
+
+    @staticmethod
+    def forward(ctx, V, ior, sigma, tracer: Tracer, ds: DeviceScene, pixel_ids):
+        ds.set_vertices(V.detach())
+        ds.set_sigma(sigma.detach())
+        ds.ior = float(ior.detach().item())
+        tracer.build_bvh(ds.V, ds.F)
+        out = tracer.trace_forward(ds, pixel_ids)
+        ctx.tracer = tracer
+        return out.rgb
+
+    @staticmethod
+    def backward(ctx, grad_rgb):
+        gV, gi, gs = ctx.tracer.trace_backward(grad_rgb.contiguous())
+        return gV, gi.reshape(()), gs, None, None, None

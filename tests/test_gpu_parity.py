@@ -1,0 +1,260 @@
+"""GPU parity: libdifftrans (through the C ABI) against the fp64 oracle, same seeded inputs.
+
+Bars (north_star): hit ids bit-exact vs brute force (ties excluded); radiance max-abs
+<= 1e-4 with <= 1e-4 of pixels path-divergent; gradients rel-L2 <= 1e-3.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle as O
+from paper_2603_00413_b200 import scenes as S
+from tests import _scenes as T
+from tests._parity import GRAD_TOL, assert_forward, compare_forward, oracle_forward, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tracer():
+    from paper_2603_00413_b200.tracer import Tracer
+    return Tracer("cuda:0")
+
+
+def run_gpu(tracer, sc, pixel_ids=None, grad=None, full_launch_grad=None):
+    from paper_2603_00413_b200.tracer import DeviceScene
+    ds = DeviceScene(sc, torch.device("cuda:0"))
+    tracer.build_bvh(ds.V, ds.F)
+    pid_t = None if pixel_ids is None else torch.as_tensor(pixel_ids, dtype=torch.int64, device="cuda:0")
+    out = tracer.trace_forward(ds, pid_t, want_capped=True, want_sig=True, stats=True)
+    res = dict(rgb=out.rgb.cpu().numpy(), sig=out.sig_topo.cpu().numpy(), capw=out.capped_w.cpu().numpy(),
+               stats=out.stats)
+    g = grad if grad is not None else full_launch_grad
+    if g is not None:
+        gV, gi, gs = tracer.trace_backward(torch.as_tensor(g, dtype=torch.float32, device="cuda:0").contiguous())
+        res.update(gV=gV.cpu().numpy(), gior=float(gi.cpu()[0]), gsig=gs.cpu().numpy())
+    torch.cuda.synchronize()
+    return res
+
+
+def parity_case(tracer, sc, pixel_ids, label, grad_seed=11):
+    """Forward + backward parity on the given pixels (pixel_ids launch)."""
+    osc = O.OracleScene(sc)
+    orc = oracle_forward(O, osc, pixel_ids)
+    gpu = run_gpu(tracer, sc, pixel_ids)
+    cmp = compare_forward(gpu["rgb"], gpu["sig"], orc)
+    assert_forward(cmp, label)
+    ok = ~(cmp["div_mask"] | cmp["flag_mask"])
+    np.testing.assert_allclose(gpu["capw"][ok], orc["capped_w"][ok], atol=1e-4, err_msg=label)
+    g = S.upstream_grad(len(pixel_ids), grad_seed)
+    g[cmp["div_mask"] | cmp["flag_mask"]] = 0.0
+    gpu = run_gpu(tracer, sc, pixel_ids, grad=g)
+    gV, gi, gs = O.backward(osc, g, pixel_ids)
+    errs = dict(V=rel_l2(gpu["gV"], gV), ior=rel_l2(gpu["gior"], gi), sigma=rel_l2(gpu["gsig"], gs))
+    for k, e in errs.items():
+        assert e <= GRAD_TOL, (label, k, errs)
+    return cmp, errs, gpu["stats"]
+
+
+# ----------------------------------------------------------------------------- BVH
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4"])
+def test_bvh_structure_and_bit_exact_vs_brute_force(tracer, cfg):
+    sc = S.CONFIGS[cfg]() if cfg in ("C1", "C2") else None
+    if cfg == "C3":
+        V, F = S.cube_sphere(204, 3)
+    elif cfg == "C4":
+        V, F = S.knot_and_gems(4)
+    else:
+        V, F = sc.V, sc.F
+    Vt = torch.as_tensor(V, device="cuda:0")
+    Ft = torch.as_tensor(F, device="cuda:0")
+    tracer.build_bvh(Vt, Ft)
+    chk = tracer.bvh_check()
+    assert chk["bad_boxes"] == 0 and chk["leaves"] == F.shape[0] and chk["distinct_faces"] == F.shape[0], chk
+    assert chk["depth"] < 128
+    g = np.random.default_rng(5)
+    n = 20000 if cfg != "C1" else 5000
+    r = 1.3 * np.abs(V).max()
+    o = g.normal(size=(n, 3))
+    o = o / np.linalg.norm(o, axis=1, keepdims=True) * r * g.uniform(1.0, 3.0, (n, 1))
+    tgt = g.uniform(-0.8, 0.8, (n, 3)) * np.abs(V).max()
+    d = tgt - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    inner = g.uniform(-0.3, 0.3, (n // 4, 3))            # rays starting inside the object
+    din = g.normal(size=(n // 4, 3))
+    din /= np.linalg.norm(din, axis=1, keepdims=True)
+    rays = np.concatenate([np.concatenate([o, d], 1), np.concatenate([inner, din], 1)]).astype(np.float32)
+    rt = torch.as_tensor(rays, device="cuda:0")
+    for t_lo in (0.0, 1e-4):
+        f_bvh, tuv_bvh = tracer.closest_hit(rt, t_lo, brute_force=False)
+        f_bf, tuv_bf = tracer.closest_hit(rt, t_lo, brute_force=True)
+        assert torch.equal(f_bvh, f_bf)
+        assert torch.equal(tuv_bvh.view(torch.int32), tuv_bf.view(torch.int32))   # bit-exact t, u, v
+    # against the fp64 oracle brute force: identical face ids except flagged ties / edges
+    m = 3000 if cfg in ("C3", "C4") else len(rays)
+    osc = O.OracleScene(S.Scene("t", V, F, 1.5, S.const_absorption(), S.analytic_env(1),
+                                T.one_view(2, 2, (0, 0, 3)), 2))
+    f_o, tuv_o, fl = O.closest_hit(osc, rays[:m].astype(np.float64))
+    f_g = f_bvh.cpu().numpy()[:m]
+    ok = fl == 0
+    assert (f_g[ok] == f_o[ok]).all(), int((f_g[ok] != f_o[ok]).sum())
+    hit = ok & (f_o >= 0)
+    np.testing.assert_allclose(tuv_bvh.cpu().numpy()[:m][hit, 0], tuv_o[hit, 0], rtol=2e-5, atol=2e-5)
+
+
+def test_vertex_normals_match_oracle(tracer):
+    sc = S.config_c2()
+    tracer.build_bvh(torch.as_tensor(sc.V, device="cuda:0"), torch.as_tensor(sc.F, device="cuda:0"))
+    n = tracer.vertex_normals(sc.V.shape[0]).cpu().numpy()
+    no = O.vertex_normals(O.OracleScene(sc))
+    assert np.abs(n - no).max() < 2e-6
+
+
+# ----------------------------------------------------------------------------- forward + backward
+def test_c1_full_image(tracer):
+    sc = S.config_c1()
+    cmp, errs, st = parity_case(tracer, sc, np.arange(sc.n_pixels), "C1")
+    assert cmp["sig_mismatch"] == 0 and cmp["divergent_unflagged"] == 0
+
+
+def test_c1_axis_pixel_slab_series(tracer):
+    """The C1 axis pixel reproduces the oracle-pinned slab series on the GPU."""
+    sc = S.config_c1()
+    gpu = run_gpu(tracer, sc, np.array([31 * 64 + 31]))
+    orc = O.render(O.OracleScene(sc), [31 * 64 + 31])
+    np.testing.assert_allclose(gpu["rgb"][0], orc["rgb"][0], atol=2e-6)
+
+
+@pytest.mark.parametrize("D,cap", [(0, S.CAP_ZERO), (1, S.CAP_ENV), (4, S.CAP_ZERO), (5, S.CAP_ENV)])
+def test_c1_depths_and_cap_policies(tracer, D, cap):
+    base = S.config_c1()
+    sc = T.scene(base.V, base.F, base.cams, env=base.env, D=D, cap=cap)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), f"C1-D{D}-cap{cap}")
+
+
+def test_c2_grid_env_sampled_pixels(tracer):
+    sc = S.config_c2()
+    pid = S.central_pixels(sc.cams, 2048, 2)
+    cmp, errs, st = parity_case(tracer, sc, pid, "C2")
+
+
+def test_c2_full_launch_sampled_compare(tracer):
+    """Full-image launch (the bench's configuration); compare 2048 sampled pixels, and the
+    gradient of a loss living only on those pixels."""
+    sc = S.config_c2()
+    pid = S.central_pixels(sc.cams, 2048, 3)
+    osc = O.OracleScene(sc)
+    orc = oracle_forward(O, osc, pid)
+    gpu = run_gpu(tracer, sc, None)
+    cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
+    assert_forward(cmp, "C2-full")
+    gfull = np.zeros((sc.n_pixels, 3), np.float32)
+    g = S.upstream_grad(len(pid), 12)
+    g[cmp["div_mask"] | cmp["flag_mask"]] = 0
+    gfull[pid] = g
+    gpu = run_gpu(tracer, sc, None, full_launch_grad=gfull)
+    gV, gi, gs = O.backward(osc, g, pid)
+    assert rel_l2(gpu["gV"], gV) <= GRAD_TOL
+    assert rel_l2(gpu["gior"], gi) <= GRAD_TOL
+    assert rel_l2(gpu["gsig"], gs) <= GRAD_TOL
+
+
+def test_sigma_grid_and_far_field(tracer):
+    V, F = S.icosphere(2)
+    cams = T.one_view(40, 28, (0.6, -0.4, 2.6), fov_deg=55)           # ragged 8x4 tiles
+    sc = T.scene(V, F, cams, env=T.small_grid_env(far_field=1), absorption=T.small_sigma_grid(V, 8), D=4)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "ico2-sigmagrid-farfield")
+    sc = T.scene(V, F, cams, env=T.small_grid_env(far_field=0), absorption=T.small_sigma_grid(V, 8), D=3,
+                 cap=S.CAP_ENV)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "ico2-sigmagrid-capenv")
+
+
+def test_flat_facets_and_tir(tracer):
+    """Unwelded flat gems (flat normals, TIR-rich) and the tetrahedron."""
+    Vg, Fg = S.gem()
+    cams = T.one_view(48, 48, (0.3, 0.5, 2.8), fov_deg=50)
+    sc = T.scene(Vg.astype(np.float32), Fg, cams, env=T.lobe_env(kappa=4.0), ior=2.4, D=6)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "gem")
+    Vt, Ft = S.tetrahedron()
+    sc = T.scene(Vt, Ft, cams, env=T.small_grid_env(), D=3)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "tet")
+
+
+def test_c3_full_size_sampled(tracer):
+    """BASELINE configs[2] at full size in the bench's launch configuration (all 64M rays of
+    100 views x 800^2, D 4); 256 sampled object pixels against the oracle."""
+    sc = S.config_c3()
+    pid = S.central_pixels(sc.cams, 256, 3)
+    osc = O.OracleScene(sc)
+    orc = oracle_forward(O, osc, pid)
+    gpu = run_gpu(tracer, sc, None)
+    cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
+    assert_forward(cmp, "C3")
+    gfull = np.zeros((sc.n_pixels, 3), np.float32)
+    g = S.upstream_grad(len(pid), 13)
+    g[cmp["div_mask"] | cmp["flag_mask"]] = 0
+    gfull[pid] = g
+    gpu = run_gpu(tracer, sc, None, full_launch_grad=gfull)
+    gV, gi, gs = O.backward(osc, g, pid)
+    assert rel_l2(gpu["gV"], gV) <= GRAD_TOL
+    assert rel_l2(gpu["gior"], gi) <= GRAD_TOL
+    assert rel_l2(gpu["gsig"], gs) <= GRAD_TOL
+
+
+def test_c4_sigma_grid_full_mesh_sampled(tracer):
+    """BASELINE configs[3]: knot + gems, 64^3 sigma grid, D 6; 256 sampled pixels."""
+    sc = S.config_c4()
+    pid = S.central_pixels(sc.cams, 256, 4)
+    parity_case(tracer, sc, pid, "C4")
+
+
+# ----------------------------------------------------------------------------- edge cases
+def test_edge_cases(tracer):
+    from paper_2603_00413_b200.tracer import DeviceScene
+    from paper_2603_00413_b200._native import DiffTransError
+    # one-triangle mesh, ragged image
+    V = np.array([[-1, -1, 0], [1, -1, 0], [0, 1, 0]], np.float32)
+    F = np.array([[0, 1, 2]], np.int32)
+    sc = T.scene(V, F, T.one_view(13, 7, (0.1, 0.2, 3.0)), env=T.lobe_env(), D=3)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "one-tri")
+    # empty pixel list
+    ds = DeviceScene(S.config_c1(), torch.device("cuda:0"))
+    tracer.build_bvh(ds.V, ds.F)
+    out = tracer.trace_forward(ds, torch.zeros(0, dtype=torch.int64, device="cuda:0"))
+    assert out.rgb.shape == (0, 3)
+    gV, gi, gs = tracer.trace_backward(torch.zeros((0, 3), device="cuda:0"))
+    assert float(gV.abs().max()) == 0.0
+    # duplicated pixels give identical radiance
+    pid = torch.tensor([100, 2080, 100, 2080], dtype=torch.int64, device="cuda:0")
+    out = tracer.trace_forward(ds, pid)
+    assert torch.equal(out.rgb[0], out.rgb[2]) and torch.equal(out.rgb[1], out.rgb[3])
+    # errors are loud
+    with pytest.raises(DiffTransError, match="EMPTY_GEOMETRY"):
+        tracer.build_bvh(torch.zeros((0, 3), device="cuda:0"), torch.zeros((0, 3), dtype=torch.int32, device="cuda:0"))
+    with pytest.raises(DiffTransError, match="INVALID_ARG"):
+        tracer.build_bvh(ds.V, ds.F)
+        tracer.trace_forward(ds, max_depth=99)
+
+
+def test_forward_deterministic(tracer):
+    from paper_2603_00413_b200.tracer import DeviceScene
+    ds = DeviceScene(S.config_c2(), torch.device("cuda:0"))
+    tracer.build_bvh(ds.V, ds.F)
+    a = tracer.trace_forward(ds, want_sig=True).rgb.clone()
+    tracer.build_bvh(ds.V, ds.F)
+    b = tracer.trace_forward(ds, want_sig=True).rgb
+    assert torch.equal(a, b)
+
+
+def test_loss_color_kernel(tracer):
+    rgb = torch.tensor([[1.1, 1.1, 1.1]], device="cuda:0")
+    tgt = torch.ones((1, 3), device="cuda:0")
+    loss, g = tracer.loss_color(rgb, tgt)
+    assert abs(float(loss) - 0.03) < 1e-6                              # S: l_color example
+    x = torch.rand((1000, 3), device="cuda:0")
+    c = torch.rand((1000, 3), device="cuda:0")
+    loss, g = tracer.loss_color(x, c)
+    ref = (((x - c) * c) ** 2).sum() / 1000
+    assert abs(float(loss) - float(ref)) < 1e-5 * float(ref)
+    assert torch.allclose(g, 2 * (x - c) * c * c / 1000, atol=1e-7)
