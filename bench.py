@@ -121,15 +121,16 @@ def algorithmic_bytes(stats, nf: int):
     seg = stats["segments_per_depth"]
     D = len(seg) - 1
     bvh = 64 * max(nf - 1, 0) + 48 * nf
-    trace = 0
-    for k in range(1, D + 1):
-        nxt = seg[k + 1] if k + 1 <= D else 0
-        trace += seg[k] * (48 + 48 + 108) + nxt * 48 + bvh
-    bwd = 0
-    for k in range(0, D + 1):
-        nxt = seg[k + 1] if k + 1 <= D else 0
-        bwd += seg[k] * (96 + 12 + 32 + 108 + 192) + nxt * 48
-    return {"trace": trace, "bwd": bwd, "trace_launches": D, "bwd_launches": D + 1}
+    # traversal (k >= 1): ray in (o, d: 32 B), hit out (16 B), the LBVH once
+    trace = sum(seg[k] * 48 + bvh for k in range(1, D + 1))
+    # shading (all levels): record in (o, d, thr, hit: 64 B), hit/tau/lsub out (48 B),
+    # vertex gather (3 ids + 3 positions + 3 normals: 108 B), children out (48 B each)
+    shade = sum(seg[k] * (64 + 48 + 108) + (seg[k + 1] if k < D else 0) * 48 for k in range(0, D + 1))
+    # backward: record in (96 B) + grad_rgb (12 B) + slots out (32 B) + gather (108 B) +
+    # 6 float4 atomics RMW (192 B) + children's slots/radiance in (48 B each)
+    bwd = sum(seg[k] * (96 + 12 + 32 + 108 + 192) + (seg[k + 1] if k < D else 0) * 48 for k in range(0, D + 1))
+    return {"trace": trace, "shade": shade, "bwd": bwd, "trace_launches": D, "shade_launches": D + 1,
+            "bwd_launches": D + 1}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -265,12 +266,13 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_src = hbm_peak()
     ab = algorithmic_bytes(last, sc.F.shape[0])
     ph = prof["ms"]
-    cls = "trace" if ph["trace"] >= ph["bwd"] else "bwd"
+    cls = max(("trace", "shade", "bwd"), key=lambda c: ph[c])
     launches = prof["launches"][cls]
     ms_per_launch = ph[cls] / max(launches, 1)
     bytes_per_launch = ab[cls] / max(ab[f"{cls}_launches"], 1)
     achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "k_trace_level" if cls == "trace" else "k_backward_level",
+    kname = {"trace": "k_traverse_level", "shade": "k_shade_level", "bwd": "k_backward_level"}[cls]
+    roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "note": "algorithmic = compulsory record/gather bytes + LBVH once per launch; node/tri re-reads "

@@ -173,7 +173,7 @@ DT_API dt_status dt_loss_color(dt_ctx* ctx, const float* rgb, const float* targe
  * time; dt_get_profile resolves pending events (synchronising on them) and returns the
  * totals since the last reset.  Traversal counters and the kernel-launch count are always
  * maintained.  Phases: */
-enum { DT_PH_BUILD = 0, DT_PH_TRACE0 = 1, DT_PH_SHADE0 = 2, DT_PH_TRACE = 3, DT_PH_GATHER = 4, DT_PH_BWD = 5,
+enum { DT_PH_BUILD = 0, DT_PH_TRACE0 = 1, DT_PH_SHADE = 2, DT_PH_TRACE = 3, DT_PH_GATHER = 4, DT_PH_BWD = 5,
        DT_PH_NORMALS_BWD = 6, DT_PH_LOSS = 7, DT_PH_COUNT = 8 };
 typedef struct {
   double ms[DT_PH_COUNT];          /* summed device time per phase                           */

@@ -50,7 +50,7 @@ class Stats(C.Structure):
                     arena_retries=int(self.arena_retries))
 
 
-PHASES = ["build", "trace0", "shade0", "trace", "gather", "bwd", "normals_bwd", "loss"]
+PHASES = ["build", "trace0", "shade", "trace", "gather", "bwd", "normals_bwd", "loss"]
 
 
 class Profile(C.Structure):

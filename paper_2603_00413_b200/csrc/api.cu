@@ -183,7 +183,6 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   cudaSetDevice(c->device);
   if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_trace_forward: call dt_build_bvh first");
   DT_ARG(ab && env && cams && opts, "dt_trace_forward: absorption/env/cams/opts must be non-NULL");
-  DT_ARG(rgb, "dt_trace_forward: rgb must be a device pointer");
   DT_ARG(opts->max_depth >= 0 && opts->max_depth <= DT_MAX_DEPTH, "dt_trace_forward: opts.max_depth=%d not in [0,%d]",
          opts->max_depth, DT_MAX_DEPTH);
   DT_ARG(opts->cap_policy == DT_CAP_ZERO || opts->cap_policy == DT_CAP_ENV, "dt_trace_forward: bad opts.cap_policy");
@@ -200,7 +199,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   int64_t npix = (int64_t)cams->n_views * cams->width * cams->height;
   int64_t n_rays = cams->pixel_ids ? cams->n_rays : npix;
   DT_ARG(n_rays >= 0 && n_rays < (1ll << 31), "dt_trace_forward: n_rays=%lld out of range", (long long)n_rays);
-  cudaStream_t st = (cudaStream_t)stream;
+  DT_ARG(rgb || n_rays == 0, "dt_trace_forward: rgb must be a device pointer");  cudaStream_t st = (cudaStream_t)stream;
   const int D = opts->max_depth;
 
   // absorption snapshot (the backward differentiates w.r.t. these values)
@@ -277,13 +276,18 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
         p.end(1);
       }
       {
-        PhaseTimer p(c, DT_PH_SHADE0, st);
-        DT_CU(launch_shade_level0(a, D, c->sm_count, st));
+        PhaseTimer p(c, DT_PH_SHADE, st);
+        DT_CU(launch_shade_level(a, 0, D, c->sm_count, st));
         p.end(1);
       }
       for (int k = 1; k <= D; ++k) {
-        PhaseTimer p(c, DT_PH_TRACE, st);
-        DT_CU(launch_forward_level(a, k, D, c->sm_count, st));
+        {
+          PhaseTimer p(c, DT_PH_TRACE, st);
+          DT_CU(launch_traverse_level(a, k, c->sm_count, st));
+          p.end(1);
+        }
+        PhaseTimer p(c, DT_PH_SHADE, st);
+        DT_CU(launch_shade_level(a, k, D, c->sm_count, st));
         p.end(1);
       }
       for (int k = std::max(D - 1, 0); k >= 0; --k) {

@@ -30,7 +30,7 @@ enum {
   LV_CNT = 0,            // [16] records per level
   LV_WORK_TRACE = 16,    // [16]
   LV_WORK_GATHER = 32,   // [16]
-  LV_WORK_BWD = 48,      // [16]
+  LV_WORK_SHADE = 48,    // [16]
   LV_OVERFLOW = 64,
   LV_STACKERR = 65,
   LV_TRACED = 66,        // primaries traversed (passed the root-box test)
@@ -151,8 +151,8 @@ namespace dt {
 // each launcher returns the CUDA error and adds the number of kernels it launched to *nl
 cudaError_t build_bvh(dt_ctx* c, const float* V, int nv, const int* F, int nf, cudaStream_t st, int* nl);
 cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count, cudaStream_t st);
-cudaError_t launch_shade_level0(const FwdLaunch& a, int max_depth, int sm_count, cudaStream_t st);
-cudaError_t launch_forward_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st);
+cudaError_t launch_shade_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st);
+cudaError_t launch_traverse_level(const FwdLaunch& a, int level, int sm_count, cudaStream_t st);
 cudaError_t launch_gather_level(const FwdLaunch& a, int level, int sm_count, cudaStream_t st);
 cudaError_t launch_backward_level(const BwdLaunch& a, int level, int sm_count, cudaStream_t st);
 cudaError_t launch_vertex_normal_backward(dt_ctx* c, cudaStream_t st);

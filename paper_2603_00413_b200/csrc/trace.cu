@@ -72,9 +72,9 @@ DT_D void shade_and_spawn(const FwdLaunch& a, int k, int max_depth, bool valid, 
   if (valid) {
     if (!is_hit) {
       float3 L = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);          // P:160 step 3
-      a.r.hit[idx] = make_float4(__int_as_float(-1), 0.f, 0.f, __int_as_float(RF_MISS));
-      a.r.lsub[idx] = f4(L, __int_as_float(-1));
-      a.r.tau[idx] = make_float4(1.f, 1.f, 1.f, __int_as_float(-1));
+      __stcs(a.r.hit + idx, make_float4(__int_as_float(-1), 0.f, 0.f, __int_as_float(RF_MISS)));
+      __stcs(a.r.lsub + idx, f4(L, __int_as_float(-1)));
+      __stcs(a.r.tau + idx, make_float4(1.f, 1.f, 1.f, __int_as_float(-1)));
       sig_add(a.sig_t, ray, topo_key(pos, EV_MISS));
       sig_add(a.sig_f, ray, face_key(pos, EV_MISS, -1));
     } else {
@@ -88,9 +88,9 @@ DT_D void shade_and_spawn(const FwdLaunch& a, int k, int max_depth, bool valid, 
         if (inside) tau = transmittance(s, o, x);
         if (s.cap_policy == 1) L = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr) * tau;
         int fl = RF_CAPPED | (inside ? RF_INSIDE : 0);
-        a.r.hit[idx] = make_float4(__int_as_float(face), t, 0.f, __int_as_float(fl));
-        a.r.lsub[idx] = f4(L, __int_as_float(-1));
-        a.r.tau[idx] = f4(tau, __int_as_float(-1));
+        __stcs(a.r.hit + idx, make_float4(__int_as_float(face), t, 0.f, __int_as_float(fl)));
+        __stcs(a.r.lsub + idx, f4(L, __int_as_float(-1)));
+        __stcs(a.r.tau + idx, f4(tau, __int_as_float(-1)));
         int ev = inside ? EV_CAP_IN : EV_CAP_OUT;
         sig_add(a.sig_t, ray, topo_key(pos, ev));
         sig_add(a.sig_f, ray, face_key(pos, ev, face));
@@ -106,7 +106,7 @@ DT_D void shade_and_spawn(const FwdLaunch& a, int k, int max_depth, bool valid, 
         spawn_r = true;                                                       // P:161 (R5)
         spawn_t = !S.tir;
         int fl = (inside ? RF_INSIDE : 0) | (S.tir ? RF_TIR : 0) | (S.degen ? RF_DEGEN : 0);
-        a.r.hit[idx] = make_float4(__int_as_float(face), t, R, __int_as_float(fl));
+        __stcs(a.r.hit + idx, make_float4(__int_as_float(face), t, R, __int_as_float(fl)));
         int ev = inside ? (S.tir ? EV_HIT_IN_TIR : EV_HIT_IN) : (S.tir ? EV_HIT_OUT_TIR : EV_HIT_OUT);
         sig_add(a.sig_t, ray, topo_key(pos, ev));
         sig_add(a.sig_f, ray, face_key(pos, ev, face));
@@ -129,9 +129,9 @@ DT_D void shade_and_spawn(const FwdLaunch& a, int k, int max_depth, bool valid, 
     int64_t j = off + base + __popc(mr & lanemask_lt());
     if (j < lim) {
       cr = j;
-      a.r.o[j] = f4(x, __int_as_float((int)ray));
-      a.r.d[j] = f4(wr, __uint_as_float(pos * 2u));
-      a.r.thr[j] = f4(thr * tau * R, w * R);
+      __stcs(a.r.o + j, f4(x, __int_as_float((int)ray)));
+      __stcs(a.r.d + j, f4(wr, __uint_as_float(pos * 2u)));
+      __stcs(a.r.thr + j, f4(thr * tau * R, w * R));
     } else {
       a.lvl[LV_OVERFLOW] = 1;
     }
@@ -139,15 +139,15 @@ DT_D void shade_and_spawn(const FwdLaunch& a, int k, int max_depth, bool valid, 
       j = off + base + nr + __popc(mt & lanemask_lt());
       if (j < lim) {
         ct = j;
-        a.r.o[j] = f4(x, __int_as_float((int)ray));
-        a.r.d[j] = f4(wt, __uint_as_float(pos * 2u + 1u));
-        a.r.thr[j] = f4(thr * tau * T, w * T);
+        __stcs(a.r.o + j, f4(x, __int_as_float((int)ray)));
+        __stcs(a.r.d + j, f4(wt, __uint_as_float(pos * 2u + 1u)));
+        __stcs(a.r.thr + j, f4(thr * tau * T, w * T));
       } else {
         a.lvl[LV_OVERFLOW] = 1;
       }
     }
-    a.r.tau[idx] = f4(tau, __int_as_float((int)ct));
-    a.r.lsub[idx] = make_float4(0.f, 0.f, 0.f, __int_as_float((int)cr));
+    __stcs(a.r.tau + idx, f4(tau, __int_as_float((int)ct)));
+    __stcs(a.r.lsub + idx, make_float4(0.f, 0.f, 0.f, __int_as_float((int)cr)));
   }
 }
 
@@ -208,10 +208,10 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_primary(FwdLaunch a, in
     int64_t idx = a.cap - 1 - (rb + __popc(m & lanemask_lt()));
     if (rec && idx < 0) { a.lvl[LV_OVERFLOW] = 1; rec = false; }
     if (rec) {
-      a.r.o[idx] = f4(o, __int_as_float((int)ray));
-      a.r.d[idx] = f4(d, __uint_as_float(1u));
-      a.r.thr[idx] = make_float4(1.f, 1.f, 1.f, 1.f);
-      a.r.hit[idx] = make_float4(__int_as_float(face), t, u, v);   // shaded by k_shade_level0
+      __stcs(a.r.o + idx, f4(o, __int_as_float((int)ray)));
+      __stcs(a.r.d + idx, f4(d, __uint_as_float(1u)));
+      __stcs(a.r.thr + idx, make_float4(1.f, 1.f, 1.f, 1.f));
+      __stcs(a.r.hit + idx, make_float4(__int_as_float(face), t, u, v));   // shaded by k_shade_level(0)
     }
   }
   if (err) a.lvl[LV_STACKERR] = 1;
@@ -220,45 +220,18 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_primary(FwdLaunch a, in
   flush_counters(a.counters, visits, tests);
 }
 
-// Level 0 shading (needs the final level-0 count, so it is a second pass over the hits).
-__global__ void __launch_bounds__(kTraceThreads) k_shade_level0(FwdLaunch a, int max_depth) {
+// Shading of level k (K10): reads each record's ray and traversal result, evaluates the
+// event and spawns the children into level k+1 (warp-ballot compaction).  Level 0 needs
+// the final level-0 count, so it always runs after the traversal pass.
+__global__ void __launch_bounds__(kTraceThreads) k_shade_level(FwdLaunch a, int k, int max_depth) {
   if (a.lvl[LV_OVERFLOW]) return;   // arena too small: the host grows it and re-runs
-  int n = a.lvl[LV_CNT + 0];
-  while (true) {
-    int base = fetch_work(a.lvl + LV_WORK_TRACE + 0);
-    if (base >= n) break;
-    int64_t item = (int64_t)base + lane_id();
-    bool valid = item < n;
-    int64_t idx = a.cap - 1 - item;
-    float3 o = f3(0, 0, 0), d = f3(0, 0, 1);
-    int64_t ray = 0;
-    int face = -1;
-    float t = 0, u = 0, v = 0;
-    if (valid) {
-      float4 ro = a.r.o[idx], rd = a.r.d[idx], h = a.r.hit[idx];
-      o = f3(ro); d = f3(rd);
-      ray = __float_as_int(ro.w);
-      face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
-    }
-    shade_and_spawn(a, 0, max_depth, valid, idx, o, d, ray, 1u, f3(1, 1, 1), 1.f, face, t, u, v);
-  }
-}
-
-// Levels 1..D_max: traverse + shade + spawn.
-__global__ void __launch_bounds__(kTraceThreads) k_trace_level(FwdLaunch a, int k, int max_depth) {
-  __shared__ int sstack[kStackShared * kTraceThreads];
-  const DevScene& s = a.s;
-  if (a.lvl[LV_OVERFLOW]) return;
-  float t_lo = a.t_eps * s.scal[6];                                            // R17
   int n = a.lvl[LV_CNT + k];
-  int64_t off = level_base(a.lvl, k);
-  int err = 0, visits = 0, tests = 0;
   while (true) {
-    int base = fetch_work(a.lvl + LV_WORK_TRACE + k);
+    int base = fetch_work(a.lvl + LV_WORK_SHADE + k);
     if (base >= n) break;
     int64_t item = (int64_t)base + lane_id();
     bool valid = item < n;
-    int64_t idx = off + item;
+    int64_t idx = rec_index(a.lvl, a.cap, k, item);
     float3 o = f3(0, 0, 0), d = f3(0, 0, 1), thr = f3(0, 0, 0);
     float w = 0.f;
     int64_t ray = 0;
@@ -266,13 +239,108 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_level(FwdLaunch a, int 
     int face = -1;
     float t = 0, u = 0, v = 0;
     if (valid) {
-      float4 ro = a.r.o[idx], rd = a.r.d[idx], rt = a.r.thr[idx];
+      float4 ro = __ldcs(a.r.o + idx), rd = __ldcs(a.r.d + idx), rt = __ldcs(a.r.thr + idx), h = __ldcs(a.r.hit + idx);
       o = f3(ro); d = f3(rd); thr = f3(rt); w = rt.w;
       ray = __float_as_int(ro.w);
       pos = __float_as_uint(rd.w);
-      face = traverse(s, o, d, t_lo, t, u, v, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
+      face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
     }
     shade_and_spawn(a, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
+  }
+}
+
+// Traversal of level k >= 1 (K9): closest hit only, hit = (face, t, u, v) written back into
+// the record.  Lanes that finish their ray refill from the level's queue (one warp-aggregated
+// atomic per refill), so short reflected rays do not idle a warp behind long refracted ones.
+constexpr int kStepBudget = 16;
+__global__ void __launch_bounds__(kTraceThreads) k_traverse_level(FwdLaunch a, int k) {
+  __shared__ int sstack_all[kStackShared * kTraceThreads];
+  const DevScene& s = a.s;
+  if (a.lvl[LV_OVERFLOW]) return;
+  const float t_lo = a.t_eps * s.scal[6];                                      // R17
+  const int n = a.lvl[LV_CNT + k];
+  const int64_t off = level_base(a.lvl, k);
+  int* work = a.lvl + LV_WORK_TRACE + k;
+  int* sstack = sstack_all + threadIdx.x;
+  int lstack[kStackLocal];
+  int err = 0, visits = 0, tests = 0;
+  int item = -1;                       // -1: needs a ray; >= n: queue exhausted
+  float3 o = f3(0, 0, 0), d = f3(0, 0, 1), inv = f3(0, 0, 0);
+  int cur = 0, sp = 0, best = -1;
+  float bt = kInf, bu = 0.f, bv = 0.f;
+  while (true) {
+    unsigned need = __ballot_sync(~0u, item < 0);
+    if (need) {
+      int leader = __ffs(need) - 1;
+      int base = 0;
+      if (lane_id() == leader) base = atomicAdd(work, __popc(need));
+      base = __shfl_sync(~0u, base, leader);
+      if (item < 0) {
+        int j = base + __popc(need & lanemask_lt());
+        if (j < n) {
+          item = j;
+          float4 ro = __ldcs(a.r.o + off + j), rd = __ldcs(a.r.d + off + j);
+          o = f3(ro);
+          d = f3(rd);
+          inv = safe_inv(d);
+          cur = s.root;
+          sp = 0;
+          best = -1;
+          bt = kInf;
+          bu = bv = 0.f;
+        } else {
+          item = n;
+        }
+      }
+    }
+    if (__all_sync(~0u, item >= n)) break;
+    if (item >= n) continue;
+    bool done = false;
+    for (int step = 0; step < kStepBudget && !done; ++step) {
+      bool descended = false;
+      if (cur >= 0) {
+        const float4* nd = s.nodes + 4 * (size_t)cur;
+        float4 na = __ldg(nd), nb = __ldg(nd + 1), nc = __ldg(nd + 2), ne = __ldg(nd + 3);
+        ++visits;
+        float t0, t1;
+        bool h0 = slab(na.x, na.y, na.z, na.w, nb.x, nb.y, o, inv, bt, t0);
+        bool h1 = slab(nb.z, nb.w, nc.x, nc.y, nc.z, nc.w, o, inv, bt, t1);
+        int c0 = __float_as_int(ne.x), c1 = __float_as_int(ne.y);
+        if (h0 && h1) {
+          int nr = t0 <= t1 ? c0 : c1, fr = t0 <= t1 ? c1 : c0;
+          if (sp < kStackShared) sstack[sp * kTraceThreads] = fr;
+          else if (sp < kStackShared + kStackLocal) lstack[sp - kStackShared] = fr;
+          else err = 1;
+          ++sp;
+          cur = nr;
+          descended = true;
+        } else if (h0 || h1) {
+          cur = h0 ? c0 : c1;
+          descended = true;
+        }
+      } else {
+        const float4* tr = s.tris + 3 * (size_t)(~cur);
+        float4 ta = __ldg(tr), tb = __ldg(tr + 1), tc = __ldg(tr + 2);
+        float t, u, v;
+        ++tests;
+        if (intersect_tri(o, d, f3(ta), f3(tb), f3(tc), t_lo, t, u, v)) {
+          int id = __float_as_int(ta.w);
+          if (t < bt || (t == bt && id < best)) { bt = t; bu = u; bv = v; best = id; }
+        }
+      }
+      if (!descended) {
+        if (sp == 0 || err) {
+          done = true;
+        } else {
+          --sp;
+          cur = sp < kStackShared ? sstack[sp * kTraceThreads] : lstack[sp - kStackShared];
+        }
+      }
+    }
+    if (done) {
+      __stcs(a.r.hit + off + item, make_float4(__int_as_float(best), bt, bu, bv));
+      item = -1;
+    }
   }
   if (err) a.lvl[LV_STACKERR] = 1;
   flush_counters(a.counters, visits, tests);
@@ -525,17 +593,17 @@ cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count
   return cudaGetLastError();
 }
 
-cudaError_t launch_shade_level0(const FwdLaunch& a, int max_depth, int sm_count, cudaStream_t st) {
+cudaError_t launch_shade_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
   static int gs = 0;
-  if (!gs) gs = persistent_blocks((const void*)k_shade_level0, kTraceThreads, sm_count);
-  k_shade_level0<<<gs, kTraceThreads, 0, st>>>(a, max_depth);
+  if (!gs) gs = persistent_blocks((const void*)k_shade_level, kTraceThreads, sm_count);
+  k_shade_level<<<gs, kTraceThreads, 0, st>>>(a, level, max_depth);
   return cudaGetLastError();
 }
 
-cudaError_t launch_forward_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
+cudaError_t launch_traverse_level(const FwdLaunch& a, int level, int sm_count, cudaStream_t st) {
   static int gl = 0;
-  if (!gl) gl = persistent_blocks((const void*)k_trace_level, kTraceThreads, sm_count);
-  k_trace_level<<<gl, kTraceThreads, 0, st>>>(a, level, max_depth);
+  if (!gl) gl = persistent_blocks((const void*)k_traverse_level, kTraceThreads, sm_count);
+  k_traverse_level<<<gl, kTraceThreads, 0, st>>>(a, level);
   return cudaGetLastError();
 }
 

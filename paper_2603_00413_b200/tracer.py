@@ -90,6 +90,11 @@ class DeviceScene:
         c.K, c.c2w = _ptr(self.K), _ptr(self.c2w)
         if pixel_ids is not None:
             assert pixel_ids.dtype == torch.int64 and pixel_ids.is_cuda and pixel_ids.is_contiguous()
+            if pixel_ids.numel() == 0:       # an empty list is not "all pixels" (NULL)
+                self._empty_ids = torch.zeros(1, dtype=torch.int64, device=pixel_ids.device)
+                pixel_ids = self._empty_ids
+                c.pixel_ids, c.n_rays = _ptr(pixel_ids), 0
+                return c
             c.pixel_ids, c.n_rays = _ptr(pixel_ids), pixel_ids.numel()
         else:
             c.pixel_ids, c.n_rays = None, self.n_pixels
