@@ -115,14 +115,16 @@ def oracle_sample(sc, n_pix: int, seed: int = 9):
     return dt, int(out["segments"].sum()), os.cpu_count()
 
 
-def algorithmic_bytes(stats, nf: int):
-    """Compulsory bytes per launch class: record streams, shading gathers,
-    children writes, and the LBVH read once per launch (served from L2 afterwards)."""
+def algorithmic_bytes(stats, prof, steps: int):
+    """Algorithmic bytes per step and launch class: record
+    streams, shading gathers, children writes, and for traversal the wide-BVH nodes (64 B)
+    and triangles (48 B) the rays fetch, counted on the device (most are served by L2)."""
     seg = stats["segments_per_depth"]
     D = len(seg) - 1
-    bvh = 64 * max(nf - 1, 0) + 48 * nf
-    # traversal (k >= 1): ray in (o, d: 32 B), hit out (16 B), the LBVH once
-    trace = sum(seg[k] * 48 + bvh for k in range(1, D + 1))
+    # traversal (k >= 1): ray in (o, d: 32 B), hit out (16 B), node and triangle fetches
+    nodes = (prof["node_visits"] - prof["node_visits_primary"]) / steps
+    tris = (prof["tri_tests"] - prof["tri_tests_primary"]) / steps
+    trace = sum(seg[k] * 48 for k in range(1, D + 1)) + nodes * 64 + tris * 48
     # shading (all levels): record in (o, d, thr, hit: 64 B), hit/tau/lsub out (48 B),
     # vertex gather (3 ids + 3 positions + 3 normals: 108 B), children out (48 B each)
     shade = sum(seg[k] * (64 + 48 + 108) + (seg[k + 1] if k < D else 0) * 48 for k in range(0, D + 1))
@@ -264,7 +266,7 @@ def run_ours(args, rank, world, local_rank):
         return None
     # ---- roofline of the dominant launch class, device time measured live (CUDA events)
     peak, peak_src = hbm_peak()
-    ab = algorithmic_bytes(last, sc.F.shape[0])
+    ab = algorithmic_bytes(last, prof, args.steps)
     ph = prof["ms"]
     cls = max(("trace", "shade", "bwd"), key=lambda c: ph[c])
     launches = prof["launches"][cls]
@@ -275,10 +277,9 @@ def run_ours(args, rank, world, local_rank):
     roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
-                "note": "algorithmic = compulsory record/gather bytes + LBVH once per launch; node/tri re-reads "
-                        "are cache traffic (l2_bytes_per_launch)",
-                "l2_bytes_per_launch": int((prof["node_visits"] * 64 + prof["tri_tests"] * 48) /
-                                           max(prof["launches"]["trace0"] + prof["launches"]["trace"], 1)),
+                "note": "SURVEY 8(d) algorithmic bytes: ray in + hit out + counted node (64 B) and triangle "
+                        "(48 B) fetches; the LBVH is L2-resident, so DRAM traffic (ncu, profiles/) is far lower",
+                "bytes_per_launch": int(bytes_per_launch), "ms_per_launch": round(ms_per_launch, 3),
                 "share_of_step": round(ph[cls] / ms, 4)}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -314,14 +315,14 @@ def run_reference(args, rank, world):
     from paper_2603_00413_b200 import scenes as S
     sc = S.CONFIGS[args.config]()
     for _ in range(args.warmup):
-        oracle_sample(sc, max(args.cpu_pixels // 4, 1), seed=100)
+        oracle_sample(sc, max(args.ref_pixels // 4, 1), seed=100)
     tot_t, tot_s = 0.0, 0
     for k in range(args.steps):
-        dt, segs, cores = oracle_sample(sc, args.cpu_pixels, seed=200 + k)
+        dt, segs, cores = oracle_sample(sc, args.ref_pixels, seed=200 + k)
         tot_t += dt
         tot_s += segs
     v = tot_s / tot_t / 1e6
-    sample = (f"each step: {args.cpu_pixels} object pixels of {args.config} (fp64 brute force fwd+bwd); "
+    sample = (f"each step: {args.ref_pixels} object pixels of {args.config} (fp64 brute force fwd+bwd); "
               f"{tot_s} segments in {tot_t:.1f}s")
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True,
@@ -338,7 +339,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-pixels", type=int, default=24)
+    ap.add_argument("--cpu-pixels", type=int, default=1024, help="oracle sample for cpu_baseline (~10-30 s)")
+    ap.add_argument("--ref-pixels", type=int, default=192, help="oracle pixels per --impl reference step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

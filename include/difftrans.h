@@ -181,6 +181,8 @@ typedef struct {
   int64_t kernel_launches;         /* all kernels this context launched since the reset     */
   int64_t node_visits;             /* LBVH inner nodes fetched by the trace kernels          */
   int64_t tri_tests;               /* ray-triangle tests by the trace kernels                */
+  int64_t node_visits_primary;     /* the part of node_visits made by camera rays (depth 0)  */
+  int64_t tri_tests_primary;       /* the part of tri_tests made by camera rays (depth 0)    */
 } dt_profile;
 DT_API dt_status dt_set_profiling(dt_ctx* ctx, int32_t enable);
 DT_API dt_status dt_get_profile(dt_ctx* ctx, dt_profile* out, int32_t reset);

@@ -132,10 +132,13 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   c->device = device;
   cudaSetDevice(device);
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (const char* v = getenv("DT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(4, atoi(v)));
+  if (const char* v = getenv("DT_TRAV_MODE")) c->trav_mode = std::max(0, std::min(2, atoi(v)));
+  if (const char* v = getenv("DT_TRAV_CHUNK")) c->trav_chunk = std::max(32, atoi(v));
   cudaError_t e;
   if ((e = cudaMalloc(&c->lvl, LV_INTS * sizeof(int))) || (e = cudaMallocHost(&c->host_lvl, LV_INTS * sizeof(int))) ||
-      (e = cudaMalloc(&c->gior, 4 * sizeof(float))) || (e = cudaMalloc(&c->counters, 2 * sizeof(unsigned long long))) ||
-      (e = cudaMemset(c->counters, 0, 2 * sizeof(unsigned long long)))) {
+      (e = cudaMalloc(&c->gior, 4 * sizeof(float))) || (e = cudaMalloc(&c->counters, 4 * sizeof(unsigned long long))) ||
+      (e = cudaMemset(c->counters, 0, 4 * sizeof(unsigned long long)))) {
     dt_destroy(c);
     return DT_ERR_CUDA;
   }
@@ -149,7 +152,7 @@ void dt_destroy(dt_ctx* c) {
   void* ptrs[] = {c->V, c->F, c->nrm, c->fnrm, c->nodes, c->tris, c->keys, c->vals, c->hist, c->children,
                   c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, c->vstart, c->vcorner, c->scal,
                   c->iscal, c->rec.o, c->lvl, c->sigma_snap, c->gV, c->gN, c->gVn, c->gS, c->fe, c->gsig, c->gior,
-                  c->counters};
+                  c->counters, c->ranges, c->bdepth, c->wflag, c->widx, c->wbox, c->wdepth};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
@@ -163,8 +166,8 @@ const char* dt_last_error(const dt_ctx* c) { return c ? c->err.c_str() : "null c
 dt_status dt_build_bvh(dt_ctx* c, const float* V, int32_t nv, const int32_t* F, int32_t nf, void* stream) {
   if (!c) return DT_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
-  DT_ARG(V && F, "dt_build_bvh: V and F must be non-NULL device pointers");
   if (nv <= 0 || nf <= 0) return fail(c, DT_ERR_EMPTY_GEOMETRY, "dt_build_bvh: empty geometry (nv=%d, nf=%d)", nv, nf);
+  DT_ARG(V && F, "dt_build_bvh: V and F must be non-NULL device pointers");
   DT_ARG(nf < (1 << 29) && nv < (1 << 29), "dt_build_bvh: nv/nf too large");
   cudaStream_t st = (cudaStream_t)stream;
   PhaseTimer pt(c, DT_PH_BUILD, st);
@@ -255,6 +258,8 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.sig_t = (unsigned long long*)sig_topo;
   a.sig_f = (unsigned long long*)sig_face;
   a.counters = c->counters;
+  a.trav_mode = c->trav_mode;
+  a.trav_chunk = c->trav_chunk;
 
   int64_t limit = arena_limit() + c->arena_cap;
   if (c->arena_cap == 0) {
@@ -390,15 +395,17 @@ dt_status dt_get_profile(dt_ctx* c, dt_profile* out, int32_t reset) {
   cudaSetDevice(c->device);
   DT_ARG(out, "dt_get_profile: out is NULL");
   resolve_profile(c);
-  unsigned long long cnt[2] = {0, 0};
+  unsigned long long cnt[4] = {0, 0, 0, 0};
   DT_CU(cudaMemcpy(cnt, c->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
   for (int i = 0; i < DT_PH_COUNT; ++i) {
     out->ms[i] = c->ph_ms[i];
     out->launches[i] = c->ph_launches[i];
   }
   out->kernel_launches = c->kernel_launches;
-  out->node_visits = (int64_t)cnt[0];
-  out->tri_tests = (int64_t)cnt[1];
+  out->node_visits = (int64_t)(cnt[0] + cnt[2]);
+  out->tri_tests = (int64_t)(cnt[1] + cnt[3]);
+  out->node_visits_primary = (int64_t)cnt[2];
+  out->tri_tests_primary = (int64_t)cnt[3];
   if (reset) {
     for (int i = 0; i < DT_PH_COUNT; ++i) { c->ph_ms[i] = 0.0; c->ph_launches[i] = 0; }
     c->kernel_launches = 0;

@@ -207,7 +207,7 @@ DT_D int delta(const unsigned* __restrict__ k, int n, int i, int j) {
 }
 
 __global__ void k_karras(const unsigned* __restrict__ k, int n, int2* __restrict__ children, int* __restrict__ parent_int,
-                         int* __restrict__ parent_leaf) {
+                         int* __restrict__ parent_leaf, int2* __restrict__ ranges) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
     int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
     int dmin = delta(k, n, i, i - d);
@@ -228,6 +228,7 @@ __global__ void k_karras(const unsigned* __restrict__ k, int n, int2* __restrict
     int left = min(i, j) == gamma ? ~gamma : gamma;
     int right = max(i, j) == gamma + 1 ? ~(gamma + 1) : gamma + 1;
     children[i] = make_int2(left, right);
+    ranges[i] = make_int2(min(i, j), max(i, j));            // leaves covered by node i
     if (left < 0) parent_leaf[~left] = i; else parent_int[left] = i;
     if (right < 0) parent_leaf[~right] = i; else parent_int[right] = i;
     if (i == 0) parent_int[0] = -1;
@@ -269,25 +270,122 @@ __global__ void k_refit(const float4* __restrict__ V, const int* __restrict__ F,
   }
 }
 
-// 64-B node: (c0lo.x, c0hi.x, c0lo.y, c0hi.y) (c0lo.z, c0hi.z, c1lo.x, c1hi.x)
-//            (c1lo.y, c1hi.y, c1lo.z, c1hi.z) (ref0, ref1, -, -); boxes inflated by `pad`.
-__global__ void k_pack_nodes(const int2* __restrict__ children, const float4* __restrict__ leafbox,
+// ----------------------------------------------------------------------------- 4-wide collapse
+// The binary Karras tree is collapsed into a 4-wide BVH by keeping the binary nodes at even
+// depth: a wide node's children are its binary grandchildren (a binary child that is a leaf,
+// or whose subtree holds <= kLeafMax triangles, becomes one leaf entry: a contiguous range of
+// leaf-ordered triangles).  Child boxes are quantised to 8 bits per plane relative to the
+// node box (conservatively: floor / ceil in float64, after the pad inflation), so a node is
+// 64 B for four children -- half the bytes per child of the binary layout, half the depth.
+//   n0 = (p.x, p.y, p.z, exponents e_x | e_y << 8 | e_z << 16)     scale_a = 2^(e_a - 127)
+//   n1 = (qlo_x, qlo_y, qlo_z, qhi_x)  n2 = (qhi_y, qhi_z, ref0, ref1)  n3 = (ref2, ref3, -, -)
+// q* hold one byte per child (child c in bits 8c..8c+7).  ref >= 0: wide node; ref = EMPTY:
+// unused slot (qlo = 255 > qhi = 0); otherwise leaf: ref = -1 - (first << 2 | (count - 1)).
+DT_D int bsize(const int2* __restrict__ ranges, int ref) { return ref < 0 ? 1 : ranges[ref].y - ranges[ref].x + 1; }
+
+__global__ void k_bdepth(const int* __restrict__ parent_int, int n_int, int* __restrict__ depth) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_int; i += gridDim.x * blockDim.x) {
+    int dd = 0;
+    for (int p = parent_int[i]; p >= 0; p = parent_int[p]) ++dd;
+    depth[i] = dd;
+  }
+}
+
+__global__ void k_wide_flags(const int* __restrict__ depth, const int2* __restrict__ ranges, int n_int,
+                             unsigned* __restrict__ flag, unsigned* __restrict__ scan_in, int leaf_max) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_int; i += gridDim.x * blockDim.x) {
+    unsigned f = (i == 0) || ((depth[i] & 1) == 0 && bsize(ranges, i) > leaf_max);
+    flag[i] = f;
+    scan_in[i] = f;
+  }
+}
+
+__global__ void k_wide_build(const int2* __restrict__ children, const int2* __restrict__ ranges,
+                             const unsigned* __restrict__ flag, const unsigned* __restrict__ widx,
+                             const int* __restrict__ depth, const float4* __restrict__ leafbox,
                              const float4* __restrict__ nodebox, int n, const int* __restrict__ ibox,
-                             float4* __restrict__ nodes) {
+                             uint4* __restrict__ wnodes, float4* __restrict__ wbox, int* __restrict__ wdepth,
+                             int* __restrict__ nwide, int leaf_max) {
   float m = fmaxf(fmaxf(fmaxf(fabsf(ord2f(ibox[0])), fabsf(ord2f(ibox[1]))), fmaxf(fabsf(ord2f(ibox[2])), fabsf(ord2f(ibox[3])))),
                   fmaxf(fabsf(ord2f(ibox[4])), fabsf(ord2f(ibox[5]))));
-  float pad = m * 4e-6f + 1e-30f;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
-    int2 ch = children[i];
-    float3 l0, h0, l1, h1;
-    load_box(leafbox, nodebox, ch.x, l0, h0);
-    load_box(leafbox, nodebox, ch.y, l1, h1);
-    float3 P = f3(pad, pad, pad);
-    l0 = l0 - P; h0 = h0 + P; l1 = l1 - P; h1 = h1 + P;
-    nodes[4 * (size_t)i + 0] = make_float4(l0.x, h0.x, l0.y, h0.y);
-    nodes[4 * (size_t)i + 1] = make_float4(l0.z, h0.z, l1.x, h1.x);
-    nodes[4 * (size_t)i + 2] = make_float4(l1.y, h1.y, l1.z, h1.z);
-    nodes[4 * (size_t)i + 3] = make_float4(__int_as_float(ch.x), __int_as_float(ch.y), 0.f, 0.f);
+  double pad = (double)m * 4e-6 + 1e-30;
+  int n_int = n - 1;
+  int total = max(n_int, 1);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    if (i == total - 1) *nwide = n_int == 0 ? 1 : (int)(widx[i] + flag[i]);
+    if (n_int > 0 && !flag[i]) continue;
+    // entries of this wide node (binary refs)
+    int ent[4], ne = 0;
+    if (n_int == 0) {
+      ent[ne++] = ~0;                                   // single triangle
+    } else {
+      int2 ch = children[i];
+      int cs[2] = {ch.x, ch.y};
+      for (int q = 0; q < 2; ++q) {
+        int c = cs[q];
+        if (c < 0 || bsize(ranges, c) <= leaf_max) {
+          ent[ne++] = c;
+        } else {
+          int2 g = children[c];
+          ent[ne++] = g.x;
+          ent[ne++] = g.y;
+        }
+      }
+    }
+    float3 ulo, uhi;
+    if (n_int == 0) load_box(leafbox, nodebox, ~0, ulo, uhi);
+    else load_box(leafbox, nodebox, i, ulo, uhi);
+    double P[3] = {(double)__double2float_rd((double)ulo.x - pad), (double)__double2float_rd((double)ulo.y - pad),
+                   (double)__double2float_rd((double)ulo.z - pad)};
+    double hiU[3] = {(double)uhi.x + pad, (double)uhi.y + pad, (double)uhi.z + pad};
+    int ex[3];
+    double sc[3];
+    for (int a = 0; a < 3; ++a) {
+      double ext = hiU[a] - P[a];
+      int k = -126;
+      if (ext > 0.0) { frexp(ext / 255.0, &k); k = max(-126, min(127, k)); }
+      ex[a] = k + 127;
+      sc[a] = ldexp(1.0, k);
+    }
+    unsigned q[6] = {0, 0, 0, 0, 0, 0};
+    int refs[4];
+    for (int c = 0; c < 4; ++c) {
+      unsigned ql[3] = {255, 255, 255}, qh[3] = {0, 0, 0};
+      refs[c] = kEmptyRef;
+      if (c < ne) {
+        int e = ent[c];
+        float3 lo, hi;
+        load_box(leafbox, nodebox, e, lo, hi);
+        const float l3[3] = {lo.x, lo.y, lo.z}, h3[3] = {hi.x, hi.y, hi.z};
+        for (int a = 0; a < 3; ++a) {
+          double fl = floor(((double)l3[a] - pad - P[a]) / sc[a]);
+          double fh = ceil(((double)h3[a] + pad - P[a]) / sc[a]);
+          ql[a] = (unsigned)fmin(fmax(fl, 0.0), 255.0);
+          qh[a] = (unsigned)fmin(fmax(fh, 0.0), 255.0);
+        }
+        if (e >= 0 && bsize(ranges, e) > leaf_max) {
+          refs[c] = (int)widx[e];
+        } else {
+          int first = e < 0 ? ~e : ranges[e].x;
+          int cnt = bsize(ranges, e);
+          refs[c] = -1 - ((first << 2) | (cnt - 1));
+        }
+      }
+      for (int a = 0; a < 3; ++a) {
+        q[a] |= ql[a] << (8 * c);
+        q[3 + a] |= qh[a] << (8 * c);
+      }
+    }
+    unsigned w = n_int == 0 ? 0u : widx[i];
+    uint4* nd = wnodes + 4 * (size_t)w;
+    nd[0] = make_uint4(__float_as_uint((float)P[0]), __float_as_uint((float)P[1]), __float_as_uint((float)P[2]),
+                       (unsigned)ex[0] | ((unsigned)ex[1] << 8) | ((unsigned)ex[2] << 16));
+    nd[1] = make_uint4(q[0], q[1], q[2], q[3]);
+    nd[2] = make_uint4(q[4], q[5], (unsigned)refs[0], (unsigned)refs[1]);
+    nd[3] = make_uint4((unsigned)refs[2], (unsigned)refs[3], 0u, 0u);
+    wbox[2 * (size_t)w] = f4(ulo, 0.f);
+    wbox[2 * (size_t)w + 1] = f4(uhi, 0.f);
+    wdepth[w] = n_int == 0 ? 0 : depth[i] / 2;
   }
 }
 
@@ -319,36 +417,53 @@ __global__ void k_init_ibox(int* ibox) {
 }
 
 // ----------------------------------------------------------------------------- checks
-__global__ void k_bvh_check(const float4* __restrict__ nodes, const float4* __restrict__ tris, const int* __restrict__ parent_int,
-                            const int* __restrict__ parent_leaf, int n, int root, unsigned long long* __restrict__ out,
-                            int* __restrict__ mark) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    int f = __float_as_int(tris[3 * (size_t)j].w);
-    atomicAdd(mark + f, 1);
-    // walk to the root; count depth
-    int depth = 0, p = n > 1 ? parent_leaf[j] : -1;
-    int ref = ~j;
-    unsigned long long bad = 0;
-    float3 v0 = f3(tris[3 * (size_t)j]), v1 = v0 + f3(tris[3 * (size_t)j + 1]), v2 = v0 + f3(tris[3 * (size_t)j + 2]);
-    float3 clo = fminf3(v0, fminf3(v1, v2)), chi = fmaxf3(v0, fmaxf3(v1, v2));
-    while (p >= 0) {
-      const float4* nd = nodes + 4 * (size_t)p;
-      float4 a = nd[0], b = nd[1], c = nd[2], e = nd[3];
-      bool left = __float_as_int(e.x) == ref;
-      float3 lo = left ? f3(a.x, a.z, b.x) : f3(b.z, c.x, c.z);
-      float3 hi = left ? f3(a.y, a.w, b.y) : f3(b.w, c.y, c.w);
-      if (!left && __float_as_int(e.y) != ref) bad++;
-      if (lo.x > clo.x || lo.y > clo.y || lo.z > clo.z || hi.x < chi.x || hi.y < chi.y || hi.z < chi.z) bad++;
-      clo = lo; chi = hi;
-      ref = p;
-      p = parent_int[p];
-      ++depth;
+// Per wide node: every decoded child box must contain its child (the child wide node's box,
+// or every triangle of a leaf); every triangle must be reached exactly once; every wide node
+// but the root must be referenced exactly once.  out: [0] violations, [1] triangles reached
+// through leaves, [2] (k_count_marks) distinct faces reached once, [3] depth.
+__global__ void k_bvh_check(const uint4* __restrict__ wnodes, const float4* __restrict__ wbox,
+                            const int* __restrict__ wdepth, const int* __restrict__ nwide_p,
+                            const float4* __restrict__ tris, unsigned long long* __restrict__ out, int* __restrict__ mark,
+                            int* __restrict__ wref) {
+  int nw = *nwide_p;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+    const uint4* nd = wnodes + 4 * (size_t)w;
+    uint4 n0 = nd[0], n1 = nd[1], n2 = nd[2], n3 = nd[3];
+    unsigned long long bad = 0, leaves = 0;
+    for (int c = 0; c < 4; ++c) {
+      int ref = wide_ref(n2, n3, c);
+      if (ref == kEmptyRef) continue;
+      float3 lo, hi;
+      decode_wide_child(n0, n1, n2, c, lo, hi);
+      float3 clo, chi;
+      if (ref >= 0) {
+        atomicAdd(wref + ref, 1);
+        clo = f3(wbox[2 * (size_t)ref]);
+        chi = f3(wbox[2 * (size_t)ref + 1]);
+        if (lo.x > clo.x || lo.y > clo.y || lo.z > clo.z || hi.x < chi.x || hi.y < chi.y || hi.z < chi.z) bad++;
+      } else {
+        int first, cnt;
+        leaf_range(ref, first, cnt);
+        for (int j = first; j < first + cnt; ++j) {
+          float3 v0 = f3(tris[3 * (size_t)j]), v1 = v0 + f3(tris[3 * (size_t)j + 1]), v2 = v0 + f3(tris[3 * (size_t)j + 2]);
+          clo = fminf3(v0, fminf3(v1, v2));
+          chi = fmaxf3(v0, fmaxf3(v1, v2));
+          if (lo.x > clo.x || lo.y > clo.y || lo.z > clo.z || hi.x < chi.x || hi.y < chi.y || hi.z < chi.z) bad++;
+          atomicAdd(mark + __float_as_int(tris[3 * (size_t)j].w), 1);
+          ++leaves;
+        }
+      }
     }
-    if (ref != root && !(n == 1 && ref == ~0)) bad++;
     atomicAdd(out + 0, bad);
-    atomicAdd(out + 1, 1ull);
-    atomicMax(out + 3, (unsigned long long)depth);
+    atomicAdd(out + 1, leaves);
+    atomicMax(out + 3, (unsigned long long)wdepth[w]);
   }
+}
+
+__global__ void k_check_refs(const int* __restrict__ wref, const int* __restrict__ nwide_p, unsigned long long* __restrict__ out) {
+  int nw = *nwide_p;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
+    if (wref[w] != (w == 0 ? 0 : 1)) atomicAdd(out + 0, 1ull);
 }
 
 __global__ void k_count_marks(const int* __restrict__ mark, int n, unsigned long long* __restrict__ out) {
@@ -372,7 +487,6 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   cudaError_t e;
   if ((size_t)nv > c->cap_nv) {
     size_t cap = nv;
-    size_t dummy;
     cudaFree(c->V); cudaFree(c->nrm); cudaFree(c->gV); cudaFree(c->gN); cudaFree(c->gVn); cudaFree(c->gS);
     cudaFree(c->vstart);
     c->V = c->nrm = c->gV = c->gN = c->gVn = c->gS = nullptr;
@@ -381,24 +495,26 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
         (e = cudaMalloc(&c->gN, cap * 16)) || (e = cudaMalloc(&c->gVn, cap * 16)) || (e = cudaMalloc(&c->gS, cap * 16)) ||
         (e = cudaMalloc(&c->vstart, (cap + 1) * sizeof(int))))
       return e;
-    (void)dummy;
     c->cap_nv = cap;
   }
   if ((size_t)nf > c->cap_nf) {
     size_t cap = nf;
-    cudaFree(c->F); cudaFree(c->fnrm); cudaFree(c->nodes); cudaFree(c->tris); cudaFree(c->keys); cudaFree(c->vals);
-    cudaFree(c->children); cudaFree(c->parent_int); cudaFree(c->parent_leaf); cudaFree(c->rflags);
-    cudaFree(c->nodebox); cudaFree(c->leafbox); cudaFree(c->vcorner); cudaFree(c->fe);
+    void* old[] = {c->F, c->fnrm, c->nodes, c->tris, c->keys, c->vals, c->children, c->parent_int, c->parent_leaf,
+                   c->rflags, c->nodebox, c->leafbox, c->vcorner, c->fe, c->ranges, c->bdepth, c->wflag, c->widx,
+                   c->wbox, c->wdepth};
+    for (void* p : old)
+      if (p) cudaFree(p);
     size_t ks = 2 * 3 * cap;   // keys/vals ping-pong sized for the 3*nf corner sort
     if ((e = cudaMalloc(&c->F, cap * 3 * sizeof(int))) || (e = cudaMalloc(&c->fnrm, cap * 16)) ||
-        (e = cudaMalloc(&c->nodes, std::max<size_t>(cap - 1, 1) * 64)) || (e = cudaMalloc(&c->tris, cap * 48)) ||
+        (e = cudaMalloc(&c->nodes, cap * 64)) || (e = cudaMalloc(&c->tris, cap * 48)) ||
         (e = cudaMalloc(&c->keys, ks * sizeof(unsigned))) || (e = cudaMalloc(&c->vals, ks * sizeof(unsigned))) ||
-        (e = cudaMalloc(&c->children, std::max<size_t>(cap - 1, 1) * sizeof(int2))) ||
-        (e = cudaMalloc(&c->parent_int, std::max<size_t>(cap - 1, 1) * sizeof(int))) ||
-        (e = cudaMalloc(&c->parent_leaf, cap * sizeof(int))) ||
-        (e = cudaMalloc(&c->rflags, std::max<size_t>(cap - 1, 1) * sizeof(int))) ||
-        (e = cudaMalloc(&c->nodebox, std::max<size_t>(cap - 1, 1) * 32)) || (e = cudaMalloc(&c->leafbox, cap * 32)) ||
-        (e = cudaMalloc(&c->vcorner, 3 * cap * sizeof(unsigned))) || (e = cudaMalloc(&c->fe, 2 * cap * 16)))
+        (e = cudaMalloc(&c->children, cap * sizeof(int2))) || (e = cudaMalloc(&c->parent_int, cap * sizeof(int))) ||
+        (e = cudaMalloc(&c->parent_leaf, cap * sizeof(int))) || (e = cudaMalloc(&c->rflags, cap * sizeof(int))) ||
+        (e = cudaMalloc(&c->nodebox, cap * 32)) || (e = cudaMalloc(&c->leafbox, cap * 32)) ||
+        (e = cudaMalloc(&c->vcorner, 3 * cap * sizeof(unsigned))) || (e = cudaMalloc(&c->fe, 2 * cap * 16)) ||
+        (e = cudaMalloc(&c->ranges, cap * sizeof(int2))) || (e = cudaMalloc(&c->bdepth, cap * sizeof(int))) ||
+        (e = cudaMalloc(&c->wflag, cap * sizeof(unsigned))) || (e = cudaMalloc(&c->widx, cap * sizeof(unsigned))) ||
+        (e = cudaMalloc(&c->wbox, cap * 32)) || (e = cudaMalloc(&c->wdepth, cap * sizeof(int))))
       return e;
     c->cap_nf = cap;
   }
@@ -411,10 +527,12 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   int gv = std::min((nv + T - 1) / T, c->sm_count * 8);
   int gf = std::min((nf + T - 1) / T, c->sm_count * 8);
   int gf3 = std::min((3 * nf + 1 + T - 1) / T, c->sm_count * 8);
+  int launches = 0;
   k_init_ibox<<<1, 32, 0, st>>>(c->iscal);
   cudaMemcpyAsync(c->F, Fin, (size_t)nf * 3 * sizeof(int), cudaMemcpyDeviceToDevice, st);
   k_snapshot<<<gv, T, 0, st>>>(Vin, nv, c->V, c->iscal);
   k_faces<<<gf, T, 0, st>>>(c->V, c->F, nf, c->fnrm, c->iscal);
+  launches += 3;
   // vertex -> incident corners CSR (sorted by vertex, then by corner id = face order)
   unsigned *ka = c->keys, *va = c->vals, *kb = c->keys + 3 * c->cap_nf, *vb = c->vals + 3 * c->cap_nf;
   k_corner_keys<<<gf3, T, 0, st>>>(c->F, 3 * nf, ka, va);
@@ -427,39 +545,54 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   k_csr<<<gf3, T, 0, st>>>(sk, 3 * nf, nv, c->vstart);
   cudaMemcpyAsync(c->vcorner, sv, (size_t)3 * nf * sizeof(unsigned), cudaMemcpyDeviceToDevice, st);
   k_vertex_normals<<<gv, T, 0, st>>>(c->vstart, c->vcorner, c->fnrm, nv, c->nrm);
-  // LBVH
+  launches += 3 + 3 * (vbits / 8);
+  // LBVH: Morton codes, radix sort, Karras hierarchy, bottom-up refit
   k_morton<<<gf, T, 0, st>>>(c->V, c->F, nf, c->iscal, ka, va);
   if ((e = radix_sort(ka, va, kb, vb, nf, 32, c->hist, st, in_tmp))) return e;
   sk = in_tmp ? kb : ka;
   sv = in_tmp ? vb : va;
+  launches += 1 + 3 * 4;
   if (nf > 1) {
     cudaMemsetAsync(c->rflags, 0, (size_t)(nf - 1) * sizeof(int), st);
-    k_karras<<<gf, T, 0, st>>>(sk, nf, c->children, c->parent_int, c->parent_leaf);
+    k_karras<<<gf, T, 0, st>>>(sk, nf, c->children, c->parent_int, c->parent_leaf, c->ranges);
+    ++launches;
   }
   k_refit<<<gf, T, 0, st>>>(c->V, c->F, sv, nf, c->children, c->parent_int, c->parent_leaf, c->rflags, c->leafbox,
                             c->nodebox);
-  if (nf > 1) k_pack_nodes<<<gf, T, 0, st>>>(c->children, c->leafbox, c->nodebox, nf, c->iscal, c->nodes);
+  // collapse to the quantised 4-wide BVH
+  if (nf > 1) {
+    k_bdepth<<<gf, T, 0, st>>>(c->parent_int, nf - 1, c->bdepth);
+    k_wide_flags<<<gf, T, 0, st>>>(c->bdepth, c->ranges, nf - 1, c->wflag, c->widx, c->leaf_max);
+    k_scan<<<1, 1024, 0, st>>>(c->widx, nf - 1);
+    launches += 3;
+  }
+  k_wide_build<<<gf, T, 0, st>>>(c->children, c->ranges, c->wflag, c->widx, c->bdepth, c->leafbox, c->nodebox, nf,
+                                 c->iscal, reinterpret_cast<uint4*>(c->nodes), c->wbox, c->wdepth, c->iscal + 12, c->leaf_max);
   k_pack_tris<<<gf, T, 0, st>>>(c->V, c->F, sv, nf, c->tris);
   k_scalars<<<1, 1, 0, st>>>(c->iscal, c->scal);
+  launches += 4;
   c->nv = nv;
   c->nf = nf;
-  // kernels: ibox, snapshot, faces, corner keys, csr, vertex normals, morton, refit,
-  // pack tris, scalars (10) + 3 per radix pass + karras/pack nodes when nf > 1
-  *nl += 10 + 3 * (vbits / 8) + 3 * 4 + (nf > 1 ? 2 : 0);
+  *nl += launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_bvh_check(dt_ctx* c, long long* out_dev, cudaStream_t st) {
   int* mark = nullptr;
+  int* wref = nullptr;
   cudaError_t e = cudaMallocAsync(&mark, (size_t)c->nf * sizeof(int), st);
   if (e) return e;
+  if ((e = cudaMallocAsync(&wref, (size_t)c->nf * sizeof(int), st))) return e;
   cudaMemsetAsync(mark, 0, (size_t)c->nf * sizeof(int), st);
+  cudaMemsetAsync(wref, 0, (size_t)c->nf * sizeof(int), st);
   cudaMemsetAsync(out_dev, 0, 4 * sizeof(long long), st);
   int g = std::min((c->nf + 255) / 256, c->sm_count * 8);
-  k_bvh_check<<<g, 256, 0, st>>>(c->nodes, c->tris, c->parent_int, c->parent_leaf, c->nf, c->nf > 1 ? 0 : ~0,
-                                 (unsigned long long*)out_dev, mark);
+  k_bvh_check<<<g, 256, 0, st>>>(reinterpret_cast<const uint4*>(c->nodes), c->wbox, c->wdepth, c->iscal + 12, c->tris,
+                                 (unsigned long long*)out_dev, mark, wref);
+  k_check_refs<<<g, 256, 0, st>>>(wref, c->iscal + 12, (unsigned long long*)out_dev);
   k_count_marks<<<g, 256, 0, st>>>(mark, c->nf, (unsigned long long*)out_dev);
   cudaFreeAsync(mark, st);
+  cudaFreeAsync(wref, st);
   return cudaGetLastError();
 }
 
@@ -472,7 +605,7 @@ DevScene scene_from_ctx(const dt_ctx* c) {
   s.nf = c->nf;
   s.nodes = c->nodes;
   s.tris = c->tris;
-  s.root = c->nf > 1 ? 0 : ~0;
+  s.root = 0;
   s.scal = c->scal;
   return s;
 }

@@ -10,6 +10,8 @@ namespace dt {
 constexpr float kInf = __builtin_huge_valf();
 constexpr int kStackShared = 16;   // short stack entries per thread in shared memory
 constexpr int kStackLocal = 112;   // spill entries per thread (local memory, L1-cached)
+constexpr int kLeafMax = 3;        // triangles per wide-BVH leaf (a contiguous leaf-order range)
+constexpr int kEmptyRef = 0x7fffffff;
 
 // per-record event codes (the protocol numbering, shared only as a spec)
 enum { EV_MISS = 0, EV_HIT_OUT = 1, EV_HIT_IN = 2, EV_HIT_OUT_TIR = 3, EV_HIT_IN_TIR = 4, EV_CAP_OUT = 5, EV_CAP_IN = 6 };
@@ -97,6 +99,28 @@ DT_D bool intersect_tri(float3 o, float3 d, float3 v0, float3 e1, float3 e2, flo
   return t > t_lo;
 }
 
+// ----------------------------------------------------------------------------- wide nodes
+// 64-B 4-wide node (layout in bvh.cu, k_wide_build): child c's box decodes to
+// lo = p + qlo * 2^(e-127), hi = p + qhi * 2^(e-127) (one fma per plane).
+DT_D float exp_scale(unsigned e) { return __uint_as_float(e << 23); }
+DT_D int wide_ref(uint4 n2, uint4 n3, int c) {
+  return (int)(c == 0 ? n2.z : c == 1 ? n2.w : c == 2 ? n3.x : n3.y);
+}
+DT_D void decode_wide_child(uint4 n0, uint4 n1, uint4 n2, int c, float3& lo, float3& hi) {
+  float3 p = f3(__uint_as_float(n0.x), __uint_as_float(n0.y), __uint_as_float(n0.z));
+  float sx = exp_scale(n0.w & 0xff), sy = exp_scale((n0.w >> 8) & 0xff), sz = exp_scale((n0.w >> 16) & 0xff);
+  int sh = 8 * c;
+  lo = f3(fmaf((float)((n1.x >> sh) & 0xff), sx, p.x), fmaf((float)((n1.y >> sh) & 0xff), sy, p.y),
+          fmaf((float)((n1.z >> sh) & 0xff), sz, p.z));
+  hi = f3(fmaf((float)((n1.w >> sh) & 0xff), sx, p.x), fmaf((float)((n2.x >> sh) & 0xff), sy, p.y),
+          fmaf((float)((n2.y >> sh) & 0xff), sz, p.z));
+}
+DT_D void leaf_range(int ref, int& first, int& cnt) {
+  int x = ~ref;
+  first = x >> 2;
+  cnt = (x & 3) + 1;
+}
+
 DT_D float3 safe_inv(float3 d) {
   const float e = 1e-20f;
   return f3(1.0f / (fabsf(d.x) < e ? copysignf(e, d.x) : d.x), 1.0f / (fabsf(d.y) < e ? copysignf(e, d.y) : d.y),
@@ -116,53 +140,103 @@ DT_D bool slab(float lx, float hx, float ly, float hy, float lz, float hz, float
   return tmin * 0.99999f <= tmax * 1.00001f;
 }
 
-// Closest hit through the LBVH.  Ties in t resolve to the lowest ORIGINAL face id (R18), so
-// the answer does not depend on the visiting order.  Returns the original face id or -1.
-// sstack: this thread's column of the block's shared short stack (stride = blockDim.x).
-DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, float& bu, float& bv, int* sstack,
-                  int stride, int& err, int& visits, int& tests) {
-  float3 inv = safe_inv(d);
-  int lstack[kStackLocal];
-  int sp = 0;
-  int best = -1;
-  bt = kInf;
-  bu = bv = 0.0f;
-  int cur = s.root;
-  while (true) {
-    if (cur >= 0) {
-      const float4* n = s.nodes + 4 * (size_t)cur;
-      float4 a = __ldg(n), b = __ldg(n + 1), c = __ldg(n + 2), e = __ldg(n + 3);
-      ++visits;
-      float t0, t1;
-      bool h0 = slab(a.x, a.y, a.z, a.w, b.x, b.y, o, inv, bt, t0);
-      bool h1 = slab(b.z, b.w, c.x, c.y, c.z, c.w, o, inv, bt, t1);
-      int c0 = __float_as_int(e.x), c1 = __float_as_int(e.y);
-      if (h0 && h1) {
-        int nr = t0 <= t1 ? c0 : c1, fr = t0 <= t1 ? c1 : c0;
-        if (sp < kStackShared) sstack[sp * stride] = fr;
-        else if (sp < kStackShared + kStackLocal) lstack[sp - kStackShared] = fr;
-        else { err = 1; break; }
-        ++sp;
-        cur = nr;
-        continue;
+// Closest-hit traversal state of one ray through the 4-wide BVH.  Ties in t resolve to the
+// lowest ORIGINAL face id (R18), so the answer does not depend on the visiting order.
+struct Trav {
+  int cur, sp, best;
+  float bt, bu, bv;
+};
+
+DT_D void trav_init(Trav& T) {
+  T.cur = 0;
+  T.sp = 0;
+  T.best = -1;
+  T.bt = kInf;
+  T.bu = T.bv = 0.0f;
+}
+
+#define DT_CX(a, b)                                              \
+  if (k##b < k##a) {                                             \
+    float tk = k##a; k##a = k##b; k##b = tk;                     \
+    int tr = r##a; r##a = r##b; r##b = tr;                       \
+  }
+
+// One traversal step: visit the current wide node (test its four child boxes, descend into
+// the nearest hit, push the others far-to-near) or the current leaf (test its triangles),
+// then pop when nothing was descended into.  Returns true when the ray is finished.
+// sstack: this thread's column of the block's shared short stack (stride = blockDim.x);
+// entries beyond kStackShared spill to lstack (local memory).
+DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_lo, Trav& T, int* sstack, int stride,
+                    int* lstack, int& err, int& visits, int& tests) {
+  bool descended = false;
+  if (T.cur >= 0) {
+    const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)T.cur;
+    uint4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+    ++visits;
+    float k0, k1, k2, k3;
+    int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float3 lo, hi;
+      decode_wide_child(n0, n1, n2, c, lo, hi);
+      float tn;
+      bool h = slab(lo.x, hi.x, lo.y, hi.y, lo.z, hi.z, o, inv, T.bt, tn);
+      int rc = c == 0 ? r0 : c == 1 ? r1 : c == 2 ? r2 : r3;
+      float key = (h && rc != kEmptyRef) ? tn : kInf;   // the slab test is symmetric in lo/hi
+      if (c == 0) k0 = key; else if (c == 1) k1 = key; else if (c == 2) k2 = key; else k3 = key;
+    }
+    DT_CX(0, 1) DT_CX(2, 3) DT_CX(0, 2) DT_CX(1, 3) DT_CX(1, 2)   // ascending by entry distance
+    if (k0 < kInf) {
+      int push[3] = {r3, r2, r1};
+      float pk[3] = {k3, k2, k1};
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        if (pk[q] < kInf) {
+          if (T.sp < kStackShared) sstack[T.sp * stride] = push[q];
+          else if (T.sp < kStackShared + kStackLocal) lstack[T.sp - kStackShared] = push[q];
+          else err = 1;
+          ++T.sp;
+        }
       }
-      if (h0) { cur = c0; continue; }
-      if (h1) { cur = c1; continue; }
-    } else {
-      const float4* tr = s.tris + 3 * (size_t)(~cur);
+      T.cur = r0;
+      descended = true;
+    }
+  } else {
+    int first, cnt;
+    leaf_range(T.cur, first, cnt);
+    for (int j = first; j < first + cnt; ++j) {
+      const float4* tr = s.tris + 3 * (size_t)j;
       float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
       float t, u, v;
       ++tests;
       if (intersect_tri(o, d, f3(a), f3(b), f3(c), t_lo, t, u, v)) {
         int id = __float_as_int(a.w);
-        if (t < bt || (t == bt && id < best)) { bt = t; bu = u; bv = v; best = id; }
+        if (t < T.bt || (t == T.bt && id < T.best)) { T.bt = t; T.bu = u; T.bv = v; T.best = id; }
       }
     }
-    if (sp == 0) break;
-    --sp;
-    cur = sp < kStackShared ? sstack[sp * stride] : lstack[sp - kStackShared];
   }
-  return best;
+  if (!descended) {
+    if (T.sp == 0 || err) return true;
+    --T.sp;
+    T.cur = T.sp < kStackShared ? sstack[T.sp * stride] : lstack[T.sp - kStackShared];
+  }
+  return false;
+}
+#undef DT_CX
+
+// Closest hit (whole traversal).  Returns the original face id or -1.
+DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, float& bu, float& bv, int* sstack,
+                  int stride, int& err, int& visits, int& tests) {
+  float3 inv = safe_inv(d);
+  int lstack[kStackLocal];
+  Trav T;
+  trav_init(T);
+  while (!trav_step(s, o, d, inv, t_lo, T, sstack, stride, lstack, err, visits, tests)) {
+  }
+  bt = T.bt;
+  bu = T.bu;
+  bv = T.bv;
+  return T.best;
 }
 
 // triangle of ORIGINAL face f from the snapshot, with the same e1/e2 rounding as the leaves

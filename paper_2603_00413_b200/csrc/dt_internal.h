@@ -58,6 +58,7 @@ struct FwdLaunch {
   unsigned long long* sig_t;
   unsigned long long* sig_f;
   unsigned long long* counters;   // [0] node visits, [1] triangle tests
+  int trav_mode, trav_chunk;
 };
 
 struct BwdLaunch {
@@ -101,6 +102,12 @@ struct dt_ctx {
   float4* leafbox = nullptr;  // [2*nf]
   int* vstart = nullptr;      // [nv+1] CSR of (vertex -> incident corners)
   unsigned* vcorner = nullptr;// [3nf] sorted corner ids (face*3 + k)
+  int2* ranges = nullptr;     // [nf-1] leaf range of each binary node
+  int* bdepth = nullptr;      // [nf-1] binary depth
+  unsigned* wflag = nullptr;  // [nf-1] binary node starts a wide node
+  unsigned* widx = nullptr;   // [nf-1] its wide-node index (exclusive scan of wflag)
+  float4* wbox = nullptr;     // [2 * n_wide] wide-node boxes (checks)
+  int* wdepth = nullptr;      // [n_wide] wide-node depth (checks)
   float* scal = nullptr;      // device scalars: [0..5] root box, [6] bbox diagonal
   int* iscal = nullptr;       // device ints: ordered-int bounds
   size_t hist_cap = 0;
@@ -125,6 +132,10 @@ struct dt_ctx {
   float* gsig = nullptr;
   float* gior = nullptr;
   size_t gsig_cap = 0;
+  // tuning knobs (env DT_LEAF_MAX, DT_TRAV_MODE, DT_TRAV_CHUNK at dt_create)
+  int leaf_max = 1;           // triangles per wide-BVH leaf (sweep r01: 1 is fastest)
+  int trav_mode = 1;          // 0: warp takes 32 rays; 1: per-lane global refill; 2: per-lane refill from a warp chunk
+  int trav_chunk = 256;       // rays per warp chunk (mode 2)
   // profiling (dt_set_profiling / dt_get_profile)
   bool prof = false;
   double ph_ms[DT_PH_COUNT] = {};

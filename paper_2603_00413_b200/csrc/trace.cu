@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_primary(FwdLaunch a, in
   if (err) a.lvl[LV_STACKERR] = 1;
   for (int o = 16; o > 0; o >>= 1) traced += __shfl_xor_sync(~0u, traced, o);
   if (lane_id() == 0 && traced) atomicAdd(a.lvl + LV_TRACED, traced);
-  flush_counters(a.counters, visits, tests);
+  flush_counters(a.counters + 2, visits, tests);   // primary rays: counters [2], [3]
 }
 
 // Shading of level k (K10): reads each record's ray and traversal result, evaluates the
@@ -266,79 +266,65 @@ __global__ void __launch_bounds__(kTraceThreads) k_traverse_level(FwdLaunch a, i
   int err = 0, visits = 0, tests = 0;
   int item = -1;                       // -1: needs a ray; >= n: queue exhausted
   float3 o = f3(0, 0, 0), d = f3(0, 0, 1), inv = f3(0, 0, 0);
-  int cur = 0, sp = 0, best = -1;
-  float bt = kInf, bu = 0.f, bv = 0.f;
+  Trav T;
+  trav_init(T);
+  int chunk_next = 0, chunk_end = 0;   // warp-uniform (mode 2)
+  const int mode = a.trav_mode;
   while (true) {
     unsigned need = __ballot_sync(~0u, item < 0);
-    if (need) {
-      int leader = __ffs(need) - 1;
-      int base = 0;
-      if (lane_id() == leader) base = atomicAdd(work, __popc(need));
-      base = __shfl_sync(~0u, base, leader);
-      if (item < 0) {
-        int j = base + __popc(need & lanemask_lt());
+    // mode 0: the warp refills only when no lane is still traversing
+    if (mode == 0 && __ballot_sync(~0u, item < 0 || item >= n) != ~0u) need = 0;
+    while (need) {
+      int j = -1;
+      if (mode == 1 || mode == 0) {
+        // global queue: one warp-aggregated atomic
+        int leader = __ffs(need) - 1;
+        int base = 0;
+        if (lane_id() == leader) base = atomicAdd(work, __popc(need));
+        base = __shfl_sync(~0u, base, leader);
+        if ((need >> lane_id()) & 1) j = base + __popc(need & lanemask_lt());
+        need = 0;
+      } else {
+        // warp-private chunk of consecutive rays (keeps a warp's rays spatially coherent)
+        if (chunk_next >= chunk_end) {
+          int b = 0;
+          if (lane_id() == 0) b = atomicAdd(work, a.trav_chunk);
+          b = __shfl_sync(~0u, b, 0);
+          chunk_next = b;
+          chunk_end = min(b + a.trav_chunk, n);
+          if (b >= n) {
+            if (item < 0) item = n;
+            break;
+          }
+        }
+        int avail = chunk_end - chunk_next;
+        int r = __popc(need & lanemask_lt());
+        if (((need >> lane_id()) & 1) && r < avail) j = chunk_next + r;
+        int taken = min(__popc(need), avail);
+        chunk_next += taken;
+        unsigned served = __ballot_sync(~0u, j >= 0);
+        need &= ~served;
+      }
+      if (j >= 0) {
         if (j < n) {
           item = j;
           float4 ro = __ldcs(a.r.o + off + j), rd = __ldcs(a.r.d + off + j);
           o = f3(ro);
           d = f3(rd);
           inv = safe_inv(d);
-          cur = s.root;
-          sp = 0;
-          best = -1;
-          bt = kInf;
-          bu = bv = 0.f;
+          trav_init(T);
         } else {
           item = n;
         }
       }
     }
     if (__all_sync(~0u, item >= n)) break;
-    if (item >= n) continue;
+    if (item < 0 || item >= n) continue;
     bool done = false;
-    for (int step = 0; step < kStepBudget && !done; ++step) {
-      bool descended = false;
-      if (cur >= 0) {
-        const float4* nd = s.nodes + 4 * (size_t)cur;
-        float4 na = __ldg(nd), nb = __ldg(nd + 1), nc = __ldg(nd + 2), ne = __ldg(nd + 3);
-        ++visits;
-        float t0, t1;
-        bool h0 = slab(na.x, na.y, na.z, na.w, nb.x, nb.y, o, inv, bt, t0);
-        bool h1 = slab(nb.z, nb.w, nc.x, nc.y, nc.z, nc.w, o, inv, bt, t1);
-        int c0 = __float_as_int(ne.x), c1 = __float_as_int(ne.y);
-        if (h0 && h1) {
-          int nr = t0 <= t1 ? c0 : c1, fr = t0 <= t1 ? c1 : c0;
-          if (sp < kStackShared) sstack[sp * kTraceThreads] = fr;
-          else if (sp < kStackShared + kStackLocal) lstack[sp - kStackShared] = fr;
-          else err = 1;
-          ++sp;
-          cur = nr;
-          descended = true;
-        } else if (h0 || h1) {
-          cur = h0 ? c0 : c1;
-          descended = true;
-        }
-      } else {
-        const float4* tr = s.tris + 3 * (size_t)(~cur);
-        float4 ta = __ldg(tr), tb = __ldg(tr + 1), tc = __ldg(tr + 2);
-        float t, u, v;
-        ++tests;
-        if (intersect_tri(o, d, f3(ta), f3(tb), f3(tc), t_lo, t, u, v)) {
-          int id = __float_as_int(ta.w);
-          if (t < bt || (t == bt && id < best)) { bt = t; bu = u; bv = v; best = id; }
-        }
-      }
-      if (!descended) {
-        if (sp == 0 || err) {
-          done = true;
-        } else {
-          --sp;
-          cur = sp < kStackShared ? sstack[sp * kTraceThreads] : lstack[sp - kStackShared];
-        }
-      }
-    }
+    for (int step = 0; step < kStepBudget && !done; ++step)
+      done = trav_step(s, o, d, inv, t_lo, T, sstack, kTraceThreads, lstack, err, visits, tests);
     if (done) {
-      __stcs(a.r.hit + off + item, make_float4(__int_as_float(best), bt, bu, bv));
+      __stcs(a.r.hit + off + item, make_float4(__int_as_float(T.best), T.bt, T.bu, T.bv));
       item = -1;
     }
   }
