@@ -91,10 +91,12 @@ def lib():
     """Load libdifftrans.so (building it with nvcc first if it is absent)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("DT_LIBDIFFTRANS", LIB_PATH)   # tuning variants (build.build(out=...))
+        if not os.path.exists(path):
             from . import build as _build
             _build.build()
-        _lib = C.CDLL(LIB_PATH)
+            path = LIB_PATH
+        _lib = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(_lib, name)
             fn.restype = res

@@ -175,14 +175,23 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
     ++visits;
     float k0, k1, k2, k3;
     int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
+    // plane distance t = (p + q 2^e - o) / d = q * A + B with A = 2^e / d, B = (p - o) / d:
+    // one FMA per plane.  Its rounding (~1 ulp of |p - o|) is far inside the 4e-6 box pad.
+    const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
+                        exp_scale((n0.w >> 16) & 0xff) * inv.z);
+    const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
+                        (__uint_as_float(n0.z) - o.z) * inv.z);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      float3 lo, hi;
-      decode_wide_child(n0, n1, n2, c, lo, hi);
-      float tn;
-      bool h = slab(lo.x, hi.x, lo.y, hi.y, lo.z, hi.z, o, inv, T.bt, tn);
+      const int sh = 8 * c;
+      float tx0 = fmaf((float)((n1.x >> sh) & 0xff), A.x, B.x), tx1 = fmaf((float)((n1.w >> sh) & 0xff), A.x, B.x);
+      float ty0 = fmaf((float)((n1.y >> sh) & 0xff), A.y, B.y), ty1 = fmaf((float)((n2.x >> sh) & 0xff), A.y, B.y);
+      float tz0 = fmaf((float)((n1.z >> sh) & 0xff), A.z, B.z), tz1 = fmaf((float)((n2.y >> sh) & 0xff), A.z, B.z);
+      float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+      float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), T.bt));
       int rc = c == 0 ? r0 : c == 1 ? r1 : c == 2 ? r2 : r3;
-      float key = (h && rc != kEmptyRef) ? tn : kInf;   // the slab test is symmetric in lo/hi
+      bool h = tmin * 0.99999f <= tmax * 1.00001f && rc != kEmptyRef;   // slab test is symmetric in lo/hi
+      float key = h ? tmin : kInf;
       if (c == 0) k0 = key; else if (c == 1) k1 = key; else if (c == 2) k2 = key; else k3 = key;
     }
     DT_CX(0, 1) DT_CX(2, 3) DT_CX(0, 2) DT_CX(1, 3) DT_CX(1, 2)   // ascending by entry distance

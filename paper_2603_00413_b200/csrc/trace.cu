@@ -27,6 +27,32 @@ namespace {
 constexpr int kTraceThreads = 128;
 constexpr int kBwdThreads = 128;
 
+// minimum resident blocks per SM (register caps); tuned in profiles/r01_launch_bounds.txt
+#ifndef DT_TRAV_MINB
+#define DT_TRAV_MINB 1
+#endif
+#ifndef DT_SHADE_MINB
+#define DT_SHADE_MINB 1
+#endif
+#ifndef DT_BWD_MINB
+#define DT_BWD_MINB 1
+#endif
+#if DT_TRAV_MINB > 1
+#define DT_TRAV_LB __launch_bounds__(kTraceThreads, DT_TRAV_MINB)
+#else
+#define DT_TRAV_LB __launch_bounds__(kTraceThreads)
+#endif
+#if DT_SHADE_MINB > 1
+#define DT_SHADE_LB __launch_bounds__(kTraceThreads, DT_SHADE_MINB)
+#else
+#define DT_SHADE_LB __launch_bounds__(kTraceThreads)
+#endif
+#if DT_BWD_MINB > 1
+#define DT_BWD_LB __launch_bounds__(kBwdThreads, DT_BWD_MINB)
+#else
+#define DT_BWD_LB __launch_bounds__(kBwdThreads)
+#endif
+
 DT_D int fetch_work(int* counter) {
   int base = 0;
   if (lane_id() == 0) base = atomicAdd(counter, 32);
@@ -154,7 +180,7 @@ DT_D void shade_and_spawn(const FwdLaunch& a, int k, int max_depth, bool valid, 
 // Level 0: camera rays.  Each warp takes 32 pixels of an 8x4 tile (or 32 consecutive
 // entries of the caller's pixel list), culls against the root box, traverses, and records
 // only the hitting rays (misses write their env radiance straight to rgb).
-__global__ void __launch_bounds__(kTraceThreads) k_trace_primary(FwdLaunch a, int max_depth) {
+__global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
   __shared__ int sstack[kStackShared * kTraceThreads];
   const DevScene& s = a.s;
   float3 blo = f3(s.scal[0], s.scal[1], s.scal[2]), bhi = f3(s.scal[3], s.scal[4], s.scal[5]);
@@ -223,7 +249,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_primary(FwdLaunch a, in
 // Shading of level k (K10): reads each record's ray and traversal result, evaluates the
 // event and spawns the children into level k+1 (warp-ballot compaction).  Level 0 needs
 // the final level-0 count, so it always runs after the traversal pass.
-__global__ void __launch_bounds__(kTraceThreads) k_shade_level(FwdLaunch a, int k, int max_depth) {
+__global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
   if (a.lvl[LV_OVERFLOW]) return;   // arena too small: the host grows it and re-runs
   int n = a.lvl[LV_CNT + k];
   while (true) {
@@ -253,7 +279,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_shade_level(FwdLaunch a, int 
 // the record.  Lanes that finish their ray refill from the level's queue (one warp-aggregated
 // atomic per refill), so short reflected rays do not idle a warp behind long refracted ones.
 constexpr int kStepBudget = 16;
-__global__ void __launch_bounds__(kTraceThreads) k_traverse_level(FwdLaunch a, int k) {
+__global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
   __shared__ int sstack_all[kStackShared * kTraceThreads];
   const DevScene& s = a.s;
   if (a.lvl[LV_OVERFLOW]) return;
@@ -365,7 +391,7 @@ DT_D void atomic_add3(float4* p, float3 v) {
   atomicAdd(p, make_float4(v.x, v.y, v.z, 0.0f));
 }
 
-__global__ void __launch_bounds__(kBwdThreads) k_backward_level(BwdLaunch a, int k, int max_depth, int64_t cap) {
+__global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, int64_t cap) {
   const DevScene& s = a.s;
   int n = a.lvl[LV_CNT + k];
   float gior = 0.0f;
