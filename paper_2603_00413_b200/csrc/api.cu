@@ -133,7 +133,8 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   cudaSetDevice(device);
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (const char* v = getenv("DT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(4, atoi(v)));
-  if (const char* v = getenv("DT_TRAV_MODE")) c->trav_mode = std::max(0, std::min(2, atoi(v)));
+  if (const char* v = getenv("DT_TRAV_MODE")) c->trav_mode = std::max(0, std::min(3, atoi(v)));
+  if (const char* v = getenv("DT_LEAF_VOTE")) c->leaf_vote = std::max(1, std::min(32, atoi(v)));
   if (const char* v = getenv("DT_TRAV_CHUNK")) c->trav_chunk = std::max(32, atoi(v));
   cudaError_t e;
   if ((e = cudaMalloc(&c->lvl, LV_INTS * sizeof(int))) || (e = cudaMallocHost(&c->host_lvl, LV_INTS * sizeof(int))) ||
@@ -260,6 +261,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.counters = c->counters;
   a.trav_mode = c->trav_mode;
   a.trav_chunk = c->trav_chunk;
+  a.leaf_vote = c->leaf_vote;
 
   int64_t limit = arena_limit() + c->arena_cap;
   if (c->arena_cap == 0) {

@@ -232,6 +232,68 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
   return false;
 }
 #undef DT_CX
+#define DT_CX2(a, b)                                             \
+  if (k##b < k##a) {                                             \
+    float tk = k##a; k##a = k##b; k##b = tk;                     \
+    int tr = r##a; r##a = r##b; r##b = tr;                       \
+  }
+
+// Split halves of trav_step for the warp-synchronous traversal with postponed leaves
+// (k_traverse_level): trav_node visits the wide node T.cur and leaves the nearest hit child
+// (node or leaf) in T.cur, or kEmptyRef if none; trav_leaf tests one leaf's triangles.
+DT_D void trav_node(const DevScene& s, float3 o, float3 inv, Trav& T, int* sstack, int stride, int* lstack, int& err,
+                    int& visits) {
+  const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)T.cur;
+  uint4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+  ++visits;
+  float k0, k1, k2, k3;
+  int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
+  const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
+                      exp_scale((n0.w >> 16) & 0xff) * inv.z);
+  const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
+                      (__uint_as_float(n0.z) - o.z) * inv.z);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int sh = 8 * c;
+    float tx0 = fmaf((float)((n1.x >> sh) & 0xff), A.x, B.x), tx1 = fmaf((float)((n1.w >> sh) & 0xff), A.x, B.x);
+    float ty0 = fmaf((float)((n1.y >> sh) & 0xff), A.y, B.y), ty1 = fmaf((float)((n2.x >> sh) & 0xff), A.y, B.y);
+    float tz0 = fmaf((float)((n1.z >> sh) & 0xff), A.z, B.z), tz1 = fmaf((float)((n2.y >> sh) & 0xff), A.z, B.z);
+    float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+    float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), T.bt));
+    int rc = c == 0 ? r0 : c == 1 ? r1 : c == 2 ? r2 : r3;
+    bool h = tmin * 0.99999f <= tmax * 1.00001f && rc != kEmptyRef;
+    float key = h ? tmin : kInf;
+    if (c == 0) k0 = key; else if (c == 1) k1 = key; else if (c == 2) k2 = key; else k3 = key;
+  }
+  DT_CX2(0, 1) DT_CX2(2, 3) DT_CX2(0, 2) DT_CX2(1, 3) DT_CX2(1, 2)
+  int push[3] = {r3, r2, r1};
+  float pk[3] = {k3, k2, k1};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    if (pk[q] < kInf) {
+      if (T.sp < kStackShared) sstack[T.sp * stride] = push[q];
+      else if (T.sp < kStackShared + kStackLocal) lstack[T.sp - kStackShared] = push[q];
+      else err = 1;
+      ++T.sp;
+    }
+  }
+  T.cur = k0 < kInf ? r0 : kEmptyRef;
+}
+
+DT_D void trav_leaf(const DevScene& s, float3 o, float3 d, float t_lo, int leaf, Trav& T, int& tests) {
+  int first, cnt;
+  leaf_range(leaf, first, cnt);
+  for (int j = first; j < first + cnt; ++j) {
+    const float4* tr = s.tris + 3 * (size_t)j;
+    float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
+    float t, u, v;
+    ++tests;
+    if (intersect_tri(o, d, f3(a), f3(b), f3(c), t_lo, t, u, v)) {
+      int id = __float_as_int(a.w);
+      if (t < T.bt || (t == T.bt && id < T.best)) { T.bt = t; T.bu = u; T.bv = v; T.best = id; }
+    }
+  }
+}
 
 // Closest hit (whole traversal).  Returns the original face id or -1.
 DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, float& bu, float& bv, int* sstack,

@@ -58,7 +58,7 @@ struct FwdLaunch {
   unsigned long long* sig_t;
   unsigned long long* sig_f;
   unsigned long long* counters;   // [0] node visits, [1] triangle tests
-  int trav_mode, trav_chunk;
+  int trav_mode, trav_chunk, leaf_vote;
 };
 
 struct BwdLaunch {
@@ -136,6 +136,7 @@ struct dt_ctx {
   int leaf_max = 1;           // triangles per wide-BVH leaf (sweep r01: 1 is fastest)
   int trav_mode = 1;          // 0: warp takes 32 rays; 1: per-lane global refill; 2: per-lane refill from a warp chunk
   int trav_chunk = 256;       // rays per warp chunk (mode 2)
+  int leaf_vote = 32;         // mode 3: lanes that must be ready before a warp leaf phase
   // profiling (dt_set_profiling / dt_get_profile)
   bool prof = false;
   double ph_ms[DT_PH_COUNT] = {};

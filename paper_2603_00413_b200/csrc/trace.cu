@@ -358,6 +358,89 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
   flush_counters(a.counters, visits, tests);
 }
 
+// Warp-synchronous variant of k_traverse_level (trav_mode 3): every lane runs the same step
+// loop; a lane that reaches a leaf parks it (one slot) and keeps descending nodes, and the
+// warp switches to a leaf phase -- all parked leaves tested together -- once at least
+// `leaf_vote` lanes have a parked leaf or no node left (Aila & Laine's postponed leaves).
+__global__ void DT_TRAV_LB k_traverse_level_ws(FwdLaunch a, int k) {
+  __shared__ int sstack_all[kStackShared * kTraceThreads];
+  const DevScene& s = a.s;
+  if (a.lvl[LV_OVERFLOW]) return;
+  const float t_lo = a.t_eps * s.scal[6];                                      // R17
+  const int n = a.lvl[LV_CNT + k];
+  const int64_t off = level_base(a.lvl, k);
+  int* work = a.lvl + LV_WORK_TRACE + k;
+  int* sstack = sstack_all + threadIdx.x;
+  int lstack[kStackLocal];
+  int err = 0, visits = 0, tests = 0;
+  int item = -1;
+  float3 o = f3(0, 0, 0), d = f3(0, 0, 1), inv = f3(0, 0, 0);
+  Trav T;
+  trav_init(T);
+  int leaf = kEmptyRef;
+  while (true) {
+    unsigned need = __ballot_sync(~0u, item < 0);
+    if (need) {
+      int leader = __ffs(need) - 1;
+      int base = 0;
+      if (lane_id() == leader) base = atomicAdd(work, __popc(need));
+      base = __shfl_sync(~0u, base, leader);
+      if (item < 0) {
+        int j = base + __popc(need & lanemask_lt());
+        if (j < n) {
+          item = j;
+          float4 ro = __ldcs(a.r.o + off + j), rd = __ldcs(a.r.d + off + j);
+          o = f3(ro);
+          d = f3(rd);
+          inv = safe_inv(d);
+          trav_init(T);
+          leaf = kEmptyRef;
+        } else {
+          item = n;
+        }
+      }
+    }
+    if (__all_sync(~0u, item >= n)) break;
+    for (int step = 0; step < kStepBudget; ++step) {
+      bool active = item >= 0 && item < n;
+      bool node_avail = active && T.cur >= 0 && T.cur != kEmptyRef;
+      bool has_leaf = active && leaf != kEmptyRef;
+      // ready = active with a parked leaf (an active lane without a node always has one)
+      unsigned act = __ballot_sync(~0u, active);
+      unsigned rdy = __ballot_sync(~0u, active && (has_leaf || !node_avail));
+      if (rdy != 0 && (rdy == act || __popc(rdy) >= a.leaf_vote)) {
+        if (has_leaf) {
+          trav_leaf(s, o, d, t_lo, leaf, T, tests);
+          leaf = kEmptyRef;
+        }
+      } else if (node_avail) {
+        trav_node(s, o, inv, T, sstack, kTraceThreads, lstack, err, visits);
+      }
+      if (active) {
+        while (true) {                 // park a leaf, pop until a node is current
+          if (T.cur == kEmptyRef) {
+            if (T.sp == 0 || err) break;
+            --T.sp;
+            T.cur = T.sp < kStackShared ? sstack[T.sp * kTraceThreads] : lstack[T.sp - kStackShared];
+          }
+          if (T.cur < 0 && leaf == kEmptyRef) {
+            leaf = T.cur;
+            T.cur = kEmptyRef;
+            continue;
+          }
+          break;
+        }
+        if (T.cur == kEmptyRef && leaf == kEmptyRef && (T.sp == 0 || err)) {
+          __stcs(a.r.hit + off + item, make_float4(__int_as_float(T.best), T.bt, T.bu, T.bv));
+          item = -1;
+        }
+      }
+    }
+  }
+  if (err) a.lvl[LV_STACKERR] = 1;
+  flush_counters(a.counters, visits, tests);
+}
+
 // Bottom-up radiance: L = tau * (R L_r + T L_t); level 0 writes the pixel.
 __global__ void k_gather(FwdLaunch a, int k) {
   if (a.lvl[LV_OVERFLOW]) return;
@@ -613,9 +696,14 @@ cudaError_t launch_shade_level(const FwdLaunch& a, int level, int max_depth, int
 }
 
 cudaError_t launch_traverse_level(const FwdLaunch& a, int level, int sm_count, cudaStream_t st) {
-  static int gl = 0;
-  if (!gl) gl = persistent_blocks((const void*)k_traverse_level, kTraceThreads, sm_count);
-  k_traverse_level<<<gl, kTraceThreads, 0, st>>>(a, level);
+  static int gl = 0, gw = 0;
+  if (a.trav_mode == 3) {
+    if (!gw) gw = persistent_blocks((const void*)k_traverse_level_ws, kTraceThreads, sm_count);
+    k_traverse_level_ws<<<gw, kTraceThreads, 0, st>>>(a, level);
+  } else {
+    if (!gl) gl = persistent_blocks((const void*)k_traverse_level, kTraceThreads, sm_count);
+    k_traverse_level<<<gl, kTraceThreads, 0, st>>>(a, level);
+  }
   return cudaGetLastError();
 }
 
