@@ -208,17 +208,18 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
 
   // absorption snapshot (the backward differentiates w.r.t. these values)
   size_t slen = ab->kind == DT_ABS_CONST ? 3 : (size_t)ab->res * ab->res * ab->res * 3;
-  if (slen > c->sigma_cap) {
+  size_t nodes = slen / 3;
+  if (nodes > c->sigma_cap) {
     if (c->sigma_snap) cudaFree(c->sigma_snap);
     if (c->gsig) cudaFree(c->gsig);
     c->sigma_snap = c->gsig = nullptr;
     c->sigma_cap = 0;
-    DT_CU(cudaMalloc(&c->sigma_snap, slen * sizeof(float)));
-    DT_CU(cudaMalloc(&c->gsig, slen * sizeof(float)));
-    c->sigma_cap = slen;
+    DT_CU(cudaMalloc(&c->sigma_snap, nodes * sizeof(float4)));
+    DT_CU(cudaMalloc(&c->gsig, nodes * sizeof(float4)));
+    c->sigma_cap = nodes;
   }
   c->sigma_len = slen;
-  DT_CU(cudaMemcpyAsync(c->sigma_snap, ab->sigma, slen * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  DT_CU(launch_pack_sigma(ab->sigma, c->sigma_snap, (int64_t)nodes, st));   // [n][3] -> float4 [n]
 
   DevScene s = scene_from_ctx(c);
   s.ior = ior;
@@ -306,9 +307,19 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
     DT_CU(cudaMemcpyAsync(c->host_lvl, c->lvl, LV_INTS * sizeof(int), cudaMemcpyDeviceToHost, st));
     DT_CU(cudaStreamSynchronize(st));
     if (!c->host_lvl[LV_OVERFLOW]) break;
-    int64_t need = 0;
-    for (int k = 0; k <= D; ++k) need += (unsigned)c->host_lvl[LV_CNT + k];
-    int64_t next = std::max<int64_t>(2 * c->arena_cap, need + need / 4 + 1024);
+    // levels up to the overflowing one have exact (attempted) counts; later levels were not
+    // run, so extrapolate them with the last known level size
+    int64_t need = 0, last = 0;
+    int known = 0;
+    for (int k = 0; k <= D; ++k) {
+      int64_t v = (unsigned)c->host_lvl[LV_CNT + k];
+      if (v == 0 && k > 0) break;
+      need += v;
+      last = v;
+      known = k;
+    }
+    need += last * (D - known);
+    int64_t next = std::max<int64_t>(c->arena_cap + c->arena_cap / 4, need + need / 8 + 65536);
     limit = arena_limit() + c->arena_cap;
     if (c->arena_cap >= limit || ++retries > 8)
       return fail(c, DT_ERR_OOM, "dt_trace_forward: record arena needs > %lld records (HBM budget %lld)",
@@ -358,7 +369,7 @@ dt_status dt_trace_backward(dt_ctx* c, const float* grad_rgb, float* grad_V, flo
   cudaStream_t st = (cudaStream_t)stream;
   DT_CU(cudaMemsetAsync(c->gV, 0, (size_t)c->nv * 16, st));
   DT_CU(cudaMemsetAsync(c->gN, 0, (size_t)c->nv * 16, st));
-  DT_CU(cudaMemsetAsync(c->gsig, 0, c->sigma_len * sizeof(float), st));
+  DT_CU(cudaMemsetAsync(c->gsig, 0, (c->sigma_len / 3) * sizeof(float4), st));
   DT_CU(cudaMemsetAsync(c->gior, 0, sizeof(float), st));
   BwdLaunch b{};
   b.s = c->fwd_scene;

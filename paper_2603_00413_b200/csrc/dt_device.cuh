@@ -37,7 +37,7 @@ struct DevScene {
   // material
   float ior;
   int abs_kind;
-  const float* sigma;
+  const float4* sigma;  // internal copy: [1] (constant) or [R^3] nodes, rgb + pad
   int sres, nsamp;
   float3 slo, shi;
   // environment
@@ -455,8 +455,7 @@ DT_D float3 sigma_at(const DevScene& s, float3 p) {
   for (int k = 0; k < 8; ++k) {
     int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
     float w = (dx ? f[0] : 1 - f[0]) * (dy ? f[1] : 1 - f[1]) * (dz ? f[2] : 1 - f[2]);
-    const float* t = s.sigma + (((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx)) * 3;
-    out += f3(__ldg(t), __ldg(t + 1), __ldg(t + 2)) * w;
+    out += f3(__ldg(s.sigma + ((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx))) * w;
   }
   return out;
 }
@@ -467,7 +466,7 @@ DT_D float3 transmittance(const DevScene& s, float3 o, float3 x) {
   float l = length(dx);
   float3 S;
   if (s.abs_kind == 0) {
-    S = f3(__ldg(s.sigma), __ldg(s.sigma + 1), __ldg(s.sigma + 2)) * l;
+    S = f3(__ldg(s.sigma)) * l;
   } else {
     int N = s.nsamp;
     S = f3(0, 0, 0);
@@ -477,39 +476,54 @@ DT_D float3 transmittance(const DevScene& s, float3 o, float3 x) {
   return f3(expf(-S.x), expf(-S.y), expf(-S.z));
 }
 
-// reverse of transmittance given gS = dL/d(optical depth); gsig: device dsigma buffer
-// (const: partial sums returned in gsc[3]; grid: atomics).
-DT_D void transmittance_backward(const DevScene& s, float3 o, float3 x, float3 gS, float3& gx, float3& go, float* gsig,
-                                 float3& gsc) {
+// Reverse of transmittance given gS = dL/d(optical depth).  Constant sigma: partial sums in
+// gsc.  Grid: trilinear scatter into gsig (float4 per node); consecutive samples that fall
+// in the same cell are merged first, so each cell visit costs 8 vector atomics.
+DT_D void transmittance_backward(const DevScene& s, float3 o, float3 x, float3 gS, float3& gx, float3& go,
+                                 float4* gsig, float3& gsc) {
   float3 dx = x - o;
   float l = length(dx);
   float gl = 0.0f;
   if (s.abs_kind == 0) {
     gsc += gS * l;
-    gl = dot(gS, f3(__ldg(s.sigma), __ldg(s.sigma + 1), __ldg(s.sigma + 2)));
+    gl = dot(gS, f3(__ldg(s.sigma)));
   } else {
     int N = s.nsamp, R = s.sres;
     float sc = l / (float)N;
     float3 gSs = gS * sc;
-    for (int j = 0; j < N; ++j) {
-      float w = ((float)j + 0.5f) / (float)N;
-      float3 p = o + dx * w;
+    float acc[8];                      // per-corner weight sums of the current cell run
+    size_t run_base = ~(size_t)0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+    for (int j = 0; j <= N; ++j) {
       int i0[3];
       float f[3], scl[3];
-      if (!sigma_cell(s, p, i0, f, scl)) continue;
+      bool inside = false;
+      float w = ((float)j + 0.5f) / (float)N;
+      float3 p = o + dx * w;
+      if (j < N) inside = sigma_cell(s, p, i0, f, scl);
+      size_t base = inside ? ((size_t)i0[2] * R + i0[1]) * R + i0[0] : ~(size_t)0;
+      if (base != run_base) {          // flush the finished run
+        if (run_base != ~(size_t)0) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            size_t node = run_base + ((size_t)(k >> 2) * R + ((k >> 1) & 1)) * R + (k & 1);
+            atomicAdd(gsig + node, make_float4(gSs.x * acc[k], gSs.y * acc[k], gSs.z * acc[k], 0.f));
+            acc[k] = 0.f;
+          }
+        }
+        run_base = base;
+      }
+      if (!inside) continue;
       float3 gp = f3(0, 0, 0), val = f3(0, 0, 0);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         int ix = k & 1, iy = (k >> 1) & 1, iz = k >> 2;
         float wx = ix ? f[0] : 1 - f[0], wy = iy ? f[1] : 1 - f[1], wz = iz ? f[2] : 1 - f[2];
         float ww = wx * wy * wz;
-        size_t node = ((size_t)(i0[2] + iz) * R + (i0[1] + iy)) * R + (i0[0] + ix);
-        const float* t = s.sigma + node * 3;
-        float3 sv = f3(__ldg(t), __ldg(t + 1), __ldg(t + 2));
+        float3 sv = f3(__ldg(s.sigma + base + ((size_t)iz * R + iy) * R + ix));
         val += sv * ww;
-        atomicAdd(gsig + node * 3 + 0, gSs.x * ww);
-        atomicAdd(gsig + node * 3 + 1, gSs.y * ww);
-        atomicAdd(gsig + node * 3 + 2, gSs.z * ww);
+        acc[k] += ww;
         float sd = dot(gSs, sv);
         gp += f3((ix ? 1.f : -1.f) * wy * wz * scl[0], wx * (iy ? 1.f : -1.f) * wz * scl[1],
                  wx * wy * (iz ? 1.f : -1.f) * scl[2]) * sd;

@@ -70,7 +70,7 @@ struct BwdLaunch {
   const float* grad_rgb;
   float4* dV;       // [nv] vertex-position adjoints (atomics)
   float4* dN;       // [nv] vertex-normal adjoints (atomics)
-  float* dsig;      // [3] or [R^3*3]
+  float4* dsig;     // [1] or [R^3] (rgb + pad)
   float* dior;      // [1]
 };
 
@@ -121,15 +121,15 @@ struct dt_ctx {
   int64_t n_rays = 0;
   dt::DevScene fwd_scene{};
   float fwd_t_eps = 1e-4f;
-  float* sigma_snap = nullptr;
-  size_t sigma_cap = 0, sigma_len = 0;
+  float4* sigma_snap = nullptr;  // [1] or [R^3] nodes (rgb + pad)
+  size_t sigma_cap = 0, sigma_len = 0;   // sigma_len = caller floats (3 or 3 R^3)
   // gradients
   float4* gV = nullptr;       // [nv]
   float4* gN = nullptr;       // [nv]
   float4* gVn = nullptr;      // [nv]  vertex-normal chain, gathered per vertex
   float4* gS = nullptr;       // [nv]  d/d(sum of face normals)
   float4* fe = nullptr;       // [2nf] per-face d/de1, d/de2
-  float* gsig = nullptr;
+  float4* gsig = nullptr;     // [1] or [R^3]: d/dsigma (rgb + pad)
   float* gior = nullptr;
   size_t gsig_cap = 0;
   // tuning knobs (env DT_LEAF_MAX, DT_TRAV_MODE, DT_TRAV_CHUNK at dt_create)
@@ -175,5 +175,6 @@ cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64
                                      float* tuv, int* err_flag, cudaStream_t st);
 cudaError_t launch_bvh_check(dt_ctx* c, long long* out_dev, cudaStream_t st);
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
+cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, cudaStream_t st);
 DevScene scene_from_ctx(const dt_ctx* c);
 }  // namespace dt

@@ -563,9 +563,7 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
   if (lane_id() == 0) {
     if (gior != 0.0f) atomicAdd(a.dior, gior);
     if (s.abs_kind == 0 && (gsc.x != 0.0f || gsc.y != 0.0f || gsc.z != 0.0f)) {
-      atomicAdd(a.dsig, gsc.x);
-      atomicAdd(a.dsig + 1, gsc.y);
-      atomicAdd(a.dsig + 2, gsc.z);
+      atomicAdd(a.dsig, make_float4(gsc.x, gsc.y, gsc.z, 0.f));
     }
   }
 }
@@ -616,6 +614,19 @@ __global__ void k_finalize(const float4* __restrict__ gV, const float4* __restri
     float3 g = f3(gV[v]) + f3(gVn[v]);
     if (acc) { out[3 * v] += g.x; out[3 * v + 1] += g.y; out[3 * v + 2] += g.z; }
     else { out[3 * v] = g.x; out[3 * v + 1] = g.y; out[3 * v + 2] = g.z; }
+  }
+}
+
+__global__ void k_pack_sigma(const float* __restrict__ in, float4* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = make_float4(in[3 * i], in[3 * i + 1], in[3 * i + 2], 0.f);
+}
+
+__global__ void k_unpack_add(const float4* __restrict__ src, float* __restrict__ dst, int64_t n, int acc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 g = src[i];
+    if (acc) { dst[3 * i] += g.x; dst[3 * i + 1] += g.y; dst[3 * i + 2] += g.z; }
+    else { dst[3 * i] = g.x; dst[3 * i + 1] = g.y; dst[3 * i + 2] = g.z; }
   }
 }
 
@@ -733,9 +744,9 @@ cudaError_t launch_finalize(dt_ctx* c, float* grad_V, float* grad_ior, float* gr
   if (grad_V) k_finalize<<<gv, 256, 0, st>>>(c->gV, c->gVn, c->nv, grad_V, accumulate);
   if (grad_ior) k_copy_add<<<1, 32, 0, st>>>(c->gior, grad_ior, 1, accumulate);
   if (grad_sigma) {
-    int64_t n = (int64_t)c->sigma_len;
-    k_copy_add<<<(int)std::min<int64_t>((n + 255) / 256, c->sm_count * 8), 256, 0, st>>>(c->gsig, grad_sigma, n,
-                                                                                         accumulate);
+    int64_t n = (int64_t)c->sigma_len / 3;
+    k_unpack_add<<<(int)std::min<int64_t>((n + 255) / 256, c->sm_count * 8), 256, 0, st>>>(c->gsig, grad_sigma, n,
+                                                                                           accumulate);
   }
   return cudaGetLastError();
 }
@@ -751,6 +762,12 @@ cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64
                                      float* tuv, int* err_flag, cudaStream_t st) {
   int g = (int)std::min<int64_t>((n + kTraceThreads - 1) / kTraceThreads, 148 * 32);
   k_debug_hit<<<std::max(g, 1), kTraceThreads, 0, st>>>(s, rays, n, t_lo, brute, face, tuv, err_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, cudaStream_t st) {
+  int g = (int)std::min<int64_t>((nodes + 255) / 256, 148 * 16);
+  k_pack_sigma<<<std::max(g, 1), 256, 0, st>>>(in, out, nodes);
   return cudaGetLastError();
 }
 
