@@ -44,7 +44,10 @@ typedef enum {
   DT_ERR_NOT_BUILT = 5,      /* dt_trace_forward before dt_build_bvh                          */
   DT_ERR_NO_FORWARD = 6,     /* dt_trace_backward without a preceding dt_trace_forward        */
   DT_ERR_NONFINITE = 7,      /* opts.check_finite and a NaN/Inf output; message names it     */
-  DT_ERR_STACK = 8           /* BVH deeper than the traversal stack (never for LBVH < 2^30)   */
+  DT_ERR_STACK = 8,          /* BVH deeper than the traversal stack (never for LBVH < 2^30)   */
+  DT_ERR_RETRY = 9           /* an asynchronous forward (opts.async) overflowed the record
+                                arena: its outputs and the backward that followed it are
+                                invalid (zero); the arena has been grown -- re-run that step  */
 } dt_status;
 
 enum { DT_ABS_CONST = 0, DT_ABS_GRID = 1 };
@@ -111,6 +114,12 @@ typedef struct {
   int32_t cap_policy;
   float t_eps;
   int32_t check_finite;      /* nonzero: verify rgb is finite (extra pass + sync)  */
+  int32_t async;             /* nonzero: do not synchronise at the end of the forward.  The
+                                arena is sized from the previous forward's measured need (+25%
+                                headroom); its overflow check is deferred to the next
+                                dt_trace_forward / dt_get_stats, which then returns
+                                DT_ERR_RETRY.  Ignored (synchronous) when stats or
+                                check_finite are requested or no previous need is known.   */
 } dt_trace_opts;
 
 /* Host-side statistics filled by dt_trace_forward when requested. */
@@ -183,7 +192,11 @@ typedef struct {
   int64_t tri_tests;               /* ray-triangle tests by the trace kernels                */
   int64_t node_visits_primary;     /* the part of node_visits made by camera rays (depth 0)  */
   int64_t tri_tests_primary;       /* the part of tri_tests made by camera rays (depth 0)    */
+  int64_t segments;                /* traced segments of all forwards since the reset        */
 } dt_profile;
+/* Statistics of the last forward (waits for it if it ran with opts.async).  Returns
+ * DT_ERR_RETRY if that asynchronous forward overflowed the arena. */
+DT_API dt_status dt_get_stats(dt_ctx* ctx, dt_stats* out);
 DT_API dt_status dt_set_profiling(dt_ctx* ctx, int32_t enable);
 DT_API dt_status dt_get_profile(dt_ctx* ctx, dt_profile* out, int32_t reset);
 

@@ -13,7 +13,9 @@ LIB_PATH = os.path.join(HERE, "libdifftrans.so")
 
 DT_OK = 0
 STATUS = {0: "DT_OK", 1: "DT_ERR_INVALID_ARG", 2: "DT_ERR_EMPTY_GEOMETRY", 3: "DT_ERR_CUDA", 4: "DT_ERR_OOM",
-          5: "DT_ERR_NOT_BUILT", 6: "DT_ERR_NO_FORWARD", 7: "DT_ERR_NONFINITE", 8: "DT_ERR_STACK"}
+          5: "DT_ERR_NOT_BUILT", 6: "DT_ERR_NO_FORWARD", 7: "DT_ERR_NONFINITE", 8: "DT_ERR_STACK",
+          9: "DT_ERR_RETRY"}
+DT_ERR_RETRY = 9
 DT_MAX_DEPTH = 15
 
 
@@ -35,7 +37,7 @@ class Cameras(C.Structure):
 
 class TraceOpts(C.Structure):
     _fields_ = [("max_depth", C.c_int32), ("cap_policy", C.c_int32), ("t_eps", C.c_float),
-                ("check_finite", C.c_int32)]
+                ("check_finite", C.c_int32), ("async_", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -56,19 +58,20 @@ PHASES = ["build", "trace0", "shade", "trace", "gather", "bwd", "normals_bwd", "
 class Profile(C.Structure):
     _fields_ = [("ms", C.c_double * len(PHASES)), ("launches", C.c_int64 * len(PHASES)),
                 ("kernel_launches", C.c_int64), ("node_visits", C.c_int64), ("tri_tests", C.c_int64),
-                ("node_visits_primary", C.c_int64), ("tri_tests_primary", C.c_int64)]
+                ("node_visits_primary", C.c_int64), ("tri_tests_primary", C.c_int64), ("segments", C.c_int64)]
 
     def as_dict(self):
         return dict(ms={p: float(self.ms[i]) for i, p in enumerate(PHASES)},
                     launches={p: int(self.launches[i]) for i, p in enumerate(PHASES)},
                     kernel_launches=int(self.kernel_launches), node_visits=int(self.node_visits),
                     tri_tests=int(self.tri_tests), node_visits_primary=int(self.node_visits_primary),
-                    tri_tests_primary=int(self.tri_tests_primary))
+                    tri_tests_primary=int(self.tri_tests_primary), segments=int(self.segments))
 
 
 _P = C.c_void_p
 SIGNATURES = {
     "dt_set_profiling": (C.c_int, [_P, C.c_int32]),
+    "dt_get_stats": (C.c_int, [_P, C.POINTER(Stats)]),
     "dt_get_profile": (C.c_int, [_P, C.POINTER(Profile), C.c_int32]),
     "dt_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     "dt_destroy": (None, [_P]),

@@ -74,18 +74,75 @@ cudaEvent_t get_event(dt_ctx* c) {
 }
 
 // Fold completed phase timings into the totals (waits on the pending events).
-void resolve_profile(dt_ctx* c) {
-  for (auto& p : c->pending) {
+// block = false: only fold the events that have already completed (never stalls the host
+// behind queued GPU work, so an asynchronous step loop keeps the GPU fed).
+void resolve_profile(dt_ctx* c, bool block = true) {
+  size_t i = 0;
+  for (; i < c->pending.size(); ++i) {
+    auto& p = c->pending[i];
+    if (block) cudaEventSynchronize(p.b);
+    else if (cudaEventQuery(p.b) != cudaSuccess) break;
     float ms = 0.f;
-    cudaEventSynchronize(p.b);
     if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) c->ph_ms[p.ph] += ms;
     c->event_pool.push_back(p.a);
     c->event_pool.push_back(p.b);
   }
-  c->pending.clear();
+  c->pending.erase(c->pending.begin(), c->pending.begin() + i);
+}
+
+// Records needed by a forward with level counts `lvl` (attempted appends; levels after an
+// overflow were not run and are extrapolated with the last known level size).
+int64_t level_need(const int* lvl, int D) {
+  int64_t need = 0, last = 0;
+  int known = 0;
+  for (int k = 0; k <= D; ++k) {
+    int64_t v = (unsigned)lvl[LV_CNT + k];
+    if (v == 0 && k > 0) break;
+    need += v;
+    last = v;
+    known = k;
+  }
+  return need + last * (D - known);
+}
+
+void fill_stats(dt_ctx* c, dt_stats* st) {
+  memset(st, 0, sizeof(*st));
+  const int* h = c->host_lvl;
+  int64_t seg = h[LV_TRACED];
+  for (int k = 0; k <= c->last_D; ++k) {
+    st->segments_per_depth[k] = h[LV_CNT + k];
+    if (k > 0) seg += h[LV_CNT + k];
+  }
+  st->primaries = c->last_rays;
+  st->primaries_traced = h[LV_TRACED];
+  st->segments = seg;
+  st->arena_capacity = c->arena_cap;
+  st->arena_retries = c->last_retries;
 }
 
 }  // namespace
+
+// Check a pending asynchronous forward: wait for its readback, record its need, and report
+// an overflow (growing the arena for the next step).
+dt_status consume_async(dt_ctx* c) {
+  if (!c->async_pending) return DT_OK;
+  c->async_pending = false;
+  cudaError_t e = cudaEventSynchronize(c->fwd_done);
+  if (e != cudaSuccess) return fail(c, DT_ERR_CUDA, "async forward: %s", cudaGetErrorString(e));
+  if (c->prof) resolve_profile(c, false);
+  int64_t need = level_need(c->host_lvl, c->last_D);
+  c->last_need = need;
+  if (c->host_lvl[LV_STACKERR]) return fail(c, DT_ERR_STACK, "async forward: BVH deeper than the traversal stack");
+  if (c->host_lvl[LV_OVERFLOW]) {
+    int64_t next = std::min<int64_t>(need + need / 2 + 65536, arena_limit() + c->arena_cap);
+    if (next > c->arena_cap && alloc_arena(c, next) != cudaSuccess)
+      return fail(c, DT_ERR_OOM, "async forward overflowed and the arena could not grow to %lld", (long long)next);
+    c->have_fwd = false;
+    return fail(c, DT_ERR_RETRY, "the previous asynchronous forward overflowed the record arena (need %lld); "
+                "re-run that step", (long long)need);
+  }
+  return DT_OK;
+}
 
 PhaseTimer::PhaseTimer(dt_ctx* c_, int ph_, cudaStream_t st_) : c(c_), ph(ph_), st(st_) {
   if (c->prof) {
@@ -117,6 +174,7 @@ const char* dt_status_string(dt_status s) {
     case DT_ERR_NO_FORWARD: return "DT_ERR_NO_FORWARD";
     case DT_ERR_NONFINITE: return "DT_ERR_NONFINITE";
     case DT_ERR_STACK: return "DT_ERR_STACK";
+    case DT_ERR_RETRY: return "DT_ERR_RETRY";
   }
   return "DT_ERR_UNKNOWN";
 }
@@ -138,8 +196,9 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   if (const char* v = getenv("DT_TRAV_CHUNK")) c->trav_chunk = std::max(32, atoi(v));
   cudaError_t e;
   if ((e = cudaMalloc(&c->lvl, LV_INTS * sizeof(int))) || (e = cudaMallocHost(&c->host_lvl, LV_INTS * sizeof(int))) ||
-      (e = cudaMalloc(&c->gior, 4 * sizeof(float))) || (e = cudaMalloc(&c->counters, 4 * sizeof(unsigned long long))) ||
-      (e = cudaMemset(c->counters, 0, 4 * sizeof(unsigned long long)))) {
+      (e = cudaMalloc(&c->gior, 4 * sizeof(float))) || (e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long))) ||
+      (e = cudaMemset(c->counters, 0, 8 * sizeof(unsigned long long))) ||
+      (e = cudaEventCreateWithFlags(&c->fwd_done, cudaEventDisableTiming))) {
     dt_destroy(c);
     return DT_ERR_CUDA;
   }
@@ -159,6 +218,7 @@ void dt_destroy(dt_ctx* c) {
   for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->host_lvl) cudaFreeHost(c->host_lvl);
+  if (c->fwd_done) cudaEventDestroy(c->fwd_done);
   delete c;
 }
 
@@ -264,10 +324,21 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.trav_chunk = c->trav_chunk;
   a.leaf_vote = c->leaf_vote;
 
-  int64_t limit = arena_limit() + c->arena_cap;
+  // a previous asynchronous forward is checked first (its readback has long completed)
+  dt_status prev = consume_async(c);
+  if (prev != DT_OK) return prev;
+  int64_t limit = 0;   // HBM budget, queried (cudaMemGetInfo) only when the arena must grow
   if (c->arena_cap == 0) {
+    limit = arena_limit();
     int64_t want = std::min<int64_t>(std::max<int64_t>(n_rays * 3, 1 << 16), limit);
     DT_CU(alloc_arena(c, want));
+  }
+  bool async = opts->async && !stats && !opts->check_finite && c->last_need > 0 && c->last_rays == n_rays;
+  if (async && c->arena_cap < c->last_need + c->last_need / 4) {   // keep 25% headroom
+    limit = arena_limit() + c->arena_cap;
+    int64_t next = std::min<int64_t>(c->last_need + c->last_need / 2 + 65536, limit);
+    if (next > c->arena_cap) DT_CU(alloc_arena(c, next));
+    async = c->arena_cap >= c->last_need + c->last_need / 4;
   }
   int retries = 0;
   while (true) {
@@ -304,32 +375,34 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
         p.end(1);
       }
     }
+    DT_CU(launch_count_segments(c->lvl, D, c->counters + 4, st));
+    c->kernel_launches += 1;
     DT_CU(cudaMemcpyAsync(c->host_lvl, c->lvl, LV_INTS * sizeof(int), cudaMemcpyDeviceToHost, st));
+    c->last_D = D;
+    c->last_rays = n_rays;
+    c->last_retries = retries;
+    if (async) {
+      DT_CU(cudaEventRecord(c->fwd_done, st));
+      c->async_pending = true;
+      break;
+    }
     DT_CU(cudaStreamSynchronize(st));
     if (!c->host_lvl[LV_OVERFLOW]) break;
-    // levels up to the overflowing one have exact (attempted) counts; later levels were not
-    // run, so extrapolate them with the last known level size
-    int64_t need = 0, last = 0;
-    int known = 0;
-    for (int k = 0; k <= D; ++k) {
-      int64_t v = (unsigned)c->host_lvl[LV_CNT + k];
-      if (v == 0 && k > 0) break;
-      need += v;
-      last = v;
-      known = k;
-    }
-    need += last * (D - known);
+    int64_t need = level_need(c->host_lvl, D);
     int64_t next = std::max<int64_t>(c->arena_cap + c->arena_cap / 4, need + need / 8 + 65536);
     limit = arena_limit() + c->arena_cap;
     if (c->arena_cap >= limit || ++retries > 8)
       return fail(c, DT_ERR_OOM, "dt_trace_forward: record arena needs > %lld records (HBM budget %lld)",
                   (long long)next, (long long)limit);
     next = std::min(next, limit);
-    cudaFree(c->rec.o);
-    c->rec = Records{};
-    c->arena_cap = 0;
     DT_CU(alloc_arena(c, next));
   }
+  c->have_fwd = true;
+  c->n_rays = n_rays;
+  c->fwd_scene = s;
+  c->fwd_t_eps = opts->t_eps;
+  if (async) return DT_OK;
+  c->last_need = level_need(c->host_lvl, D);
   if (c->prof) resolve_profile(c);   // all recorded events are complete after the sync
   if (c->host_lvl[LV_STACKERR]) return fail(c, DT_ERR_STACK, "dt_trace_forward: BVH deeper than the traversal stack");
   if (opts->check_finite && n_rays > 0) {
@@ -340,24 +413,18 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
     DT_CU(cudaStreamSynchronize(st));
     if (flag) return fail(c, DT_ERR_NONFINITE, "dt_trace_forward: rgb has non-finite values");
   }
-  if (stats) {
-    memset(stats, 0, sizeof(*stats));
-    int64_t seg = c->host_lvl[LV_TRACED];
-    for (int k = 0; k <= D; ++k) {
-      stats->segments_per_depth[k] = c->host_lvl[LV_CNT + k];
-      if (k > 0) seg += c->host_lvl[LV_CNT + k];
-    }
-    stats->primaries = n_rays;
-    stats->primaries_traced = c->host_lvl[LV_TRACED];
-    stats->segments = seg;
-    stats->arena_capacity = c->arena_cap;
-    stats->arena_retries = retries;
-  }
-  c->have_fwd = true;
-  c->n_rays = n_rays;
-  c->fwd_scene = s;
-  c->fwd_t_eps = opts->t_eps;
+  if (stats) fill_stats(c, stats);
   return DT_OK;
+}
+
+dt_status dt_get_stats(dt_ctx* c, dt_stats* out) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  DT_ARG(out, "dt_get_stats: out is NULL");
+  if (!c->have_fwd) return fail(c, DT_ERR_NO_FORWARD, "dt_get_stats: no forward on this context");
+  dt_status prev = consume_async(c);
+  fill_stats(c, out);
+  return prev;
 }
 
 dt_status dt_trace_backward(dt_ctx* c, const float* grad_rgb, float* grad_V, float* grad_ior, float* grad_sigma,
@@ -365,6 +432,8 @@ dt_status dt_trace_backward(dt_ctx* c, const float* grad_rgb, float* grad_V, flo
   if (!c) return DT_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
   if (!c->have_fwd) return fail(c, DT_ERR_NO_FORWARD, "dt_trace_backward: no forward on this context");
+  // an asynchronous forward is not waited for: the backward kernels skip an overflowed arena
+  // on the device, and the overflow is reported by the next forward / dt_get_stats
   DT_ARG(grad_rgb || c->n_rays == 0, "dt_trace_backward: grad_rgb is NULL");
   cudaStream_t st = (cudaStream_t)stream;
   DT_CU(cudaMemsetAsync(c->gV, 0, (size_t)c->nv * 16, st));
@@ -408,7 +477,7 @@ dt_status dt_get_profile(dt_ctx* c, dt_profile* out, int32_t reset) {
   cudaSetDevice(c->device);
   DT_ARG(out, "dt_get_profile: out is NULL");
   resolve_profile(c);
-  unsigned long long cnt[4] = {0, 0, 0, 0};
+  unsigned long long cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   DT_CU(cudaMemcpy(cnt, c->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
   for (int i = 0; i < DT_PH_COUNT; ++i) {
     out->ms[i] = c->ph_ms[i];
@@ -419,6 +488,7 @@ dt_status dt_get_profile(dt_ctx* c, dt_profile* out, int32_t reset) {
   out->tri_tests = (int64_t)(cnt[1] + cnt[3]);
   out->node_visits_primary = (int64_t)cnt[2];
   out->tri_tests_primary = (int64_t)cnt[3];
+  out->segments = (int64_t)cnt[4];
   if (reset) {
     for (int i = 0; i < DT_PH_COUNT; ++i) { c->ph_ms[i] = 0.0; c->ph_launches[i] = 0; }
     c->kernel_launches = 0;

@@ -142,7 +142,13 @@ struct dt_ctx {
   double ph_ms[DT_PH_COUNT] = {};
   long long ph_launches[DT_PH_COUNT] = {};
   long long kernel_launches = 0;
-  unsigned long long* counters = nullptr;       // device [2]: node visits, triangle tests
+  unsigned long long* counters = nullptr;       // device [8]: visits, tests (secondary), visits, tests
+                                                //   (camera rays), segments
+  // last forward's wavefront readback (host_lvl) and the asynchronous-forward state
+  int last_D = 0, last_retries = 0;
+  int64_t last_rays = 0, last_need = 0;
+  bool async_pending = false;
+  cudaEvent_t fwd_done = nullptr;
   struct Pending { int ph; cudaEvent_t a, b; };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
@@ -177,4 +183,6 @@ cudaError_t launch_bvh_check(dt_ctx* c, long long* out_dev, cudaStream_t st);
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, cudaStream_t st);
 DevScene scene_from_ctx(const dt_ctx* c);
+cudaError_t launch_count_segments(const int* lvl, int max_depth, unsigned long long* seg, cudaStream_t st);
 }  // namespace dt
+dt_status consume_async(dt_ctx* c);

@@ -476,6 +476,7 @@ DT_D void atomic_add3(float4* p, float3 v) {
 
 __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, int64_t cap) {
   const DevScene& s = a.s;
+  if (a.lvl[LV_OVERFLOW]) return;   // an overflowed (asynchronous) forward: nothing valid to replay
   int n = a.lvl[LV_CNT + k];
   float gior = 0.0f;
   float3 gsc = f3(0, 0, 0);
@@ -649,6 +650,13 @@ __global__ void k_loss_color(const float* __restrict__ rgb, const float* __restr
   if (lane_id() == 0) atomicAdd(loss, acc * inv_b);
 }
 
+__global__ void k_count_segments(const int* __restrict__ lvl, int D, unsigned long long* __restrict__ seg) {
+  if (lvl[LV_OVERFLOW]) return;
+  unsigned long long s = (unsigned)lvl[LV_TRACED];
+  for (int k = 1; k <= D; ++k) s += (unsigned)lvl[LV_CNT + k];
+  *seg += s;
+}
+
 __global__ void k_check_finite(const float* __restrict__ x, int64_t n, int* flag) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (!isfinite(x[i])) *flag = 1;
@@ -768,6 +776,11 @@ cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64
 cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, cudaStream_t st) {
   int g = (int)std::min<int64_t>((nodes + 255) / 256, 148 * 16);
   k_pack_sigma<<<std::max(g, 1), 256, 0, st>>>(in, out, nodes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_segments(const int* lvl, int max_depth, unsigned long long* seg, cudaStream_t st) {
+  k_count_segments<<<1, 1, 0, st>>>(lvl, max_depth, seg);
   return cudaGetLastError();
 }
 

@@ -144,7 +144,9 @@ class Tracer:
     def trace_forward(self, ds: DeviceScene, pixel_ids: Optional[torch.Tensor] = None, ior: Optional[float] = None,
                       max_depth: Optional[int] = None, cap_policy: Optional[int] = None, want_capped=False,
                       want_sig=False, stats=False, check_finite=False, rgb: Optional[torch.Tensor] = None,
-                      stream=None) -> ForwardOut:
+                      async_: bool = False, stream=None) -> ForwardOut:
+        """async_: no end-of-call synchronisation (see dt_trace_opts.async); an arena overflow
+        of this call is reported by the next call as DiffTransError('DT_ERR_RETRY ...')."""
         cams = ds.cameras(pixel_ids)
         n = cams.n_rays
         dev = self.device
@@ -158,6 +160,7 @@ class Tracer:
         opts.cap_policy = ds.cap_policy if cap_policy is None else cap_policy
         opts.t_eps = ds.t_eps
         opts.check_finite = int(check_finite)
+        opts.async_ = int(async_)
         ds.absorption.sigma = _ptr(ds.sigma)
         st_out = N.Stats() if stats else None
         rc = self._lib.dt_trace_forward(self.h, float(ds.ior if ior is None else ior), C.byref(ds.absorption),
@@ -165,6 +168,7 @@ class Tracer:
                                         _ptr(st), _ptr(sf), C.byref(st_out) if stats else None, _stream(stream))
         self._check(rc, self.h)
         self.n_rays = n
+        self._last_depth = opts.max_depth
         self._sigma_shape = tuple(ds.sigma.shape)
         self._nv = ds.V.shape[0]
         self._keep = [ds]          # env buffers must outlive the backward
@@ -196,6 +200,12 @@ class Tracer:
         self._check(self._lib.dt_loss_color(self.h, _ptr(rgb), _ptr(target), n, _ptr(grad_rgb), _ptr(loss),
                                             _stream(stream)), self.h)
         return loss, grad_rgb
+
+    def get_stats(self) -> dict:
+        st = N.Stats()
+        rc = self._lib.dt_get_stats(self.h, C.byref(st))
+        self._check(rc, self.h)
+        return st.as_dict(self._last_depth)
 
     # ------------------------------------------------------------------ profiling
     def set_profiling(self, enable: bool):
