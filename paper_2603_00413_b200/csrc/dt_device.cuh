@@ -103,6 +103,12 @@ DT_D bool intersect_tri(float3 o, float3 d, float3 v0, float3 e1, float3 e2, flo
 // 64-B 4-wide node (layout in bvh.cu, k_wide_build): child c's box decodes to
 // lo = p + qlo * 2^(e-127), hi = p + qhi * 2^(e-127) (one fma per plane).
 DT_D float exp_scale(unsigned e) { return __uint_as_float(e << 23); }
+// One 256-bit read-only load (sm_100: LDG.E.ENL2.256): a 64-B node is two instructions.
+DT_D void ldg256(const uint4* p, uint4& a, uint4& b) {
+  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p));
+}
 DT_D int wide_ref(uint4 n2, uint4 n3, int c) {
   return (int)(c == 0 ? n2.z : c == 1 ? n2.w : c == 2 ? n3.x : n3.y);
 }
@@ -171,7 +177,9 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
   bool descended = false;
   if (T.cur >= 0) {
     const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)T.cur;
-    uint4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+    uint4 n0, n1, n2, n3;
+    ldg256(nd, n0, n1);
+    ldg256(nd + 2, n2, n3);
     ++visits;
     float k0, k1, k2, k3;
     int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
@@ -244,7 +252,9 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
 DT_D void trav_node(const DevScene& s, float3 o, float3 inv, Trav& T, int* sstack, int stride, int* lstack, int& err,
                     int& visits) {
   const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)T.cur;
-  uint4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+  uint4 n0, n1, n2, n3;
+  ldg256(nd, n0, n1);
+  ldg256(nd + 2, n2, n3);
   ++visits;
   float k0, k1, k2, k3;
   int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;

@@ -278,6 +278,48 @@ def test_forward_deterministic(tracer):
     assert torch.equal(a, b)
 
 
+def test_async_forward_matches_and_reports_overflow(tracer):
+    """opts.async: identical results to the synchronous forward; an arena overflow of an
+    asynchronous forward is reported by the next call as DT_ERR_RETRY, after which the
+    step re-runs correctly."""
+    from paper_2603_00413_b200.tracer import DeviceScene, Tracer
+    from paper_2603_00413_b200._native import DiffTransError
+    tr = Tracer("cuda:0")
+    sc = S.config_c2()
+    ds = DeviceScene(sc, torch.device("cuda:0"))
+    tr.build_bvh(ds.V, ds.F)
+    ref = tr.trace_forward(ds).rgb.clone()
+    g = torch.as_tensor(S.upstream_grad(sc.n_pixels, 3), device="cuda:0")
+    gV_ref = tr.trace_backward(g)[0].clone()
+    for _ in range(2):
+        tr.build_bvh(ds.V, ds.F)
+        out = tr.trace_forward(ds, async_=True)
+        gV = tr.trace_backward(g)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(out.rgb, ref)
+    assert float((gV - gV_ref).norm() / gV_ref.norm()) < 1e-5      # float atomics: ulp-level order noise
+    st = tr.get_stats()
+    assert st["segments"] > 0
+    # shrink the object so the next synchronous forward measures a small need, then trace
+    # the full object asynchronously: the arena (sized from the small need) overflows
+    # (depth 8 makes the full object need more records than the initial 3 per ray)
+    ref8 = tr.trace_forward(ds, max_depth=8).rgb.clone()
+    small = DeviceScene(sc, torch.device("cuda:0"))
+    small.set_vertices(ds.V * 0.05)
+    tr2 = Tracer("cuda:0")
+    tr2.build_bvh(small.V, small.F)
+    tr2.trace_forward(small, max_depth=8)
+    tr2.build_bvh(ds.V, ds.F)
+    tr2.trace_forward(ds, max_depth=8, async_=True)
+    with pytest.raises(DiffTransError, match="RETRY"):
+        tr2.get_stats()
+    tr2.build_bvh(ds.V, ds.F)
+    again = tr2.trace_forward(ds, max_depth=8, async_=True).rgb
+    torch.cuda.synchronize()
+    tr2.get_stats()
+    assert torch.equal(again, ref8)
+
+
 def test_loss_color_kernel(tracer):
     rgb = torch.tensor([[1.1, 1.1, 1.1]], device="cuda:0")
     tgt = torch.ones((1, 3), device="cuda:0")
