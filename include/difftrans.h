@@ -194,6 +194,47 @@ typedef struct {
   int64_t tri_tests_primary;       /* the part of tri_tests made by camera rays (depth 0)    */
   int64_t segments;                /* traced segments of all forwards since the reset        */
 } dt_profile;
+/* ---------------------------------------------------------------------------------------
+ * The optimisation step around the tracer (PAPER P:176-194, P:439-443,
+ * P:511-527).  All device pointers; `loss` outputs are device float arrays, overwritten.
+ * --------------------------------------------------------------------------------------- */
+
+/* Photometric losses of P:177-185 and their gradient w.r.t. the rendered colours, fused:
+ *   L_color = (1/B) sum_i ||(c^_i - c_i) * c_i||^2                         (elementwise *)
+ *   L_tone  = (1/B) sum_i [(1 - cos(c^_i, c_i))^2 - var(c_i)]
+ * B = n; pairs with |c^| or |c| <= 1e-6 are skipped in L_tone (its cosine is undefined);
+ * var is the population variance of the 3 channels (constant w.r.t. c^).  mask (optional,
+ * [n]) multiplies each ray's terms (e.g. to drop rays the caller considers capped).
+ * grad_rgb = lambda_color dL_color/dc^ + lambda_tone dL_tone/dc^  ([n][3], overwritten);
+ * loss[0] = L_color, loss[1] = L_tone (unweighted). */
+DT_API dt_status dt_loss_rt(dt_ctx* ctx, const float* rgb, const float* target, const float* mask, int64_t n,
+                            float lambda_color, float lambda_tone, float* grad_rgb, float* loss, void* stream);
+
+/* Absorption regularisers on n caller-drawn points v_i ([n][3]) with perturbations xi_i:
+ *   L_mat-smooth = (1/n) sum_i sum_c |mu_c(v_i) - mu_c(v_i + xi_i)|
+ *   L_vol        = (1/n) sum_i ||mu(v_i)||^2                              (mean form)
+ * mu is the absorption field of `absorption` (R11: zero outside the grid box; constant
+ * sigma everywhere).  grad_sigma (same layout as absorption.sigma) is ACCUMULATED with
+ * lambda_smooth dL_mat/dsigma + lambda_vol dL_vol/dsigma; loss[0] = L_mat, loss[1] = L_vol.
+ * (|x| has derivative sign(x), 0 at 0.) */
+DT_API dt_status dt_sigma_regularizers(dt_ctx* ctx, const dt_absorption* absorption, const float* points,
+                                       const float* xi, int64_t n, float lambda_smooth, float lambda_vol,
+                                       float* grad_sigma, float* loss, void* stream);
+
+/* Adam (beta = (0.9, 0.999), weight decay 1e-6 added to the gradient as in
+ * torch.optim.Adam) on n parameters, in place: m, v are [n] state buffers (zero at step 1).
+ * uniform != 0: AdamUniform (Nicolet et al., cited at P:186) -- one second-moment statistic
+ * for the whole block, v[0] = beta2 v[0] + (1 - beta2) max_i g_i^2, so every coordinate
+ * keeps its gradient's relative scale (R26).  step = t >= 1 (bias correction). */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;
+  int32_t step;
+  int32_t uniform;
+  float clamp_lo, clamp_hi;  /* projection after the update (e.g. IoR in [1, 3], sigma >= 0) */
+} dt_adam;
+DT_API dt_status dt_adam_step(dt_ctx* ctx, float* param, const float* grad, float* m, float* v, int64_t n,
+                              const dt_adam* cfg, void* stream);
+
 /* Statistics of the last forward (waits for it if it ran with opts.async).  Returns
  * DT_ERR_RETRY if that asynchronous forward overflowed the arena. */
 DT_API dt_status dt_get_stats(dt_ctx* ctx, dt_stats* out);

@@ -52,6 +52,12 @@ class Stats(C.Structure):
                     arena_retries=int(self.arena_retries))
 
 
+class Adam(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("weight_decay", C.c_float), ("step", C.c_int32), ("uniform", C.c_int32), ("clamp_lo", C.c_float),
+                ("clamp_hi", C.c_float)]
+
+
 PHASES = ["build", "trace0", "shade", "trace", "gather", "bwd", "normals_bwd", "loss"]
 
 
@@ -82,6 +88,10 @@ SIGNATURES = {
                                    C.POINTER(TraceOpts), _P, _P, _P, _P, C.POINTER(Stats), _P]),
     "dt_trace_backward": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, _P]),
     "dt_loss_color": (C.c_int, [_P, _P, _P, C.c_int64, _P, _P, _P]),
+    "dt_loss_rt": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_float, C.c_float, _P, _P, _P]),
+    "dt_sigma_regularizers": (C.c_int, [_P, C.POINTER(Absorption), _P, _P, C.c_int64, C.c_float, C.c_float, _P, _P,
+                                        _P]),
+    "dt_adam_step": (C.c_int, [_P, _P, _P, _P, _P, C.c_int64, C.POINTER(Adam), _P]),
     "dt_debug_closest_hit": (C.c_int, [_P, _P, C.c_int64, C.c_float, C.c_int32, _P, _P, _P]),
     "dt_debug_bvh_check": (C.c_int, [_P, C.POINTER(C.c_int64), _P]),
     "dt_debug_vertex_normals": (C.c_int, [_P, _P, _P]),

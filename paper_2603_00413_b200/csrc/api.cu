@@ -198,7 +198,8 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   if ((e = cudaMalloc(&c->lvl, LV_INTS * sizeof(int))) || (e = cudaMallocHost(&c->host_lvl, LV_INTS * sizeof(int))) ||
       (e = cudaMalloc(&c->gior, 4 * sizeof(float))) || (e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long))) ||
       (e = cudaMemset(c->counters, 0, 8 * sizeof(unsigned long long))) ||
-      (e = cudaEventCreateWithFlags(&c->fwd_done, cudaEventDisableTiming))) {
+      (e = cudaEventCreateWithFlags(&c->fwd_done, cudaEventDisableTiming)) ||
+      (e = cudaMalloc(&c->scratch, 16 * sizeof(unsigned)))) {
     dt_destroy(c);
     return DT_ERR_CUDA;
   }
@@ -212,7 +213,7 @@ void dt_destroy(dt_ctx* c) {
   void* ptrs[] = {c->V, c->F, c->nrm, c->fnrm, c->nodes, c->tris, c->keys, c->vals, c->hist, c->children,
                   c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, c->vstart, c->vcorner, c->scal,
                   c->iscal, c->rec.o, c->lvl, c->sigma_snap, c->gV, c->gN, c->gVn, c->gS, c->fe, c->gsig, c->gior,
-                  c->counters, c->ranges, c->bdepth, c->wflag, c->widx, c->wbox, c->wdepth};
+                  c->counters, c->ranges, c->bdepth, c->wflag, c->widx, c->wbox, c->wdepth, c->scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
@@ -506,6 +507,46 @@ dt_status dt_loss_color(dt_ctx* c, const float* rgb, const float* target, int64_
   PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
   DT_CU(launch_loss_color(rgb, target, n, grad_rgb, loss, (cudaStream_t)stream));
   p.end(1);
+  return DT_OK;
+}
+
+dt_status dt_loss_rt(dt_ctx* c, const float* rgb, const float* target, const float* mask, int64_t n, float lambda_color,
+                     float lambda_tone, float* grad_rgb, float* loss, void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  DT_ARG(loss && (n == 0 || (rgb && target && grad_rgb)), "dt_loss_rt: NULL argument");
+  DT_ARG(n >= 0, "dt_loss_rt: n < 0");
+  PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
+  DT_CU(launch_loss_rt(rgb, target, mask, n, lambda_color, lambda_tone, grad_rgb, loss, (cudaStream_t)stream));
+  p.end(n > 0 ? 1 : 0);
+  return DT_OK;
+}
+
+dt_status dt_sigma_regularizers(dt_ctx* c, const dt_absorption* ab, const float* points, const float* xi, int64_t n,
+                                float lambda_smooth, float lambda_vol, float* grad_sigma, float* loss, void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  DT_ARG(ab && ab->sigma && grad_sigma && loss, "dt_sigma_regularizers: NULL argument");
+  DT_ARG(ab->kind == DT_ABS_CONST || (ab->kind == DT_ABS_GRID && ab->res >= 2), "dt_sigma_regularizers: bad absorption");
+  DT_ARG(n >= 0 && (n == 0 || ab->kind == DT_ABS_CONST || (points && xi)), "dt_sigma_regularizers: points/xi");
+  PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
+  DT_CU(launch_sigma_reg(ab, points, xi, n, lambda_smooth, lambda_vol, grad_sigma, loss, (cudaStream_t)stream));
+  p.end(1);
+  return DT_OK;
+}
+
+dt_status dt_adam_step(dt_ctx* c, float* param, const float* grad, float* m, float* v, int64_t n, const dt_adam* cfg,
+                       void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  DT_ARG(cfg && param && grad && m && v, "dt_adam_step: NULL argument");
+  DT_ARG(n > 0 && cfg->step >= 1 && cfg->lr >= 0.f && cfg->beta1 >= 0.f && cfg->beta1 < 1.f && cfg->beta2 >= 0.f &&
+             cfg->beta2 < 1.f && cfg->eps > 0.f,
+         "dt_adam_step: bad configuration (n=%lld step=%d)", (long long)n, cfg->step);
+  PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
+  int nl = 0;
+  DT_CU(launch_adam(param, grad, m, v, n, cfg, c->scratch, (cudaStream_t)stream, &nl));
+  p.end(nl);
   return DT_OK;
 }
 

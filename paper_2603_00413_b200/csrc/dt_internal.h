@@ -149,6 +149,7 @@ struct dt_ctx {
   int64_t last_rays = 0, last_need = 0;
   bool async_pending = false;
   cudaEvent_t fwd_done = nullptr;
+  unsigned* scratch = nullptr;                  // device [16] (AdamUniform max)
   struct Pending { int ph; cudaEvent_t a, b; };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
@@ -184,5 +185,12 @@ cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream
 cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, cudaStream_t st);
 DevScene scene_from_ctx(const dt_ctx* c);
 cudaError_t launch_count_segments(const int* lvl, int max_depth, unsigned long long* seg, cudaStream_t st);
+// optim.cu
+cudaError_t launch_loss_rt(const float* rgb, const float* tgt, const float* mask, int64_t n, float lc, float lt,
+                           float* grad, float* loss, cudaStream_t st);
+cudaError_t launch_sigma_reg(const dt_absorption* ab, const float* pts, const float* xi, int64_t n, float ls, float lv,
+                             float* gsig, float* loss, cudaStream_t st);
+cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n, const dt_adam* c, unsigned* scratch,
+                        cudaStream_t st, int* nl);
 }  // namespace dt
 dt_status consume_async(dt_ctx* c);

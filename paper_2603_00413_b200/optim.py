@@ -1,0 +1,99 @@
+"""The refine-stage optimisation loop around the tracer.
+
+One iteration, every arithmetic step in libdifftrans kernels:
+  dt_build_bvh -> dt_trace_forward -> dt_loss_rt (L_color + L_tone)
+  -> dt_trace_backward -> dt_sigma_regularizers (L_mat-smooth, L_vol)
+  -> dt_adam_step on sigma ("material", lr 3e-3), IoR (lr 1e-4 while the geometry is
+     frozen, then 1e-3) and, after the first k iterations, the vertices (AdamUniform, lr 1e-3).
+Adam: beta = (0.9, 0.999), weight decay 1e-6.  Loss weights lambda_1 = 1,
+lambda_2 = 0.001, lambda_4 = 0.0005; lambda_3 is not given by the paper (SPEC
+default 0.01).  The IoR stays in [1, 3] and sigma >= 0 (projection after each update).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+
+from .tracer import DeviceScene, Tracer
+
+
+@dataclass
+class RefineConfig:
+    freeze_iters: int = 300                 # k, P:513-525 ("k = 300 / 500 / 1000")
+    lr_material: float = 3e-3
+    lr_ior_frozen: float = 1e-4
+    lr_ior: float = 1e-3                    # P:527 (after the freeze-geometry stage)
+    lr_vertices: float = 1e-3               # P:527, AdamUniform
+    betas: tuple = (0.9, 0.999)
+    weight_decay: float = 1e-6
+    eps: float = 1e-8
+    lambda_color: float = 1.0               # lambda_1
+    lambda_tone: float = 0.001              # lambda_2
+    lambda_smooth: float = 0.01             # lambda_3: unstated in the paper (SPEC default)
+    lambda_vol: float = 0.0005              # lambda_4
+    n_reg_points: int = 4096
+    reg_sigma_perturb: float = 0.02         # xi ~ N(0, s^2) as a fraction of the sigma box
+    ior_range: tuple = (1.0, 3.0)
+
+
+@dataclass
+class StepResult:
+    loss: torch.Tensor                      # [4] device: L_color, L_tone, L_mat-smooth, L_vol
+    ior: float
+
+
+class RefineOptimizer:
+    """Jointly optimises vertices, IoR and absorption of a DeviceScene against target images."""
+
+    def __init__(self, tracer: Tracer, ds: DeviceScene, cfg: Optional[RefineConfig] = None, seed: int = 0):
+        self.tr, self.ds, self.cfg = tracer, ds, cfg or RefineConfig()
+        dev = ds.V.device
+        self.V = ds.V.clone().contiguous()
+        self.ior = torch.tensor([ds.ior], dtype=torch.float32, device=dev)
+        self.sigma = ds.sigma.clone().contiguous()
+        self.mV, self.vV = torch.zeros_like(self.V), torch.zeros(1, device=dev)          # AdamUniform: scalar v
+        self.mI, self.vI = torch.zeros_like(self.ior), torch.zeros_like(self.ior)
+        self.mS, self.vS = torch.zeros_like(self.sigma), torch.zeros_like(self.sigma)
+        self.gen = torch.Generator(device=dev)
+        self.gen.manual_seed(seed)
+        self.it = 0
+        self.loss = torch.zeros(4, dtype=torch.float32, device=dev)
+
+    def _reg_points(self):
+        ab = self.ds.absorption
+        dev = self.sigma.device
+        n = self.cfg.n_reg_points
+        lo = torch.tensor(list(ab.box_lo), device=dev)
+        hi = torch.tensor(list(ab.box_hi), device=dev)
+        pts = lo + (hi - lo) * torch.rand((n, 3), generator=self.gen, device=dev)
+        xi = torch.randn((n, 3), generator=self.gen, device=dev) * (self.cfg.reg_sigma_perturb * (hi - lo))
+        return pts.contiguous(), xi.contiguous()
+
+    def step(self, target: torch.Tensor, pixel_ids: Optional[torch.Tensor] = None) -> StepResult:
+        c, tr, ds = self.cfg, self.tr, self.ds
+        self.it += 1
+        ds.set_vertices(self.V)
+        ds.set_sigma(self.sigma)
+        ds.ior = float(self.ior.item())                  # the ABI takes the IoR by value (one 4-B read)
+        tr.build_bvh(ds.V, ds.F)
+        out = tr.trace_forward(ds, pixel_ids)
+        lrt, grad_rgb = tr.loss_rt(out.rgb, target, c.lambda_color, c.lambda_tone)
+        gV, gI, gS = tr.trace_backward(grad_rgb)
+        if ds.absorption.kind == 1:
+            pts, xi = self._reg_points()
+        else:
+            pts = xi = None
+        lreg = tr.sigma_regularizers(ds, pts, xi, gS, c.lambda_smooth, c.lambda_vol)
+        frozen = self.it <= c.freeze_iters
+        tr.adam_step(self.sigma, gS, self.mS, self.vS, self.it, c.lr_material, c.betas, c.eps, c.weight_decay,
+                     clamp=(0.0, float("inf")))
+        tr.adam_step(self.ior, gI, self.mI, self.vI, self.it, c.lr_ior_frozen if frozen else c.lr_ior, c.betas, c.eps,
+                     c.weight_decay, clamp=c.ior_range)
+        if not frozen:
+            tr.adam_step(self.V, gV, self.mV, self.vV, self.it - c.freeze_iters, c.lr_vertices, c.betas, c.eps,
+                         c.weight_decay, uniform=True)
+        self.loss[:2] = lrt
+        self.loss[2:] = lreg
+        return StepResult(self.loss, ds.ior)

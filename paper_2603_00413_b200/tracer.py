@@ -207,6 +207,45 @@ class Tracer:
         self._check(rc, self.h)
         return st.as_dict(self._last_depth)
 
+    # ------------------------------------------------------------------ optimisation step (NEXT-1)
+    def loss_rt(self, rgb: torch.Tensor, target: torch.Tensor, lambda_color: float = 1.0, lambda_tone: float = 0.001,
+                mask: Optional[torch.Tensor] = None, grad_rgb: Optional[torch.Tensor] = None,
+                loss: Optional[torch.Tensor] = None, stream=None):
+        """Fused L_color + L_tone: returns (loss[2] = [L_color, L_tone], grad_rgb)."""
+        n = rgb.shape[0]
+        if grad_rgb is None:
+            grad_rgb = torch.empty_like(rgb)
+        if loss is None:
+            loss = torch.empty(2, dtype=torch.float32, device=rgb.device)
+        self._check(self._lib.dt_loss_rt(self.h, _ptr(rgb), _ptr(target), _ptr(mask), n, float(lambda_color),
+                                         float(lambda_tone), _ptr(grad_rgb), _ptr(loss), _stream(stream)), self.h)
+        return loss, grad_rgb
+
+    def sigma_regularizers(self, ds: "DeviceScene", points: torch.Tensor, xi: torch.Tensor, grad_sigma: torch.Tensor,
+                           lambda_smooth: float, lambda_vol: float, loss: Optional[torch.Tensor] = None, stream=None):
+        """L_mat-smooth / L_vol; accumulates into grad_sigma."""
+        if loss is None:
+            loss = torch.empty(2, dtype=torch.float32, device=grad_sigma.device)
+        ds.absorption.sigma = _ptr(ds.sigma)
+        self._check(self._lib.dt_sigma_regularizers(self.h, C.byref(ds.absorption), _ptr(points), _ptr(xi),
+                                                    points.shape[0] if points is not None else 0, float(lambda_smooth),
+                                                    float(lambda_vol), _ptr(grad_sigma), _ptr(loss),
+                                                    _stream(stream)), self.h)
+        return loss
+
+    def adam_step(self, param: torch.Tensor, grad: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: int,
+                  lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0, uniform=False,
+                  clamp=(-float("inf"), float("inf")), stream=None):
+        """In-place Adam / AdamUniform update of `param`."""
+        for t in (param, grad, m, v):
+            assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+        cfg = N.Adam()
+        cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay = lr, betas[0], betas[1], eps, weight_decay
+        cfg.step, cfg.uniform = int(step), int(uniform)
+        cfg.clamp_lo, cfg.clamp_hi = float(clamp[0]), float(clamp[1])
+        self._check(self._lib.dt_adam_step(self.h, _ptr(param), _ptr(grad), _ptr(m), _ptr(v), param.numel(),
+                                           C.byref(cfg), _stream(stream)), self.h)
+
     # ------------------------------------------------------------------ profiling
     def set_profiling(self, enable: bool):
         self._check(self._lib.dt_set_profiling(self.h, int(enable)), self.h)
