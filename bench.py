@@ -1,8 +1,11 @@
 """Benchmark: one optimisation step of the DiffTrans refine-stage tracer on B200.
 
-A step = LBVH rebuild (dt_build_bvh) + recursive forward trace of every ray of the
-workload (dt_trace_forward) + fused L_color loss/gradient (dt_loss_color) + backward
-replay (dt_trace_backward) [+ NCCL all-reduce of the gradients when N > 1].
+A step = one RefineOptimizer.step (the paper's refine loop after the freeze-geometry
+stage): LBVH rebuild (dt_build_bvh) + recursive forward trace of every ray of
+the workload (dt_trace_forward, IoR read on the device) + fused L_color/L_tone loss and
+gradient (dt_loss_rt) + backward replay (dt_trace_backward) [+ NCCL all-reduce of the
+gradients when N > 1] + L_mat-smooth/L_vol (dt_sigma_regularizers) + Adam on sigma and
+the IoR and AdamUniform on the vertices (dt_adam_step).
 Metric (BASELINE.json): Mray.bounce/s fwd+bwd = traced segments / step time.
 
   python bench.py [--gpus N --steps K --warmup W --config C3 --impl ours|reference]
@@ -57,6 +60,10 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()                      # wait for nvidia-smi to come up, then keep
+            while not self.lines and time.time() - t0 < 5:   # only samples of the timed region
+                time.sleep(0.02)
+            self.lines.clear()
         except Exception:
             self.proc = None
 
@@ -141,6 +148,7 @@ def run_ours(args, rank, world, local_rank):
 
     from paper_2603_00413_b200 import dist as DD
     from paper_2603_00413_b200 import scenes as S
+    from paper_2603_00413_b200.optim import RefineConfig, RefineOptimizer
     from paper_2603_00413_b200.tracer import DeviceScene, Tracer
 
     dev = torch.device(f"cuda:{local_rank}")
@@ -158,22 +166,15 @@ def run_ours(args, rank, world, local_rank):
     tr.build_bvh(dt_.V, dt_.F)
     target = tr.trace_forward(dt_, pid).rgb.clone()
     del dt_
-    rgb = torch.empty((n_rays, 3), dtype=torch.float32, device=dev)
-    grad = torch.empty_like(rgb)
-    loss = torch.empty(1, dtype=torch.float32, device=dev)
-    gV = torch.empty((sc.V.shape[0], 3), dtype=torch.float32, device=dev)
-    gi = torch.empty(1, dtype=torch.float32, device=dev)
-    gs = torch.empty(tuple(ds.sigma.shape), dtype=torch.float32, device=dev)
-    flat = None
+    # the paper's refine loop after the freeze-geometry stage: vertices (AdamUniform),
+    # IoR and sigma all updated every step; gradients all-reduced across ranks before the updates
+    n_global = ds.n_pixels
+    hook = (lambda gV, gI, gS: DD.allreduce_grads(gV, gI, gS)) if world > 1 else None
+    opt = RefineOptimizer(tr, ds, RefineConfig(freeze_iters=0), seed=5, grad_hook=hook,
+                          loss_scale=n_rays / n_global)
 
     def step(async_=True):
-        nonlocal flat
-        tr.build_bvh(ds.V, ds.F)
-        tr.trace_forward(ds, pid, rgb=rgb, async_=async_)
-        tr.loss_color(rgb, target, grad, loss)
-        tr.trace_backward(grad, gV, gi, gs)
-        if world > 1:
-            flat = DD.allreduce_grads(gV, gi, gs, flat)
+        opt.step(target, pid, async_=async_)
 
     for w in range(args.warmup):
         step(async_=w > 0)          # the first (synchronous) step sizes the record arena
@@ -213,34 +214,19 @@ def run_ours(args, rank, world, local_rank):
     # ---- end-to-end through the public API with host buffers (pinned), same metric
     e2e = None
     if not args.no_e2e:
-        hV = torch.empty((sc.V.shape[0], 3), dtype=torch.float32, pin_memory=True)
-        hV.copy_(torch.as_tensor(sc.V))
-        hsig = torch.as_tensor(sc.absorption.sigma).clone().pin_memory()
+        # per step: this step's target pixels in from pinned host memory, the losses and the
+        # updated IoR back (the optimiser state -- V, sigma, moments -- stays resident in HBM)
         htgt = torch.empty((n_rays, 3), dtype=torch.float32, pin_memory=True)
         htgt.copy_(target.cpu())
-        hgV = torch.empty_like(hV, pin_memory=True)
-        hgi = torch.empty(1, pin_memory=True)
-        hgs = torch.empty_like(hsig, pin_memory=True)
-        hloss = torch.empty(1, pin_memory=True)
-        dV = ds.V
-        dsig = ds.sigma
-        tgt_d = target
+        hloss = torch.empty(4, pin_memory=True)
+        hior = torch.empty(1, pin_memory=True)
+        tgt_d = torch.empty_like(target)
 
         def e2e_step():
-            nonlocal flat
-            dV.copy_(hV, non_blocking=True)
-            dsig.copy_(hsig, non_blocking=True)
             tgt_d.copy_(htgt, non_blocking=True)
-            tr.build_bvh(dV, ds.F)
-            tr.trace_forward(ds, pid, rgb=rgb, async_=True)
-            tr.loss_color(rgb, tgt_d, grad, loss)
-            tr.trace_backward(grad, gV, gi, gs)
-            if world > 1:
-                flat = DD.allreduce_grads(gV, gi, gs, flat)
-            hgV.copy_(gV, non_blocking=True)
-            hgi.copy_(gi, non_blocking=True)
-            hgs.copy_(gs, non_blocking=True)
-            hloss.copy_(loss, non_blocking=True)
+            r = opt.step(tgt_d, pid, async_=True)
+            hloss.copy_(r.loss, non_blocking=True)
+            hior.copy_(r.ior, non_blocking=True)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -261,8 +247,8 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(mx, op=dist.ReduceOp.MAX)
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
             ms2, s2 = float(mx[0]), float(t[1])
-        h2d = hV.numel() * 4 + hsig.numel() * 4 + htgt.numel() * 4
-        d2h = hgV.numel() * 4 + hgi.numel() * 4 + hgs.numel() * 4 + 4
+        h2d = htgt.numel() * 4
+        d2h = hloss.numel() * 4 + hior.numel() * 4
         e2e = {"value": s2 / (ms2 / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms2 / args.steps}
 
@@ -339,7 +325,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -120,6 +120,10 @@ typedef struct {
                                 dt_trace_forward / dt_get_stats, which then returns
                                 DT_ERR_RETRY.  Ignored (synchronous) when stats or
                                 check_finite are requested or no previous need is known.   */
+  const float* ior_device;   /* optional device float[1]: when non-NULL the IoR is read from
+                                it by the kernels (forward and the matching backward) instead
+                                of the `ior` argument, so an on-device optimiser update needs
+                                no host round trip.  Must not change before the backward.    */
 } dt_trace_opts;
 
 /* Host-side statistics filled by dt_trace_forward when requested. */

@@ -37,7 +37,7 @@ class Cameras(C.Structure):
 
 class TraceOpts(C.Structure):
     _fields_ = [("max_depth", C.c_int32), ("cap_policy", C.c_int32), ("t_eps", C.c_float),
-                ("check_finite", C.c_int32), ("async_", C.c_int32)]
+                ("check_finite", C.c_int32), ("async_", C.c_int32), ("ior_device", C.c_void_p)]
 
 
 class Stats(C.Structure):

@@ -284,6 +284,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
 
   DevScene s = scene_from_ctx(c);
   s.ior = ior;
+  s.ior_ptr = opts->ior_device;
   s.abs_kind = ab->kind;
   s.sigma = c->sigma_snap;
   s.sres = ab->res;

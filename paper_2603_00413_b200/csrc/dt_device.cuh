@@ -36,6 +36,7 @@ struct DevScene {
   const float* scal;    // device scalars: [0..5] root box lo/hi, [6] t_min
   // material
   float ior;
+  const float* ior_ptr;  // optional device IoR (dt_trace_opts.ior_device), read once per thread
   int abs_kind;
   const float4* sigma;  // internal copy: [1] (constant) or [R^3] nodes, rgb + pad
   int sres, nsamp;
@@ -337,7 +338,7 @@ struct Shade {
   bool inside, tir, clamped, degen, fb;
 };
 
-DT_D void shade_forward(const DevScene& s, int i0, int i1, int i2, float3 e1, float3 e2, float3 d, float u, float v,
+DT_D void shade_forward(const DevScene& s, float ior, int i0, int i1, int i2, float3 e1, float3 e2, float3 d, float u, float v,
                         bool inside, Shade& S) {
   S.inside = inside;
   S.b0 = 1.0f - u - v; S.b1 = u; S.b2 = v;
@@ -349,8 +350,8 @@ DT_D void shade_forward(const DevScene& s, int i0, int i1, int i2, float3 e1, fl
   else { float3 c = cross(e1, e2); S.ns = c * (1.0f / length(c)); }
   S.sg = inside ? -1.0f : 1.0f;
   S.n = S.ns * S.sg;
-  S.eta_i = inside ? s.ior : 1.0f;
-  S.eta_t = inside ? 1.0f : s.ior;
+  S.eta_i = inside ? ior : 1.0f;
+  S.eta_t = inside ? 1.0f : ior;
   S.wi = -d;
   S.c_raw = dot(S.wi, S.n);
   S.clamped = !(S.c_raw > 0.0f);

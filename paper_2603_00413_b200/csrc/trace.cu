@@ -88,7 +88,7 @@ DT_D void flush_counters(unsigned long long* c, int visits, int tests) {
 
 // Shade one traced segment (record idx at level k) and spawn its children into level k+1.
 // All 32 lanes of the warp must call this (the compaction is a warp collective).
-DT_D void shade_and_spawn(const FwdLaunch& a, int k, int max_depth, bool valid, int64_t idx, float3 o, float3 d,
+DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int k, int max_depth, bool valid, int64_t idx, float3 o, float3 d,
                           int64_t ray, uint32_t pos, float3 thr, float w, int face, float t, float u, float v) {
   const DevScene& s = a.s;
   bool is_hit = valid && face >= 0;
@@ -123,7 +123,7 @@ DT_D void shade_and_spawn(const FwdLaunch& a, int k, int max_depth, bool valid, 
         if (a.capw) atomicAdd(a.capw + ray, w);
       } else {
         Shade S;
-        shade_forward(s, i0, i1, i2, e1, e2, d, u, v, inside, S);
+        shade_forward(s, ior, i0, i1, i2, e1, e2, d, u, v, inside, S);
         if (inside) tau = transmittance(s, o, x);                             // P:162 (R9)
         R = S.R;
         T = S.T;
@@ -251,6 +251,7 @@ __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
 // the final level-0 count, so it always runs after the traversal pass.
 __global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
   if (a.lvl[LV_OVERFLOW]) return;   // arena too small: the host grows it and re-runs
+  const float ior = a.s.ior_ptr ? __ldg(a.s.ior_ptr) : a.s.ior;
   int n = a.lvl[LV_CNT + k];
   while (true) {
     int base = fetch_work(a.lvl + LV_WORK_SHADE + k);
@@ -271,7 +272,7 @@ __global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
       pos = __float_as_uint(rd.w);
       face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
     }
-    shade_and_spawn(a, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
+    shade_and_spawn(a, ior, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
   }
 }
 
@@ -477,6 +478,7 @@ DT_D void atomic_add3(float4* p, float3 v) {
 __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, int64_t cap) {
   const DevScene& s = a.s;
   if (a.lvl[LV_OVERFLOW]) return;   // an overflowed (asynchronous) forward: nothing valid to replay
+  const float ior = s.ior_ptr ? __ldg(s.ior_ptr) : s.ior;
   int n = a.lvl[LV_CNT + k];
   float gior = 0.0f;
   float3 gsc = f3(0, 0, 0);
@@ -515,7 +517,7 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
         gNk[0] = gNk[1] = gNk[2] = f3(0, 0, 0);
       } else {
         Shade S;
-        shade_forward(s, i0, i1, i2, e1, e2, d, u, v, inside, S);
+        shade_forward(s, ior, i0, i1, i2, e1, e2, d, u, v, inside, S);
         float4 ls = a.r.lsub[idx], tu = a.r.tau[idx];
         int cr = __float_as_int(ls.w), ct = __float_as_int(tu.w);
         float3 Lr = f3(0, 0, 0), Lt = f3(0, 0, 0), gwr = f3(0, 0, 0), gwt = f3(0, 0, 0);

@@ -12,7 +12,7 @@ default 0.01).  The IoR stays in [1, 3] and sigma >= 0 (projection after each up
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Optional
+from typing import Callable, Optional
 
 import torch
 
@@ -41,14 +41,20 @@ class RefineConfig:
 @dataclass
 class StepResult:
     loss: torch.Tensor                      # [4] device: L_color, L_tone, L_mat-smooth, L_vol
-    ior: float
+    ior: torch.Tensor                       # [1] device: the IoR after this step's update
 
 
 class RefineOptimizer:
     """Jointly optimises vertices, IoR and absorption of a DeviceScene against target images."""
 
-    def __init__(self, tracer: Tracer, ds: DeviceScene, cfg: Optional[RefineConfig] = None, seed: int = 0):
+    def __init__(self, tracer: Tracer, ds: DeviceScene, cfg: Optional[RefineConfig] = None, seed: int = 0,
+                 grad_hook: Optional[Callable] = None, loss_scale: float = 1.0):
+        """grad_hook(gV, g_ior, g_sigma): called on the ray-loss gradients before the
+        regularisers and the updates (data parallel: dist.allreduce_grads).  loss_scale scales
+        lambda_color / lambda_tone; with rays sharded over ranks, n_local / n_global makes the
+        summed gradient that of the global mean (loss_rt normalises by the local ray count)."""
         self.tr, self.ds, self.cfg = tracer, ds, cfg or RefineConfig()
+        self.grad_hook, self.loss_scale = grad_hook, float(loss_scale)
         dev = ds.V.device
         self.V = ds.V.clone().contiguous()
         self.ior = torch.tensor([ds.ior], dtype=torch.float32, device=dev)
@@ -71,16 +77,21 @@ class RefineOptimizer:
         xi = torch.randn((n, 3), generator=self.gen, device=dev) * (self.cfg.reg_sigma_perturb * (hi - lo))
         return pts.contiguous(), xi.contiguous()
 
-    def step(self, target: torch.Tensor, pixel_ids: Optional[torch.Tensor] = None) -> StepResult:
+    def step(self, target: torch.Tensor, pixel_ids: Optional[torch.Tensor] = None, async_: bool = False) -> StepResult:
+        """One iteration, queued on the current stream.  async_: the forward does not wait for its
+        arena-overflow check (an overflow surfaces as DT_ERR_RETRY on the next call; see
+        Tracer.trace_forward) so consecutive steps queue back to back with no host stall."""
         c, tr, ds = self.cfg, self.tr, self.ds
         self.it += 1
         ds.set_vertices(self.V)
         ds.set_sigma(self.sigma)
-        ds.ior = float(self.ior.item())                  # the ABI takes the IoR by value (one 4-B read)
         tr.build_bvh(ds.V, ds.F)
-        out = tr.trace_forward(ds, pixel_ids)
-        lrt, grad_rgb = tr.loss_rt(out.rgb, target, c.lambda_color, c.lambda_tone)
+        # the kernels read the IoR from self.ior (dt_trace_opts.ior_device): no host round trip
+        out = tr.trace_forward(ds, pixel_ids, ior_device=self.ior, async_=async_)
+        lrt, grad_rgb = tr.loss_rt(out.rgb, target, c.lambda_color * self.loss_scale, c.lambda_tone * self.loss_scale)
         gV, gI, gS = tr.trace_backward(grad_rgb)
+        if self.grad_hook is not None:
+            self.grad_hook(gV, gI, gS)
         if ds.absorption.kind == 1:
             pts, xi = self._reg_points()
         else:
@@ -96,4 +107,4 @@ class RefineOptimizer:
                          c.weight_decay, uniform=True)
         self.loss[:2] = lrt
         self.loss[2:] = lreg
-        return StepResult(self.loss, ds.ior)
+        return StepResult(self.loss, self.ior)

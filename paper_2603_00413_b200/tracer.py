@@ -144,9 +144,12 @@ class Tracer:
     def trace_forward(self, ds: DeviceScene, pixel_ids: Optional[torch.Tensor] = None, ior: Optional[float] = None,
                       max_depth: Optional[int] = None, cap_policy: Optional[int] = None, want_capped=False,
                       want_sig=False, stats=False, check_finite=False, rgb: Optional[torch.Tensor] = None,
-                      async_: bool = False, stream=None) -> ForwardOut:
+                      async_: bool = False, ior_device: Optional[torch.Tensor] = None,
+                      stream=None) -> ForwardOut:
         """async_: no end-of-call synchronisation (see dt_trace_opts.async); an arena overflow
-        of this call is reported by the next call as DiffTransError('DT_ERR_RETRY ...')."""
+        of this call is reported by the next call as DiffTransError('DT_ERR_RETRY ...').
+        ior_device: a device float32[1] the kernels read the IoR from (no host round trip when an
+        on-device optimiser updates it); it must not change before the matching backward."""
         cams = ds.cameras(pixel_ids)
         n = cams.n_rays
         dev = self.device
@@ -161,6 +164,9 @@ class Tracer:
         opts.t_eps = ds.t_eps
         opts.check_finite = int(check_finite)
         opts.async_ = int(async_)
+        if ior_device is not None:
+            assert ior_device.is_cuda and ior_device.dtype == torch.float32 and ior_device.numel() >= 1
+            opts.ior_device = ior_device.data_ptr()
         ds.absorption.sigma = _ptr(ds.sigma)
         st_out = N.Stats() if stats else None
         rc = self._lib.dt_trace_forward(self.h, float(ds.ior if ior is None else ior), C.byref(ds.absorption),
