@@ -442,112 +442,177 @@ DT_D void mt_backward(float3 d, float3 e1, float3 e2, float t, float u, float v,
 }
 
 // ----------------------------------------------------------------------------- absorption
-DT_D bool sigma_cell(const DevScene& s, float3 p, int i0[3], float f[3], float scale[3]) {
-  const float lo[3] = {s.slo.x, s.slo.y, s.slo.z}, hi[3] = {s.shi.x, s.shi.y, s.shi.z};
-  const float pp[3] = {p.x, p.y, p.z};
-  int R = s.sres;
-  for (int a = 0; a < 3; ++a) {
-    float g = (pp[a] - lo[a]) / (hi[a] - lo[a]) * (float)(R - 1);
-    if (g < 0.0f || g > (float)(R - 1)) return false;     // zero outside the box (R11)
-    i0[a] = min((int)floorf(g), R - 2);
-    f[a] = g - (float)i0[a];
-    scale[a] = (float)(R - 1) / (hi[a] - lo[a]);
-  }
-  return true;
+DT_D size_t cell_node(size_t base, int k, int R) {
+  return base + ((size_t)(k >> 2) * R + ((k >> 1) & 1)) * R + (k & 1);
 }
 
-DT_D float3 sigma_at(const DevScene& s, float3 p) {
-  int i0[3];
-  float f[3], sc[3];
-  if (!sigma_cell(s, p, i0, f, sc)) return f3(0, 0, 0);
-  int R = s.sres;
-  float3 out = f3(0, 0, 0);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
-    float w = (dx ? f[0] : 1 - f[0]) * (dy ? f[1] : 1 - f[1]) * (dz ? f[2] : 1 - f[2]);
-    out += f3(__ldg(s.sigma + ((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx))) * w;
-  }
-  return out;
-}
-
-// tau = exp(-sum_j mu(x_j) dx) over o -> x, midpoint rule with N samples (R10)
-DT_D float3 transmittance(const DevScene& s, float3 o, float3 x) {
-  float3 dx = x - o;
-  float l = length(dx);
-  float3 S;
-  if (s.abs_kind == 0) {
-    S = f3(__ldg(s.sigma)) * l;
-  } else {
-    int N = s.nsamp;
-    S = f3(0, 0, 0);
-    for (int j = 0; j < N; ++j) S += sigma_at(s, o + dx * (((float)j + 0.5f) / (float)N));
-    S = S * (l / (float)N);
-  }
+// Optical depth of a constant-sigma segment and its reverse (ABS = DT_ABS_CONST).
+DT_D float3 transmittance_const(const DevScene& s, float3 o, float3 x) {
+  const float3 S = f3(__ldg(s.sigma)) * length(x - o);
   return f3(expf(-S.x), expf(-S.y), expf(-S.z));
 }
 
-// Reverse of transmittance given gS = dL/d(optical depth).  Constant sigma: partial sums in
-// gsc.  Grid: trilinear scatter into gsig (float4 per node); consecutive samples that fall
-// in the same cell are merged first, so each cell visit costs 8 vector atomics.
-DT_D void transmittance_backward(const DevScene& s, float3 o, float3 x, float3 gS, float3& gx, float3& go,
-                                 float4* gsig, float3& gsc) {
-  float3 dx = x - o;
-  float l = length(dx);
-  float gl = 0.0f;
-  if (s.abs_kind == 0) {
-    gsc += gS * l;
-    gl = dot(gS, f3(__ldg(s.sigma)));
-  } else {
-    int N = s.nsamp, R = s.sres;
-    float sc = l / (float)N;
-    float3 gSs = gS * sc;
-    float acc[8];                      // per-corner weight sums of the current cell run
-    size_t run_base = ~(size_t)0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-    for (int j = 0; j <= N; ++j) {
-      int i0[3];
-      float f[3], scl[3];
-      bool inside = false;
-      float w = ((float)j + 0.5f) / (float)N;
-      float3 p = o + dx * w;
-      if (j < N) inside = sigma_cell(s, p, i0, f, scl);
-      size_t base = inside ? ((size_t)i0[2] * R + i0[1]) * R + i0[0] : ~(size_t)0;
-      if (base != run_base) {          // flush the finished run
-        if (run_base != ~(size_t)0) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            size_t node = run_base + ((size_t)(k >> 2) * R + ((k >> 1) & 1)) * R + (k & 1);
-            atomicAdd(gsig + node, make_float4(gSs.x * acc[k], gSs.y * acc[k], gSs.z * acc[k], 0.f));
-            acc[k] = 0.f;
-          }
-        }
-        run_base = base;
-      }
-      if (!inside) continue;
-      float3 gp = f3(0, 0, 0), val = f3(0, 0, 0);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        int ix = k & 1, iy = (k >> 1) & 1, iz = k >> 2;
-        float wx = ix ? f[0] : 1 - f[0], wy = iy ? f[1] : 1 - f[1], wz = iz ? f[2] : 1 - f[2];
-        float ww = wx * wy * wz;
-        float3 sv = f3(__ldg(s.sigma + base + ((size_t)iz * R + iy) * R + ix));
-        val += sv * ww;
-        acc[k] += ww;
-        float sd = dot(gSs, sv);
-        gp += f3((ix ? 1.f : -1.f) * wy * wz * scl[0], wx * (iy ? 1.f : -1.f) * wz * scl[1],
-                 wx * wy * (iz ? 1.f : -1.f) * scl[2]) * sd;
-      }
-      gl += dot(gS, val) / (float)N;
-      go += gp * (1.0f - w);
-      gx += gp * w;
-    }
-  }
+DT_D void transmittance_const_backward(const DevScene& s, float3 o, float3 x, float3 gS, float3& gx, float3& go,
+                                       float3& gsc) {
+  const float3 dx = x - o;
+  const float l = length(dx);
+  gsc += gS * l;
   if (l > 0.0f) {
-    float3 u = dx * (1.0f / l);
+    const float3 u = dx * (1.0f / l);
+    const float gl = dot(gS, f3(__ldg(s.sigma)));
     gx += u * gl;
     go -= u * gl;
+  }
+}
+
+// Sigma grid (ABS = DT_ABS_GRID): the N midpoint samples x_j = o + t_j (x - o),
+// t_j = (j + 1/2)/N, of ONE segment are evaluated by the whole warp, lane l taking samples
+// l, l + 32, ...  (R10, R11).  A warp therefore walks its interior segments one after the
+// other with every lane busy and all 8 corner loads of a lane's sample in flight at once,
+// instead of each lane walking its own segment sample by sample (divergent, latency bound).
+// Must be called by all 32 lanes with warp-uniform arguments.
+struct GridMap {
+  float3 lo, scl;          // g = (p - lo) * scl, scl = (R-1)/(hi-lo)
+  int R, N;
+};
+
+DT_D GridMap grid_map(const DevScene& s) {
+  GridMap m;
+  m.R = s.sres;
+  m.N = s.nsamp;
+  m.lo = s.slo;
+  m.scl = f3((float)(m.R - 1) / (s.shi.x - s.slo.x), (float)(m.R - 1) / (s.shi.y - s.slo.y),
+             (float)(m.R - 1) / (s.shi.z - s.slo.z));
+  return m;
+}
+
+// Cell and local coordinates of p (zero outside the box, R11).
+DT_D bool grid_cell(const GridMap& m, float3 p, int& base, float f[3]) {
+  const float g[3] = {(p.x - m.lo.x) * m.scl.x, (p.y - m.lo.y) * m.scl.y, (p.z - m.lo.z) * m.scl.z};
+  const float top = (float)(m.R - 1);
+  if (!(g[0] >= 0.f && g[0] <= top && g[1] >= 0.f && g[1] <= top && g[2] >= 0.f && g[2] <= top)) return false;
+  int i[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    i[a] = min((int)floorf(g[a]), m.R - 2);
+    f[a] = g[a] - (float)i[a];
+  }
+  base = (i[2] * m.R + i[1]) * m.R + i[0];
+  return true;
+}
+
+DT_D void corner_weights(const float f[3], float w[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    w[k] = ((k & 1) ? f[0] : 1 - f[0]) * ((k & 2) ? f[1] : 1 - f[1]) * ((k & 4) ? f[2] : 1 - f[2]);
+}
+
+// sum_j mu(x_j) * |x - o| / N (the optical depth of R10), returned on every lane.
+DT_D float3 warp_optical_depth(const DevScene& s, const GridMap& m, float3 o, float3 x) {
+  const float3 dx = x - o;
+  float3 S = f3(0, 0, 0);
+  for (int j = lane_id(); j < m.N; j += 32) {
+    int base;
+    float f[3], w[8];
+    if (!grid_cell(m, o + dx * (((float)j + 0.5f) / (float)m.N), base, f)) continue;
+    corner_weights(f, w);
+    float4 c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = __ldg(s.sigma + cell_node(base, k, m.R));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S += f3(c[k]) * w[k];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    S.x += __shfl_xor_sync(~0u, S.x, off);
+    S.y += __shfl_xor_sync(~0u, S.y, off);
+    S.z += __shfl_xor_sync(~0u, S.z, off);
+  }
+  return S * (length(dx) / (float)m.N);
+}
+
+// Reverse of warp_optical_depth given gS = dL/d(optical depth): scatters gS * (l/N) * w_k
+// into the float4 grid adjoint gsig and returns the position adjoints of o and x on every
+// lane.  Lanes whose samples fall in the same cell (contiguous lanes: a segment enters a
+// convex cell once) merge their corner weights with a segmented shuffle reduction first, so
+// each (cell, 32-sample round) costs 8 vector atomics.
+DT_D void warp_transmittance_backward(const DevScene& s, const GridMap& m, float3 o, float3 x, float3 gS,
+                                      float4* gsig, float3& gx, float3& go) {
+  const float3 dx = x - o;
+  const float l = length(dx);
+  const float invN = 1.0f / (float)m.N, sc = l * invN;
+  const float3 gSs = gS * sc;
+  const int lane = lane_id();
+  float gl = 0.f;
+  float3 gsum = f3(0, 0, 0), gtsum = f3(0, 0, 0);
+  for (int j0 = 0; j0 < m.N; j0 += 32) {
+    const int j = j0 + lane;
+    const float t = ((float)j + 0.5f) * invN;
+    int base = -1;
+    float f[3], w[8];
+    const bool in = j < m.N && grid_cell(m, o + dx * t, base, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = 0.f;
+    if (in) {
+      corner_weights(f, w);
+      float4 c[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = __ldg(s.sigma + cell_node(base, k, m.R));
+      float gk[8], gv = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        gk[k] = dot(gS, f3(c[k]));
+        gv += w[k] * gk[k];
+      }
+      // d/dg of sum_k gk_k w_k: differences over each axis' bit
+      float3 gp = f3(0, 0, 0);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int u = p & 1, v = p >> 1;
+        const float fu0 = u ? f[0] : 1 - f[0], fu1 = u ? f[1] : 1 - f[1];
+        const float fv1 = v ? f[1] : 1 - f[1], fv2 = v ? f[2] : 1 - f[2];
+        gp.x += (gk[1 | (u << 1) | (v << 2)] - gk[(u << 1) | (v << 2)]) * fu1 * fv2;
+        gp.y += (gk[u | 2 | (v << 2)] - gk[u | (v << 2)]) * fu0 * fv2;
+        gp.z += (gk[u | (v << 1) | 4] - gk[u | (v << 1)]) * fu0 * fv1;
+      }
+      gl += gv;
+      gsum += gp;
+      gtsum += gp * t;
+    }
+    const unsigned same = __match_any_sync(~0u, base);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const float o2 = __shfl_down_sync(~0u, w[k], off);
+        if (lane + off < 32 && ((same >> (lane + off)) & 1u)) w[k] += o2;
+      }
+    }
+    if (in && lane == __ffs(same) - 1) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        atomicAdd(gsig + cell_node(base, k, m.R), make_float4(gSs.x * w[k], gSs.y * w[k], gSs.z * w[k], 0.f));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    gl += __shfl_xor_sync(~0u, gl, off);
+    gsum.x += __shfl_xor_sync(~0u, gsum.x, off);
+    gsum.y += __shfl_xor_sync(~0u, gsum.y, off);
+    gsum.z += __shfl_xor_sync(~0u, gsum.z, off);
+    gtsum.x += __shfl_xor_sync(~0u, gtsum.x, off);
+    gtsum.y += __shfl_xor_sync(~0u, gtsum.y, off);
+    gtsum.z += __shfl_xor_sync(~0u, gtsum.z, off);
+  }
+  // grad_p mu = grad_g mu * scl; quadrature weight sc; x_j = o (1 - t_j) + x t_j
+  const float3 k3 = m.scl * sc;
+  const float3 gxt = f3(gtsum.x * k3.x, gtsum.y * k3.y, gtsum.z * k3.z);
+  gx = gxt;
+  go = f3(gsum.x * k3.x, gsum.y * k3.y, gsum.z * k3.z) - gxt;
+  if (l > 0.0f) {                      // d l / d(x, o) times sum_j gS . mu(x_j) / N
+    const float3 u = dx * (1.0f / l);
+    gx += u * (gl * invN);
+    go -= u * (gl * invN);
   }
 }
 

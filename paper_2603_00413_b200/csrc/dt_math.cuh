@@ -39,3 +39,6 @@ DT_D float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
 
 DT_D unsigned lanemask_lt() { unsigned m; asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m)); return m; }
 DT_D int lane_id() { return threadIdx.x & 31; }
+DT_D float3 shfl3(float3 v, int src) {
+  return f3(__shfl_sync(~0u, v.x, src), __shfl_sync(~0u, v.y, src), __shfl_sync(~0u, v.z, src));
+}

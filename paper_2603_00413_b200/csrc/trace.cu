@@ -88,12 +88,13 @@ DT_D void flush_counters(unsigned long long* c, int visits, int tests) {
 
 // Shade one traced segment (record idx at level k) and spawn its children into level k+1.
 // All 32 lanes of the warp must call this (the compaction is a warp collective).
+template <int ABS>
 DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int k, int max_depth, bool valid, int64_t idx, float3 o, float3 d,
                           int64_t ray, uint32_t pos, float3 thr, float w, int face, float t, float u, float v) {
   const DevScene& s = a.s;
   bool is_hit = valid && face >= 0;
-  bool spawn_r = false, spawn_t = false;
-  float3 x = f3(0, 0, 0), wr = x, wt = x, tau = f3(1, 1, 1);
+  bool spawn_r = false, spawn_t = false, need_tau = false, capped = false;
+  float3 x = f3(0, 0, 0), wr = x, wt = x, tau = f3(1, 1, 1), capL = x;
   float R = 0.f, T = 0.f;
   if (valid) {
     if (!is_hit) {
@@ -109,14 +110,12 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int k, int max_depth, b
       face_tri(s, face, i0, i1, i2, v0, e1, e2);
       bool inside = dot(d, cross(e1, e2)) > 0.0f;                             // R8
       x = o + d * t;
+      need_tau = inside;
       if (k == max_depth) {                                                   // capped (R12, R13)
-        float3 L = f3(0, 0, 0);
-        if (inside) tau = transmittance(s, o, x);
-        if (s.cap_policy == 1) L = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr) * tau;
+        capped = true;
+        if (s.cap_policy == 1) capL = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);   // times tau below
         int fl = RF_CAPPED | (inside ? RF_INSIDE : 0);
         __stcs(a.r.hit + idx, make_float4(__int_as_float(face), t, 0.f, __int_as_float(fl)));
-        __stcs(a.r.lsub + idx, f4(L, __int_as_float(-1)));
-        __stcs(a.r.tau + idx, f4(tau, __int_as_float(-1)));
         int ev = inside ? EV_CAP_IN : EV_CAP_OUT;
         sig_add(a.sig_t, ray, topo_key(pos, ev));
         sig_add(a.sig_f, ray, face_key(pos, ev, face));
@@ -124,7 +123,6 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int k, int max_depth, b
       } else {
         Shade S;
         shade_forward(s, ior, i0, i1, i2, e1, e2, d, u, v, inside, S);
-        if (inside) tau = transmittance(s, o, x);                             // P:162 (R9)
         R = S.R;
         T = S.T;
         wr = S.wr;
@@ -138,6 +136,22 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int k, int max_depth, b
         sig_add(a.sig_f, ray, face_key(pos, ev, face));
       }
     }
+  }
+  // interior transmittance of the segment o -> x (R9)
+  if (ABS == 0) {
+    if (need_tau) tau = transmittance_const(s, o, x);
+  } else {
+    const GridMap gm = grid_map(s);
+    for (unsigned m = __ballot_sync(~0u, need_tau); m; m &= m - 1) {      // warp-cooperative walks
+      const int src = __ffs(m) - 1;
+      const float3 so = shfl3(o, src), sx = shfl3(x, src);
+      const float3 Sd = warp_optical_depth(s, gm, so, sx);
+      if (lane_id() == src) tau = f3(expf(-Sd.x), expf(-Sd.y), expf(-Sd.z));
+    }
+  }
+  if (capped) {
+    __stcs(a.r.lsub + idx, f4(capL * tau, __int_as_float(-1)));
+    __stcs(a.r.tau + idx, f4(tau, __int_as_float(-1)));
   }
   // warp-ballot compaction of the children: the warp's reflect children first, then its
   // refract children, each group contiguous in level k+1
@@ -249,6 +263,7 @@ __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
 // Shading of level k (K10): reads each record's ray and traversal result, evaluates the
 // event and spawns the children into level k+1 (warp-ballot compaction).  Level 0 needs
 // the final level-0 count, so it always runs after the traversal pass.
+template <int ABS>
 __global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
   if (a.lvl[LV_OVERFLOW]) return;   // arena too small: the host grows it and re-runs
   const float ior = a.s.ior_ptr ? __ldg(a.s.ior_ptr) : a.s.ior;
@@ -272,7 +287,7 @@ __global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
       pos = __float_as_uint(rd.w);
       face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
     }
-    shade_and_spawn(a, ior, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
+    shade_and_spawn<ABS>(a, ior, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
   }
 }
 
@@ -475,72 +490,98 @@ DT_D void atomic_add3(float4* p, float3 v) {
   atomicAdd(p, make_float4(v.x, v.y, v.z, 0.0f));
 }
 
+// Backward replay of level k (K12): per record, the local VJP at fixed topology.  Three
+// phases per warp-iteration so that the sigma-grid walks (ABS = grid) run warp-cooperatively:
+// (A) per lane: env / interface adjoints up to the interior segment's optical-depth adjoint
+// gS; (B) the transmittance adjoints of the warp's interior segments, one segment at a time
+// by the whole warp (or per lane for constant sigma); (C) per lane: x = o + t d and the
+// Moller-Trumbore reverse, vertex and normal atomics, parent-slot adjoints.
+template <int ABS>
 __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, int64_t cap) {
   const DevScene& s = a.s;
   if (a.lvl[LV_OVERFLOW]) return;   // an overflowed (asynchronous) forward: nothing valid to replay
   const float ior = s.ior_ptr ? __ldg(s.ior_ptr) : s.ior;
-  int n = a.lvl[LV_CNT + k];
+  const int n = a.lvl[LV_CNT + k];
   float gior = 0.0f;
   float3 gsc = f3(0, 0, 0);
-  for (int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; item < n; item += (int64_t)gridDim.x * blockDim.x) {
-    int64_t idx = rec_index(a.lvl, cap, k, item);
-    float4 ro = a.r.o[idx], rd = a.r.d[idx], rt = a.r.thr[idx], h = a.r.hit[idx];
-    float3 o = f3(ro), d = f3(rd);
-    int64_t ray = __float_as_int(ro.w);
-    int fl = __float_as_int(h.w);
-    const float* g = a.grad_rgb + 3 * ray;
-    float3 adj = f3(__ldg(g), __ldg(g + 1), __ldg(g + 2)) * f3(rt);            // a_n = grad * throughput
-    float3 go = f3(0, 0, 0), gd = f3(0, 0, 0);
-    if (fl & RF_MISS) {
-      env_eval(s, o, d, adj, &go, &gd);
-    } else if ((fl & RF_CAPPED) && s.cap_policy == 0) {
-      // capped branches return 0: no dependence
-    } else {
-      int face = __float_as_int(h.x);
-      int i0, i1, i2;
-      float3 v0, e1, e2;
-      face_tri(s, face, i0, i1, i2, v0, e1, e2);
-      float t, u, v;
-      intersect_tri(o, d, v0, e1, e2, -kInf, t, u, v);                      // replay (bit-identical)
-      float3 x = o + d * t;
-      bool inside = (fl & RF_INSIDE) != 0;
-      float3 tau = f3(a.r.tau[idx]);
-      float3 gx = f3(0, 0, 0);
-      float gu = 0.f, gv = 0.f;
-      float3 gVk[3], gNk[3];
-      if (fl & RF_CAPPED) {                                                   // CAP_ENV leaf
-        float3 E = env_eval(s, o, d, adj * tau, &go, &gd);
-        if (inside) {
-          float3 gS = -(adj * E * tau);
-          transmittance_backward(s, o, x, gS, gx, go, a.dsig, gsc);
-        }
-        gNk[0] = gNk[1] = gNk[2] = f3(0, 0, 0);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t wbase = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); wbase < n; wbase += stride) {
+    const int64_t item = wbase + lane_id();
+    const bool valid = item < n;
+    int64_t idx = 0;
+    float3 o = f3(0, 0, 0), d = f3(0, 0, 1), x = o, gS = o;
+    float3 go = f3(0, 0, 0), gd = f3(0, 0, 0), gx = f3(0, 0, 0);
+    float3 e1 = o, e2 = o, gNk[3];
+    float t = 0.f, u = 0.f, v = 0.f, gu = 0.f, gv = 0.f;
+    int fl = 0, i0 = 0, i1 = 0, i2 = 0;
+    bool geo = false, walk = false;
+    // ---- (A)
+    if (valid) {
+      idx = rec_index(a.lvl, cap, k, item);
+      float4 ro = a.r.o[idx], rd = a.r.d[idx], rt = a.r.thr[idx], h = a.r.hit[idx];
+      o = f3(ro);
+      d = f3(rd);
+      int64_t ray = __float_as_int(ro.w);
+      fl = __float_as_int(h.w);
+      const float* g = a.grad_rgb + 3 * ray;
+      float3 adj = f3(__ldg(g), __ldg(g + 1), __ldg(g + 2)) * f3(rt);          // a_n = grad * throughput
+      if (fl & RF_MISS) {
+        env_eval(s, o, d, adj, &go, &gd);
+      } else if ((fl & RF_CAPPED) && s.cap_policy == 0) {
+        // capped branches return 0: no dependence
       } else {
-        Shade S;
-        shade_forward(s, ior, i0, i1, i2, e1, e2, d, u, v, inside, S);
-        float4 ls = a.r.lsub[idx], tu = a.r.tau[idx];
-        int cr = __float_as_int(ls.w), ct = __float_as_int(tu.w);
-        float3 Lr = f3(0, 0, 0), Lt = f3(0, 0, 0), gwr = f3(0, 0, 0), gwt = f3(0, 0, 0);
-        if (cr >= 0) { Lr = f3(a.r.lsub[cr]); gx += f3(a.r.go[cr]); gwr = f3(a.r.gd[cr]); }
-        if (ct >= 0) { Lt = f3(a.r.lsub[ct]); gx += f3(a.r.go[ct]); gwt = f3(a.r.gd[ct]); }
-        float3 ap = adj * tau;
-        float3 Lc = Lr * S.R + Lt * S.T;
-        float gR = S.tir ? 0.0f : dot(ap, Lr - Lt);
-        if (inside) {
-          float3 gS = -(adj * Lc * tau);
-          transmittance_backward(s, o, x, gS, gx, go, a.dsig, gsc);
+        geo = true;
+        int face = __float_as_int(h.x);
+        float3 v0;
+        face_tri(s, face, i0, i1, i2, v0, e1, e2);
+        intersect_tri(o, d, v0, e1, e2, -kInf, t, u, v);                    // replay (bit-identical)
+        x = o + d * t;
+        bool inside = (fl & RF_INSIDE) != 0;
+        float4 tu = a.r.tau[idx];
+        float3 tau = f3(tu);
+        if (fl & RF_CAPPED) {                                                 // CAP_ENV leaf
+          float3 E = env_eval(s, o, d, adj * tau, &go, &gd);
+          if (inside) { walk = true; gS = -(adj * E * tau); }
+          gNk[0] = gNk[1] = gNk[2] = f3(0, 0, 0);
+        } else {
+          Shade S;
+          shade_forward(s, ior, i0, i1, i2, e1, e2, d, u, v, inside, S);
+          float4 ls = a.r.lsub[idx];
+          int cr = __float_as_int(ls.w), ct = __float_as_int(tu.w);
+          float3 Lr = f3(0, 0, 0), Lt = f3(0, 0, 0), gwr = f3(0, 0, 0), gwt = f3(0, 0, 0);
+          if (cr >= 0) { Lr = f3(a.r.lsub[cr]); gx += f3(a.r.go[cr]); gwr = f3(a.r.gd[cr]); }
+          if (ct >= 0) { Lt = f3(a.r.lsub[ct]); gx += f3(a.r.go[ct]); gwt = f3(a.r.gd[ct]); }
+          float3 ap = adj * tau;
+          float3 Lc = Lr * S.R + Lt * S.T;
+          float gR = S.tir ? 0.0f : dot(ap, Lr - Lt);
+          if (inside) { walk = true; gS = -(adj * Lc * tau); }
+          float3 gd_s;
+          float gi;
+          float3 n0 = f3(__ldg(s.nrm + i0)), n1 = f3(__ldg(s.nrm + i1)), n2 = f3(__ldg(s.nrm + i2));
+          shade_backward(S, gR, gwr, gwt, n0, n1, n2, gd_s, gu, gv, gNk, gi);
+          gd += gd_s;
+          gior += gi;
         }
-        float3 gd_s;
-        float gi;
-        float3 n0 = f3(__ldg(s.nrm + i0)), n1 = f3(__ldg(s.nrm + i1)), n2 = f3(__ldg(s.nrm + i2));
-        shade_backward(S, gR, gwr, gwt, n0, n1, n2, gd_s, gu, gv, gNk, gi);
-        gd += gd_s;
-        gior += gi;
       }
-      // x = o + t d, then the Moller-Trumbore solve
+    }
+    // ---- (B) interior transmittance o -> x
+    if (ABS == 0) {
+      if (walk) transmittance_const_backward(s, o, x, gS, gx, go, gsc);
+    } else {
+      const GridMap gm = grid_map(s);
+      for (unsigned m = __ballot_sync(~0u, walk); m; m &= m - 1) {
+        const int src = __ffs(m) - 1;
+        float3 wgx, wgo;
+        warp_transmittance_backward(s, gm, shfl3(o, src), shfl3(x, src), shfl3(gS, src), a.dsig, wgx, wgo);
+        if (lane_id() == src) { gx += wgx; go += wgo; }
+      }
+    }
+    // ---- (C) x = o + t d, then the Moller-Trumbore solve
+    if (geo) {
       go += gx;
       gd += gx * t;
       float gt = dot(gx, d);
+      float3 gVk[3];
       mt_backward(d, e1, e2, t, u, v, gu, gv, gt, go, gd, gVk);
       atomic_add3(a.dV + i0, gVk[0]);
       atomic_add3(a.dV + i1, gVk[1]);
@@ -551,7 +592,7 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
         atomic_add3(a.dN + i2, gNk[2]);
       }
     }
-    if (k > 0) {                                                              // camera rays: dropped (R22)
+    if (valid && k > 0) {                                                     // camera rays: dropped (R22)
       a.r.go[idx] = f4(go, 0.f);
       a.r.gd[idx] = f4(gd, 0.f);
     }
@@ -565,7 +606,7 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
   }
   if (lane_id() == 0) {
     if (gior != 0.0f) atomicAdd(a.dior, gior);
-    if (s.abs_kind == 0 && (gsc.x != 0.0f || gsc.y != 0.0f || gsc.z != 0.0f)) {
+    if (ABS == 0 && (gsc.x != 0.0f || gsc.y != 0.0f || gsc.z != 0.0f)) {
       atomicAdd(a.dsig, make_float4(gsc.x, gsc.y, gsc.z, 0.f));
     }
   }
@@ -710,9 +751,14 @@ cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count
 }
 
 cudaError_t launch_shade_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
-  static int gs = 0;
-  if (!gs) gs = persistent_blocks((const void*)k_shade_level, kTraceThreads, sm_count);
-  k_shade_level<<<gs, kTraceThreads, 0, st>>>(a, level, max_depth);
+  static int gs0 = 0, gs1 = 0;
+  if (a.s.abs_kind == 0) {
+    if (!gs0) gs0 = persistent_blocks((const void*)k_shade_level<0>, kTraceThreads, sm_count);
+    k_shade_level<0><<<gs0, kTraceThreads, 0, st>>>(a, level, max_depth);
+  } else {
+    if (!gs1) gs1 = persistent_blocks((const void*)k_shade_level<1>, kTraceThreads, sm_count);
+    k_shade_level<1><<<gs1, kTraceThreads, 0, st>>>(a, level, max_depth);
+  }
   return cudaGetLastError();
 }
 
@@ -734,9 +780,14 @@ cudaError_t launch_gather_level(const FwdLaunch& a, int level, int sm_count, cud
 }
 
 cudaError_t launch_backward_level(const BwdLaunch& a, int level, int sm_count, cudaStream_t st) {
-  static int gb = 0;
-  if (!gb) gb = persistent_blocks((const void*)k_backward_level, kBwdThreads, sm_count);
-  k_backward_level<<<gb, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
+  static int gb0 = 0, gb1 = 0;
+  if (a.s.abs_kind == 0) {
+    if (!gb0) gb0 = persistent_blocks((const void*)k_backward_level<0>, kBwdThreads, sm_count);
+    k_backward_level<0><<<gb0, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
+  } else {
+    if (!gb1) gb1 = persistent_blocks((const void*)k_backward_level<1>, kBwdThreads, sm_count);
+    k_backward_level<1><<<gb1, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
+  }
   return cudaGetLastError();
 }
 
