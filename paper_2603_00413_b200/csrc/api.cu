@@ -275,12 +275,12 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
     if (c->gsig) cudaFree(c->gsig);
     c->sigma_snap = c->gsig = nullptr;
     c->sigma_cap = 0;
-    DT_CU(cudaMalloc(&c->sigma_snap, nodes * sizeof(float4)));
+    DT_CU(cudaMalloc(&c->sigma_snap, 2 * nodes * sizeof(float4)));
     DT_CU(cudaMalloc(&c->gsig, nodes * sizeof(float4)));
     c->sigma_cap = nodes;
   }
   c->sigma_len = slen;
-  DT_CU(launch_pack_sigma(ab->sigma, c->sigma_snap, (int64_t)nodes, st));   // [n][3] -> float4 [n]
+  DT_CU(launch_pack_sigma(ab->sigma, c->sigma_snap, (int64_t)nodes, ab->kind == DT_ABS_CONST ? 1 : ab->res, st));
 
   DevScene s = scene_from_ctx(c);
   s.ior = ior;

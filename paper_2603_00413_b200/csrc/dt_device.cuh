@@ -8,6 +8,14 @@
 namespace dt {
 
 constexpr float kInf = __builtin_huge_valf();
+#ifndef DT_WALK_LANES
+#define DT_WALK_LANES 8
+#endif
+#ifndef DT_WALK_LANES_BWD
+#define DT_WALK_LANES_BWD 4
+#endif
+constexpr int kWalkLanes = DT_WALK_LANES;          // lanes per sigma-grid segment walk, forward
+constexpr int kWalkLanesBwd = DT_WALK_LANES_BWD;   // and backward (measured: tools/sweep_walk.sh)
 constexpr int kStackShared = 16;   // short stack entries per thread in shared memory
 constexpr int kStackLocal = 112;   // spill entries per thread (local memory, L1-cached)
 constexpr int kLeafMax = 3;        // triangles per wide-BVH leaf (a contiguous leaf-order range)
@@ -108,6 +116,11 @@ DT_D float exp_scale(unsigned e) { return __uint_as_float(e << 23); }
 DT_D void ldg256(const uint4* p, uint4& a, uint4& b) {
   asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p));
+}
+DT_D void ldg256f(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
       : "l"(p));
 }
 DT_D int wide_ref(uint4 n2, uint4 n3, int c) {
@@ -466,11 +479,9 @@ DT_D void transmittance_const_backward(const DevScene& s, float3 o, float3 x, fl
 }
 
 // Sigma grid (ABS = DT_ABS_GRID): the N midpoint samples x_j = o + t_j (x - o),
-// t_j = (j + 1/2)/N, of ONE segment are evaluated by the whole warp, lane l taking samples
-// l, l + 32, ...  (R10, R11).  A warp therefore walks its interior segments one after the
-// other with every lane busy and all 8 corner loads of a lane's sample in flight at once,
-// instead of each lane walking its own segment sample by sample (divergent, latency bound).
-// Must be called by all 32 lanes with warp-uniform arguments.
+// t_j = (j + 1/2)/N, of an interior segment (R10, R11) are evaluated cooperatively by a group
+// of lanes (group_* below) instead of by the segment's own lane alone (which would leave
+// the warp divergent and serialise ~N/3 dependent corner fetches per lane).
 struct GridMap {
   float3 lo, scl;          // g = (p - lo) * scl, scl = (R-1)/(hi-lo)
   int R, N;
@@ -501,29 +512,85 @@ DT_D bool grid_cell(const GridMap& m, float3 p, int& base, float f[3]) {
   return true;
 }
 
+// The 8 corner values of a cell: 4 x-pair loads (256-bit) of the packed grid.
+DT_D void grid_corners(const DevScene& s, const GridMap& m, int base, float3 c[8]) {
+#pragma unroll
+  for (int yz = 0; yz < 4; ++yz) {
+    float4 p, q;
+    ldg256f(s.sigma + 2 * cell_node((size_t)base, yz << 1, m.R), p, q);
+    c[yz << 1] = f3(p.x, p.y, p.z);
+    c[(yz << 1) | 1] = f3(p.w, q.x, q.y);
+  }
+}
+
 DT_D void corner_weights(const float f[3], float w[8]) {
 #pragma unroll
   for (int k = 0; k < 8; ++k)
     w[k] = ((k & 1) ? f[0] : 1 - f[0]) * ((k & 2) ? f[1] : 1 - f[1]) * ((k & 4) ? f[2] : 1 - f[2]);
 }
 
-// sum_j mu(x_j) * |x - o| / N (the optical depth of R10), returned on every lane.
-DT_D float3 warp_optical_depth(const DevScene& s, const GridMap& m, float3 o, float3 x) {
+// Segments are walked by groups of G lanes (G | 32): the warp takes up to 32/G pending
+// segments at a time, and lane i of a group takes the P = ceil(N/G) consecutive samples
+// [iP, iP + P).  Consecutive samples mostly share a cell, so a lane loads a cell's corners
+// once per run of samples (one dependent load batch per ~3 samples), and the 32/G walks of
+// the warp proceed side by side (memory-level parallelism across segments).
+// group_take: assigns the next pending lanes of the warp-uniform `mask` to the groups;
+// returns this lane's group source lane (-1: idle group) and, in `myq`, the group that walks
+// this lane's own segment (-1: none).
+template <int G>
+DT_D int group_take(unsigned& mask, int& myq) {
+  const int grp = lane_id() / G;
+  int mine = -1;
+  myq = -1;
+#pragma unroll
+  for (int q = 0; q < 32 / G; ++q) {
+    const int src = mask ? __ffs(mask) - 1 : -1;
+    if (mask) mask &= mask - 1;
+    if (q == grp) mine = src;
+    if (src == lane_id()) myq = q;
+  }
+  return mine;
+}
+
+// sum_j mu(x_j) * |x - o| / N (the optical depth of R10) of the group's segment, returned on
+// every lane of the group.  All 32 lanes call it (inactive groups pass active = false).
+template <int G>
+DT_D float3 group_optical_depth(const DevScene& s, const GridMap& m, float3 o, float3 x, bool active) {
   const float3 dx = x - o;
   float3 S = f3(0, 0, 0);
-  for (int j = lane_id(); j < m.N; j += 32) {
-    int base;
-    float f[3], w[8];
-    if (!grid_cell(m, o + dx * (((float)j + 0.5f) / (float)m.N), base, f)) continue;
-    corner_weights(f, w);
-    float4 c[8];
+  if (active) {
+    const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
+    int cur = -1;
+    float3 c[8];
+    float acc[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) c[k] = __ldg(s.sigma + cell_node(base, k, m.R));
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+    for (int j = j0; j < j1; ++j) {
+      int base;
+      float f[3], w[8];
+      if (!grid_cell(m, o + dx * (((float)j + 0.5f) / (float)m.N), base, f)) continue;
+      if (base != cur) {               // new cell: fold the finished run, fetch the corners
+        if (cur >= 0) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) S += f3(c[k]) * w[k];
+          for (int k = 0; k < 8; ++k) {
+            S += c[k] * acc[k];
+            acc[k] = 0.f;
+          }
+        }
+        grid_corners(s, m, base, c);   // consumed at the run's end: latency behind the run
+        cur = base;
+      }
+      corner_weights(f, w);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += w[k];
+    }
+    if (cur >= 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) S += c[k] * acc[k];
+    }
   }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
+  for (int off = G / 2; off > 0; off >>= 1) {
     S.x += __shfl_xor_sync(~0u, S.x, off);
     S.y += __shfl_xor_sync(~0u, S.y, off);
     S.z += __shfl_xor_sync(~0u, S.z, off);
@@ -531,37 +598,49 @@ DT_D float3 warp_optical_depth(const DevScene& s, const GridMap& m, float3 o, fl
   return S * (length(dx) / (float)m.N);
 }
 
-// Reverse of warp_optical_depth given gS = dL/d(optical depth): scatters gS * (l/N) * w_k
-// into the float4 grid adjoint gsig and returns the position adjoints of o and x on every
-// lane.  Lanes whose samples fall in the same cell (contiguous lanes: a segment enters a
-// convex cell once) merge their corner weights with a segmented shuffle reduction first, so
-// each (cell, 32-sample round) costs 8 vector atomics.
-DT_D void warp_transmittance_backward(const DevScene& s, const GridMap& m, float3 o, float3 x, float3 gS,
-                                      float4* gsig, float3& gx, float3& go) {
+// Reverse of group_optical_depth given gS = dL/d(optical depth): scatters gS * (l/N) * w_k
+// into the float4 grid adjoint gsig (each lane merges its run of samples per cell, then 8
+// vector atomics per cell visit) and returns the position adjoints of o and x on every lane
+// of the group.
+template <int G>
+DT_D void group_transmittance_backward(const DevScene& s, const GridMap& m, float3 o, float3 x, float3 gS,
+                                       bool active, float4* gsig, float3& gx, float3& go) {
   const float3 dx = x - o;
   const float l = length(dx);
   const float invN = 1.0f / (float)m.N, sc = l * invN;
   const float3 gSs = gS * sc;
-  const int lane = lane_id();
   float gl = 0.f;
   float3 gsum = f3(0, 0, 0), gtsum = f3(0, 0, 0);
-  for (int j0 = 0; j0 < m.N; j0 += 32) {
-    const int j = j0 + lane;
-    const float t = ((float)j + 0.5f) * invN;
-    int base = -1;
-    float f[3], w[8];
-    const bool in = j < m.N && grid_cell(m, o + dx * t, base, f);
+  if (active) {
+    const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
+    int cur = -1;
+    float acc[8], gk[8];               // the run's weight sums; gS . sigma_k of its cell
 #pragma unroll
-    for (int k = 0; k < 8; ++k) w[k] = 0.f;
-    if (in) {
+    for (int k = 0; k < 8; ++k) acc[k] = gk[k] = 0.f;
+    for (int j = j0; j < j1; ++j) {
+      const float t = ((float)j + 0.5f) * invN;
+      int base;
+      float f[3], w[8];
+      if (!grid_cell(m, o + dx * t, base, f)) continue;
+      if (base != cur) {
+        if (cur >= 0) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            atomicAdd(gsig + cell_node((size_t)cur, k, m.R), make_float4(gSs.x * acc[k], gSs.y * acc[k], gSs.z * acc[k], 0.f));
+            acc[k] = 0.f;
+          }
+        }
+        float3 c[8];
+        grid_corners(s, m, base, c);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) gk[k] = dot(gS, c[k]);
+        cur = base;
+      }
       corner_weights(f, w);
-      float4 c[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) c[k] = __ldg(s.sigma + cell_node(base, k, m.R));
-      float gk[8], gv = 0.f;
+      float gv = 0.f;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        gk[k] = dot(gS, f3(c[k]));
+        acc[k] += w[k];
         gv += w[k] * gk[k];
       }
       // d/dg of sum_k gk_k w_k: differences over each axis' bit
@@ -579,23 +658,14 @@ DT_D void warp_transmittance_backward(const DevScene& s, const GridMap& m, float
       gsum += gp;
       gtsum += gp * t;
     }
-    const unsigned same = __match_any_sync(~0u, base);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const float o2 = __shfl_down_sync(~0u, w[k], off);
-        if (lane + off < 32 && ((same >> (lane + off)) & 1u)) w[k] += o2;
-      }
-    }
-    if (in && lane == __ffs(same) - 1) {
+    if (cur >= 0) {
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        atomicAdd(gsig + cell_node(base, k, m.R), make_float4(gSs.x * w[k], gSs.y * w[k], gSs.z * w[k], 0.f));
+        atomicAdd(gsig + cell_node((size_t)cur, k, m.R), make_float4(gSs.x * acc[k], gSs.y * acc[k], gSs.z * acc[k], 0.f));
     }
   }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
+  for (int off = G / 2; off > 0; off >>= 1) {
     gl += __shfl_xor_sync(~0u, gl, off);
     gsum.x += __shfl_xor_sync(~0u, gsum.x, off);
     gsum.y += __shfl_xor_sync(~0u, gsum.y, off);

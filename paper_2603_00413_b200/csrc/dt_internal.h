@@ -121,7 +121,7 @@ struct dt_ctx {
   int64_t n_rays = 0;
   dt::DevScene fwd_scene{};
   float fwd_t_eps = 1e-4f;
-  float4* sigma_snap = nullptr;  // [1] or [R^3] nodes (rgb + pad)
+  float4* sigma_snap = nullptr;  // [1] or [R^3] nodes, 2 float4 each: x-pairs (k_pack_sigma)
   size_t sigma_cap = 0, sigma_len = 0;   // sigma_len = caller floats (3 or 3 R^3)
   // gradients
   float4* gV = nullptr;       // [nv]
@@ -182,7 +182,7 @@ cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64
                                      float* tuv, int* err_flag, cudaStream_t st);
 cudaError_t launch_bvh_check(dt_ctx* c, long long* out_dev, cudaStream_t st);
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
-cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, cudaStream_t st);
+cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, int res, cudaStream_t st);
 DevScene scene_from_ctx(const dt_ctx* c);
 cudaError_t launch_count_segments(const int* lvl, int max_depth, unsigned long long* seg, cudaStream_t st);
 // optim.cu

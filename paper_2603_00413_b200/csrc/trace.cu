@@ -142,11 +142,12 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int k, int max_depth, b
     if (need_tau) tau = transmittance_const(s, o, x);
   } else {
     const GridMap gm = grid_map(s);
-    for (unsigned m = __ballot_sync(~0u, need_tau); m; m &= m - 1) {      // warp-cooperative walks
-      const int src = __ffs(m) - 1;
-      const float3 so = shfl3(o, src), sx = shfl3(x, src);
-      const float3 Sd = warp_optical_depth(s, gm, so, sx);
-      if (lane_id() == src) tau = f3(expf(-Sd.x), expf(-Sd.y), expf(-Sd.z));
+    for (unsigned m = __ballot_sync(~0u, need_tau); m;) {                // cooperative walks
+      int myq;
+      const int src = group_take<kWalkLanes>(m, myq), sl = max(src, 0);
+      const float3 Sd = group_optical_depth<kWalkLanes>(s, gm, shfl3(o, sl), shfl3(x, sl), src >= 0);
+      const float3 mine = shfl3(Sd, max(myq, 0) * kWalkLanes);
+      if (myq >= 0) tau = f3(expf(-mine.x), expf(-mine.y), expf(-mine.z));
     }
   }
   if (capped) {
@@ -569,11 +570,14 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
       if (walk) transmittance_const_backward(s, o, x, gS, gx, go, gsc);
     } else {
       const GridMap gm = grid_map(s);
-      for (unsigned m = __ballot_sync(~0u, walk); m; m &= m - 1) {
-        const int src = __ffs(m) - 1;
+      for (unsigned m = __ballot_sync(~0u, walk); m;) {
+        int myq;
+        const int src = group_take<kWalkLanesBwd>(m, myq), sl = max(src, 0);
         float3 wgx, wgo;
-        warp_transmittance_backward(s, gm, shfl3(o, src), shfl3(x, src), shfl3(gS, src), a.dsig, wgx, wgo);
-        if (lane_id() == src) { gx += wgx; go += wgo; }
+        group_transmittance_backward<kWalkLanesBwd>(s, gm, shfl3(o, sl), shfl3(x, sl), shfl3(gS, sl), src >= 0,
+                                                    a.dsig, wgx, wgo);
+        const float3 mx = shfl3(wgx, max(myq, 0) * kWalkLanesBwd), mo = shfl3(wgo, max(myq, 0) * kWalkLanesBwd);
+        if (myq >= 0) { gx += mx; go += mo; }
       }
     }
     // ---- (C) x = o + t d, then the Moller-Trumbore solve
@@ -661,9 +665,17 @@ __global__ void k_finalize(const float4* __restrict__ gV, const float4* __restri
   }
 }
 
-__global__ void k_pack_sigma(const float* __restrict__ in, float4* __restrict__ out, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = make_float4(in[3 * i], in[3 * i + 1], in[3 * i + 2], 0.f);
+// sigma [n][3] -> x-pairs: out[2i], out[2i+1] = (sigma_i, sigma_{i+1 along x}, 0, 0), 32 B per
+// node so that one 256-bit load fetches both x-corners of a cell edge (res = x extent; the
+// last x node of a row pairs with zeros; constant sigma: res = 1).
+__global__ void k_pack_sigma(const float* __restrict__ in, float4* __restrict__ out, int64_t n, int res) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool nx = (i % res) + 1 < res;
+    const float a = in[3 * i], b = in[3 * i + 1], c = in[3 * i + 2];
+    const float d = nx ? in[3 * i + 3] : 0.f, e = nx ? in[3 * i + 4] : 0.f, f = nx ? in[3 * i + 5] : 0.f;
+    out[2 * i] = make_float4(a, b, c, d);
+    out[2 * i + 1] = make_float4(e, f, 0.f, 0.f);
+  }
 }
 
 __global__ void k_unpack_add(const float4* __restrict__ src, float* __restrict__ dst, int64_t n, int acc) {
@@ -826,9 +838,9 @@ cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, cudaStream_t st) {
+cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, int res, cudaStream_t st) {
   int g = (int)std::min<int64_t>((nodes + 255) / 256, 148 * 16);
-  k_pack_sigma<<<std::max(g, 1), 256, 0, st>>>(in, out, nodes);
+  k_pack_sigma<<<std::max(g, 1), 256, 0, st>>>(in, out, nodes, std::max(res, 1));
   return cudaGetLastError();
 }
 
