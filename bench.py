@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import dataclasses
+import glob
 import json
 import os
 import subprocess
@@ -42,18 +43,46 @@ def hbm_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock and throttle reasons sampled during the timed region: NVML polled every 10 ms
+    from a thread (so short runs still get samples), else nvidia-smi -lms 200."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []           # (sm_mhz, max_mhz, set of reasons)
+        self.stop_flag = threading.Event()
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self.nvml = pynvml
+
+            def poll():
+                while not self.stop_flag.is_set():
+                    sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, mx, {n for n, b in bits.items() if r & b}))
+                    time.sleep(0.01)
+
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -72,29 +101,33 @@ class ClockSampler:
             self.lines.append(ln.strip())
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 7:
-                continue
+        if self.nvml is not None:
+            self.stop_flag.set()
+            self.t.join(timeout=1)
+            src = "nvml"
+        elif self.proc is not None:
+            self.proc.terminate()
             try:
-                sm.append(float(p[0]))
-                mx.append(float(p[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            src = "nvidia-smi"
+            for ln in self.lines:
+                p = [x.strip() for x in ln.split(",")]
+                if len(p) < 7:
+                    continue
+                try:
+                    self.samples.append((float(p[0]), float(p[1]),
+                                         {nm for nm, v in zip(self.NAMES, p[3:7]) if v.lower().startswith("active")}))
+                except ValueError:
+                    continue
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
+        sm = [x[0] for x in self.samples]
+        reasons = set().union(*[x[2] for x in self.samples]) if self.samples else set()
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(x[1] for x in self.samples) if self.samples else None,
+                "reasons": sorted(reasons), "samples": len(sm), "source": src}
 
 
 def target_scene(sc):
@@ -264,9 +297,17 @@ def run_ours(args, rank, world, local_rank):
     bytes_per_launch = ab[cls] / max(ab[f"{cls}_launches"], 1)
     achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9
     kname = {"trace": "k_traverse_level", "shade": "k_shade_level", "bwd": "k_backward_level"}[cls]
+    traffic, traffic_src = None, None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*traffic*.json"))):
+        try:
+            t = json.load(open(f))
+        except Exception:
+            continue
+        if t.get("config") == args.config and t.get("kernel") == kname:
+            traffic, traffic_src = float(t["dram_bytes_per_launch"]), os.path.relpath(f, ROOT)
     roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                 "note": "SURVEY 8(d) algorithmic bytes: ray in + hit out + counted node (64 B) and triangle "
                         "(48 B) fetches; the LBVH is L2-resident, so DRAM traffic (ncu, profiles/) is far lower",
                 "bytes_per_launch": int(bytes_per_launch), "ms_per_launch": round(ms_per_launch, 3),

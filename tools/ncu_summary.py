@@ -51,8 +51,9 @@ def report(path):
 
 if __name__ == "__main__":
     tag, launch_csv, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
-    md = [f"# ncu summary {tag}", "", "Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`):", "",
-          launches(launch_csv), ""]
+    md = [f"# ncu summary {tag}", ""]
+    if launch_csv != "-":
+        md += ["Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`):", "", launches(launch_csv), ""]
     for r in reps:
         md += [f"## {r}", "", report(r), ""]
     print("\n".join(md))
