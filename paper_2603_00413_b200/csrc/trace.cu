@@ -65,9 +65,6 @@ DT_D int64_t level_base(const int* lvl, int k) {
   for (int j = 1; j < k; ++j) off += lvl[LV_CNT + j];
   return off;
 }
-DT_D int64_t rec_index(const int* lvl, int64_t cap, int k, int64_t item) {
-  return k == 0 ? cap - 1 - item : level_base(lvl, k) + item;
-}
 
 DT_D void sig_add(unsigned long long* sig, int64_t r, uint64_t key) {
   if (sig) atomicAdd(sig + r, (unsigned long long)dt_mix64(key));
@@ -89,7 +86,8 @@ DT_D void flush_counters(unsigned long long* c, int visits, int tests) {
 // Shade one traced segment (record idx at level k) and spawn its children into level k+1.
 // All 32 lanes of the warp must call this (the compaction is a warp collective).
 template <int ABS>
-DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int k, int max_depth, bool valid, int64_t idx, float3 o, float3 d,
+DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int64_t lim, int k, int max_depth,
+                          bool valid, int64_t idx, float3 o, float3 d,
                           int64_t ray, uint32_t pos, float3 thr, float w, int face, float t, float u, float v) {
   const DevScene& s = a.s;
   bool is_hit = valid && face >= 0;
@@ -164,8 +162,7 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int k, int max_depth, b
     base = __shfl_sync(~0u, base, 0);
   }
   if (spawn_r) {
-    int64_t off = level_base(a.lvl, k + 1);
-    int64_t lim = a.cap - a.lvl[LV_CNT + 0];
+    const int64_t off = child_off;
     int64_t cr = -1, ct = -1;
     int64_t j = off + base + __popc(mr & lanemask_lt());
     if (j < lim) {
@@ -200,9 +197,10 @@ __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
   const DevScene& s = a.s;
   float3 blo = f3(s.scal[0], s.scal[1], s.scal[2]), bhi = f3(s.scal[3], s.scal[4], s.scal[5]);
   int err = 0, visits = 0, tests = 0, traced = 0;
-  while (true) {
-    int base = fetch_work(a.lvl + LV_WORK_PRIMARY);
-    if (base >= a.n_items) break;
+  int base = fetch_work(a.lvl + LV_WORK_PRIMARY);
+  while (base < a.n_items) {
+    int next = 0;                     // the next chunk's atomic is in flight during this one
+    if (lane_id() == 0) next = atomicAdd(a.lvl + LV_WORK_PRIMARY, 32);
     int64_t item = (int64_t)base + lane_id();
     bool valid = item < a.n_items;
     int64_t pid = 0;
@@ -254,6 +252,7 @@ __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
       __stcs(a.r.thr + idx, make_float4(1.f, 1.f, 1.f, 1.f));
       __stcs(a.r.hit + idx, make_float4(__int_as_float(face), t, u, v));   // shaded by k_shade_level(0)
     }
+    base = __shfl_sync(~0u, next, 0);
   }
   if (err) a.lvl[LV_STACKERR] = 1;
   for (int o = 16; o > 0; o >>= 1) traced += __shfl_xor_sync(~0u, traced, o);
@@ -268,13 +267,16 @@ template <int ABS>
 __global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
   if (a.lvl[LV_OVERFLOW]) return;   // arena too small: the host grows it and re-runs
   const float ior = a.s.ior_ptr ? __ldg(a.s.ior_ptr) : a.s.ior;
-  int n = a.lvl[LV_CNT + k];
-  while (true) {
-    int base = fetch_work(a.lvl + LV_WORK_SHADE + k);
-    if (base >= n) break;
-    int64_t item = (int64_t)base + lane_id();
-    bool valid = item < n;
-    int64_t idx = rec_index(a.lvl, a.cap, k, item);
+  // level offsets are fixed while this kernel runs (only level k+1's count grows): read once
+  const int n = a.lvl[LV_CNT + k];
+  const int64_t off = k == 0 ? 0 : level_base(a.lvl, k);
+  const int64_t child_off = level_base(a.lvl, k + 1);
+  const int64_t lim = a.cap - a.lvl[LV_CNT + 0];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t wbase = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); wbase < n; wbase += stride) {
+    const int64_t item = wbase + lane_id();
+    const bool valid = item < n;
+    const int64_t idx = k == 0 ? a.cap - 1 - item : off + item;
     float3 o = f3(0, 0, 0), d = f3(0, 0, 1), thr = f3(0, 0, 0);
     float w = 0.f;
     int64_t ray = 0;
@@ -288,7 +290,7 @@ __global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
       pos = __float_as_uint(rd.w);
       face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
     }
-    shade_and_spawn<ABS>(a, ior, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
+    shade_and_spawn<ABS>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
   }
 }
 
@@ -461,9 +463,10 @@ __global__ void DT_TRAV_LB k_traverse_level_ws(FwdLaunch a, int k) {
 // Bottom-up radiance: L = tau * (R L_r + T L_t); level 0 writes the pixel.
 __global__ void k_gather(FwdLaunch a, int k) {
   if (a.lvl[LV_OVERFLOW]) return;
-  int n = a.lvl[LV_CNT + k];
+  const int n = a.lvl[LV_CNT + k];
+  const int64_t off = k == 0 ? 0 : level_base(a.lvl, k);
   for (int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; item < n; item += (int64_t)gridDim.x * blockDim.x) {
-    int64_t idx = rec_index(a.lvl, a.cap, k, item);
+    const int64_t idx = k == 0 ? a.cap - 1 - item : off + item;
     float4 h = a.r.hit[idx];
     int fl = __float_as_int(h.w);
     float4 ls = a.r.lsub[idx];
@@ -503,6 +506,7 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
   if (a.lvl[LV_OVERFLOW]) return;   // an overflowed (asynchronous) forward: nothing valid to replay
   const float ior = s.ior_ptr ? __ldg(s.ior_ptr) : s.ior;
   const int n = a.lvl[LV_CNT + k];
+  const int64_t off = k == 0 ? 0 : level_base(a.lvl, k);
   float gior = 0.0f;
   float3 gsc = f3(0, 0, 0);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -518,7 +522,7 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
     bool geo = false, walk = false;
     // ---- (A)
     if (valid) {
-      idx = rec_index(a.lvl, cap, k, item);
+      idx = k == 0 ? cap - 1 - item : off + item;
       float4 ro = a.r.o[idx], rd = a.r.d[idx], rt = a.r.thr[idx], h = a.r.hit[idx];
       o = f3(ro);
       d = f3(rd);
