@@ -44,6 +44,7 @@ class _Scene(C.Structure):
         ("c2w", C.c_void_p),
         ("max_depth", C.c_int32), ("cap_policy", C.c_int32), ("t_eps", C.c_double),
         ("V64", C.c_void_p), ("sigma64", C.c_void_p),
+        ("hash_levels", C.c_int32), ("hash_log2_size", C.c_int32), ("hash_res", C.c_int32 * 32),
     ]
 
 
@@ -92,6 +93,11 @@ class OracleScene:
             s.sigma_lo = (C.c_float * 3)(*[float(x) for x in ab.box_lo])
             s.sigma_hi = (C.c_float * 3)(*[float(x) for x in ab.box_hi])
         s.n_samples = ab.n_samples
+        if ab.kind == 2:                                   # hash grid (R29)
+            T = ab.sigma.shape[1]
+            assert T & (T - 1) == 0 and len(ab.level_res) <= 32
+            s.hash_levels, s.hash_log2_size = len(ab.level_res), T.bit_length() - 1
+            s.hash_res = (C.c_int32 * 32)(*[int(x) for x in ab.level_res])
         s.env_kind = env.kind
         amb = env.ambient if env.ambient is not None else np.zeros(3)
         s.ambient = (C.c_float * 3)(*[float(x) for x in amb])

@@ -117,6 +117,13 @@ void vertex_normals(const std::vector<V3<S>>& V, const int32_t* F, int nf, std::
   }
 }
 
+// Number of absorption parameters (R11, R29).
+size_t sigma_len(const dto_scene* sc) {
+  if (sc->abs_kind == 0) return 3;
+  if (sc->abs_kind == 2) return (size_t)sc->hash_levels * ((size_t)1 << sc->hash_log2_size) * 3;
+  return (size_t)sc->sigma_res * sc->sigma_res * sc->sigma_res * 3;
+}
+
 template <class S>
 Model<S> make_model(const dto_scene* sc, const double* tV, double tior, const double* tsig) {
   Model<S> m;
@@ -130,7 +137,7 @@ Model<S> make_model(const dto_scene* sc, const double* tV, double tior, const do
   }
   vertex_normals(m.V, sc->F, m.nf, m.nrm);
   m.ior = lift<S>(sc->ior, tior);
-  size_t ns = sc->abs_kind == 0 ? 3 : (size_t)sc->sigma_res * sc->sigma_res * sc->sigma_res * 3;
+  size_t ns = sigma_len(sc);
   m.sigma.resize(ns);
   for (size_t i = 0; i < ns; ++i)
     m.sigma[i] = lift<S>(sc->sigma64 ? sc->sigma64[i] : (double)sc->sigma[i], tsig ? tsig[i] : 0.0);
@@ -254,10 +261,54 @@ Iface<S> interface(V3<S> d, V3<S> n, S eta_i, S eta_t) {
 }
 
 // ----------------------------------------------------------------------------- absorption
+// Table entry of corner (x, y, z) of hash level l (R29): iNGP's dense index while the level's
+// (N+1)^3 vertices fit in the table, else its spatial hash with primes (1, 2654435761,
+// 805459861), xor-combined in 32-bit arithmetic, modulo T = 2^log2_size.
+size_t hash_entry(const dto_scene* sc, int l, int x, int y, int z) {
+  const uint32_t T = 1u << sc->hash_log2_size;
+  const uint64_t n1 = (uint64_t)sc->hash_res[l] + 1;
+  size_t e;
+  if (n1 * n1 * n1 <= T) e = (size_t)(x + n1 * (y + n1 * (uint64_t)z));
+  else e = (size_t)(((uint32_t)x * 1u ^ (uint32_t)y * 2654435761u ^ (uint32_t)z * 805459861u) & (T - 1));
+  return (size_t)l * T + e;
+}
+
+// mu_t(p) of the hash grid: sum over levels of the trilinear interpolation of the level's
+// (N_l + 1)^3 vertex values (looked up through hash_entry); zero outside the box (R11).
+template <class S>
+void sigma_at_hash(const Model<S>& m, V3<S> p, S out[3]) {
+  const dto_scene* sc = m.sc;
+  for (int c = 0; c < 3; ++c) out[c] = S(0.0);
+  S u[3];
+  for (int a = 0; a < 3; ++a) {
+    S lo = S((double)sc->sigma_lo[a]), hi = S((double)sc->sigma_hi[a]);
+    u[a] = (comp(p, a) - lo) / (hi - lo);
+    if (val(u[a]) < 0.0 || val(u[a]) > 1.0) return;
+  }
+  for (int l = 0; l < sc->hash_levels; ++l) {
+    const int N = sc->hash_res[l];
+    int i0[3];
+    S f[3];
+    for (int a = 0; a < 3; ++a) {
+      S g = u[a] * S((double)N);
+      i0[a] = std::min((int)std::floor(val(g)), N - 1);
+      f[a] = g - S((double)i0[a]);
+    }
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+          S w = (dx ? f[0] : S(1.0) - f[0]) * (dy ? f[1] : S(1.0) - f[1]) * (dz ? f[2] : S(1.0) - f[2]);
+          size_t e = hash_entry(sc, l, i0[0] + dx, i0[1] + dy, i0[2] + dz);
+          for (int c = 0; c < 3; ++c) out[c] = out[c] + w * m.sigma[e * 3 + c];
+        }
+  }
+}
+
 // mu_t(p): R^3 vertex-centred nodes over the fixed box, trilinear, zero outside (R11).
 template <class S>
 void sigma_at(const Model<S>& m, V3<S> p, S out[3]) {
   const dto_scene* sc = m.sc;
+  if (sc->abs_kind == 2) { sigma_at_hash(m, p, out); return; }
   int R = sc->sigma_res;
   S g[3];
   int i0[3];
@@ -448,8 +499,49 @@ struct Bwd { V3d L, go, gd; };
 
 // d value / d p of the vertex-centred sigma grid, accumulating the node adjoints.
 // Returns gp = sum_c gS_c * scale * grad sigma_c(p); adds gS_c * scale * w to node c.
+V3d sigma_bwd_hash(const Model<double>& m, V3d p, const double gSs[3], Grad& G, double Sv[3]) {
+  const dto_scene* sc = m.sc;
+  Sv[0] = Sv[1] = Sv[2] = 0.0;
+  double u[3], inv[3];
+  for (int a = 0; a < 3; ++a) {
+    double lo = sc->sigma_lo[a], hi = sc->sigma_hi[a];
+    u[a] = (comp(p, a) - lo) / (hi - lo);
+    if (u[a] < 0.0 || u[a] > 1.0) return {0, 0, 0};
+    inv[a] = 1.0 / (hi - lo);
+  }
+  V3d gp = {0, 0, 0};
+  for (int l = 0; l < sc->hash_levels; ++l) {
+    const int N = sc->hash_res[l];
+    int i0[3];
+    double f[3];
+    for (int a = 0; a < 3; ++a) {
+      double g = u[a] * N;
+      i0[a] = std::min((int)std::floor(g), N - 1);
+      f[a] = g - i0[a];
+    }
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+          double wx = dx ? f[0] : 1 - f[0], wy = dy ? f[1] : 1 - f[1], wz = dz ? f[2] : 1 - f[2];
+          double w = wx * wy * wz;
+          double sx = dx ? 1.0 : -1.0, sy = dy ? 1.0 : -1.0, sz = dz ? 1.0 : -1.0;
+          size_t e = hash_entry(sc, l, i0[0] + dx, i0[1] + dy, i0[2] + dz);
+          for (int c = 0; c < 3; ++c) {
+            double s = m.sigma[e * 3 + c];
+            Sv[c] += w * s;
+            G.gsig[e * 3 + c] += gSs[c] * w;
+            gp.x += gSs[c] * s * sx * wy * wz * N * inv[0];
+            gp.y += gSs[c] * s * wx * sy * wz * N * inv[1];
+            gp.z += gSs[c] * s * wx * wy * sz * N * inv[2];
+          }
+        }
+  }
+  return gp;
+}
+
 V3d sigma_bwd(const Model<double>& m, V3d p, const double gSs[3], Grad& G, double Sv[3]) {
   const dto_scene* sc = m.sc;
+  if (sc->abs_kind == 2) return sigma_bwd_hash(m, p, gSs, G, Sv);
   int R = sc->sigma_res;
   double g[3], f[3], inv[3];
   int i0[3];
@@ -913,7 +1005,7 @@ int dto_env(const dto_scene* s, const double* o, const double* d, double* out) {
 int dto_transmittance(const dto_scene* s, const double* o, const double* x, double* out) {
   Model<double> m;
   m.sc = s;
-  size_t ns = s->abs_kind == 0 ? 3 : (size_t)s->sigma_res * s->sigma_res * s->sigma_res * 3;
+  size_t ns = sigma_len(s);
   if (s->sigma64) m.sigma.assign(s->sigma64, s->sigma64 + ns);
   else m.sigma.assign(s->sigma, s->sigma + ns);
   V3d t = transmittance(m, V3d{o[0], o[1], o[2]}, V3d{x[0], x[1], x[2]});

@@ -23,7 +23,7 @@ typedef struct {
   const int32_t* F;
   double ior;                       /* eta_o of the object, P:110 (R1)                 */
   /* absorption mu_t, P:124-138 (R10, R11) */
-  int32_t abs_kind;                 /* 0 = constant [3], 1 = grid [R][R][R][3] = [z][y][x][c] */
+  int32_t abs_kind;                 /* 0 = constant [3], 1 = grid [R][R][R][3] = [z][y][x][c], 2 = hash */
   const float* sigma;
   int32_t sigma_res;
   float sigma_lo[3], sigma_hi[3];
@@ -50,6 +50,13 @@ typedef struct {
   /* optional float64 overrides (NULL = use V / sigma): finite-difference pins perturb in double */
   const double* V64;
   const double* sigma64;
+  /* abs_kind 2 = multiresolution hash grid ("differentiable 3D texture", R29): sigma ->
+   * tables [hash_levels][2^hash_log2_size][3]; level l has hash_res[l] cells per axis over the
+   * box; mu = sum over levels of the trilinear lookup (dense index when (N+1)^3 <= T, else
+   * the spatial hash (x * 1) ^ (y * 2654435761) ^ (z * 805459861) mod T). */
+  int32_t hash_levels;
+  int32_t hash_log2_size;
+  int32_t hash_res[32];
 } dto_scene;
 
 /* Per-ray flag bits (parity protocol). */

@@ -34,6 +34,7 @@ ENV_ANALYTIC = 0
 ENV_GRID = 1
 ABS_CONST = 0
 ABS_GRID = 1
+ABS_HASH = 2
 CAP_ZERO = 0
 CAP_ENV = 1
 
@@ -396,14 +397,21 @@ def constant_env(value=(1.0, 1.0, 1.0)) -> Env:
 @dataclasses.dataclass
 class Absorption:
     kind: int
-    sigma: np.ndarray                # [3] or [R,R,R,3] = [z][y][x][c]
+    sigma: np.ndarray                # [3], [R,R,R,3] = [z][y][x][c], or hash tables [L,T,3]
     box_lo: np.ndarray = None
     box_hi: np.ndarray = None
     n_samples: int = 64
+    level_res: np.ndarray = None     # hash: int32 [L] cells per axis of each level (N_l)
 
     @property
     def res(self):
-        return 0 if self.kind == ABS_CONST else self.sigma.shape[0]
+        if self.kind == ABS_CONST:
+            return 0
+        return self.sigma.shape[1] if self.kind == ABS_HASH else self.sigma.shape[0]
+
+    @property
+    def levels(self):
+        return 0 if self.level_res is None else len(self.level_res)
 
 
 def const_absorption(sigma=(0.2, 0.5, 1.0)) -> Absorption:
@@ -427,6 +435,33 @@ def grid_absorption(V: np.ndarray, res: int, seed: int, n_samples: int = 64, vma
     sig = s[..., None] * top + (1 - s[..., None]) * bot
     sig = np.clip(sig * (1.0 + ripple[..., None]), 0.0, vmax)
     return Absorption(ABS_GRID, sig.astype(np.float32), lo.astype(np.float32), hi.astype(np.float32), n_samples)
+
+
+def hash_level_res(levels: int, base: int, top: int) -> np.ndarray:
+    """N_l = floor(N_min b^l), b = exp((ln N_max - ln N_min) / (L - 1)) (iNGP's geometric
+    progression of grid resolutions; R29).  Integers, computed once here."""
+    if levels == 1:
+        return np.array([base], np.int32)
+    b = np.exp((np.log(top) - np.log(base)) / (levels - 1))
+    return np.floor(base * b ** np.arange(levels) + 1e-9).astype(np.int32)
+
+
+def hash_absorption(V: np.ndarray, seed: int, levels: int = 16, log2_size: int = 19, base: int = 16, top: int = 512,
+                    n_samples: int = 64, vmax: float = 3.0, detail: float = 0.05) -> Absorption:
+    """Multiresolution hash-grid absorption (the paper's iNGP "3D texture"; R29) over
+    the object box + 5%: level 0 (dense) holds the two-tone field of grid_absorption at its
+    (N_0 + 1)^3 vertices, every finer level small non-negative noise U[0, detail vmax / L]
+    (all entries >= 0, so mu >= 0).  Tables [L][T][3], T = 2^log2_size."""
+    res = hash_level_res(levels, base, top)
+    T = 1 << log2_size
+    coarse = grid_absorption(V, int(res[0]) + 1, seed, n_samples, vmax)
+    g = rng(seed, 43)
+    tab = g.uniform(0.0, detail * vmax / levels, (levels, T, 3)).astype(np.float32)
+    n0 = (int(res[0]) + 1) ** 3
+    assert n0 <= T, "level 0 must be dense"
+    tab[0, :n0] = coarse.sigma.reshape(-1, 3)
+    tab[0, n0:] = 0.0
+    return Absorption(ABS_HASH, tab, coarse.box_lo, coarse.box_hi, n_samples, res)
 
 
 # --------------------------------------------------------------------------- scene
@@ -479,6 +514,16 @@ def config_c4(seed: int = 4, n_views: int = 50, res: int = 800, vres: int = 128,
     return Scene("C4", V, F, 1.5, grid_absorption(V, sigma_res, seed), grid_env(seed, vres, pres), cams, 6)
 
 
+def config_c4h(seed: int = 4, n_views: int = 8, res: int = 800, vres: int = 128, pres: int = 1024,
+               levels: int = 16, log2_size: int = 19) -> Scene:
+    """NEXT-2 workload: C4's geometry with the paper's hash-grid absorption texture (R29),
+    8 views (each interior sample reads 16 levels x 8 corners)."""
+    V, F = knot_and_gems(seed)
+    r = float(np.linalg.norm(V, axis=1).max())
+    cams = hemisphere_cameras(n_views, res, res, 3.0 * r, r, seed)
+    return Scene("C4H", V, F, 1.5, hash_absorption(V, seed, levels, log2_size), grid_env(seed, vres, pres), cams, 6)
+
+
 def config_c5(seed: int = 5, n_views: int = 200, res: int = 1024, vres: int = 128, pres: int = 1024) -> Scene:
     V, F = cube_sphere(289, seed)
     r = float(np.linalg.norm(V, axis=1).max())
@@ -486,7 +531,7 @@ def config_c5(seed: int = 5, n_views: int = 200, res: int = 1024, vres: int = 12
     return Scene("C5", V, F, 1.5, const_absorption(), grid_env(seed, vres, pres), cams, 4)
 
 
-CONFIGS = {"C1": config_c1, "C2": config_c2, "C3": config_c3, "C4": config_c4, "C5": config_c5}
+CONFIGS = {"C1": config_c1, "C2": config_c2, "C3": config_c3, "C4": config_c4, "C4H": config_c4h, "C5": config_c5}
 
 
 # --------------------------------------------------------------------------- sampling helpers

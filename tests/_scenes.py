@@ -44,3 +44,8 @@ def linear_grid_env(vres=5, pres=4, radius=10.0, coeff=((1, 0, 0), (0, 1, 0), (0
 
 def small_sigma_grid(V, res=6, seed=3):
     return S.grid_absorption(np.asarray(V), res, seed, n_samples=16)
+
+
+def small_hash_grid(V, levels=3, log2_size=6, base=2, top=8, seed=3, n_samples=16):
+    """Tiny hash-grid absorption (R29): level 0 dense, finer levels hashed with collisions."""
+    return S.hash_absorption(np.asarray(V), seed, levels, log2_size, base, top, n_samples=n_samples, detail=0.6)
