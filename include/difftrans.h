@@ -50,7 +50,7 @@ typedef enum {
                                 invalid (zero); the arena has been grown -- re-run that step  */
 } dt_status;
 
-enum { DT_ABS_CONST = 0, DT_ABS_GRID = 1 };
+enum { DT_ABS_CONST = 0, DT_ABS_GRID = 1, DT_ABS_HASH = 2 };
 enum { DT_ENV_ANALYTIC = 0, DT_ENV_GRID = 1 };
 enum { DT_CAP_ZERO = 0, DT_CAP_ENV = 1 };
 #define DT_MAX_DEPTH 15
@@ -58,14 +58,24 @@ enum { DT_CAP_ZERO = 0, DT_CAP_ENV = 1 };
 /* Absorption rate mu_t(x), P:124-138 ("differentiable 3D texture").  Per-channel RGB (R11).
  *  CONST: sigma -> float[3].
  *  GRID:  sigma -> float[res][res][res][3] = [z][y][x][c], vertex-centred nodes spanning the
- *         fixed box [box_lo, box_hi]; trilinear; zero outside the box (R11).  Interior
- *         segments integrate it with n_samples midpoint samples (R10). */
+ *         fixed box [box_lo, box_hi]; trilinear; zero outside the box (R11).
+ *  HASH:  the paper's iNGP texture (P:138 cites Mueller et al.; R29): sigma -> tables
+ *         float[levels][2^log2_size][3]; level l is a grid of level_res[l] cells per axis over
+ *         the box, its (N+1)^3 vertices stored densely (index x + (N+1)(y + (N+1) z)) while they
+ *         fit in the table, else through iNGP's spatial hash (x*1 ^ y*2654435761 ^
+ *         z*805459861) mod 2^log2_size; mu(x) = sum over levels of the trilinear lookups, zero
+ *         outside the box.  res is ignored.  levels in [1, 32], log2_size in [1, 26].
+ * Interior segments integrate mu with n_samples midpoint samples (R10).  The
+ * gradient (dt_trace_backward grad_sigma) has sigma's layout. */
 typedef struct {
   int32_t kind;
   const float* sigma;
   int32_t res;
   float box_lo[3], box_hi[3];
   int32_t n_samples;
+  int32_t levels;          /* HASH only */
+  int32_t log2_size;       /* HASH only */
+  int32_t level_res[32];   /* HASH only: cells per axis of each level (N_l >= 1) */
 } dt_absorption;
 
 /* Frozen environment radiance, P:91 and P:160 step 3 (R14).

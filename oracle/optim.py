@@ -53,6 +53,35 @@ def _trilinear(sig, lo, hi, p):
     return val, nodes
 
 
+def _hash_lookup(ab, sig, lo, hi, p):
+    """value and (entry, weight) list of the hash texture at p (R29): the sum over levels of
+    the trilinear lookup, corner (x, y, z) of level l stored at x + (N+1)(y + (N+1) z) while
+    (N+1)^3 <= T, else at iNGP's hash (x * 1 ^ y * 2654435761 ^ z * 805459861) mod T."""
+    u = (np.asarray(p, np.float64) - lo) / (hi - lo)
+    if np.any(u < 0) or np.any(u > 1):
+        return np.zeros(3), []
+    T = sig.shape[1]
+    val = np.zeros(3)
+    ents = []
+    for l, N in enumerate(ab.level_res):
+        N = int(N)
+        g = u * N
+        i0 = np.minimum(np.floor(g).astype(int), N - 1)
+        f = g - i0
+        for dz in (0, 1):
+            for dy in (0, 1):
+                for dx in (0, 1):
+                    x, y, z = int(i0[0] + dx), int(i0[1] + dy), int(i0[2] + dz)
+                    if (N + 1) ** 3 <= T:
+                        e = x + (N + 1) * (y + (N + 1) * z)
+                    else:
+                        e = ((x * 1) ^ (y * 2654435761) ^ (z * 805459861)) % (1 << 32) % T
+                    w = (f[0] if dx else 1 - f[0]) * (f[1] if dy else 1 - f[1]) * (f[2] if dz else 1 - f[2])
+                    val += w * sig[l, e]
+                    ents.append(((l, e), w))
+    return val, ents
+
+
 def sigma_regularizers(absorption, points, xi, lambda_smooth, lambda_vol):
     """(L_mat, L_vol, grad) for scenes.Absorption; grad has sigma's shape."""
     sig = np.asarray(absorption.sigma, np.float64)
@@ -60,13 +89,17 @@ def sigma_regularizers(absorption, points, xi, lambda_smooth, lambda_vol):
         return 0.0, float(sig @ sig), 2.0 * lambda_vol * sig
     lo = np.asarray(absorption.box_lo, np.float64)
     hi = np.asarray(absorption.box_hi, np.float64)
+    if absorption.kind == 2:
+        lookup = lambda p: _hash_lookup(absorption, sig, lo, hi, p)
+    else:
+        lookup = lambda p: _trilinear(sig, lo, hi, p)
     pts = np.asarray(points, np.float64)
     n = pts.shape[0]
     grad = np.zeros_like(sig)
     Lm = Lv = 0.0
     for i in range(n):
-        mv, nv = _trilinear(sig, lo, hi, pts[i])
-        mu, nu = _trilinear(sig, lo, hi, pts[i] + np.asarray(xi[i], np.float64))
+        mv, nv = lookup(pts[i])
+        mu, nu = lookup(pts[i] + np.asarray(xi[i], np.float64))
         d = mv - mu
         Lm += float(np.abs(d).sum())
         Lv += float(mv @ mv)

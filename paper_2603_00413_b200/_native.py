@@ -21,7 +21,8 @@ DT_MAX_DEPTH = 15
 
 class Absorption(C.Structure):
     _fields_ = [("kind", C.c_int32), ("sigma", C.c_void_p), ("res", C.c_int32), ("box_lo", C.c_float * 3),
-                ("box_hi", C.c_float * 3), ("n_samples", C.c_int32)]
+                ("box_hi", C.c_float * 3), ("n_samples", C.c_int32), ("levels", C.c_int32), ("log2_size", C.c_int32),
+                ("level_res", C.c_int32 * 32)]
 
 
 class Env(C.Structure):

@@ -56,6 +56,24 @@ cudaError_t alloc_arena(dt_ctx* c, int64_t cap) {
   return cudaSuccess;
 }
 
+// Absorption parameter block checks and sizes (R11, R29).
+bool abs_valid(const dt_absorption* ab) {
+  if (ab->kind == DT_ABS_CONST) return true;
+  if (ab->n_samples < 1) return false;
+  if (ab->kind == DT_ABS_GRID) return ab->res >= 2;
+  if (ab->kind != DT_ABS_HASH || ab->levels < 1 || ab->levels > 32 || ab->log2_size < 1 || ab->log2_size > 26)
+    return false;
+  for (int l = 0; l < ab->levels; ++l)
+    if (ab->level_res[l] < 1 || ab->level_res[l] > (1 << 20)) return false;
+  return true;
+}
+
+size_t abs_nodes(const dt_absorption* ab) {
+  if (ab->kind == DT_ABS_CONST) return 1;
+  if (ab->kind == DT_ABS_HASH) return (size_t)ab->levels << ab->log2_size;
+  return (size_t)ab->res * ab->res * ab->res;
+}
+
 int64_t arena_limit() {
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
@@ -256,8 +274,8 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   DT_ARG(cams->K && cams->c2w && cams->n_views > 0 && cams->width > 0 && cams->height > 0,
          "dt_trace_forward: cams (K, c2w, n_views, width, height) invalid");
   DT_ARG(ab->sigma, "dt_trace_forward: absorption.sigma is NULL");
-  DT_ARG(ab->kind == DT_ABS_CONST || (ab->kind == DT_ABS_GRID && ab->res >= 2 && ab->n_samples >= 1),
-         "dt_trace_forward: absorption (kind=%d res=%d n_samples=%d) invalid", ab->kind, ab->res, ab->n_samples);
+  DT_ARG(abs_valid(ab), "dt_trace_forward: absorption (kind=%d res=%d n_samples=%d levels=%d log2_size=%d) invalid",
+         ab->kind, ab->res, ab->n_samples, ab->levels, ab->log2_size);
   DT_ARG((env->kind == DT_ENV_ANALYTIC && (env->n_lobes == 0 || env->lobes)) ||
              (env->kind == DT_ENV_GRID && env->voxel && env->planes && env->vres >= 2 && env->pres >= 2 && env->radius > 0),
          "dt_trace_forward: env (kind=%d) invalid", env->kind);
@@ -268,8 +286,8 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   const int D = opts->max_depth;
 
   // absorption snapshot (the backward differentiates w.r.t. these values)
-  size_t slen = ab->kind == DT_ABS_CONST ? 3 : (size_t)ab->res * ab->res * ab->res * 3;
-  size_t nodes = slen / 3;
+  size_t nodes = abs_nodes(ab);
+  size_t slen = nodes * 3;
   if (nodes > c->sigma_cap) {
     if (c->sigma_snap) cudaFree(c->sigma_snap);
     if (c->gsig) cudaFree(c->gsig);
@@ -280,7 +298,9 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
     c->sigma_cap = nodes;
   }
   c->sigma_len = slen;
-  DT_CU(launch_pack_sigma(ab->sigma, c->sigma_snap, (int64_t)nodes, ab->kind == DT_ABS_CONST ? 1 : ab->res, st));
+  // grid: x-pairs (32 B per node); constant / hash: one float4 per node / table entry
+  DT_CU(launch_pack_sigma(ab->sigma, c->sigma_snap, (int64_t)nodes, ab->kind == DT_ABS_GRID ? ab->res : 1,
+                          ab->kind == DT_ABS_GRID, st));
 
   DevScene s = scene_from_ctx(c);
   s.ior = ior;
@@ -291,6 +311,16 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   s.nsamp = std::max(1, ab->n_samples);
   s.slo = f3(ab->box_lo[0], ab->box_lo[1], ab->box_lo[2]);
   s.shi = f3(ab->box_hi[0], ab->box_hi[1], ab->box_hi[2]);
+  if (ab->kind == DT_ABS_HASH) {
+    s.hlevels = ab->levels;
+    s.hlog2 = ab->log2_size;
+    s.hdense = 0u;
+    for (int l = 0; l < ab->levels; ++l) {
+      s.hres[l] = ab->level_res[l];
+      const double n1 = ab->level_res[l] + 1.0;
+      if (n1 * n1 * n1 <= (double)(1u << ab->log2_size)) s.hdense |= 1u << l;
+    }
+  }
   s.env_kind = env->kind;
   s.ambient = f3(env->ambient[0], env->ambient[1], env->ambient[2]);
   s.lobes = env->lobes;
@@ -528,7 +558,7 @@ dt_status dt_sigma_regularizers(dt_ctx* c, const dt_absorption* ab, const float*
   if (!c) return DT_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
   DT_ARG(ab && ab->sigma && grad_sigma && loss, "dt_sigma_regularizers: NULL argument");
-  DT_ARG(ab->kind == DT_ABS_CONST || (ab->kind == DT_ABS_GRID && ab->res >= 2), "dt_sigma_regularizers: bad absorption");
+  DT_ARG(abs_valid(ab), "dt_sigma_regularizers: bad absorption");
   DT_ARG(n >= 0 && (n == 0 || ab->kind == DT_ABS_CONST || (points && xi)), "dt_sigma_regularizers: points/xi");
   PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
   DT_CU(launch_sigma_reg(ab, points, xi, n, lambda_smooth, lambda_vol, grad_sigma, loss, (cudaStream_t)stream));

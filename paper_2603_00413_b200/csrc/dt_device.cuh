@@ -46,9 +46,12 @@ struct DevScene {
   float ior;
   const float* ior_ptr;  // optional device IoR (dt_trace_opts.ior_device), read once per thread
   int abs_kind;
-  const float4* sigma;  // internal copy: [1] (constant) or [R^3] nodes, rgb + pad
+  const float4* sigma;  // internal copy: [1] (constant), [R^3] x-pairs (grid), [L*T] entries (hash)
   int sres, nsamp;
   float3 slo, shi;
+  int hlevels, hlog2;   // hash texture (R29): levels, log2 table size
+  unsigned hdense;      // bit l: level l indexed densely ((N_l+1)^3 <= T)
+  int hres[32];         // cells per axis of each level
   // environment
   int env_kind;
   float3 ambient;
@@ -492,9 +495,102 @@ DT_D GridMap grid_map(const DevScene& s) {
   m.R = s.sres;
   m.N = s.nsamp;
   m.lo = s.slo;
-  m.scl = f3((float)(m.R - 1) / (s.shi.x - s.slo.x), (float)(m.R - 1) / (s.shi.y - s.slo.y),
-             (float)(m.R - 1) / (s.shi.z - s.slo.z));
+  const float span = s.abs_kind == 2 ? 1.0f : (float)(m.R - 1);   // hash: unit box coordinates
+  m.scl = f3(span / (s.shi.x - s.slo.x), span / (s.shi.y - s.slo.y), span / (s.shi.z - s.slo.z));
   return m;
+}
+
+DT_D void corner_weights(const float f[3], float w[8]);
+
+// ---- hash texture (ABS = DT_ABS_HASH, R29): mu(p) = sum_l trilinear lookup of level l
+// Table entry of corner (x, y, z) at level l (N cells per axis, T = 2^hlog2 entries).
+DT_D uint32_t hash_index(const DevScene& s, int l, int N, int x, int y, int z) {
+  const uint32_t T1 = (1u << s.hlog2) - 1u;
+  if ((s.hdense >> l) & 1u) {
+    const uint32_t n1 = (uint32_t)N + 1u;
+    return (uint32_t)x + n1 * ((uint32_t)y + n1 * (uint32_t)z);
+  }
+  return ((uint32_t)x ^ ((uint32_t)y * 2654435761u) ^ ((uint32_t)z * 805459861u)) & T1;
+}
+
+// Unit-box coordinates of p; false outside the box (zero there, R11).
+DT_D bool hash_unit(const GridMap& m, float3 p, float u[3]) {
+  u[0] = (p.x - m.lo.x) * m.scl.x;
+  u[1] = (p.y - m.lo.y) * m.scl.y;
+  u[2] = (p.z - m.lo.z) * m.scl.z;
+  return u[0] >= 0.f && u[0] <= 1.f && u[1] >= 0.f && u[1] <= 1.f && u[2] >= 0.f && u[2] <= 1.f;
+}
+
+DT_D void hash_cell(const float u[3], int N, int i[3], float f[3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float g = u[a] * (float)N;
+    i[a] = min((int)floorf(g), N - 1);
+    f[a] = g - (float)i[a];
+  }
+}
+
+DT_D float3 hash_mu(const DevScene& s, const GridMap& m, float3 p) {
+  float u[3];
+  float3 S = f3(0, 0, 0);
+  if (!hash_unit(m, p, u)) return S;
+  const size_t T = (size_t)1 << s.hlog2;
+#pragma unroll 2
+  for (int l = 0; l < s.hlevels; ++l) {
+    const int N = s.hres[l];
+    int i[3];
+    float f[3], w[8];
+    hash_cell(u, N, i, f);
+    corner_weights(f, w);
+    const float4* tab = s.sigma + (size_t)l * T;
+    float4 c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = __ldg(tab + hash_index(s, l, N, i[0] + (k & 1), i[1] + ((k >> 1) & 1), i[2] + (k >> 2)));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S += f3(c[k]) * w[k];
+  }
+  return S;
+}
+
+// Reverse of hash_mu at one sample: scatters gSs * w into the table adjoint; returns
+// gv = gS . mu(p) and adds d(gS . mu)/du (unit-box coordinates) to gp.
+DT_D float hash_mu_bwd(const DevScene& s, const GridMap& m, float3 p, float3 gS, float3 gSs, float4* gsig,
+                       float3& gp) {
+  float u[3];
+  if (!hash_unit(m, p, u)) return 0.f;
+  const size_t T = (size_t)1 << s.hlog2;
+  float gv = 0.f;
+#pragma unroll 2
+  for (int l = 0; l < s.hlevels; ++l) {
+    const int N = s.hres[l];
+    int i[3];
+    float f[3], w[8];
+    hash_cell(u, N, i, f);
+    corner_weights(f, w);
+    uint32_t e[8];
+    float gk[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) e[k] = hash_index(s, l, N, i[0] + (k & 1), i[1] + ((k >> 1) & 1), i[2] + (k >> 2));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) gk[k] = dot(gS, f3(__ldg(s.sigma + (size_t)l * T + e[k])));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      gv += w[k] * gk[k];
+      atomicAdd(gsig + (size_t)l * T + e[k], make_float4(gSs.x * w[k], gSs.y * w[k], gSs.z * w[k], 0.f));
+    }
+    float3 gl = f3(0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int a = q & 1, b = q >> 1;
+      const float fa0 = a ? f[0] : 1 - f[0], fa1 = a ? f[1] : 1 - f[1];
+      const float fb1 = b ? f[1] : 1 - f[1], fb2 = b ? f[2] : 1 - f[2];
+      gl.x += (gk[1 | (a << 1) | (b << 2)] - gk[(a << 1) | (b << 2)]) * fa1 * fb2;
+      gl.y += (gk[a | 2 | (b << 2)] - gk[a | (b << 2)]) * fa0 * fb2;
+      gl.z += (gk[a | (b << 1) | 4] - gk[a | (b << 1)]) * fa0 * fb1;
+    }
+    gp += gl * (float)N;                  // d g_l / d u = N_l
+  }
+  return gv;
 }
 
 // Cell and local coordinates of p (zero outside the box, R11).
@@ -554,11 +650,14 @@ DT_D int group_take(unsigned& mask, int& myq) {
 
 // sum_j mu(x_j) * |x - o| / N (the optical depth of R10) of the group's segment, returned on
 // every lane of the group.  All 32 lanes call it (inactive groups pass active = false).
-template <int G>
+template <int G, int ABS>
 DT_D float3 group_optical_depth(const DevScene& s, const GridMap& m, float3 o, float3 x, bool active) {
   const float3 dx = x - o;
   float3 S = f3(0, 0, 0);
-  if (active) {
+  if (ABS == 2 && active) {            // hash texture: every sample reads all levels
+    const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
+    for (int j = j0; j < j1; ++j) S += hash_mu(s, m, o + dx * (((float)j + 0.5f) / (float)m.N));
+  } else if (active) {
     const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
     int cur = -1;
     float3 c[8];
@@ -602,7 +701,7 @@ DT_D float3 group_optical_depth(const DevScene& s, const GridMap& m, float3 o, f
 // into the float4 grid adjoint gsig (each lane merges its run of samples per cell, then 8
 // vector atomics per cell visit) and returns the position adjoints of o and x on every lane
 // of the group.
-template <int G>
+template <int G, int ABS>
 DT_D void group_transmittance_backward(const DevScene& s, const GridMap& m, float3 o, float3 x, float3 gS,
                                        bool active, float4* gsig, float3& gx, float3& go) {
   const float3 dx = x - o;
@@ -611,7 +710,16 @@ DT_D void group_transmittance_backward(const DevScene& s, const GridMap& m, floa
   const float3 gSs = gS * sc;
   float gl = 0.f;
   float3 gsum = f3(0, 0, 0), gtsum = f3(0, 0, 0);
-  if (active) {
+  if (ABS == 2 && active) {            // hash texture
+    const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
+    for (int j = j0; j < j1; ++j) {
+      const float t = ((float)j + 0.5f) * invN;
+      float3 gp = f3(0, 0, 0);
+      gl += hash_mu_bwd(s, m, o + dx * t, gS, gSs, gsig, gp);
+      gsum += gp;
+      gtsum += gp * t;
+    }
+  } else if (active) {
     const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
     int cur = -1;
     float acc[8], gk[8];               // the run's weight sums; gS . sigma_k of its cell

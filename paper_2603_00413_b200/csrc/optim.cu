@@ -107,6 +107,75 @@ __global__ void k_sigma_reg_grid(const float* __restrict__ sig, int R, float3 lo
   }
 }
 
+// hash texture (R29) on the caller's [L][T][3] tables: value at p, and the scatter of g * w
+struct HashTab {
+  int L, log2;
+  unsigned dense;
+  int res[32];
+  float3 lo, scl;   // unit-box coordinates u = (p - lo) * scl
+};
+
+DT_D uint32_t htab_index(const HashTab& h, int l, int x, int y, int z) {
+  if ((h.dense >> l) & 1u) {
+    const uint32_t n1 = (uint32_t)h.res[l] + 1u;
+    return (uint32_t)x + n1 * ((uint32_t)y + n1 * (uint32_t)z);
+  }
+  return ((uint32_t)x ^ ((uint32_t)y * 2654435761u) ^ ((uint32_t)z * 805459861u)) & ((1u << h.log2) - 1u);
+}
+
+// visit(l_entry_offset, weight) for the 8 corners of every level; false outside the box
+template <class Fn>
+DT_D bool htab_visit(const HashTab& h, float3 p, Fn visit) {
+  const float u[3] = {(p.x - h.lo.x) * h.scl.x, (p.y - h.lo.y) * h.scl.y, (p.z - h.lo.z) * h.scl.z};
+  if (!(u[0] >= 0.f && u[0] <= 1.f && u[1] >= 0.f && u[1] <= 1.f && u[2] >= 0.f && u[2] <= 1.f)) return false;
+  for (int l = 0; l < h.L; ++l) {
+    const int N = h.res[l];
+    int i[3];
+    float f[3];
+    for (int a = 0; a < 3; ++a) {
+      const float g = u[a] * (float)N;
+      i[a] = min((int)floorf(g), N - 1);
+      f[a] = g - (float)i[a];
+    }
+    for (int k = 0; k < 8; ++k) {
+      const int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
+      const float w = (dx ? f[0] : 1 - f[0]) * (dy ? f[1] : 1 - f[1]) * (dz ? f[2] : 1 - f[2]);
+      visit(((size_t)l << h.log2) + htab_index(h, l, i[0] + dx, i[1] + dy, i[2] + dz), w);
+    }
+  }
+  return true;
+}
+
+__global__ void k_sigma_reg_hash(const float* __restrict__ sig, HashTab h, const float* __restrict__ pts,
+                                 const float* __restrict__ xi, int64_t n, float inv_n, float ls, float lv,
+                                 float* __restrict__ gsig, float* __restrict__ loss) {
+  float acc_s = 0.f, acc_v = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float3 v = f3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    const float3 u = v + f3(xi[3 * i], xi[3 * i + 1], xi[3 * i + 2]);
+    float3 mv = f3(0, 0, 0), mu = f3(0, 0, 0);
+    htab_visit(h, v, [&](size_t e, float w) { mv += f3(sig[3 * e], sig[3 * e + 1], sig[3 * e + 2]) * w; });
+    htab_visit(h, u, [&](size_t e, float w) { mu += f3(sig[3 * e], sig[3 * e + 1], sig[3 * e + 2]) * w; });
+    const float3 dd = mv - mu;
+    acc_s += fabsf(dd.x) + fabsf(dd.y) + fabsf(dd.z);
+    acc_v += dot(mv, mv);
+    const float3 s = f3(sgnf(dd.x), sgnf(dd.y), sgnf(dd.z)) * (ls * inv_n);
+    const float3 gvv = s + mv * (2.0f * lv * inv_n);
+    htab_visit(h, v, [&](size_t e, float w) {
+      atomicAdd(gsig + 3 * e, gvv.x * w); atomicAdd(gsig + 3 * e + 1, gvv.y * w); atomicAdd(gsig + 3 * e + 2, gvv.z * w);
+    });
+    htab_visit(h, u, [&](size_t e, float w) {
+      atomicAdd(gsig + 3 * e, -s.x * w); atomicAdd(gsig + 3 * e + 1, -s.y * w); atomicAdd(gsig + 3 * e + 2, -s.z * w);
+    });
+  }
+  acc_s = warp_sum(acc_s);
+  acc_v = warp_sum(acc_v);
+  if (lane_id() == 0) {
+    atomicAdd(loss, acc_s * inv_n);
+    atomicAdd(loss + 1, acc_v * inv_n);
+  }
+}
+
 // constant sigma: mu(x) = sigma everywhere, so L_mat = 0 and L_vol = |sigma|^2
 __global__ void k_sigma_reg_const(const float* __restrict__ sig, float lv, float* __restrict__ gsig, float* __restrict__ loss) {
   float3 s = f3(sig[0], sig[1], sig[2]);
@@ -166,6 +235,19 @@ cudaError_t launch_sigma_reg(const dt_absorption* ab, const float* pts, const fl
   cudaMemsetAsync(loss, 0, 2 * sizeof(float), st);
   if (ab->kind == DT_ABS_CONST) {
     k_sigma_reg_const<<<1, 1, 0, st>>>(ab->sigma, lv, gsig, loss);
+  } else if (ab->kind == DT_ABS_HASH && n > 0) {
+    HashTab h{};
+    h.L = ab->levels;
+    h.log2 = ab->log2_size;
+    for (int l = 0; l < ab->levels; ++l) {
+      h.res[l] = ab->level_res[l];
+      const double n1 = ab->level_res[l] + 1.0;
+      if (n1 * n1 * n1 <= (double)(1u << ab->log2_size)) h.dense |= 1u << l;
+    }
+    h.lo = f3(ab->box_lo[0], ab->box_lo[1], ab->box_lo[2]);
+    h.scl = f3(1.0f / (ab->box_hi[0] - ab->box_lo[0]), 1.0f / (ab->box_hi[1] - ab->box_lo[1]),
+               1.0f / (ab->box_hi[2] - ab->box_lo[2]));
+    k_sigma_reg_hash<<<grid_for(n), 256, 0, st>>>(ab->sigma, h, pts, xi, n, 1.0f / (float)n, ls, lv, gsig, loss);
   } else if (n > 0) {
     k_sigma_reg_grid<<<grid_for(n), 256, 0, st>>>(ab->sigma, ab->res, f3(ab->box_lo[0], ab->box_lo[1], ab->box_lo[2]),
                                                  f3(ab->box_hi[0], ab->box_hi[1], ab->box_hi[2]), pts, xi, n,

@@ -143,7 +143,7 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
     for (unsigned m = __ballot_sync(~0u, need_tau); m;) {                // cooperative walks
       int myq;
       const int src = group_take<kWalkLanes>(m, myq), sl = max(src, 0);
-      const float3 Sd = group_optical_depth<kWalkLanes>(s, gm, shfl3(o, sl), shfl3(x, sl), src >= 0);
+      const float3 Sd = group_optical_depth<kWalkLanes, ABS>(s, gm, shfl3(o, sl), shfl3(x, sl), src >= 0);
       const float3 mine = shfl3(Sd, max(myq, 0) * kWalkLanes);
       if (myq >= 0) tau = f3(expf(-mine.x), expf(-mine.y), expf(-mine.z));
     }
@@ -578,8 +578,8 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
         int myq;
         const int src = group_take<kWalkLanesBwd>(m, myq), sl = max(src, 0);
         float3 wgx, wgo;
-        group_transmittance_backward<kWalkLanesBwd>(s, gm, shfl3(o, sl), shfl3(x, sl), shfl3(gS, sl), src >= 0,
-                                                    a.dsig, wgx, wgo);
+        group_transmittance_backward<kWalkLanesBwd, ABS>(s, gm, shfl3(o, sl), shfl3(x, sl), shfl3(gS, sl), src >= 0,
+                                                         a.dsig, wgx, wgo);
         const float3 mx = shfl3(wgx, max(myq, 0) * kWalkLanesBwd), mo = shfl3(wgo, max(myq, 0) * kWalkLanesBwd);
         if (myq >= 0) { gx += mx; go += mo; }
       }
@@ -672,8 +672,12 @@ __global__ void k_finalize(const float4* __restrict__ gV, const float4* __restri
 // sigma [n][3] -> x-pairs: out[2i], out[2i+1] = (sigma_i, sigma_{i+1 along x}, 0, 0), 32 B per
 // node so that one 256-bit load fetches both x-corners of a cell edge (res = x extent; the
 // last x node of a row pairs with zeros; constant sigma: res = 1).
-__global__ void k_pack_sigma(const float* __restrict__ in, float4* __restrict__ out, int64_t n, int res) {
+__global__ void k_pack_sigma(const float* __restrict__ in, float4* __restrict__ out, int64_t n, int res, int pairs) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!pairs) {                     // plain float4 per node / table entry
+      out[i] = make_float4(in[3 * i], in[3 * i + 1], in[3 * i + 2], 0.f);
+      continue;
+    }
     const bool nx = (i % res) + 1 < res;
     const float a = in[3 * i], b = in[3 * i + 1], c = in[3 * i + 2];
     const float d = nx ? in[3 * i + 3] : 0.f, e = nx ? in[3 * i + 4] : 0.f, f = nx ? in[3 * i + 5] : 0.f;
@@ -767,13 +771,16 @@ cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count
 }
 
 cudaError_t launch_shade_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
-  static int gs0 = 0, gs1 = 0;
+  static int gs0 = 0, gs1 = 0, gs2 = 0;
   if (a.s.abs_kind == 0) {
     if (!gs0) gs0 = persistent_blocks((const void*)k_shade_level<0>, kTraceThreads, sm_count);
     k_shade_level<0><<<gs0, kTraceThreads, 0, st>>>(a, level, max_depth);
-  } else {
+  } else if (a.s.abs_kind == 1) {
     if (!gs1) gs1 = persistent_blocks((const void*)k_shade_level<1>, kTraceThreads, sm_count);
     k_shade_level<1><<<gs1, kTraceThreads, 0, st>>>(a, level, max_depth);
+  } else {
+    if (!gs2) gs2 = persistent_blocks((const void*)k_shade_level<2>, kTraceThreads, sm_count);
+    k_shade_level<2><<<gs2, kTraceThreads, 0, st>>>(a, level, max_depth);
   }
   return cudaGetLastError();
 }
@@ -796,13 +803,16 @@ cudaError_t launch_gather_level(const FwdLaunch& a, int level, int sm_count, cud
 }
 
 cudaError_t launch_backward_level(const BwdLaunch& a, int level, int sm_count, cudaStream_t st) {
-  static int gb0 = 0, gb1 = 0;
+  static int gb0 = 0, gb1 = 0, gb2 = 0;
   if (a.s.abs_kind == 0) {
     if (!gb0) gb0 = persistent_blocks((const void*)k_backward_level<0>, kBwdThreads, sm_count);
     k_backward_level<0><<<gb0, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
-  } else {
+  } else if (a.s.abs_kind == 1) {
     if (!gb1) gb1 = persistent_blocks((const void*)k_backward_level<1>, kBwdThreads, sm_count);
     k_backward_level<1><<<gb1, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
+  } else {
+    if (!gb2) gb2 = persistent_blocks((const void*)k_backward_level<2>, kBwdThreads, sm_count);
+    k_backward_level<2><<<gb2, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
   }
   return cudaGetLastError();
 }
@@ -842,9 +852,9 @@ cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, int res, cudaStream_t st) {
+cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, int res, bool pairs, cudaStream_t st) {
   int g = (int)std::min<int64_t>((nodes + 255) / 256, 148 * 16);
-  k_pack_sigma<<<std::max(g, 1), 256, 0, st>>>(in, out, nodes, std::max(res, 1));
+  k_pack_sigma<<<std::max(g, 1), 256, 0, st>>>(in, out, nodes, std::max(res, 1), pairs ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -92,7 +92,7 @@ class RefineOptimizer:
         gV, gI, gS = tr.trace_backward(grad_rgb)
         if self.grad_hook is not None:
             self.grad_hook(gV, gI, gS)
-        if ds.absorption.kind == 1:
+        if ds.absorption.kind in (1, 2):          # grid / hash texture: sampled regularisers
             pts, xi = self._reg_points()
         else:
             pts = xi = None

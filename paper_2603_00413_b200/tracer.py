@@ -50,6 +50,11 @@ class DeviceScene:
             self.absorption.box_lo = (C.c_float * 3)(*map(float, ab.box_lo))
             self.absorption.box_hi = (C.c_float * 3)(*map(float, ab.box_hi))
         self.absorption.n_samples = ab.n_samples
+        if ab.kind == 2:                      # hash-grid texture (R29)
+            T = ab.sigma.shape[1]
+            self.absorption.levels = len(ab.level_res)
+            self.absorption.log2_size = T.bit_length() - 1
+            self.absorption.level_res = (C.c_int32 * 32)(*[int(x) for x in ab.level_res])
         env = sc.env
         self.env = N.Env()
         self.env.kind = env.kind

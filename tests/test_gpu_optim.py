@@ -58,6 +58,24 @@ def test_sigma_regularizers_match_oracle(tracer):
     np.testing.assert_allclose(gs.cpu().numpy(), [0.2, 0.5, 1.0], rtol=1e-6)
 
 
+def test_sigma_regularizers_hash_match_oracle(tracer):
+    from paper_2603_00413_b200.tracer import DeviceScene
+    V, F = S.icosphere(2)
+    sc = T.scene(V, F, T.one_view(8, 8, (0, 0, 3)), absorption=T.small_hash_grid(V, levels=4, log2_size=8, top=16))
+    ds = DeviceScene(sc, torch.device("cuda:0"))
+    g = np.random.default_rng(6)
+    ab = sc.absorption
+    pts = g.uniform(ab.box_lo, ab.box_hi, (2000, 3)).astype(np.float32)
+    xi = (g.normal(size=(2000, 3)) * 0.05).astype(np.float32)
+    gs = torch.zeros_like(ds.sigma)
+    loss = tracer.sigma_regularizers(ds, torch.as_tensor(pts, device="cuda:0"), torch.as_tensor(xi, device="cuda:0"),
+                                     gs, 0.3, 0.7)
+    Lm, Lv, go = OO.sigma_regularizers(ab, pts, xi, 0.3, 0.7)
+    l = loss.cpu().numpy()
+    assert abs(l[0] - Lm) < 1e-4 * Lm and abs(l[1] - Lv) < 1e-4 * Lv
+    assert rel_l2(gs.cpu().numpy(), go) < 1e-4
+
+
 @pytest.mark.parametrize("uniform", [False, True])
 def test_adam_matches_oracle(tracer, uniform):
     g = np.random.default_rng(5)

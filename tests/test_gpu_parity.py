@@ -201,6 +201,46 @@ def test_sigma_grid_and_far_field(tracer):
     parity_case(tracer, sc, np.arange(sc.n_pixels), "ico2-sigmagrid-capenv")
 
 
+def test_hash_texture(tracer):
+    """NEXT-2: hash-grid absorption (R29), dense and hashed (colliding) levels, both caps."""
+    V, F = S.icosphere(2)
+    cams = T.one_view(40, 28, (0.6, -0.4, 2.6), fov_deg=55)
+    ab = T.small_hash_grid(V, levels=4, log2_size=8, base=2, top=16, n_samples=24)
+    sc = T.scene(V, F, cams, env=T.small_grid_env(far_field=1), absorption=ab, D=4)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "ico2-hash")
+    sc = T.scene(V, F, cams, env=T.lobe_env(kappa=3.0), absorption=ab, D=3, cap=S.CAP_ENV)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "ico2-hash-capenv")
+
+
+def test_hash_dense_level_equals_grid(tracer):
+    """One dense hash level is the vertex grid (R29 special case): same radiance/gradients."""
+    import dataclasses
+    V, F = S.icosphere(2)
+    cams = T.one_view(32, 32, (0.5, 0.3, 2.7), fov_deg=50)
+    grid = T.small_sigma_grid(V, 8)
+    R = grid.sigma.shape[0]
+    tab = np.zeros((1, 1024, 3), np.float32)
+    tab[0, :R ** 3] = grid.sigma.reshape(-1, 3)
+    hashed = S.Absorption(S.ABS_HASH, tab, grid.box_lo, grid.box_hi, grid.n_samples, np.array([R - 1], np.int32))
+    a = T.scene(V, F, cams, env=T.lobe_env(kappa=3.0), absorption=grid, D=4)
+    b = dataclasses.replace(a, absorption=hashed)
+    g = S.upstream_grad(a.n_pixels, 21)
+    ra = run_gpu(tracer, a, np.arange(a.n_pixels), grad=g)
+    rb = run_gpu(tracer, b, np.arange(b.n_pixels), grad=g)
+    np.testing.assert_allclose(rb["rgb"], ra["rgb"], atol=2e-5)
+    assert rel_l2(rb["gV"], ra["gV"]) < 1e-4
+    assert rel_l2(rb["gsig"][0, :R ** 3], ra["gsig"].reshape(-1, 3)) < 1e-4
+    assert np.abs(rb["gsig"][0, R ** 3:]).max() == 0.0
+
+
+def test_c4h_hash_texture_full_mesh_sampled(tracer):
+    """NEXT-2 workload: C4's knot + gems with the 16-level hash texture; 128 sampled pixels
+    (table 2^16 per level here to keep the oracle's per-thread adjoint small)."""
+    sc = S.config_c4h(log2_size=16)
+    pid = S.central_pixels(sc.cams, 128, 7)
+    parity_case(tracer, sc, pid, "C4H")
+
+
 def test_flat_facets_and_tir(tracer):
     """Unwelded flat gems (flat normals, TIR-rich) and the tetrahedron."""
     Vg, Fg = S.gem()

@@ -28,7 +28,8 @@ def ingp_hash(x, y, z, T_):
 def optical_depth(sc, o, x):
     osc = O.OracleScene(sc)
     tau = np.zeros(3)
-    O.lib().dto_transmittance(osc.ref, O._p(np.asarray(o, np.float64)), O._p(np.asarray(x, np.float64)), O._p(tau))
+    a0, a1 = np.ascontiguousarray(o, np.float64), np.ascontiguousarray(x, np.float64)   # keep alive for the call
+    O.lib().dto_transmittance(osc.ref, O._p(a0), O._p(a1), O._p(tau))
     return -np.log(tau)
 
 

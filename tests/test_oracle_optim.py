@@ -107,3 +107,37 @@ def test_adam_converges_on_quadratic():
     for t in range(1, 2001):
         x, m, v = OO.adam(x, 2 * x, m, v, t, 0.01)
     assert np.abs(x).max() < 1e-3
+
+
+def test_hash_regularizers_match_cpp_oracle_and_fd():
+    """oracle/optim.py's numpy hash lookup (R29) against the C++ oracle's mu (an independent
+    implementation: one midpoint sample of a tiny segment), and FD of its gradient."""
+    import oracle as O
+    V, F = S.icosphere(1)
+    ab = T.small_hash_grid(V, levels=3, log2_size=6)
+    sc = T.scene(V, F, T.one_view(4, 4, (0, 0, 3)), absorption=ab)
+    osc = O.OracleScene(sc)
+    g = np.random.default_rng(2)
+    sig = ab.sigma.astype(np.float64)
+    lo, hi = np.asarray(ab.box_lo, np.float64), np.asarray(ab.box_hi, np.float64)
+    for p in g.uniform(lo, hi, (20, 3)):
+        d = np.array([0.0, 0.0, 1e-4])
+        tau = np.zeros(3)
+        a0, a1 = np.ascontiguousarray(p - d / 2), np.ascontiguousarray(p + d / 2)   # keep alive
+        O.lib().dto_transmittance(osc.ref, O._p(a0), O._p(a1), O._p(tau))
+        mu_cpp = -np.log(tau) / 1e-4
+        mu_np, _ = OO._hash_lookup(ab, sig, lo, hi, p)
+        np.testing.assert_allclose(mu_np, mu_cpp, rtol=1e-9)
+    pts = g.uniform(lo, hi, (30, 3))
+    xi = g.normal(size=(30, 3)) * 0.05
+    ls, lv = 0.3, 0.7
+    _, _, grad = OO.sigma_regularizers(ab, pts, xi, ls, lv)
+    import dataclasses
+    h = 1e-7
+    for j in np.argsort(-np.abs(grad.ravel()))[:10]:
+        a, b = sig.copy().ravel(), sig.copy().ravel()
+        a[j] += h
+        b[j] -= h
+        fa = np.dot([ls, lv], OO.sigma_regularizers(dataclasses.replace(ab, sigma=a.reshape(sig.shape)), pts, xi, ls, lv)[:2])
+        fb = np.dot([ls, lv], OO.sigma_regularizers(dataclasses.replace(ab, sigma=b.reshape(sig.shape)), pts, xi, ls, lv)[:2])
+        assert abs((fa - fb) / (2 * h) - grad.ravel()[j]) < 1e-6 * max(1, abs(grad.ravel()[j]))
