@@ -14,8 +14,17 @@ constexpr float kInf = __builtin_huge_valf();
 #ifndef DT_WALK_LANES_BWD
 #define DT_WALK_LANES_BWD 4
 #endif
+#ifndef DT_WALK_LANES_HASH
+#define DT_WALK_LANES_HASH 8
+#endif
+#ifndef DT_WALK_LANES_HASH_BWD
+#define DT_WALK_LANES_HASH_BWD 4
+#endif
 constexpr int kWalkLanes = DT_WALK_LANES;          // lanes per sigma-grid segment walk, forward
 constexpr int kWalkLanesBwd = DT_WALK_LANES_BWD;   // and backward (measured: tools/sweep_walk.sh)
+// lanes per segment walk of the hash texture, by absorption kind
+template <int ABS> struct WalkLanes { static constexpr int fwd = kWalkLanes, bwd = kWalkLanesBwd; };
+template <> struct WalkLanes<2> { static constexpr int fwd = DT_WALK_LANES_HASH, bwd = DT_WALK_LANES_HASH_BWD; };
 constexpr int kStackShared = 16;   // short stack entries per thread in shared memory
 constexpr int kStackLocal = 112;   // spill entries per thread (local memory, L1-cached)
 constexpr int kLeafMax = 3;        // triangles per wide-BVH leaf (a contiguous leaf-order range)
@@ -530,69 +539,6 @@ DT_D void hash_cell(const float u[3], int N, int i[3], float f[3]) {
   }
 }
 
-DT_D float3 hash_mu(const DevScene& s, const GridMap& m, float3 p) {
-  float u[3];
-  float3 S = f3(0, 0, 0);
-  if (!hash_unit(m, p, u)) return S;
-  const size_t T = (size_t)1 << s.hlog2;
-#pragma unroll 2
-  for (int l = 0; l < s.hlevels; ++l) {
-    const int N = s.hres[l];
-    int i[3];
-    float f[3], w[8];
-    hash_cell(u, N, i, f);
-    corner_weights(f, w);
-    const float4* tab = s.sigma + (size_t)l * T;
-    float4 c[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) c[k] = __ldg(tab + hash_index(s, l, N, i[0] + (k & 1), i[1] + ((k >> 1) & 1), i[2] + (k >> 2)));
-#pragma unroll
-    for (int k = 0; k < 8; ++k) S += f3(c[k]) * w[k];
-  }
-  return S;
-}
-
-// Reverse of hash_mu at one sample: scatters gSs * w into the table adjoint; returns
-// gv = gS . mu(p) and adds d(gS . mu)/du (unit-box coordinates) to gp.
-DT_D float hash_mu_bwd(const DevScene& s, const GridMap& m, float3 p, float3 gS, float3 gSs, float4* gsig,
-                       float3& gp) {
-  float u[3];
-  if (!hash_unit(m, p, u)) return 0.f;
-  const size_t T = (size_t)1 << s.hlog2;
-  float gv = 0.f;
-#pragma unroll 2
-  for (int l = 0; l < s.hlevels; ++l) {
-    const int N = s.hres[l];
-    int i[3];
-    float f[3], w[8];
-    hash_cell(u, N, i, f);
-    corner_weights(f, w);
-    uint32_t e[8];
-    float gk[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) e[k] = hash_index(s, l, N, i[0] + (k & 1), i[1] + ((k >> 1) & 1), i[2] + (k >> 2));
-#pragma unroll
-    for (int k = 0; k < 8; ++k) gk[k] = dot(gS, f3(__ldg(s.sigma + (size_t)l * T + e[k])));
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      gv += w[k] * gk[k];
-      atomicAdd(gsig + (size_t)l * T + e[k], make_float4(gSs.x * w[k], gSs.y * w[k], gSs.z * w[k], 0.f));
-    }
-    float3 gl = f3(0, 0, 0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int a = q & 1, b = q >> 1;
-      const float fa0 = a ? f[0] : 1 - f[0], fa1 = a ? f[1] : 1 - f[1];
-      const float fb1 = b ? f[1] : 1 - f[1], fb2 = b ? f[2] : 1 - f[2];
-      gl.x += (gk[1 | (a << 1) | (b << 2)] - gk[(a << 1) | (b << 2)]) * fa1 * fb2;
-      gl.y += (gk[a | 2 | (b << 2)] - gk[a | (b << 2)]) * fa0 * fb2;
-      gl.z += (gk[a | (b << 1) | 4] - gk[a | (b << 1)]) * fa0 * fb1;
-    }
-    gp += gl * (float)N;                  // d g_l / d u = N_l
-  }
-  return gv;
-}
-
 // Cell and local coordinates of p (zero outside the box, R11).
 DT_D bool grid_cell(const GridMap& m, float3 p, int& base, float f[3]) {
   const float g[3] = {(p.x - m.lo.x) * m.scl.x, (p.y - m.lo.y) * m.scl.y, (p.z - m.lo.z) * m.scl.z};
@@ -654,9 +600,45 @@ template <int G, int ABS>
 DT_D float3 group_optical_depth(const DevScene& s, const GridMap& m, float3 o, float3 x, bool active) {
   const float3 dx = x - o;
   float3 S = f3(0, 0, 0);
-  if (ABS == 2 && active) {            // hash texture: every sample reads all levels
+  if (ABS == 2 && active) {            // hash texture: level by level, corners reused per cell run
     const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
-    for (int j = j0; j < j1; ++j) S += hash_mu(s, m, o + dx * (((float)j + 0.5f) / (float)m.N));
+    const size_t T = (size_t)1 << s.hlog2;
+    for (int l = 0; l < s.hlevels; ++l) {
+      const int N = s.hres[l];
+      const float4* tab = s.sigma + (size_t)l * T;
+      int cur[3] = {-1, -1, -1};
+      float3 c[8];
+      float acc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+      for (int j = j0; j < j1; ++j) {
+        float u[3];
+        if (!hash_unit(m, o + dx * (((float)j + 0.5f) / (float)m.N), u)) continue;
+        int i[3];
+        float f[3], w[8];
+        hash_cell(u, N, i, f);
+        if (i[0] != cur[0] || i[1] != cur[1] || i[2] != cur[2]) {
+          if (cur[0] >= 0) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              S += c[k] * acc[k];
+              acc[k] = 0.f;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            c[k] = f3(__ldg(tab + hash_index(s, l, N, i[0] + (k & 1), i[1] + ((k >> 1) & 1), i[2] + (k >> 2))));
+          cur[0] = i[0]; cur[1] = i[1]; cur[2] = i[2];
+        }
+        corner_weights(f, w);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += w[k];
+      }
+      if (cur[0] >= 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) S += c[k] * acc[k];
+      }
+    }
   } else if (active) {
     const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
     int cur = -1;
@@ -710,14 +692,65 @@ DT_D void group_transmittance_backward(const DevScene& s, const GridMap& m, floa
   const float3 gSs = gS * sc;
   float gl = 0.f;
   float3 gsum = f3(0, 0, 0), gtsum = f3(0, 0, 0);
-  if (ABS == 2 && active) {            // hash texture
+  if (ABS == 2 && active) {            // hash texture: level by level, merged per cell run
     const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
-    for (int j = j0; j < j1; ++j) {
-      const float t = ((float)j + 0.5f) * invN;
-      float3 gp = f3(0, 0, 0);
-      gl += hash_mu_bwd(s, m, o + dx * t, gS, gSs, gsig, gp);
-      gsum += gp;
-      gtsum += gp * t;
+    const size_t T = (size_t)1 << s.hlog2;
+    for (int l = 0; l < s.hlevels; ++l) {
+      const int N = s.hres[l];
+      const size_t lt = (size_t)l * T;
+      int cur[3] = {-1, -1, -1};
+      uint32_t e[8];
+      float gk[8], acc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { acc[k] = gk[k] = 0.f; e[k] = 0u; }
+      for (int j = j0; j < j1; ++j) {
+        const float t = ((float)j + 0.5f) * invN;
+        float u[3];
+        if (!hash_unit(m, o + dx * t, u)) continue;
+        int i[3];
+        float f[3], w[8];
+        hash_cell(u, N, i, f);
+        if (i[0] != cur[0] || i[1] != cur[1] || i[2] != cur[2]) {
+          if (cur[0] >= 0) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              atomicAdd(gsig + lt + e[k], make_float4(gSs.x * acc[k], gSs.y * acc[k], gSs.z * acc[k], 0.f));
+              acc[k] = 0.f;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) e[k] = hash_index(s, l, N, i[0] + (k & 1), i[1] + ((k >> 1) & 1), i[2] + (k >> 2));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) gk[k] = dot(gS, f3(__ldg(s.sigma + lt + e[k])));
+          cur[0] = i[0]; cur[1] = i[1]; cur[2] = i[2];
+        }
+        corner_weights(f, w);
+        float gv = 0.f;
+        float3 gp = f3(0, 0, 0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          acc[k] += w[k];
+          gv += w[k] * gk[k];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int a = q & 1, b = q >> 1;
+          const float fa0 = a ? f[0] : 1 - f[0], fa1 = a ? f[1] : 1 - f[1];
+          const float fb1 = b ? f[1] : 1 - f[1], fb2 = b ? f[2] : 1 - f[2];
+          gp.x += (gk[1 | (a << 1) | (b << 2)] - gk[(a << 1) | (b << 2)]) * fa1 * fb2;
+          gp.y += (gk[a | 2 | (b << 2)] - gk[a | (b << 2)]) * fa0 * fb2;
+          gp.z += (gk[a | (b << 1) | 4] - gk[a | (b << 1)]) * fa0 * fb1;
+        }
+        gp = gp * (float)N;              // d g_l / d u = N_l
+        gl += gv;
+        gsum += gp;
+        gtsum += gp * t;
+      }
+      if (cur[0] >= 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          atomicAdd(gsig + lt + e[k], make_float4(gSs.x * acc[k], gSs.y * acc[k], gSs.z * acc[k], 0.f));
+      }
     }
   } else if (active) {
     const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);

@@ -142,9 +142,10 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
     const GridMap gm = grid_map(s);
     for (unsigned m = __ballot_sync(~0u, need_tau); m;) {                // cooperative walks
       int myq;
-      const int src = group_take<kWalkLanes>(m, myq), sl = max(src, 0);
-      const float3 Sd = group_optical_depth<kWalkLanes, ABS>(s, gm, shfl3(o, sl), shfl3(x, sl), src >= 0);
-      const float3 mine = shfl3(Sd, max(myq, 0) * kWalkLanes);
+      constexpr int G = WalkLanes<ABS>::fwd;
+      const int src = group_take<G>(m, myq), sl = max(src, 0);
+      const float3 Sd = group_optical_depth<G, ABS>(s, gm, shfl3(o, sl), shfl3(x, sl), src >= 0);
+      const float3 mine = shfl3(Sd, max(myq, 0) * G);
       if (myq >= 0) tau = f3(expf(-mine.x), expf(-mine.y), expf(-mine.z));
     }
   }
@@ -576,11 +577,12 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
       const GridMap gm = grid_map(s);
       for (unsigned m = __ballot_sync(~0u, walk); m;) {
         int myq;
-        const int src = group_take<kWalkLanesBwd>(m, myq), sl = max(src, 0);
+        constexpr int G = WalkLanes<ABS>::bwd;
+        const int src = group_take<G>(m, myq), sl = max(src, 0);
         float3 wgx, wgo;
-        group_transmittance_backward<kWalkLanesBwd, ABS>(s, gm, shfl3(o, sl), shfl3(x, sl), shfl3(gS, sl), src >= 0,
-                                                         a.dsig, wgx, wgo);
-        const float3 mx = shfl3(wgx, max(myq, 0) * kWalkLanesBwd), mo = shfl3(wgo, max(myq, 0) * kWalkLanesBwd);
+        group_transmittance_backward<G, ABS>(s, gm, shfl3(o, sl), shfl3(x, sl), shfl3(gS, sl), src >= 0, a.dsig, wgx,
+                                             wgo);
+        const float3 mx = shfl3(wgx, max(myq, 0) * G), mo = shfl3(wgo, max(myq, 0) * G);
         if (myq >= 0) { gx += mx; go += mo; }
       }
     }
