@@ -141,8 +141,8 @@ def target_scene(sc):
     return dataclasses.replace(sc, V=V, ior=1.45, absorption=ab)
 
 
-def oracle_sample(sc, n_pix: int, seed: int = 9):
-    """Bounded oracle run (forward + backward) on n_pix object pixels: (seconds, segments, threads)."""
+def oracle_sample(sc, n_pix: int, seed: int = 9, backward: bool = True):
+    """Bounded oracle run (forward [+ backward]) on n_pix object pixels: (seconds, segments, threads)."""
     import oracle as O
     from paper_2603_00413_b200 import scenes as S
     osc = O.OracleScene(sc)
@@ -150,7 +150,8 @@ def oracle_sample(sc, n_pix: int, seed: int = 9):
     g = S.upstream_grad(len(pid), seed)
     t0 = time.perf_counter()
     out = O.render(osc, pid)
-    O.backward(osc, g, pid)
+    if backward:
+        O.backward(osc, g, pid)
     dt = time.perf_counter() - t0
     return dt, int(out["segments"].sum()), os.cpu_count()
 
@@ -193,21 +194,32 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         pid = torch.as_tensor(DD.tile_pixel_ids(sc.cams.n_views, sc.cams.width, sc.cams.height, rank, world), device=dev)
     n_rays = ds.n_pixels if pid is None else pid.numel()
-    # ground-truth colours for the loss (not timed)
-    tgt_sc = target_scene(sc)
-    dt_ = DeviceScene(tgt_sc, dev)
-    tr.build_bvh(dt_.V, dt_.F)
-    target = tr.trace_forward(dt_, pid).rgb.clone()
-    del dt_
-    # the paper's refine loop after the freeze-geometry stage: vertices (AdamUniform),
-    # IoR and sigma all updated every step; gradients all-reduced across ranks before the updates
-    n_global = ds.n_pixels
-    hook = (lambda gV, gI, gS: DD.allreduce_grads(gV, gI, gS)) if world > 1 else None
-    opt = RefineOptimizer(tr, ds, RefineConfig(freeze_iters=0), seed=5, grad_hook=hook,
-                          loss_scale=n_rays / n_global)
+    infer = args.mode == "infer"
+    rgb = torch.empty((n_rays, 3), dtype=torch.float32, device=dev)
+    if infer:
+        # NEXT-3 inference (relighting / novel views): forward only, fixed mesh (its
+        # BVH built once), every view re-rendered each step under the scene's (swapped) env
+        tr.build_bvh(ds.V, ds.F)
 
-    def step(async_=True):
-        opt.step(target, pid, async_=async_)
+        def step(async_=True):
+            tr.trace_forward(ds, pid, rgb=rgb, async_=async_)
+    else:
+        # ground-truth colours for the loss (not timed)
+        tgt_sc = target_scene(sc)
+        dt_ = DeviceScene(tgt_sc, dev)
+        tr.build_bvh(dt_.V, dt_.F)
+        target = tr.trace_forward(dt_, pid).rgb.clone()
+        del dt_
+        # the paper's refine loop after the freeze-geometry stage: vertices
+        # (AdamUniform), IoR and sigma all updated every step; gradients all-reduced across ranks
+        # before the updates
+        n_global = ds.n_pixels
+        hook = (lambda gV, gI, gS: DD.allreduce_grads(gV, gI, gS)) if world > 1 else None
+        opt = RefineOptimizer(tr, ds, RefineConfig(freeze_iters=0), seed=5, grad_hook=hook,
+                              loss_scale=n_rays / n_global)
+
+        def step(async_=True):
+            opt.step(target, pid, async_=async_)
 
     for w in range(args.warmup):
         step(async_=w > 0)          # the first (synchronous) step sizes the record arena
@@ -247,19 +259,36 @@ def run_ours(args, rank, world, local_rank):
     # ---- end-to-end through the public API with host buffers (pinned), same metric
     e2e = None
     if not args.no_e2e:
-        # per step: this step's target pixels in from pinned host memory, the losses and the
-        # updated IoR back (the optimiser state -- V, sigma, moments -- stays resident in HBM)
-        htgt = torch.empty((n_rays, 3), dtype=torch.float32, pin_memory=True)
-        htgt.copy_(target.cpu())
-        hloss = torch.empty(4, pin_memory=True)
-        hior = torch.empty(1, pin_memory=True)
-        tgt_d = torch.empty_like(target)
+        if infer:
+            # per step: the swapped environment's textures in from pinned host memory, the
+            # rendered image back
+            env_dev = [t for t in (ds.voxel, ds.planes) if t is not None]
+            env_host = [t.cpu().pin_memory() for t in env_dev]
+            himg = torch.empty((n_rays, 3), dtype=torch.float32, pin_memory=True)
 
-        def e2e_step():
-            tgt_d.copy_(htgt, non_blocking=True)
-            r = opt.step(tgt_d, pid, async_=True)
-            hloss.copy_(r.loss, non_blocking=True)
-            hior.copy_(r.ior, non_blocking=True)
+            def e2e_step():
+                for d_, h_ in zip(env_dev, env_host):
+                    d_.copy_(h_, non_blocking=True)
+                tr.trace_forward(ds, pid, rgb=rgb, async_=True)
+                himg.copy_(rgb, non_blocking=True)
+            h2d_bytes = sum(t.numel() * 4 for t in env_host)
+            d2h_bytes = himg.numel() * 4
+        else:
+            # per step: this step's target pixels in from pinned host memory, the losses and the
+            # updated IoR back (the optimiser state -- V, sigma, moments -- stays resident in HBM)
+            htgt = torch.empty((n_rays, 3), dtype=torch.float32, pin_memory=True)
+            htgt.copy_(target.cpu())
+            hloss = torch.empty(4, pin_memory=True)
+            hior = torch.empty(1, pin_memory=True)
+            tgt_d = torch.empty_like(target)
+
+            def e2e_step():
+                tgt_d.copy_(htgt, non_blocking=True)
+                r = opt.step(tgt_d, pid, async_=True)
+                hloss.copy_(r.loss, non_blocking=True)
+                hior.copy_(r.ior, non_blocking=True)
+            h2d_bytes = htgt.numel() * 4
+            d2h_bytes = hloss.numel() * 4 + hior.numel() * 4
 
         e2e_step()
         torch.cuda.synchronize()
@@ -280,8 +309,7 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(mx, op=dist.ReduceOp.MAX)
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
             ms2, s2 = float(mx[0]), float(t[1])
-        h2d = htgt.numel() * 4
-        d2h = hloss.numel() * 4 + hior.numel() * 4
+        h2d, d2h = h2d_bytes, d2h_bytes
         e2e = {"value": s2 / (ms2 / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms2 / args.steps}
 
@@ -314,22 +342,26 @@ def run_ours(args, rank, world, local_rank):
                 "share_of_step": round(ph[cls] / ms, 4)}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        dt, osegs, cores = oracle_sample(sc, args.cpu_pixels)
+        dt, osegs, cores = oracle_sample(sc, args.cpu_pixels, backward=not infer)
         cpu = {"value": osegs / dt / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{args.cpu_pixels} object pixels of {args.config}, fwd+bwd, fp64 brute force, "
+               "sample": f"{args.cpu_pixels} object pixels of {args.config}, {'fwd' if infer else 'fwd+bwd'}, "
+                         f"fp64 brute force, "
                          f"{osegs} segments in {dt:.1f}s"}
     line = {
-        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC if not infer else "Mrays·bounces/s forward-only (relighting / novel-view inference, D 8)",
+        "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: {sc.F.shape[0]} tris, {sc.cams.n_views} views "
                                f"{sc.cams.width}x{sc.cams.height}, depth {sc.max_depth}, "
-                               f"{'const' if sc.absorption.kind == 0 else 'grid'} sigma, "
-                               f"{'analytic' if sc.env.kind == 0 else 'voxel+triplane'} env",
+                               f"{['const', 'grid', 'hash-grid'][sc.absorption.kind]} sigma, "
+                               f"{'analytic' if sc.env.kind == 0 else 'voxel+triplane'} env, "
+                               f"{'forward only' if infer else 'fwd+bwd+optimiser step'}",
                    "rays_per_step": int(n_rays) * world, "segments_per_step": int(segs / args.steps),
                    "segments_per_depth": last["segments_per_depth"], "parallelism": f"rays{world}",
                    "l2": "working set > L2: path-record arena "
-                         f"{last['arena_capacity'] * 128 / 1e9:.1f} GB streamed every step; LBVH rebuilt in-step"},
+                         f"{last['arena_capacity'] * 128 / 1e9:.1f} GB streamed every step; "
+                         + ("LBVH built once (fixed mesh)" if infer else "LBVH rebuilt in-step")},
         "clocks": clk, "e2e": e2e, "gpu_launches": int(prof["kernel_launches"]), "roofline": roofline,
         "cpu_baseline": cpu,
         "phase_ms_per_step": {k: round(v / args.steps, 3) for k, v in ph.items()},
@@ -345,15 +377,17 @@ def run_reference(args, rank, world):
         return None
     from paper_2603_00413_b200 import scenes as S
     sc = S.CONFIGS[args.config]()
+    bwd = args.mode != "infer"
     for _ in range(args.warmup):
-        oracle_sample(sc, max(args.ref_pixels // 4, 1), seed=100)
+        oracle_sample(sc, max(args.ref_pixels // 4, 1), seed=100, backward=bwd)
     tot_t, tot_s = 0.0, 0
     for k in range(args.steps):
-        dt, segs, cores = oracle_sample(sc, args.ref_pixels, seed=200 + k)
+        dt, segs, cores = oracle_sample(sc, args.ref_pixels, seed=200 + k, backward=bwd)
         tot_t += dt
         tot_s += segs
     v = tot_s / tot_t / 1e6
-    sample = (f"each step: {args.ref_pixels} object pixels of {args.config} (fp64 brute force fwd+bwd); "
+    sample = (f"each step: {args.ref_pixels} object pixels of {args.config} (fp64 brute force "
+              f"{'fwd+bwd' if bwd else 'fwd'}); "
               f"{tot_s} segments in {tot_t:.1f}s")
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True,
@@ -368,13 +402,17 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default=None, help="default C3 (train) / C3R (infer)")
+    ap.add_argument("--mode", default="train", choices=["train", "infer"],
+                    help="train: one refine-loop optimisation step; infer: forward-only rendering (NEXT-3)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-pixels", type=int, default=1024, help="oracle sample for cpu_baseline (~10-30 s)")
     ap.add_argument("--ref-pixels", type=int, default=192, help="oracle pixels per --impl reference step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "C3R" if args.mode == "infer" else "C3"
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

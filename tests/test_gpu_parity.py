@@ -273,6 +273,19 @@ def test_c3_full_size_sampled(tracer):
     assert e_ior <= GRAD_TOL and e_sig <= GRAD_TOL, (e_ior, e_sig)
 
 
+def test_c3r_relighting_depth8_full_size_sampled(tracer):
+    """NEXT-3 inference workload: C3's mesh under a swapped env at D_max = 8, the bench's
+    full-image forward launch; 256 sampled object pixels against the oracle."""
+    sc = S.config_c3r()
+    pid = S.central_pixels(sc.cams, 256, 5)
+    osc = O.OracleScene(sc)
+    orc = oracle_forward(O, osc, pid)
+    gpu = run_gpu(tracer, sc, None)
+    cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
+    assert_forward(cmp, "C3R")
+    assert gpu["stats"]["segments_per_depth"][8] > 0
+
+
 def test_c4_sigma_grid_full_mesh_sampled(tracer):
     """BASELINE configs[3]: knot + gems, 64^3 sigma grid, D 6; 256 sampled pixels."""
     sc = S.config_c4()
