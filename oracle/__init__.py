@@ -45,6 +45,7 @@ class _Scene(C.Structure):
         ("max_depth", C.c_int32), ("cap_policy", C.c_int32), ("t_eps", C.c_double),
         ("V64", C.c_void_p), ("sigma64", C.c_void_p),
         ("hash_levels", C.c_int32), ("hash_log2_size", C.c_int32), ("hash_res", C.c_int32 * 32),
+        ("env_samples", C.c_int32),
     ]
 
 
@@ -108,6 +109,7 @@ class OracleScene:
         s.pres = 0 if self.planes is None else self.planes.shape[1]
         s.env_radius = env.radius
         s.far_field = env.far_field
+        s.env_samples = env.n_samples
         s.n_views, s.width, s.height = self.K.shape[0], sc.cams.width, sc.cams.height
         s.K, s.c2w = _p(self.K), _p(self.c2w)
         s.max_depth, s.cap_policy, s.t_eps = sc.max_depth, sc.cap_policy, sc.t_eps

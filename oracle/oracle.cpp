@@ -396,6 +396,73 @@ V3<S> bilerp_plane(const dto_scene* sc, int k, S a, S b) {  // a = column coord,
     }
   return out;
 }
+// Density channel (w) of the same textures (R30).
+template <class S>
+S trilerp_vox_w(const dto_scene* sc, V3<S> p) {
+  bool c;
+  S g[3] = {grid_coord(p.x, sc->env_radius, sc->vres, c), grid_coord(p.y, sc->env_radius, sc->vres, c),
+            grid_coord(p.z, sc->env_radius, sc->vres, c)};
+  int R = sc->vres, i0[3];
+  S f[3];
+  for (int a = 0; a < 3; ++a) { i0[a] = std::min((int)std::floor(val(g[a])), R - 2); f[a] = g[a] - S((double)i0[a]); }
+  S out = S(0.0);
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        S w = (dx ? f[0] : S(1.0) - f[0]) * (dy ? f[1] : S(1.0) - f[1]) * (dz ? f[2] : S(1.0) - f[2]);
+        out = out + w * S((double)sc->voxel[(((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx)) * 4 + 3]);
+      }
+  return out;
+}
+template <class S>
+S bilerp_plane_w(const dto_scene* sc, int k, S a, S b) {
+  bool c;
+  int R = sc->pres;
+  S ga = grid_coord(a, sc->env_radius, R, c), gb = grid_coord(b, sc->env_radius, R, c);
+  int ia = std::min((int)std::floor(val(ga)), R - 2), ib = std::min((int)std::floor(val(gb)), R - 2);
+  S fa = ga - S((double)ia), fb = gb - S((double)ib);
+  S out = S(0.0);
+  for (int db = 0; db < 2; ++db)
+    for (int da = 0; da < 2; ++da)
+      out = out + (da ? fa : S(1.0) - fa) * (db ? fb : S(1.0) - fb) *
+                      S((double)sc->planes[(((size_t)k * R + (ib + db)) * R + (ia + da)) * 4 + 3]);
+  return out;
+}
+// Env field at p: colour = trilinear voxel + three bilinear planes (rgb), density = the same
+// sum over the w channel, clamped at 0 (R30).
+template <class S>
+V3<S> env_colour(const dto_scene* sc, V3<S> p) {
+  return trilerp_vox(sc, p) + bilerp_plane(sc, 0, p.x, p.y) + bilerp_plane(sc, 1, p.x, p.z) +
+         bilerp_plane(sc, 2, p.y, p.z);
+}
+template <class S>
+S env_density(const dto_scene* sc, V3<S> p) {
+  S s = trilerp_vox_w(sc, p) + bilerp_plane_w(sc, 0, p.x, p.y) + bilerp_plane_w(sc, 1, p.x, p.z) +
+        bilerp_plane_w(sc, 2, p.y, p.z);
+  return val(s) > 0.0 ? s : S(0.0);
+}
+
+// Volume rendering of the env field along an exterior segment o -> x (R30; NeRF-style
+// quadrature with M midpoint samples t_i = (i + 1/2)/M, Delta = |x - o|/M):
+//   V = sum_i T_i (1 - exp(-sigma_i Delta)) c_i,  T_i = exp(-Delta sum_{j<i} sigma_j),
+//   Tn = T_M (transmittance of the whole segment, scalar).
+template <class S>
+void env_volume(const dto_scene* sc, V3<S> o, V3<S> x, V3<S>& Vr, S& Tn) {
+  const int M = sc->env_samples;
+  S delta = norm(x - o) / S((double)M);
+  S od = S(0.0);
+  Vr = zero3<S>();
+  for (int i = 0; i < M; ++i) {
+    V3<S> p = o + scl(x - o, S((i + 0.5) / M));
+    S sg = env_density(sc, p);
+    S Ti = exp(-od);
+    S ai = S(1.0) - exp(-sg * delta);
+    Vr = Vr + scl(env_colour(sc, p), Ti * ai);
+    od = od + sg * delta;
+  }
+  Tn = exp(-od);
+}
+
 template <class S>
 V3<S> shell_point(const dto_scene* sc, V3<S> o, V3<S> dh) {
   if (sc->far_field) return scl(dh, S((double)sc->env_radius));
@@ -452,6 +519,13 @@ V3<S> trace(const Model<S>& m, V3<S> o, V3<S> d, int k, uint64_t pos, double w, 
   if (h.face < 0) {                                                 // step 3: miss -> env
     st.sig_topo += mix64(topo_key(pos, EV_MISS));
     st.sig_face += mix64(face_key(pos, EV_MISS, -1));
+    if (sc->env_kind == 2) {                                        // volume out to the shell (R30)
+      V3<S> ps = shell_point(sc, o, scl(d, S(1.0) / norm(d)));
+      V3<S> Vr;
+      S Tn;
+      env_volume(sc, o, ps, Vr, Tn);
+      return Vr + scl(env(sc, o, d), Tn);
+    }
     return env(sc, o, d);
   }
   const int32_t* F = sc->F + 3 * h.face;
@@ -464,6 +538,12 @@ V3<S> trace(const Model<S>& m, V3<S> o, V3<S> d, int k, uint64_t pos, double w, 
     st.sig_topo += mix64(topo_key(pos, ev));
     st.sig_face += mix64(face_key(pos, ev, h.face));
     st.capped_w += w;
+    if (!inside && sc->env_kind == 2) {                             // exterior: its volume part stays
+      V3<S> Vr;
+      S Tn;
+      env_volume(sc, o, x, Vr, Tn);
+      return sc->cap_policy == 0 ? Vr : Vr + scl(env(sc, o, d), Tn);
+    }
     if (sc->cap_policy == 0) return zero3<S>();
     V3<S> E = env(sc, o, d);
     return inside ? mul(transmittance(m, o, x), E) : E;
@@ -486,6 +566,12 @@ V3<S> trace(const Model<S>& m, V3<S> o, V3<S> d, int k, uint64_t pos, double w, 
     L = L + scl(Lt, I.T);
   }
   if (inside) L = mul(transmittance(m, o, x), L);                  // step 5, P:162 (R9)
+  if (!inside && sc->env_kind == 2) {                               // env mixed in before x (R30)
+    V3<S> Vr;
+    S Tn;
+    env_volume(sc, o, x, Vr, Tn);
+    L = Vr + scl(L, Tn);
+  }
   return L;
 }
 
@@ -603,7 +689,7 @@ void transmittance_bwd(const Model<double>& m, V3d o, V3d x, const double gS[3],
 }
 
 // d/dp of one clamped grid coordinate's trilinear / bilinear lookup.
-V3d trilerp_vox_bwd(const dto_scene* sc, V3d p, V3d a) {
+V3d trilerp_vox_bwd(const dto_scene* sc, V3d p, V3d a, double aw = 0.0) {
   bool c[3];
   double g[3] = {grid_coord(p.x, sc->env_radius, sc->vres, c[0]), grid_coord(p.y, sc->env_radius, sc->vres, c[1]),
                  grid_coord(p.z, sc->env_radius, sc->vres, c[2])};
@@ -616,7 +702,7 @@ V3d trilerp_vox_bwd(const dto_scene* sc, V3d p, V3d a) {
       for (int dx = 0; dx < 2; ++dx) {
         double wx = dx ? f[0] : 1 - f[0], wy = dy ? f[1] : 1 - f[1], wz = dz ? f[2] : 1 - f[2];
         const float* t = sc->voxel + (((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx)) * 4;
-        double s = a.x * t[0] + a.y * t[1] + a.z * t[2];
+        double s = a.x * t[0] + a.y * t[1] + a.z * t[2] + aw * t[3];
         gp.x += s * (dx ? 1 : -1) * wy * wz;
         gp.y += s * wx * (dy ? 1 : -1) * wz;
         gp.z += s * wx * wy * (dz ? 1 : -1);
@@ -627,7 +713,8 @@ V3d trilerp_vox_bwd(const dto_scene* sc, V3d p, V3d a) {
   if (c[2]) gp.z = 0;
   return gp;
 }
-void bilerp_plane_bwd(const dto_scene* sc, int k, double a, double b, V3d adj, double& ga_out, double& gb_out) {
+void bilerp_plane_bwd(const dto_scene* sc, int k, double a, double b, V3d adj, double& ga_out, double& gb_out,
+                      double aw = 0.0) {
   bool ca, cb;
   int R = sc->pres;
   double ga = grid_coord(a, sc->env_radius, R, ca), gb = grid_coord(b, sc->env_radius, R, cb);
@@ -637,7 +724,7 @@ void bilerp_plane_bwd(const dto_scene* sc, int k, double a, double b, V3d adj, d
   for (int db = 0; db < 2; ++db)
     for (int da = 0; da < 2; ++da) {
       const float* t = sc->planes + (((size_t)k * R + (ib + db)) * R + (ia + da)) * 4;
-      double s = adj.x * t[0] + adj.y * t[1] + adj.z * t[2];
+      double s = adj.x * t[0] + adj.y * t[1] + adj.z * t[2] + aw * t[3];
       da_ += s * (da ? 1 : -1) * (db ? fb : 1 - fb);
       db_ += s * (da ? fa : 1 - fa) * (db ? 1 : -1);
     }
@@ -646,6 +733,29 @@ void bilerp_plane_bwd(const dto_scene* sc, int k, double a, double b, V3d adj, d
 }
 
 // Reverse of env(o, d) given the RGB adjoint a: returns (go, gd).
+// Reverse of the shell point p = o + ts dh (||p|| = R_e) or p = R_e dh (far field): adds the
+// adjoints of o and dh for gp = dL/dp.
+void shell_point_bwd(const dto_scene* sc, V3d o, V3d dh, V3d gp, V3d& go, V3d& gdh) {
+  if (sc->far_field) {
+    gdh = gdh + scl(gp, (double)sc->env_radius);
+    return;
+  }
+  double b = dot(o, dh), Re = sc->env_radius;
+  double sq = std::sqrt(b * b - dot(o, o) + Re * Re);
+  double ts = -b + sq;
+  // p = o + ts dh
+  go = go + gp;
+  gdh = gdh + scl(gp, ts);
+  double gts = dot(gp, dh);
+  // ts = -b + sqrt(disc), disc = b^2 - o.o + Re^2
+  double gdisc = gts / (2.0 * sq);
+  double gb = -gts + gdisc * 2.0 * b;
+  go = go - scl(o, 2.0 * gdisc);
+  // b = o . dh
+  go = go + scl(dh, gb);
+  gdh = gdh + scl(o, gb);
+}
+
 void env_bwd(const dto_scene* sc, V3d o, V3d d, V3d a, V3d& go, V3d& gd) {
   double dn = norm(d);
   V3d dh = scl(d, 1.0 / dn);
@@ -666,26 +776,62 @@ void env_bwd(const dto_scene* sc, V3d o, V3d d, V3d a, V3d& go, V3d& gd) {
     bilerp_plane_bwd(sc, 0, p.x, p.y, a, g1, g2); gp.x += g1; gp.y += g2;
     bilerp_plane_bwd(sc, 1, p.x, p.z, a, g1, g2); gp.x += g1; gp.z += g2;
     bilerp_plane_bwd(sc, 2, p.y, p.z, a, g1, g2); gp.y += g1; gp.z += g2;
-    if (sc->far_field) {
-      gdh = scl(gp, (double)sc->env_radius);
-    } else {
-      double b = dot(o, dh), Re = sc->env_radius;
-      double sq = std::sqrt(b * b - dot(o, o) + Re * Re);
-      double ts = -b + sq;
-      // p = o + ts dh
-      go = go + gp;
-      gdh = gdh + scl(gp, ts);
-      double gts = dot(gp, dh);
-      // ts = -b + sqrt(disc), disc = b^2 - o.o + Re^2
-      double gdisc = gts / (2.0 * sq);
-      double gb = -gts + gdisc * 2.0 * b;
-      go = go - scl(o, 2.0 * gdisc);
-      // b = o . dh
-      go = go + scl(dh, gb);
-      gdh = gdh + scl(o, gb);
-    }
+    shell_point_bwd(sc, o, dh, gp, go, gdh);
   }
   gd = scl(gdh - scl(dh, dot(dh, gdh)), 1.0 / dn);   // through dh = d/|d|
+}
+
+// d a . (colour(p)) + aw * density(p) / dp of the volumetric env field (R30); the density
+// clamp at 0 passes no gradient (aw must be 0 there).
+V3d env_field_bwd(const dto_scene* sc, V3d p, V3d a, double aw) {
+  V3d gp = trilerp_vox_bwd(sc, p, a, aw);
+  double g1, g2;
+  bilerp_plane_bwd(sc, 0, p.x, p.y, a, g1, g2, aw); gp.x += g1; gp.y += g2;
+  bilerp_plane_bwd(sc, 1, p.x, p.z, a, g1, g2, aw); gp.x += g1; gp.z += g2;
+  bilerp_plane_bwd(sc, 2, p.y, p.z, a, g1, g2, aw); gp.y += g1; gp.z += g2;
+  return gp;
+}
+
+// Reverse of env_volume(o, x) given aV = dL/dV (rgb) and aT = dL/dTn: adds the adjoints of
+// the segment end points to go, gx.  With T_0 = 1 and V = sum_i (T_i - T_{i+1}) c_i:
+// dL/dT_i = s_i - s_{i-1} (0 < i < M), dL/dT_M = aT - s_{M-1}, s_i = aV . c_i;
+// dL/dsigma_j = -Delta sum_{i>j} dL/dT_i T_i;  dL/dDelta = -sum_i dL/dT_i T_i sum_{j<i} sigma_j.
+void env_volume_bwd(const dto_scene* sc, V3d o, V3d x, V3d aV, double aT, V3d& go, V3d& gx) {
+  const int M = sc->env_samples;
+  V3d dx = x - o;
+  double l = norm(dx), delta = l / M;
+  std::vector<double> sg(M), raw(M), pre(M + 1, 0.0), T(M + 1, 1.0), s(M), gT(M + 1, 0.0);
+  for (int i = 0; i < M; ++i) {
+    V3d p = o + scl(dx, (i + 0.5) / M);
+    raw[i] = trilerp_vox_w<double>(sc, p) + bilerp_plane_w<double>(sc, 0, p.x, p.y) +
+             bilerp_plane_w<double>(sc, 1, p.x, p.z) + bilerp_plane_w<double>(sc, 2, p.y, p.z);
+    sg[i] = raw[i] > 0.0 ? raw[i] : 0.0;
+    s[i] = dot(aV, env_colour<double>(sc, p));
+    pre[i + 1] = pre[i] + sg[i];
+    T[i + 1] = std::exp(-delta * pre[i + 1]);
+  }
+  for (int i = 1; i < M; ++i) gT[i] = s[i] - s[i - 1];
+  gT[M] = aT - s[M - 1];
+  double acc = 0.0, gdelta = 0.0;
+  std::vector<double> gsg(M);
+  for (int i = M; i >= 1; --i) {
+    acc += gT[i] * T[i];
+    gsg[i - 1] = -delta * acc;
+    gdelta -= gT[i] * T[i] * pre[i];
+  }
+  for (int i = 0; i < M; ++i) {
+    double t = (i + 0.5) / M;
+    V3d p = o + scl(dx, t);
+    V3d gp = env_field_bwd(sc, p, scl(aV, T[i] - T[i + 1]), raw[i] > 0.0 ? gsg[i] : 0.0);
+    go = go + scl(gp, 1.0 - t);
+    gx = gx + scl(gp, t);
+  }
+  if (l > 0.0) {
+    V3d u = scl(dx, 1.0 / l);
+    double gl = gdelta / M;
+    gx = gx + scl(u, gl);
+    go = go - scl(u, gl);
+  }
 }
 
 // Reverse of the Moller-Trumbore solve M [u v t]^T = o - v0, M = [e1 e2 -d] (R15): with
@@ -712,6 +858,21 @@ Bwd trace_bwd(const Model<double>& m, V3d o, V3d d, int k, V3d a, Grad& G) {
   Hit h = closest_hit(m, o, d, t_lo);
   Bwd out{{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   if (h.face < 0) {                                                 // leaf: env (R22: env frozen)
+    if (sc->env_kind == 2) {                                        // volume out to the shell (R30)
+      V3d dh = scl(d, 1.0 / norm(d));
+      V3d ps = shell_point<double>(sc, o, dh);
+      V3d Vr, E = env<double>(sc, o, d);
+      double Tn;
+      env_volume(sc, o, ps, Vr, Tn);
+      out.L = Vr + scl(E, Tn);
+      env_bwd(sc, o, d, scl(a, Tn), out.go, out.gd);
+      V3d gov = {0, 0, 0}, gps = {0, 0, 0}, gdh = {0, 0, 0};
+      env_volume_bwd(sc, o, ps, a, dot(a, E), gov, gps);
+      shell_point_bwd(sc, o, dh, gps, gov, gdh);
+      out.go = out.go + gov;
+      out.gd = out.gd + scl(gdh - scl(dh, dot(dh, gdh)), 1.0 / norm(d));
+      return out;
+    }
     out.L = env<double>(sc, o, d);
     env_bwd(sc, o, d, a, out.go, out.gd);
     return out;
@@ -723,7 +884,20 @@ Bwd trace_bwd(const Model<double>& m, V3d o, V3d d, int k, V3d a, Grad& G) {
   bool inside = dot(d, gnrm) > 0.0;
   V3d gx = {0, 0, 0};
   double gu = 0, gv = 0;
-  if (k == sc->max_depth) {                                         // capped leaf (R13)
+  if (k == sc->max_depth && !inside && sc->env_kind == 2) {         // capped exterior, volume env
+    V3d Vr;
+    double Tn;
+    env_volume(sc, o, x, Vr, Tn);
+    double aT = 0.0;
+    out.L = Vr;
+    if (sc->cap_policy == 1) {
+      V3d E = env<double>(sc, o, d);
+      out.L = out.L + scl(E, Tn);
+      env_bwd(sc, o, d, scl(a, Tn), out.go, out.gd);
+      aT = dot(a, E);
+    }
+    env_volume_bwd(sc, o, x, a, aT, out.go, gx);
+  } else if (k == sc->max_depth) {                                  // capped leaf (R13)
     if (sc->cap_policy == 0) return out;
     V3d E = env<double>(sc, o, d);
     if (!inside) { out.L = E; env_bwd(sc, o, d, a, out.go, out.gd); return out; }
@@ -741,16 +915,24 @@ Bwd trace_bwd(const Model<double>& m, V3d o, V3d d, int k, V3d a, Grad& G) {
     double eta_i = inside ? m.ior : 1.0, eta_t = inside ? 1.0 : m.ior;
     Iface<double> I = interface(d, n, eta_i, eta_t);
     V3d tau = inside ? transmittance(m, o, x) : V3d{1, 1, 1};
+    const bool vol = !inside && sc->env_kind == 2;                  // exterior: env mixed in (R30)
+    V3d Vr = {0, 0, 0};
+    if (vol) {
+      double Tn;
+      env_volume(sc, o, x, Vr, Tn);
+      tau = {Tn, Tn, Tn};
+    }
     V3d ap = mul(a, tau);
     // ---- children (their adjoints carry R and T)
     Bwd cr = trace_bwd(m, x, I.wr, k + 1, scl(ap, I.R), G);
     Bwd ct = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
     if (!I.tir) ct = trace_bwd(m, x, I.wt, k + 1, scl(ap, I.T), G);
     V3d Lc = scl(cr.L, I.R) + scl(ct.L, I.T);
-    out.L = mul(tau, Lc);
+    out.L = Vr + mul(tau, Lc);
     // ---- reverse, last operation first
     gx = cr.go + ct.go;
     V3d gwr = cr.gd, gwt = ct.gd;
+    if (vol) env_volume_bwd(sc, o, x, a, dot(a, Lc), out.go, gx);
     if (inside) {
       double gS[3] = {-a.x * Lc.x * tau.x, -a.y * Lc.y * tau.y, -a.z * Lc.z * tau.z};
       transmittance_bwd(m, o, x, gS, gx, out.go, G);

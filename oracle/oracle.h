@@ -29,7 +29,7 @@ typedef struct {
   float sigma_lo[3], sigma_hi[3];
   int32_t n_samples;                /* N_sigma midpoint samples per interior segment    */
   /* frozen environment, P:91 / P:160 (R14) */
-  int32_t env_kind;                 /* 0 = analytic lobes, 1 = voxel + triplane shell   */
+  int32_t env_kind;                 /* 0 = analytic lobes, 1 = voxel + triplane shell, 2 = volume */
   float ambient[3];
   const float* lobes;               /* [n_lobes][7] = mu(3), kappa, w(3)                */
   int32_t n_lobes;
@@ -57,6 +57,11 @@ typedef struct {
   int32_t hash_levels;
   int32_t hash_log2_size;
   int32_t hash_res[32];
+  /* env_kind 2 = volumetric env (P:91 MERF grid + triplanes, "mixed with the
+   * environmental radiance prior to the intersection point"; R30): the voxel/planes textures
+   * give colour (rgb) and density (w, clamped >= 0); every exterior segment is volume
+   * rendered with env_samples midpoint samples; escaping rays end in the shell lookup. */
+  int32_t env_samples;
 } dto_scene;
 
 /* Per-ray flag bits (parity protocol). */

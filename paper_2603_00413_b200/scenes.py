@@ -32,6 +32,7 @@ import numpy as np
 
 ENV_ANALYTIC = 0
 ENV_GRID = 1
+ENV_VOLUME = 2
 ABS_CONST = 0
 ABS_GRID = 1
 ABS_HASH = 2
@@ -347,6 +348,7 @@ class Env:
     planes: np.ndarray = None       # [3,pres,pres,4]: P_xy[y][x], P_xz[z][x], P_yz[z][y]
     radius: float = 10.0
     far_field: int = 0
+    n_samples: int = 32             # ENV_VOLUME: midpoint samples per exterior segment (R30)
 
 
 def analytic_env(seed: int, n_lobes: int = 8, ambient: float = 0.2) -> Env:
@@ -371,6 +373,26 @@ def _smooth_field(g, coords, n_waves, lo, hi, scale):
         acc = (acc - acc.min()) / max(acc.max() - acc.min(), 1e-12)
         out[..., c] = lo + (hi - lo) * acc
     return out
+
+
+def volume_env(seed: int, vres: int, pres: int, radius: float = 10.0, density: float = 0.12,
+               n_samples: int = 32) -> Env:
+    """Volumetric env (P:91 MERF coarse grid + fine triplanes; R30): grid_env's colour
+    textures plus a density channel (w): a smooth voxel field in [0, density] and plane
+    fields in [0, density / 4] (per unit length), so a camera-to-object segment loses a few
+    percent and an escaping ray tens of percent before the shell."""
+    env = grid_env(seed, vres, pres, radius, 0)
+    g = rng(seed, 33)
+    ax = np.linspace(-1.0, 1.0, vres)
+    zz, yy, xx = np.meshgrid(ax, ax, ax, indexing="ij")
+    env.voxel[..., 3] = _smooth_field(g, np.stack([xx, yy, zz], -1), 4, 0.0, density, 3.0)[..., 0]
+    ap = np.linspace(-1.0, 1.0, pres)
+    bb, aa = np.meshgrid(ap, ap, indexing="ij")
+    for i in range(3):
+        env.planes[i, ..., 3] = _smooth_field(g, np.stack([aa, bb], -1), 6, 0.0, density / 4, 8.0)[..., 0]
+    env.kind = ENV_VOLUME
+    env.n_samples = n_samples
+    return env
 
 
 def grid_env(seed: int, vres: int, pres: int, radius: float = 10.0, far_field: int = 0) -> Env:

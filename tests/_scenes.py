@@ -42,6 +42,11 @@ def linear_grid_env(vres=5, pres=4, radius=10.0, coeff=((1, 0, 0), (0, 1, 0), (0
     return S.Env(S.ENV_GRID, voxel=vox, planes=planes, radius=radius, far_field=0)
 
 
+def small_volume_env(seed=7, vres=8, pres=16, radius=6.0, density=0.15, n_samples=12):
+    """Tiny volumetric env (R30): grid_env colours plus a smooth density channel."""
+    return S.volume_env(seed, vres, pres, radius, density, n_samples)
+
+
 def small_sigma_grid(V, res=6, seed=3):
     return S.grid_absorption(np.asarray(V), res, seed, n_samples=16)
 

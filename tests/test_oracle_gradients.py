@@ -30,6 +30,8 @@ def fd_scenes():
     V0, F0 = S.icosphere(0)
     out["ico0_sigmagrid"] = T.scene(V0, F0, cams, env=T.lobe_env(kappa=2.0),
                                     absorption=T.small_sigma_grid(V0, 5), D=3)
+    out["ico1_volenv"] = T.scene(V, F, cams, env=T.small_volume_env(), D=3)
+    out["ico1_volenv_capenv"] = T.scene(V, F, cams, env=T.small_volume_env(seed=8), D=2, cap=S.CAP_ENV)
     out["ico0_hashgrid"] = T.scene(V0, F0, cams, env=T.lobe_env(kappa=2.0),
                                    absorption=T.small_hash_grid(V0), D=3)
     Vt, Ft = S.tetrahedron()
