@@ -51,7 +51,7 @@ typedef enum {
 } dt_status;
 
 enum { DT_ABS_CONST = 0, DT_ABS_GRID = 1, DT_ABS_HASH = 2 };
-enum { DT_ENV_ANALYTIC = 0, DT_ENV_GRID = 1 };
+enum { DT_ENV_ANALYTIC = 0, DT_ENV_GRID = 1, DT_ENV_VOLUME = 2 };
 enum { DT_CAP_ZERO = 0, DT_CAP_ENV = 1 };
 #define DT_MAX_DEPTH 15
 
@@ -86,6 +86,14 @@ typedef struct {
  *            + bilinear(P_xz, p.x, p.z) + bilinear(P_yz, p.y, p.z).  voxel -> float
  *            [vres][vres][vres][4] = [z][y][x][rgb_]; planes -> float [3][pres][pres][4]
  *            (P_xy[y][x], P_xz[z][x], P_yz[z][y]); both span [-radius, radius].
+ *  VOLUME:   the same textures read as a frozen radiance field (P:91 MERF coarse grid + fine
+ *            triplanes; R30): rgb = colour, w = density (clamped at 0).  Every exterior
+ *            segment o -> x (camera and reflected/refracted rays outside the object; x = the
+ *            next hit, or the shell point for an escaping ray) is volume rendered with
+ *            n_samples midpoint samples, V = sum_i T_i (1 - exp(-sigma_i D)) c_i, and its
+ *            continuation is attenuated by T = exp(-D sum sigma_i) ("mixed with
+ *            the environmental radiance prior to the intersection point").  Escaping rays end
+ *            in the GRID shell lookup.  far_field must be 0.
  *  The env is not differentiated (R22).  It must stay alive and unchanged until the
  *  matching dt_trace_backward returns (the backward replays the lookups). */
 typedef struct {
@@ -99,6 +107,7 @@ typedef struct {
   int32_t pres;
   float radius;
   int32_t far_field;
+  int32_t n_samples;       /* VOLUME only: midpoint samples per exterior segment (>= 1) */
 } dt_env;
 
 /* Pinhole cameras, OpenCV axes (R19): d_cam = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1),

@@ -188,13 +188,15 @@ def camera_rays(osc: OracleScene, pixel_ids):
 
 FLAG_ILLCOND = 8
 F32_DIR_ERR = 1.2e-7     # ~2 ulp of a float32 unit direction component
+F32_POS_ERR = 1.2e-7     # ~2 ulp (relative to the mesh extent) of float32 geometry
 
 
 def ill_conditioned(osc: OracleScene, pixel_ids, tol: float = 5e-5, n_dirs: int = 2, nthreads: int = 0):
     """Pixels whose radiance moves by more than `tol` when the camera ray direction moves by
-    the float32 rounding of its components (F32_DIR_ERR): float32 arithmetic cannot hold them
+    the float32 rounding of its components (F32_DIR_ERR), or when the vertices move by the
+    float32 rounding of the mesh geometry (F32_POS_ERR): float32 arithmetic cannot hold them
     to 1e-4 whatever the implementation.  Estimated with float64 central
-    differences along random tangents (eps = 1e-7, far inside the smooth region)."""
+    differences along random tangents / displacements (eps = 1e-7, inside the smooth region)."""
     rays = camera_rays(osc, pixel_ids)
     n = rays.shape[0]
     g = np.random.default_rng(1234)
@@ -213,7 +215,30 @@ def ill_conditioned(osc: OracleScene, pixel_ids, tol: float = 5e-5, n_dirs: int 
         s = np.abs(a["rgb"] - b["rgb"]).max(1) / (2 * eps)
         s[a["sig_topo"] != b["sig_topo"]] = np.inf
         sens = np.maximum(sens, s)
-    return sens * F32_DIR_ERR > tol
+    ill = sens * F32_DIR_ERR > tol
+    # geometry: the device reads the same float32 vertices but derives edges, normals and hit
+    # points in float32 (~1-2 ulp of the mesh extent each); same estimate along random
+    # per-vertex displacements of that size
+    scale = float(np.abs(osc.V).max()) or 1.0
+    h = 1e-7 * scale
+    V0 = osc.V.astype(np.float64) if osc.V64 is None else osc.V64
+    old = osc.s.V64
+    sens_v = np.zeros(n)
+    try:
+        for k in range(n_dirs):
+            U = g.normal(size=V0.shape)
+            U /= np.linalg.norm(U, axis=1, keepdims=True)
+            Vp, Vm = np.ascontiguousarray(V0 + h * U), np.ascontiguousarray(V0 - h * U)
+            osc.s.V64 = _p(Vp)
+            a = render(osc, pixel_ids, nthreads=nthreads)
+            osc.s.V64 = _p(Vm)
+            b = render(osc, pixel_ids, nthreads=nthreads)
+            s = np.abs(a["rgb"] - b["rgb"]).max(1) / (2 * h)
+            s[a["sig_topo"] != b["sig_topo"]] = np.inf
+            sens_v = np.maximum(sens_v, s)
+    finally:
+        osc.s.V64 = old
+    return ill | (sens_v * F32_POS_ERR * scale > tol)
 
 
 def vertex_normals(osc: OracleScene):

@@ -554,7 +554,7 @@ V3<S> trace(const Model<S>& m, V3<S> o, V3<S> d, int k, uint64_t pos, double w, 
   S eta_i = inside ? m.ior : S(1.0), eta_t = inside ? S(1.0) : m.ior;
   Iface<S> I = interface(d, n, eta_i, eta_t);
   if (val(I.c_raw) < 1e-3) st.flags |= DTO_FLAG_GRAZING;
-  if (std::fabs(val(I.q)) < 1e-4) st.flags |= DTO_FLAG_NEARTIR;
+  if (std::fabs(val(I.q)) < 1e-3) st.flags |= DTO_FLAG_NEARTIR;   // dR/dc_i ~ 1/sqrt(q) > 100 here
   int ev = inside ? (I.tir ? EV_HIT_IN_TIR : EV_HIT_IN) : (I.tir ? EV_HIT_OUT_TIR : EV_HIT_OUT);
   st.sig_topo += mix64(topo_key(pos, ev));
   st.sig_face += mix64(face_key(pos, ev, h.face));

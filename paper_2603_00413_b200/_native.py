@@ -28,7 +28,7 @@ class Absorption(C.Structure):
 class Env(C.Structure):
     _fields_ = [("kind", C.c_int32), ("ambient", C.c_float * 3), ("lobes", C.c_void_p), ("n_lobes", C.c_int32),
                 ("voxel", C.c_void_p), ("vres", C.c_int32), ("planes", C.c_void_p), ("pres", C.c_int32),
-                ("radius", C.c_float), ("far_field", C.c_int32)]
+                ("radius", C.c_float), ("far_field", C.c_int32), ("n_samples", C.c_int32)]
 
 
 class Cameras(C.Structure):

@@ -277,7 +277,9 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   DT_ARG(abs_valid(ab), "dt_trace_forward: absorption (kind=%d res=%d n_samples=%d levels=%d log2_size=%d) invalid",
          ab->kind, ab->res, ab->n_samples, ab->levels, ab->log2_size);
   DT_ARG((env->kind == DT_ENV_ANALYTIC && (env->n_lobes == 0 || env->lobes)) ||
-             (env->kind == DT_ENV_GRID && env->voxel && env->planes && env->vres >= 2 && env->pres >= 2 && env->radius > 0),
+             ((env->kind == DT_ENV_GRID || env->kind == DT_ENV_VOLUME) && env->voxel && env->planes && env->vres >= 2 &&
+              env->pres >= 2 && env->radius > 0 &&
+              (env->kind == DT_ENV_GRID || (env->n_samples >= 1 && !env->far_field))),
          "dt_trace_forward: env (kind=%d) invalid", env->kind);
   int64_t npix = (int64_t)cams->n_views * cams->width * cams->height;
   int64_t n_rays = cams->pixel_ids ? cams->n_rays : npix;
@@ -328,6 +330,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   s.voxel = (const float4*)env->voxel;
   s.vres = env->vres;
   s.planes = (const float4*)env->planes;
+  s.env_nsamp = env->kind == DT_ENV_VOLUME ? env->n_samples : 0;
   s.pres = env->pres;
   s.radius = env->radius;
   s.far_field = env->far_field;

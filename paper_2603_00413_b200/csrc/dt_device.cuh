@@ -70,6 +70,7 @@ struct DevScene {
   int vres;
   const float4* planes;
   int pres;
+  int env_nsamp;        // volumetric env: samples per exterior segment (R30)
   float radius;
   int far_field;
   // options
@@ -890,6 +891,199 @@ DT_D float3 env_plane(const DevScene& s, int k, float a_, float b_, float3 adj, 
     *gb = cb ? 0.f : db * sc;
   }
   return out;
+}
+
+// Reverse of the shell point p = o + ts dh (or R_e dh in the far field): adds the adjoints
+// of o and dh for gp = dL/dp (ts, sq from shell_point).
+DT_D void shell_point_bwd(const DevScene& s, float3 o, float3 dh, float ts, float sq, float3 gp, float3& go,
+                          float3& gdh) {
+  if (s.far_field) {
+    gdh += gp * s.radius;
+    return;
+  }
+  float b = dot(o, dh);
+  go += gp;
+  gdh += gp * ts;
+  float gts = dot(gp, dh);
+  float gdisc = sq > 0.0f ? gts / (2.0f * sq) : 0.0f;
+  float gb = -gts + gdisc * 2.0f * b;
+  go -= o * (2.0f * gdisc);
+  go += dh * gb;
+  gdh += o * gb;
+}
+
+// ---- volumetric env (env_kind 2, R30): the voxel/plane textures carry colour (rgb) and
+// density (w).  env_field: rgb and the raw (unclamped) density at p; env_field_bwd: d/dp of
+// a . rgb + aw * density.
+DT_D float4 env_field(const DevScene& s, float3 p) {
+  bool c;
+  const float g[3] = {grid_coord(p.x, s.radius, s.vres, c), grid_coord(p.y, s.radius, s.vres, c),
+                      grid_coord(p.z, s.radius, s.vres, c)};
+  const int R = s.vres;
+  int i0[3];
+  float f[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { i0[k] = min((int)floorf(g[k]), R - 2); f[k] = g[k] - (float)i0[k]; }
+  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
+    const float w = (dx ? f[0] : 1 - f[0]) * (dy ? f[1] : 1 - f[1]) * (dz ? f[2] : 1 - f[2]);
+    const float4 t = __ldg(s.voxel + ((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx));
+    out.x += t.x * w; out.y += t.y * w; out.z += t.z * w; out.w += t.w * w;
+  }
+  const float pa[3] = {p.x, p.x, p.y}, pb[3] = {p.y, p.z, p.z};
+  const int Rp = s.pres;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    bool ca, cb;
+    const float ga = grid_coord(pa[k], s.radius, Rp, ca), gb = grid_coord(pb[k], s.radius, Rp, cb);
+    const int ia = min((int)floorf(ga), Rp - 2), ib = min((int)floorf(gb), Rp - 2);
+    const float fa = ga - (float)ia, fb = gb - (float)ib;
+    const float4* P = s.planes + (size_t)k * Rp * Rp;
+    const float4 t00 = __ldg(P + (size_t)ib * Rp + ia), t01 = __ldg(P + (size_t)ib * Rp + ia + 1);
+    const float4 t10 = __ldg(P + (size_t)(ib + 1) * Rp + ia), t11 = __ldg(P + (size_t)(ib + 1) * Rp + ia + 1);
+    const float w00 = (1 - fa) * (1 - fb), w01 = fa * (1 - fb), w10 = (1 - fa) * fb, w11 = fa * fb;
+    out.x += t00.x * w00 + t01.x * w01 + t10.x * w10 + t11.x * w11;
+    out.y += t00.y * w00 + t01.y * w01 + t10.y * w10 + t11.y * w11;
+    out.z += t00.z * w00 + t01.z * w01 + t10.z * w10 + t11.z * w11;
+    out.w += t00.w * w00 + t01.w * w01 + t10.w * w10 + t11.w * w11;
+  }
+  return out;
+}
+
+DT_D float3 env_field_bwd(const DevScene& s, float3 p, float3 a, float aw) {
+  bool c[3];
+  const float g[3] = {grid_coord(p.x, s.radius, s.vres, c[0]), grid_coord(p.y, s.radius, s.vres, c[1]),
+                      grid_coord(p.z, s.radius, s.vres, c[2])};
+  const int R = s.vres;
+  int i0[3];
+  float f[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { i0[k] = min((int)floorf(g[k]), R - 2); f[k] = g[k] - (float)i0[k]; }
+  float3 gg = f3(0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
+    const float wx = dx ? f[0] : 1 - f[0], wy = dy ? f[1] : 1 - f[1], wz = dz ? f[2] : 1 - f[2];
+    const float4 t = __ldg(s.voxel + ((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx));
+    const float sd = a.x * t.x + a.y * t.y + a.z * t.z + aw * t.w;
+    gg += f3((dx ? 1.f : -1.f) * wy * wz, wx * (dy ? 1.f : -1.f) * wz, wx * wy * (dz ? 1.f : -1.f)) * sd;
+  }
+  const float sv = (float)(R - 1) / (2.0f * s.radius);
+  float3 gp = f3(c[0] ? 0.f : gg.x * sv, c[1] ? 0.f : gg.y * sv, c[2] ? 0.f : gg.z * sv);
+  const float pa[3] = {p.x, p.x, p.y}, pb[3] = {p.y, p.z, p.z};
+  const int Rp = s.pres;
+  const float spl = (float)(Rp - 1) / (2.0f * s.radius);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    bool ca, cb;
+    const float ga = grid_coord(pa[k], s.radius, Rp, ca), gb = grid_coord(pb[k], s.radius, Rp, cb);
+    const int ia = min((int)floorf(ga), Rp - 2), ib = min((int)floorf(gb), Rp - 2);
+    const float fa = ga - (float)ia, fb = gb - (float)ib;
+    const float4* P = s.planes + (size_t)k * Rp * Rp;
+    const float4 t00 = __ldg(P + (size_t)ib * Rp + ia), t01 = __ldg(P + (size_t)ib * Rp + ia + 1);
+    const float4 t10 = __ldg(P + (size_t)(ib + 1) * Rp + ia), t11 = __ldg(P + (size_t)(ib + 1) * Rp + ia + 1);
+    const float s00 = dot(a, f3(t00)) + aw * t00.w, s01 = dot(a, f3(t01)) + aw * t01.w;
+    const float s10 = dot(a, f3(t10)) + aw * t10.w, s11 = dot(a, f3(t11)) + aw * t11.w;
+    const float da = ca ? 0.f : ((s01 - s00) * (1 - fb) + (s11 - s10) * fb) * spl;
+    const float db = cb ? 0.f : ((s10 - s00) * (1 - fa) + (s11 - s01) * fa) * spl;
+    if (k == 0) { gp.x += da; gp.y += db; }
+    else if (k == 1) { gp.x += da; gp.z += db; }
+    else { gp.y += da; gp.z += db; }
+  }
+  return gp;
+}
+
+// Emission-absorption quadrature along an exterior segment o -> x (R30, M midpoint samples):
+// V = sum_i T_i (1 - exp(-sigma_i Delta)) c_i, T_i = exp(-Delta sum_{j<i} sigma_j), Tn = T_M.
+DT_D void env_volume(const DevScene& s, float3 o, float3 x, float3& V, float& Tn) {
+  const int M = s.env_nsamp;
+  const float3 dx = x - o;
+  const float delta = length(dx) / (float)M;
+  float od = 0.f;
+  V = f3(0, 0, 0);
+  for (int i = 0; i < M; ++i) {
+    const float4 f = env_field(s, o + dx * (((float)i + 0.5f) / (float)M));
+    const float sg = fmaxf(f.w, 0.f);
+    V += f3(f) * (expf(-od) * (1.f - expf(-sg * delta)));
+    od += sg * delta;
+  }
+  Tn = expf(-od);
+}
+
+// Reverse of env_volume given aV = dL/dV and aT = dL/dTn: adds the end-point adjoints to go,
+// gx.  Two passes over the samples (no per-sample storage): with s_i = aV . c_i and
+// dL/dT_i = s_i - s_{i-1} (0 < i < M), dL/dT_M = aT - s_{M-1}, the density adjoint is
+// dL/dsigma_j = -Delta (Q - sum_{i<=j} dL/dT_i T_i) with Q = sum_{i=1..M} dL/dT_i T_i.
+DT_D void env_volume_bwd(const DevScene& s, float3 o, float3 x, float3 aV, float aT, float3& go, float3& gx) {
+  const int M = s.env_nsamp;
+  const float3 dx = x - o;
+  const float l = length(dx), delta = l / (float)M;
+  float Q = 0.f, gdelta = 0.f, pre = 0.f, sprev = 0.f;
+  for (int i = 0; i < M; ++i) {              // pass 1: Q and dL/dDelta
+    const float4 f = env_field(s, o + dx * (((float)i + 0.5f) / (float)M));
+    const float si = dot(aV, f3(f));
+    if (i > 0) {
+      const float term = (si - sprev) * expf(-delta * pre);
+      Q += term;
+      gdelta -= term * pre;
+    }
+    pre += fmaxf(f.w, 0.f);
+    sprev = si;
+  }
+  {
+    const float term = (aT - sprev) * expf(-delta * pre);
+    Q += term;
+    gdelta -= term * pre;
+  }
+  float P = 0.f;
+  pre = 0.f;
+  sprev = 0.f;
+  for (int j = 0; j < M; ++j) {              // pass 2: position adjoints of the samples
+    const float t = ((float)j + 0.5f) / (float)M;
+    const float3 p = o + dx * t;
+    const float4 f = env_field(s, p);
+    const float sj = dot(aV, f3(f)), sg = fmaxf(f.w, 0.f);
+    const float Tj = expf(-delta * pre), Tj1 = expf(-delta * (pre + sg));
+    if (j > 0) P += (sj - sprev) * Tj;
+    const float gsg = -delta * (Q - P);
+    const float3 gp = env_field_bwd(s, p, aV * (Tj - Tj1), f.w > 0.f ? gsg : 0.f);
+    go += gp * (1.f - t);
+    gx += gp * t;
+    pre += sg;
+    sprev = sj;
+  }
+  if (l > 0.f) {
+    const float3 u = dx * (1.0f / l);
+    const float gl = gdelta / (float)M;
+    gx += u * gl;
+    go -= u * gl;
+  }
+}
+
+// Radiance of an escaping ray: the shell lookup (R14), preceded by the volume rendering of
+// the segment out to the shell for the volumetric env (R30).  With go/gd: also the reverse.
+DT_D float3 env_eval(const DevScene& s, float3 o, float3 d, float3 a, float3* go, float3* gd);
+template <bool VOL>
+DT_D float3 env_escape(const DevScene& s, float3 o, float3 d, float3 a, float3* go, float3* gd) {
+  if (!VOL) return env_eval(s, o, d, a, go, gd);
+  const float dn = length(d);
+  const float3 dh = d * (1.0f / dn);
+  float ts, sq;
+  const float3 ps = shell_point(s, o, dh, ts, sq);
+  float3 V;
+  float Tn;
+  env_volume(s, o, ps, V, Tn);
+  const float3 E = env_eval(s, o, d, a * Tn, go, gd);
+  if (go) {
+    float3 gov = f3(0, 0, 0), gps = f3(0, 0, 0), gdh = f3(0, 0, 0);
+    env_volume_bwd(s, o, ps, a, dot(a, E), gov, gps);
+    shell_point_bwd(s, o, dh, ts, sq, gps, gov, gdh);
+    *go += gov;
+    *gd += (gdh - dh * dot(dh, gdh)) * (1.0f / dn);
+  }
+  return V + E * Tn;
 }
 
 // Env(o, d) (P:160 step 3).  If go/gd are non-null, also the reverse for adjoint a.

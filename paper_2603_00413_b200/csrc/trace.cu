@@ -53,6 +53,15 @@ constexpr int kBwdThreads = 128;
 #define DT_BWD_LB __launch_bounds__(kBwdThreads)
 #endif
 
+// register caps of the sigma-grid kernels (k_*_grid: their cooperative walks inflate the
+// allocation; measured: tools/sweep_regs.sh)
+#ifndef DT_SHADE_GRID_REGS
+#define DT_SHADE_GRID_REGS 96
+#endif
+#ifndef DT_BWD_GRID_REGS
+#define DT_BWD_GRID_REGS 128
+#endif
+
 DT_D int fetch_work(int* counter) {
   int base = 0;
   if (lane_id() == 0) base = atomicAdd(counter, 32);
@@ -85,18 +94,19 @@ DT_D void flush_counters(unsigned long long* c, int visits, int tests) {
 
 // Shade one traced segment (record idx at level k) and spawn its children into level k+1.
 // All 32 lanes of the warp must call this (the compaction is a warp collective).
-template <int ABS>
+template <int ABS, bool VOL>
 DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int64_t lim, int k, int max_depth,
                           bool valid, int64_t idx, float3 o, float3 d,
                           int64_t ray, uint32_t pos, float3 thr, float w, int face, float t, float u, float v) {
   const DevScene& s = a.s;
   bool is_hit = valid && face >= 0;
-  bool spawn_r = false, spawn_t = false, need_tau = false, capped = false;
-  float3 x = f3(0, 0, 0), wr = x, wt = x, tau = f3(1, 1, 1), capL = x;
+  bool spawn_r = false, spawn_t = false, need_tau = false, capped = false, volx = false;
+  float3 x = f3(0, 0, 0), wr = x, wt = x, tau = f3(1, 1, 1), capL = x, Vx = x;
+  float Tx = 1.f;
   float R = 0.f, T = 0.f;
   if (valid) {
     if (!is_hit) {
-      float3 L = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);          // P:160 step 3
+      float3 L = env_escape<VOL>(s, o, d, f3(0, 0, 0), nullptr, nullptr);   // P:160 step 3 (R30)
       __stcs(a.r.hit + idx, make_float4(__int_as_float(-1), 0.f, 0.f, __int_as_float(RF_MISS)));
       __stcs(a.r.lsub + idx, f4(L, __int_as_float(-1)));
       __stcs(a.r.tau + idx, make_float4(1.f, 1.f, 1.f, __int_as_float(-1)));
@@ -109,6 +119,8 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
       bool inside = dot(d, cross(e1, e2)) > 0.0f;                             // R8
       x = o + d * t;
       need_tau = inside;
+      volx = VOL && !inside;                                                  // exterior, volumetric env
+      if (volx) env_volume(s, o, x, Vx, Tx);                                  // R30
       if (k == max_depth) {                                                   // capped (R12, R13)
         capped = true;
         if (s.cap_policy == 1) capL = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);   // times tau below
@@ -149,8 +161,9 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
       if (myq >= 0) tau = f3(expf(-mine.x), expf(-mine.y), expf(-mine.z));
     }
   }
+  if (volx) tau = f3(Tx, Tx, Tx);            // exterior: the continuation is seen through the env volume
   if (capped) {
-    __stcs(a.r.lsub + idx, f4(capL * tau, __int_as_float(-1)));
+    __stcs(a.r.lsub + idx, f4(volx ? Vx + capL * tau : capL * tau, __int_as_float(-1)));
     __stcs(a.r.tau + idx, f4(tau, __int_as_float(-1)));
   }
   // warp-ballot compaction of the children: the warp's reflect children first, then its
@@ -186,13 +199,14 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
       }
     }
     __stcs(a.r.tau + idx, f4(tau, __int_as_float((int)ct)));
-    __stcs(a.r.lsub + idx, make_float4(0.f, 0.f, 0.f, __int_as_float((int)cr)));
+    __stcs(a.r.lsub + idx, f4(Vx, __int_as_float((int)cr)));            // V: the segment's own env emission
   }
 }
 
 // Level 0: camera rays.  Each warp takes 32 pixels of an 8x4 tile (or 32 consecutive
 // entries of the caller's pixel list), culls against the root box, traverses, and records
 // only the hitting rays (misses write their env radiance straight to rgb).
+template <bool VOL>
 __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
   __shared__ int sstack[kStackShared * kTraceThreads];
   const DevScene& s = a.s;
@@ -232,7 +246,7 @@ __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
         face = traverse(s, o, d, 0.0f, t, u, v, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
       }
       if (face < 0) {
-        float3 L = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);
+        float3 L = env_escape<VOL>(s, o, d, f3(0, 0, 0), nullptr, nullptr);
         a.rgb[3 * ray] = L.x; a.rgb[3 * ray + 1] = L.y; a.rgb[3 * ray + 2] = L.z;
         sig_add(a.sig_t, ray, topo_key(1u, EV_MISS));
         sig_add(a.sig_f, ray, face_key(1u, EV_MISS, -1));
@@ -264,8 +278,12 @@ __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
 // Shading of level k (K10): reads each record's ray and traversal result, evaluates the
 // event and spawns the children into level k+1 (warp-ballot compaction).  Level 0 needs
 // the final level-0 count, so it always runs after the traversal pass.
-template <int ABS>
-__global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
+// Work distribution: constant-sigma / non-volume levels cost about the same per record, so
+// warps stride statically; with a sigma grid or hash texture (cooperative interior walks) or
+// a volumetric env the cost varies a lot, so warps take 32-record chunks from the level's
+// counter, the next chunk's atomic in flight while the current one is shaded.
+template <int ABS, bool VOL>
+DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
   if (a.lvl[LV_OVERFLOW]) return;   // arena too small: the host grows it and re-runs
   const float ior = a.s.ior_ptr ? __ldg(a.s.ior_ptr) : a.s.ior;
   // level offsets are fixed while this kernel runs (only level k+1's count grows): read once
@@ -274,7 +292,12 @@ __global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
   const int64_t child_off = level_base(a.lvl, k + 1);
   const int64_t lim = a.cap - a.lvl[LV_CNT + 0];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t wbase = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); wbase < n; wbase += stride) {
+  constexpr bool kDyn = ABS != 0 || VOL;
+  int* const ctr = a.lvl + LV_WORK_SHADE + k;
+  int64_t wbase = kDyn ? (int64_t)fetch_work(ctr) : blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31);
+  while (wbase < n) {
+    int next = 0;
+    if (kDyn && lane_id() == 0) next = atomicAdd(ctr, 32);
     const int64_t item = wbase + lane_id();
     const bool valid = item < n;
     const int64_t idx = k == 0 ? a.cap - 1 - item : off + item;
@@ -291,8 +314,19 @@ __global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
       pos = __float_as_uint(rd.w);
       face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
     }
-    shade_and_spawn<ABS>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
+    shade_and_spawn<ABS, VOL>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
+    wbase = kDyn ? (int64_t)__shfl_sync(~0u, next, 0) : wbase + stride;
   }
+}
+
+template <int ABS, bool VOL>
+__global__ void DT_SHADE_LB k_shade_level(FwdLaunch a, int k, int max_depth) {
+  shade_level_body<ABS, VOL>(a, k, max_depth);
+}
+template <bool VOL>
+__global__ void __maxnreg__(DT_SHADE_GRID_REGS)
+    k_shade_level_grid(FwdLaunch a, int k, int max_depth) {
+  shade_level_body<1, VOL>(a, k, max_depth);
 }
 
 // Traversal of level k >= 1 (K9): closest hit only, hit = (face, t, u, v) written back into
@@ -480,7 +514,7 @@ __global__ void k_gather(FwdLaunch a, int k) {
       float R = h.z;
       float3 Lr = cr >= 0 ? f3(a.r.lsub[cr]) : f3(0, 0, 0);
       float3 Lt = ct >= 0 ? f3(a.r.lsub[ct]) : f3(0, 0, 0);
-      L = f3(tu) * (Lr * R + Lt * (1.0f - R));
+      L = f3(ls) + f3(tu) * (Lr * R + Lt * (1.0f - R));   // own emission (R30; 0 otherwise) + tau * children
       a.r.lsub[idx] = f4(L, ls.w);
     }
     if (k == 0) {
@@ -501,8 +535,8 @@ DT_D void atomic_add3(float4* p, float3 v) {
 // gS; (B) the transmittance adjoints of the warp's interior segments, one segment at a time
 // by the whole warp (or per lane for constant sigma); (C) per lane: x = o + t d and the
 // Moller-Trumbore reverse, vertex and normal atomics, parent-slot adjoints.
-template <int ABS>
-__global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, int64_t cap) {
+template <int ABS, bool VOL>
+DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t cap) {
   const DevScene& s = a.s;
   if (a.lvl[LV_OVERFLOW]) return;   // an overflowed (asynchronous) forward: nothing valid to replay
   const float ior = s.ior_ptr ? __ldg(s.ior_ptr) : s.ior;
@@ -531,9 +565,10 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
       fl = __float_as_int(h.w);
       const float* g = a.grad_rgb + 3 * ray;
       float3 adj = f3(__ldg(g), __ldg(g + 1), __ldg(g + 2)) * f3(rt);          // a_n = grad * throughput
+      const bool volx = VOL && !(fl & (RF_MISS | RF_INSIDE));                 // exterior segment, R30
       if (fl & RF_MISS) {
-        env_eval(s, o, d, adj, &go, &gd);
-      } else if ((fl & RF_CAPPED) && s.cap_policy == 0) {
+        env_escape<VOL>(s, o, d, adj, &go, &gd);
+      } else if ((fl & RF_CAPPED) && s.cap_policy == 0 && !volx) {
         // capped branches return 0: no dependence
       } else {
         geo = true;
@@ -546,8 +581,14 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
         float4 tu = a.r.tau[idx];
         float3 tau = f3(tu);
         if (fl & RF_CAPPED) {                                                 // CAP_ENV leaf
-          float3 E = env_eval(s, o, d, adj * tau, &go, &gd);
-          if (inside) { walk = true; gS = -(adj * E * tau); }
+          if (volx) {                                                         // V + Tn * (E or 0)
+            float aT = 0.f;
+            if (s.cap_policy == 1) aT = dot(adj, env_eval(s, o, d, adj * tau, &go, &gd));
+            env_volume_bwd(s, o, x, adj, aT, go, gx);
+          } else {
+            float3 E = env_eval(s, o, d, adj * tau, &go, &gd);
+            if (inside) { walk = true; gS = -(adj * E * tau); }
+          }
           gNk[0] = gNk[1] = gNk[2] = f3(0, 0, 0);
         } else {
           Shade S;
@@ -561,6 +602,7 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
           float3 Lc = Lr * S.R + Lt * S.T;
           float gR = S.tir ? 0.0f : dot(ap, Lr - Lt);
           if (inside) { walk = true; gS = -(adj * Lc * tau); }
+          if (volx) env_volume_bwd(s, o, x, adj, dot(adj, Lc), go, gx);      // V + Tn * Lc (R30)
           float3 gd_s;
           float gi;
           float3 n0 = f3(__ldg(s.nrm + i0)), n1 = f3(__ldg(s.nrm + i1)), n2 = f3(__ldg(s.nrm + i2));
@@ -620,6 +662,16 @@ __global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, in
       atomicAdd(a.dsig, make_float4(gsc.x, gsc.y, gsc.z, 0.f));
     }
   }
+}
+
+template <int ABS, bool VOL>
+__global__ void DT_BWD_LB k_backward_level(BwdLaunch a, int k, int max_depth, int64_t cap) {
+  backward_level_body<ABS, VOL>(a, k, max_depth, cap);
+}
+template <bool VOL>
+__global__ void __maxnreg__(DT_BWD_GRID_REGS)
+    k_backward_level_grid(BwdLaunch a, int k, int max_depth, int64_t cap) {
+  backward_level_body<1, VOL>(a, k, max_depth, cap);
 }
 
 // Vertex-normal chain (reverse of P:170-173): dN -> d(sum of unit face normals) per vertex,
@@ -765,25 +817,35 @@ int persistent_blocks(const void* fn, int threads, int sm_count) {
 
 }  // namespace
 
+template <class K>
+void launch_persistent(K kernel, int& grid, int threads, int sm_count, cudaStream_t st, const FwdLaunch& a, int x) {
+  if (!grid) grid = persistent_blocks((const void*)kernel, threads, sm_count);
+  kernel<<<grid, threads, 0, st>>>(a, x);
+}
+
 cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count, cudaStream_t st) {
-  static int gp = 0;
-  if (!gp) gp = persistent_blocks((const void*)k_trace_primary, kTraceThreads, sm_count);
-  k_trace_primary<<<gp, kTraceThreads, 0, st>>>(a, max_depth);
+  static int g[2] = {0, 0};
+  if (a.s.env_kind == 2) launch_persistent(k_trace_primary<true>, g[1], kTraceThreads, sm_count, st, a, max_depth);
+  else launch_persistent(k_trace_primary<false>, g[0], kTraceThreads, sm_count, st, a, max_depth);
   return cudaGetLastError();
 }
 
+// k_shade_level<ABS, VOL>: absorption kind and volumetric env are compile-time so each
+// variant carries only its own registers
+template <int ABS>
+void shade_dispatch(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
+  static int g[2] = {0, 0};
+  const bool vol = a.s.env_kind == 2;
+  auto kern = ABS == 1 ? (vol ? k_shade_level_grid<true> : k_shade_level_grid<false>)
+                       : (vol ? k_shade_level<ABS, true> : k_shade_level<ABS, false>);
+  if (!g[vol]) g[vol] = persistent_blocks((const void*)kern, kTraceThreads, sm_count);
+  kern<<<g[vol], kTraceThreads, 0, st>>>(a, level, max_depth);
+}
+
 cudaError_t launch_shade_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
-  static int gs0 = 0, gs1 = 0, gs2 = 0;
-  if (a.s.abs_kind == 0) {
-    if (!gs0) gs0 = persistent_blocks((const void*)k_shade_level<0>, kTraceThreads, sm_count);
-    k_shade_level<0><<<gs0, kTraceThreads, 0, st>>>(a, level, max_depth);
-  } else if (a.s.abs_kind == 1) {
-    if (!gs1) gs1 = persistent_blocks((const void*)k_shade_level<1>, kTraceThreads, sm_count);
-    k_shade_level<1><<<gs1, kTraceThreads, 0, st>>>(a, level, max_depth);
-  } else {
-    if (!gs2) gs2 = persistent_blocks((const void*)k_shade_level<2>, kTraceThreads, sm_count);
-    k_shade_level<2><<<gs2, kTraceThreads, 0, st>>>(a, level, max_depth);
-  }
+  if (a.s.abs_kind == 0) shade_dispatch<0>(a, level, max_depth, sm_count, st);
+  else if (a.s.abs_kind == 1) shade_dispatch<1>(a, level, max_depth, sm_count, st);
+  else shade_dispatch<2>(a, level, max_depth, sm_count, st);
   return cudaGetLastError();
 }
 
@@ -804,18 +866,20 @@ cudaError_t launch_gather_level(const FwdLaunch& a, int level, int sm_count, cud
   return cudaGetLastError();
 }
 
+template <int ABS>
+void backward_dispatch(const BwdLaunch& a, int level, int sm_count, cudaStream_t st) {
+  static int g[2] = {0, 0};
+  const bool vol = a.s.env_kind == 2;
+  auto kern = ABS == 1 ? (vol ? k_backward_level_grid<true> : k_backward_level_grid<false>)
+                       : (vol ? k_backward_level<ABS, true> : k_backward_level<ABS, false>);
+  if (!g[vol]) g[vol] = persistent_blocks((const void*)kern, kBwdThreads, sm_count);
+  kern<<<g[vol], kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
+}
+
 cudaError_t launch_backward_level(const BwdLaunch& a, int level, int sm_count, cudaStream_t st) {
-  static int gb0 = 0, gb1 = 0, gb2 = 0;
-  if (a.s.abs_kind == 0) {
-    if (!gb0) gb0 = persistent_blocks((const void*)k_backward_level<0>, kBwdThreads, sm_count);
-    k_backward_level<0><<<gb0, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
-  } else if (a.s.abs_kind == 1) {
-    if (!gb1) gb1 = persistent_blocks((const void*)k_backward_level<1>, kBwdThreads, sm_count);
-    k_backward_level<1><<<gb1, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
-  } else {
-    if (!gb2) gb2 = persistent_blocks((const void*)k_backward_level<2>, kBwdThreads, sm_count);
-    k_backward_level<2><<<gb2, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
-  }
+  if (a.s.abs_kind == 0) backward_dispatch<0>(a, level, sm_count, st);
+  else if (a.s.abs_kind == 1) backward_dispatch<1>(a, level, sm_count, st);
+  else backward_dispatch<2>(a, level, sm_count, st);
   return cudaGetLastError();
 }
 

@@ -538,6 +538,17 @@ def config_c3r(seed: int = 3, n_views: int = 100, res: int = 800, vres: int = 12
     return Scene("C3R", V, F, 1.5, const_absorption(), grid_env(env_seed, vres, pres), cams, 8)
 
 
+def config_c3v(seed: int = 3, n_views: int = 100, res: int = 800, vres: int = 128, pres: int = 1024,
+               env_samples: int = 32) -> Scene:
+    """NEXT-3 volumetric-env workload: C3's mesh and cameras with the MERF-style env volume
+    rendered along every exterior segment (R30)."""
+    V, F = cube_sphere(204, seed)
+    r = float(np.linalg.norm(V, axis=1).max())
+    cams = hemisphere_cameras(n_views, res, res, 3.0 * r, r, seed)
+    env = volume_env(seed, vres, pres, n_samples=env_samples)
+    return Scene("C3V", V, F, 1.5, const_absorption(), env, cams, 4)
+
+
 def config_c4(seed: int = 4, n_views: int = 50, res: int = 800, vres: int = 128, pres: int = 1024,
               sigma_res: int = 64) -> Scene:
     V, F = knot_and_gems(seed)
@@ -563,7 +574,8 @@ def config_c5(seed: int = 5, n_views: int = 200, res: int = 1024, vres: int = 12
     return Scene("C5", V, F, 1.5, const_absorption(), grid_env(seed, vres, pres), cams, 4)
 
 
-CONFIGS = {"C1": config_c1, "C2": config_c2, "C3": config_c3, "C3R": config_c3r, "C4": config_c4, "C4H": config_c4h,
+CONFIGS = {"C1": config_c1, "C2": config_c2, "C3": config_c3, "C3R": config_c3r, "C3V": config_c3v, "C4": config_c4,
+           "C4H": config_c4h,
            "C5": config_c5}
 
 

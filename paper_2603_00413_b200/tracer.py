@@ -70,6 +70,7 @@ class DeviceScene:
         self.env.pres = 0 if self.planes is None else self.planes.shape[1]
         self.env.radius = float(env.radius)
         self.env.far_field = int(env.far_field)
+        self.env.n_samples = int(getattr(env, "n_samples", 0))
         cams = sc.cams
         self.K = _dev(cams.K, torch.float32, device)
         self.c2w = _dev(cams.c2w, torch.float32, device)

@@ -212,6 +212,36 @@ def test_hash_texture(tracer):
     parity_case(tracer, sc, np.arange(sc.n_pixels), "ico2-hash-capenv")
 
 
+def test_volume_env(tracer):
+    """NEXT-3: volumetric env (R30) -- exterior segments volume rendered, escaping rays to the
+    shell; both cap policies, with a sigma grid inside."""
+    V, F = S.icosphere(2)
+    cams = T.one_view(40, 28, (0.6, -0.4, 2.6), fov_deg=55)
+    sc = T.scene(V, F, cams, env=T.small_volume_env(), D=4)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "ico2-volenv")
+    sc = T.scene(V, F, cams, env=T.small_volume_env(seed=9, density=0.3), absorption=T.small_sigma_grid(V, 6), D=3,
+                 cap=S.CAP_ENV)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "ico2-volenv-capenv-grid")
+
+
+def test_c3v_volume_env_full_size_sampled(tracer):
+    """NEXT-3 workload at full size (bench launch), 128 sampled object pixels."""
+    sc = S.config_c3v()
+    pid = S.central_pixels(sc.cams, 128, 6)
+    osc = O.OracleScene(sc)
+    orc = oracle_forward(O, osc, pid)
+    gpu = run_gpu(tracer, sc, None)
+    cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
+    assert_forward(cmp, "C3V")
+    gfull = np.zeros((sc.n_pixels, 3), np.float32)
+    g = S.upstream_grad(len(pid), 17)
+    g[cmp["div_mask"] | cmp["flag_mask"]] = 0
+    gfull[pid] = g
+    gpu = run_gpu(tracer, sc, None, full_launch_grad=gfull)
+    gV, gi, gs = O.backward(osc, g, pid)
+    assert rel_l2(gpu["gV"], gV) <= GRAD_TOL
+
+
 def test_hash_dense_level_equals_grid(tracer):
     """One dense hash level is the vertex grid (R29 special case): same radiance/gradients."""
     import dataclasses
