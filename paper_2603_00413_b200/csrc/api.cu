@@ -42,7 +42,8 @@ cudaError_t alloc_arena(dt_ctx* c, int64_t cap) {
   c->rec = Records{};
   c->arena_cap = 0;
   float4* base = nullptr;
-  cudaError_t e = cudaMalloc(&base, (size_t)cap * kRecordBytes);
+  const int lanes = kRecordBytes / 16 + (c->arena_vol ? 2 : 0);
+  cudaError_t e = cudaMalloc(&base, (size_t)cap * lanes * 16);
   if (e != cudaSuccess) return e;
   c->rec.o = base;
   c->rec.d = base + cap;
@@ -52,6 +53,10 @@ cudaError_t alloc_arena(dt_ctx* c, int64_t cap) {
   c->rec.lsub = base + 5 * cap;
   c->rec.go = base + 6 * cap;
   c->rec.gd = base + 7 * cap;
+  if (c->arena_vol) {
+    c->rec.mq = base + 8 * cap;
+    c->rec.mg = base + 9 * cap;
+  }
   c->arena_cap = cap;
   return cudaSuccess;
 }
@@ -74,10 +79,10 @@ size_t abs_nodes(const dt_absorption* ab) {
   return (size_t)ab->res * ab->res * ab->res;
 }
 
-int64_t arena_limit() {
+int64_t arena_limit(const dt_ctx* c) {
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  return (int64_t)((double)fr * 0.70 / kRecordBytes);
+  return (int64_t)((double)fr * 0.70 / (kRecordBytes + (c->arena_vol ? 32 : 0)));
 }
 
 cudaEvent_t get_event(dt_ctx* c) {
@@ -152,7 +157,7 @@ dt_status consume_async(dt_ctx* c) {
   c->last_need = need;
   if (c->host_lvl[LV_STACKERR]) return fail(c, DT_ERR_STACK, "async forward: BVH deeper than the traversal stack");
   if (c->host_lvl[LV_OVERFLOW]) {
-    int64_t next = std::min<int64_t>(need + need / 2 + 65536, arena_limit() + c->arena_cap);
+    int64_t next = std::min<int64_t>(need + need / 2 + 65536, arena_limit(c) + c->arena_cap);
     if (next > c->arena_cap && alloc_arena(c, next) != cudaSuccess)
       return fail(c, DT_ERR_OOM, "async forward overflowed and the arena could not grow to %lld", (long long)next);
     c->have_fwd = false;
@@ -363,14 +368,18 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   dt_status prev = consume_async(c);
   if (prev != DT_OK) return prev;
   int64_t limit = 0;   // HBM budget, queried (cudaMemGetInfo) only when the arena must grow
+  if (env->kind == DT_ENV_VOLUME && !c->arena_vol) {   // the volume needs two more record lanes
+    c->arena_vol = true;
+    if (c->arena_cap > 0) DT_CU(alloc_arena(c, c->arena_cap));
+  }
   if (c->arena_cap == 0) {
-    limit = arena_limit();
+    limit = arena_limit(c);
     int64_t want = std::min<int64_t>(std::max<int64_t>(n_rays * 3, 1 << 16), limit);
     DT_CU(alloc_arena(c, want));
   }
   bool async = opts->async && !stats && !opts->check_finite && c->last_need > 0 && c->last_rays == n_rays;
   if (async && c->arena_cap < c->last_need + c->last_need / 4) {   // keep 25% headroom
-    limit = arena_limit() + c->arena_cap;
+    limit = arena_limit(c) + c->arena_cap;
     int64_t next = std::min<int64_t>(c->last_need + c->last_need / 2 + 65536, limit);
     if (next > c->arena_cap) DT_CU(alloc_arena(c, next));
     async = c->arena_cap >= c->last_need + c->last_need / 4;
@@ -425,7 +434,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
     if (!c->host_lvl[LV_OVERFLOW]) break;
     int64_t need = level_need(c->host_lvl, D);
     int64_t next = std::max<int64_t>(c->arena_cap + c->arena_cap / 4, need + need / 8 + 65536);
-    limit = arena_limit() + c->arena_cap;
+    limit = arena_limit(c) + c->arena_cap;
     if (c->arena_cap >= limit || ++retries > 8)
       return fail(c, DT_ERR_OOM, "dt_trace_forward: record arena needs > %lld records (HBM budget %lld)",
                   (long long)next, (long long)limit);

@@ -913,8 +913,8 @@ DT_D void shell_point_bwd(const DevScene& s, float3 o, float3 dh, float ts, floa
 }
 
 // ---- volumetric env (env_kind 2, R30): the voxel/plane textures carry colour (rgb) and
-// density (w).  env_field: rgb and the raw (unclamped) density at p; env_field_bwd: d/dp of
-// a . rgb + aw * density.
+// density (w).  env_field: rgb and the raw (unclamped) density at p; env_field_jac: also
+// its Jacobian d/dp (both clamp-aware: a clamped grid coordinate passes no gradient).
 DT_D float4 env_field(const DevScene& s, float3 p) {
   bool c;
   const float g[3] = {grid_coord(p.x, s.radius, s.vres, c), grid_coord(p.y, s.radius, s.vres, c),
@@ -952,7 +952,9 @@ DT_D float4 env_field(const DevScene& s, float3 p) {
   return out;
 }
 
-DT_D float3 env_field_bwd(const DevScene& s, float3 p, float3 a, float aw) {
+// Value (rgb, raw density) and its Jacobian J[c] = d value_c / dp (c = r, g, b, density),
+// one pass over the 20 texels.
+DT_D float4 env_field_jac(const DevScene& s, float3 p, float3 J[4]) {
   bool c[3];
   const float g[3] = {grid_coord(p.x, s.radius, s.vres, c[0]), grid_coord(p.y, s.radius, s.vres, c[1]),
                       grid_coord(p.z, s.radius, s.vres, c[2])};
@@ -961,17 +963,22 @@ DT_D float3 env_field_bwd(const DevScene& s, float3 p, float3 a, float aw) {
   float f[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) { i0[k] = min((int)floorf(g[k]), R - 2); f[k] = g[k] - (float)i0[k]; }
-  float3 gg = f3(0, 0, 0);
+  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+  float3 gv[4] = {f3(0, 0, 0), f3(0, 0, 0), f3(0, 0, 0), f3(0, 0, 0)};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
     const float wx = dx ? f[0] : 1 - f[0], wy = dy ? f[1] : 1 - f[1], wz = dz ? f[2] : 1 - f[2];
+    const float w = wx * wy * wz;
     const float4 t = __ldg(s.voxel + ((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx));
-    const float sd = a.x * t.x + a.y * t.y + a.z * t.z + aw * t.w;
-    gg += f3((dx ? 1.f : -1.f) * wy * wz, wx * (dy ? 1.f : -1.f) * wz, wx * wy * (dz ? 1.f : -1.f)) * sd;
+    out.x += t.x * w; out.y += t.y * w; out.z += t.z * w; out.w += t.w * w;
+    const float3 dw = f3((dx ? 1.f : -1.f) * wy * wz, wx * (dy ? 1.f : -1.f) * wz, wx * wy * (dz ? 1.f : -1.f));
+    gv[0] += dw * t.x; gv[1] += dw * t.y; gv[2] += dw * t.z; gv[3] += dw * t.w;
   }
   const float sv = (float)(R - 1) / (2.0f * s.radius);
-  float3 gp = f3(c[0] ? 0.f : gg.x * sv, c[1] ? 0.f : gg.y * sv, c[2] ? 0.f : gg.z * sv);
+  const float3 msk = f3(c[0] ? 0.f : sv, c[1] ? 0.f : sv, c[2] ? 0.f : sv);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) J[q] = gv[q] * msk;
   const float pa[3] = {p.x, p.x, p.y}, pb[3] = {p.y, p.z, p.z};
   const int Rp = s.pres;
   const float spl = (float)(Rp - 1) / (2.0f * s.radius);
@@ -984,71 +991,94 @@ DT_D float3 env_field_bwd(const DevScene& s, float3 p, float3 a, float aw) {
     const float4* P = s.planes + (size_t)k * Rp * Rp;
     const float4 t00 = __ldg(P + (size_t)ib * Rp + ia), t01 = __ldg(P + (size_t)ib * Rp + ia + 1);
     const float4 t10 = __ldg(P + (size_t)(ib + 1) * Rp + ia), t11 = __ldg(P + (size_t)(ib + 1) * Rp + ia + 1);
-    const float s00 = dot(a, f3(t00)) + aw * t00.w, s01 = dot(a, f3(t01)) + aw * t01.w;
-    const float s10 = dot(a, f3(t10)) + aw * t10.w, s11 = dot(a, f3(t11)) + aw * t11.w;
-    const float da = ca ? 0.f : ((s01 - s00) * (1 - fb) + (s11 - s10) * fb) * spl;
-    const float db = cb ? 0.f : ((s10 - s00) * (1 - fa) + (s11 - s01) * fa) * spl;
-    if (k == 0) { gp.x += da; gp.y += db; }
-    else if (k == 1) { gp.x += da; gp.z += db; }
-    else { gp.y += da; gp.z += db; }
+    const float w00 = (1 - fa) * (1 - fb), w01 = fa * (1 - fb), w10 = (1 - fa) * fb, w11 = fa * fb;
+    out.x += t00.x * w00 + t01.x * w01 + t10.x * w10 + t11.x * w11;
+    out.y += t00.y * w00 + t01.y * w01 + t10.y * w10 + t11.y * w11;
+    out.z += t00.z * w00 + t01.z * w01 + t10.z * w10 + t11.z * w11;
+    out.w += t00.w * w00 + t01.w * w01 + t10.w * w10 + t11.w * w11;
+    // d/da and d/db of the bilinear value, per channel
+    const float ka = ca ? 0.f : spl, kb = cb ? 0.f : spl;
+    const float4 da = make_float4(((t01.x - t00.x) * (1 - fb) + (t11.x - t10.x) * fb) * ka,
+                                  ((t01.y - t00.y) * (1 - fb) + (t11.y - t10.y) * fb) * ka,
+                                  ((t01.z - t00.z) * (1 - fb) + (t11.z - t10.z) * fb) * ka,
+                                  ((t01.w - t00.w) * (1 - fb) + (t11.w - t10.w) * fb) * ka);
+    const float4 db = make_float4(((t10.x - t00.x) * (1 - fa) + (t11.x - t01.x) * fa) * kb,
+                                  ((t10.y - t00.y) * (1 - fa) + (t11.y - t01.y) * fa) * kb,
+                                  ((t10.z - t00.z) * (1 - fa) + (t11.z - t01.z) * fa) * kb,
+                                  ((t10.w - t00.w) * (1 - fa) + (t11.w - t01.w) * fa) * kb);
+    const float dav[4] = {da.x, da.y, da.z, da.w}, dbv[4] = {db.x, db.y, db.z, db.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (k == 0) { J[q].x += dav[q]; J[q].y += dbv[q]; }
+      else if (k == 1) { J[q].x += dav[q]; J[q].z += dbv[q]; }
+      else { J[q].y += dav[q]; J[q].z += dbv[q]; }
+    }
   }
-  return gp;
+  return out;
 }
 
 // Emission-absorption quadrature along an exterior segment o -> x (R30, M midpoint samples):
 // V = sum_i T_i (1 - exp(-sigma_i Delta)) c_i, T_i = exp(-Delta sum_{j<i} sigma_j), Tn = T_M.
-DT_D void env_volume(const DevScene& s, float3 o, float3 x, float3& V, float& Tn) {
+// mom (optional): the adjoint-independent sums the reverse needs, so it makes one pass:
+//   Qc = sum_{0<i<M} (c_i - c_{i-1}) T_i - c_{M-1} T_M,
+//   Go = -sum_{0<i<M} (c_i - c_{i-1}) T_i od_i + c_{M-1} T_M od_M,  od_i = Delta sum_{j<i} sigma_j.
+struct VolMom {
+  float3 Qc, Go;
+  float odM;
+};
+
+DT_D void env_volume(const DevScene& s, float3 o, float3 x, float3& V, float& Tn, VolMom* mom = nullptr) {
   const int M = s.env_nsamp;
   const float3 dx = x - o;
   const float delta = length(dx) / (float)M;
   float od = 0.f;
+  float3 cprev = f3(0, 0, 0), Qc = f3(0, 0, 0), Go = f3(0, 0, 0);
   V = f3(0, 0, 0);
+#pragma unroll 2
   for (int i = 0; i < M; ++i) {
     const float4 f = env_field(s, o + dx * (((float)i + 0.5f) / (float)M));
-    const float sg = fmaxf(f.w, 0.f);
-    V += f3(f) * (expf(-od) * (1.f - expf(-sg * delta)));
+    const float3 c = f3(f);
+    const float sg = fmaxf(f.w, 0.f), Ti = expf(-od);
+    V += c * (Ti * (1.f - expf(-sg * delta)));
+    if (i > 0) {
+      Qc += (c - cprev) * Ti;
+      Go -= (c - cprev) * (Ti * od);
+    }
     od += sg * delta;
+    cprev = c;
   }
   Tn = expf(-od);
+  if (mom) {
+    mom->Qc = Qc - cprev * Tn;
+    mom->Go = Go + cprev * (Tn * od);
+    mom->odM = od;
+  }
 }
 
 // Reverse of env_volume given aV = dL/dV and aT = dL/dTn: adds the end-point adjoints to go,
-// gx.  Two passes over the samples (no per-sample storage): with s_i = aV . c_i and
-// dL/dT_i = s_i - s_{i-1} (0 < i < M), dL/dT_M = aT - s_{M-1}, the density adjoint is
-// dL/dsigma_j = -Delta (Q - sum_{i<=j} dL/dT_i T_i) with Q = sum_{i=1..M} dL/dT_i T_i.
-DT_D void env_volume_bwd(const DevScene& s, float3 o, float3 x, float3 aV, float aT, float3& go, float3& gx) {
+// gx.  With s_i = aV . c_i, dL/dT_i = s_i - s_{i-1} (0 < i < M), dL/dT_M = aT - s_{M-1}:
+// dL/dsigma_j = -Delta (Q - sum_{0<i<=j} dL/dT_i T_i), Q = sum_{i=1..M} dL/dT_i T_i
+// = aV . Qc + aT Tn, and Delta dL/dDelta = aV . Go - aT Tn od_M (the forward's moments), so
+// one pass over the samples remains.
+DT_D void env_volume_bwd(const DevScene& s, float3 o, float3 x, float3 aV, float aT, float Tn, const VolMom& mom,
+                         float3& go, float3& gx) {
   const int M = s.env_nsamp;
   const float3 dx = x - o;
   const float l = length(dx), delta = l / (float)M;
-  float Q = 0.f, gdelta = 0.f, pre = 0.f, sprev = 0.f;
-  for (int i = 0; i < M; ++i) {              // pass 1: Q and dL/dDelta
-    const float4 f = env_field(s, o + dx * (((float)i + 0.5f) / (float)M));
-    const float si = dot(aV, f3(f));
-    if (i > 0) {
-      const float term = (si - sprev) * expf(-delta * pre);
-      Q += term;
-      gdelta -= term * pre;
-    }
-    pre += fmaxf(f.w, 0.f);
-    sprev = si;
-  }
-  {
-    const float term = (aT - sprev) * expf(-delta * pre);
-    Q += term;
-    gdelta -= term * pre;
-  }
-  float P = 0.f;
-  pre = 0.f;
-  sprev = 0.f;
-  for (int j = 0; j < M; ++j) {              // pass 2: position adjoints of the samples
+  const float Q = dot(aV, mom.Qc) + aT * Tn;
+  float P = 0.f, pre = 0.f, sprev = 0.f;
+#pragma unroll 2
+  for (int j = 0; j < M; ++j) {
     const float t = ((float)j + 0.5f) / (float)M;
     const float3 p = o + dx * t;
-    const float4 f = env_field(s, p);
+    float3 J[4];
+    const float4 f = env_field_jac(s, p, J);
     const float sj = dot(aV, f3(f)), sg = fmaxf(f.w, 0.f);
     const float Tj = expf(-delta * pre), Tj1 = expf(-delta * (pre + sg));
     if (j > 0) P += (sj - sprev) * Tj;
-    const float gsg = -delta * (Q - P);
-    const float3 gp = env_field_bwd(s, p, aV * (Tj - Tj1), f.w > 0.f ? gsg : 0.f);
+    const float gsg = f.w > 0.f ? -delta * (Q - P) : 0.f;
+    const float3 ac = aV * (Tj - Tj1);
+    const float3 gp = J[0] * ac.x + J[1] * ac.y + J[2] * ac.z + J[3] * gsg;
     go += gp * (1.f - t);
     gx += gp * t;
     pre += sg;
@@ -1056,34 +1086,39 @@ DT_D void env_volume_bwd(const DevScene& s, float3 o, float3 x, float3 aV, float
   }
   if (l > 0.f) {
     const float3 u = dx * (1.0f / l);
-    const float gl = gdelta / (float)M;
+    const float gl = (dot(aV, mom.Go) - aT * Tn * mom.odM) / l;   // dL/dDelta / M
     gx += u * gl;
     go -= u * gl;
   }
 }
 
 // Radiance of an escaping ray: the shell lookup (R14), preceded by the volume rendering of
-// the segment out to the shell for the volumetric env (R30).  With go/gd: also the reverse.
+// the segment out to the shell for the volumetric env (R30).  Forward: Tn and mom (if given)
+// returned for the record.  Reverse (go/gd non-null): uses the recorded Tn, mom.
 DT_D float3 env_eval(const DevScene& s, float3 o, float3 d, float3 a, float3* go, float3* gd);
 template <bool VOL>
-DT_D float3 env_escape(const DevScene& s, float3 o, float3 d, float3 a, float3* go, float3* gd) {
+DT_D float3 env_escape(const DevScene& s, float3 o, float3 d, float3 a, float3* go, float3* gd, float* Tn_io = nullptr,
+                       VolMom* mom_io = nullptr) {
   if (!VOL) return env_eval(s, o, d, a, go, gd);
   const float dn = length(d);
   const float3 dh = d * (1.0f / dn);
   float ts, sq;
   const float3 ps = shell_point(s, o, dh, ts, sq);
-  float3 V;
-  float Tn;
-  env_volume(s, o, ps, V, Tn);
-  const float3 E = env_eval(s, o, d, a * Tn, go, gd);
-  if (go) {
-    float3 gov = f3(0, 0, 0), gps = f3(0, 0, 0), gdh = f3(0, 0, 0);
-    env_volume_bwd(s, o, ps, a, dot(a, E), gov, gps);
-    shell_point_bwd(s, o, dh, ts, sq, gps, gov, gdh);
-    *go += gov;
-    *gd += (gdh - dh * dot(dh, gdh)) * (1.0f / dn);
+  if (!go) {                                   // forward
+    float3 V;
+    float Tn;
+    env_volume(s, o, ps, V, Tn, mom_io);
+    if (Tn_io) *Tn_io = Tn;
+    return V + env_eval(s, o, d, a, nullptr, nullptr) * Tn;
   }
-  return V + E * Tn;
+  const float Tn = *Tn_io;                     // reverse, from the record
+  const float3 E = env_eval(s, o, d, a * Tn, go, gd);
+  float3 gov = f3(0, 0, 0), gps = f3(0, 0, 0), gdh = f3(0, 0, 0);
+  env_volume_bwd(s, o, ps, a, dot(a, E), Tn, *mom_io, gov, gps);
+  shell_point_bwd(s, o, dh, ts, sq, gps, gov, gdh);
+  *go += gov;
+  *gd += (gdh - dh * dot(dh, gdh)) * (1.0f / dn);
+  return E;
 }
 
 // Env(o, d) (P:160 step 3).  If go/gd are non-null, also the reverse for adjoint a.

@@ -22,6 +22,8 @@ struct Records {
   float4* lsub;  // radiance returned by the subtree (rgb), reflect child index (int bits)
   float4* go;    // backward: dL/d(origin) of this segment, for the parent
   float4* gd;    // backward: dL/d(direction)
+  float4* mq;    // volumetric env only (else null): the forward's volume moments Qc | od_M
+  float4* mg;    //   and Go (env_volume), read by every backward of that forward
 };
 constexpr int kRecordBytes = 8 * 16;
 
@@ -113,6 +115,7 @@ struct dt_ctx {
   size_t hist_cap = 0;
   // record arena
   int64_t arena_cap = 0;
+  bool arena_vol = false;       // arena carries the two volume-moment lanes (volumetric env)
   dt::Records rec{};
   int* lvl = nullptr;
   int* host_lvl = nullptr;    // pinned

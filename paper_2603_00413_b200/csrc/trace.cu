@@ -106,10 +106,16 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
   float R = 0.f, T = 0.f;
   if (valid) {
     if (!is_hit) {
-      float3 L = env_escape<VOL>(s, o, d, f3(0, 0, 0), nullptr, nullptr);   // P:160 step 3 (R30)
+      float Tm = 1.f;
+      VolMom mom;
+      float3 L = env_escape<VOL>(s, o, d, f3(0, 0, 0), nullptr, nullptr, &Tm, &mom);   // P:160 step 3 (R30)
       __stcs(a.r.hit + idx, make_float4(__int_as_float(-1), 0.f, 0.f, __int_as_float(RF_MISS)));
       __stcs(a.r.lsub + idx, f4(L, __int_as_float(-1)));
-      __stcs(a.r.tau + idx, make_float4(1.f, 1.f, 1.f, __int_as_float(-1)));
+      __stcs(a.r.tau + idx, make_float4(Tm, Tm, Tm, __int_as_float(-1)));
+      if (VOL) {                             // the volume's moments, for the backward
+        __stcs(a.r.mq + idx, f4(mom.Qc, mom.odM));
+        __stcs(a.r.mg + idx, f4(mom.Go, 0.f));
+      }
       sig_add(a.sig_t, ray, topo_key(pos, EV_MISS));
       sig_add(a.sig_f, ray, face_key(pos, EV_MISS, -1));
     } else {
@@ -120,7 +126,12 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
       x = o + d * t;
       need_tau = inside;
       volx = VOL && !inside;                                                  // exterior, volumetric env
-      if (volx) env_volume(s, o, x, Vx, Tx);                                  // R30
+      if (volx) {                                                             // R30
+        VolMom mom;
+        env_volume(s, o, x, Vx, Tx, &mom);
+        __stcs(a.r.mq + idx, f4(mom.Qc, mom.odM));                            // for the backward
+        __stcs(a.r.mg + idx, f4(mom.Go, 0.f));
+      }
       if (k == max_depth) {                                                   // capped (R12, R13)
         capped = true;
         if (s.cap_policy == 1) capL = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);   // times tau below
@@ -566,8 +577,16 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
       const float* g = a.grad_rgb + 3 * ray;
       float3 adj = f3(__ldg(g), __ldg(g + 1), __ldg(g + 2)) * f3(rt);          // a_n = grad * throughput
       const bool volx = VOL && !(fl & (RF_MISS | RF_INSIDE));                 // exterior segment, R30
+      VolMom mom;
+      if (VOL && !(fl & RF_INSIDE)) {                                         // recorded by the forward
+        const float4 q = a.r.mq[idx], g4 = a.r.mg[idx];
+        mom.Qc = f3(q);
+        mom.odM = q.w;
+        mom.Go = f3(g4);
+      }
       if (fl & RF_MISS) {
-        env_escape<VOL>(s, o, d, adj, &go, &gd);
+        float Tm = a.r.tau[idx].x;
+        env_escape<VOL>(s, o, d, adj, &go, &gd, &Tm, &mom);
       } else if ((fl & RF_CAPPED) && s.cap_policy == 0 && !volx) {
         // capped branches return 0: no dependence
       } else {
@@ -584,7 +603,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
           if (volx) {                                                         // V + Tn * (E or 0)
             float aT = 0.f;
             if (s.cap_policy == 1) aT = dot(adj, env_eval(s, o, d, adj * tau, &go, &gd));
-            env_volume_bwd(s, o, x, adj, aT, go, gx);
+            env_volume_bwd(s, o, x, adj, aT, tau.x, mom, go, gx);
           } else {
             float3 E = env_eval(s, o, d, adj * tau, &go, &gd);
             if (inside) { walk = true; gS = -(adj * E * tau); }
@@ -602,7 +621,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
           float3 Lc = Lr * S.R + Lt * S.T;
           float gR = S.tir ? 0.0f : dot(ap, Lr - Lt);
           if (inside) { walk = true; gS = -(adj * Lc * tau); }
-          if (volx) env_volume_bwd(s, o, x, adj, dot(adj, Lc), go, gx);      // V + Tn * Lc (R30)
+          if (volx) env_volume_bwd(s, o, x, adj, dot(adj, Lc), tau.x, mom, go, gx);   // V + Tn * Lc (R30)
           float3 gd_s;
           float gi;
           float3 n0 = f3(__ldg(s.nrm + i0)), n1 = f3(__ldg(s.nrm + i1)), n2 = f3(__ldg(s.nrm + i2));
