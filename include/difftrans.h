@@ -244,6 +244,17 @@ DT_API dt_status dt_sigma_regularizers(dt_ctx* ctx, const dt_absorption* absorpt
                                        const float* xi, int64_t n, float lambda_smooth, float lambda_vol,
                                        float* grad_sigma, float* loss, void* stream);
 
+/* Periodic mesh regularisers of the current dt_build_bvh snapshot:
+ *   L_edge = (1/|E'|) sum_{(i,j) in E'} (1 - n_i . n_j)^2   (n = R6 vertex normals)
+ *   L_lap  = (1/|V|) sum_i |v_i - mean_{j in N(i)} v_j|^2   (Nicolet et al.'s uniform
+ *            Laplacian, read as its energy, R31)
+ * E' = the mesh's undirected edges, N(i) = vertex i's neighbours (from the faces).
+ * grad_V [nv][3] (device) += lambda_edge dL_edge/dV + lambda_lap dL_lap/dV; loss [2] (device)
+ * = (L_edge, L_lap), unweighted.  Deterministic (per-vertex gathers).  DT_ERR_NOT_BUILT
+ * before dt_build_bvh. */
+DT_API dt_status dt_mesh_regularizers(dt_ctx* ctx, float lambda_edge, float lambda_lap, float* grad_V, float* loss,
+                                      void* stream);
+
 /* Adam (beta = (0.9, 0.999), weight decay 1e-6 added to the gradient as in
  * torch.optim.Adam) on n parameters, in place: m, v are [n] state buffers (zero at step 1).
  * uniform != 0: AdamUniform (Nicolet et al., cited at P:186) -- one second-moment statistic

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdifftrans.so")
-SOURCES = ["bvh.cu", "trace.cu", "optim.cu", "api.cu"]
+SOURCES = ["bvh.cu", "trace.cu", "optim.cu", "meshreg.cu", "api.cu"]
 HEADERS = ["dt_math.cuh", "dt_device.cuh", "dt_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -236,7 +236,8 @@ void dt_destroy(dt_ctx* c) {
   void* ptrs[] = {c->V, c->F, c->nrm, c->fnrm, c->nodes, c->tris, c->keys, c->vals, c->hist, c->children,
                   c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, c->vstart, c->vcorner, c->scal,
                   c->iscal, c->rec.o, c->lvl, c->sigma_snap, c->gV, c->gN, c->gVn, c->gS, c->fe, c->gsig, c->gior,
-                  c->counters, c->ranges, c->bdepth, c->wflag, c->widx, c->wbox, c->wdepth, c->scratch};
+                  c->counters, c->ranges, c->bdepth, c->wflag, c->widx, c->wbox, c->wdepth, c->scratch,
+                  c->nbr_start, c->nbr_cnt, c->nbr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
@@ -589,6 +590,20 @@ dt_status dt_adam_step(dt_ctx* c, float* param, const float* grad, float* m, flo
   PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
   int nl = 0;
   DT_CU(launch_adam(param, grad, m, v, n, cfg, c->scratch, (cudaStream_t)stream, &nl));
+  p.end(nl);
+  return DT_OK;
+}
+
+dt_status dt_mesh_regularizers(dt_ctx* c, float lambda_edge, float lambda_lap, float* grad_V, float* loss,
+                               void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_mesh_regularizers: call dt_build_bvh first");
+  DT_ARG(grad_V && loss, "dt_mesh_regularizers: grad_V and loss must be device pointers");
+  DT_ARG(lambda_edge >= 0.f && lambda_lap >= 0.f, "dt_mesh_regularizers: lambdas must be >= 0");
+  PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
+  int nl = 0;
+  DT_CU(launch_mesh_regularizers(c, lambda_edge, lambda_lap, grad_V, loss, (cudaStream_t)stream, &nl));
   p.end(nl);
   return DT_OK;
 }

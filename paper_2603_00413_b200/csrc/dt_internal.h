@@ -131,6 +131,11 @@ struct dt_ctx {
   float4* gN = nullptr;       // [nv]
   float4* gVn = nullptr;      // [nv]  vertex-normal chain, gathered per vertex
   float4* gS = nullptr;       // [nv]  d/d(sum of face normals)
+  int* nbr_start = nullptr;   // [nv+1] vertex neighbour CSR (mesh regularisers)
+  int* nbr_cnt = nullptr;     // [nv+1]
+  int* nbr = nullptr;         // [<= 6 nf]
+  int nbr_cap_v = 0;
+  int64_t nbr_cap = 0;
   float4* fe = nullptr;       // [2nf] per-face d/de1, d/de2
   float4* gsig = nullptr;     // [1] or [R^3]: d/dsigma (rgb + pad)
   float* gior = nullptr;
@@ -178,6 +183,8 @@ cudaError_t launch_traverse_level(const FwdLaunch& a, int level, int sm_count, c
 cudaError_t launch_gather_level(const FwdLaunch& a, int level, int sm_count, cudaStream_t st);
 cudaError_t launch_backward_level(const BwdLaunch& a, int level, int sm_count, cudaStream_t st);
 cudaError_t launch_vertex_normal_backward(dt_ctx* c, cudaStream_t st);
+cudaError_t launch_mesh_regularizers(dt_ctx* c, float lambda_edge, float lambda_lap, float* grad_V, float* loss,
+                                     cudaStream_t st, int* nl);
 cudaError_t launch_finalize(dt_ctx* c, float* grad_V, float* grad_ior, float* grad_sigma, int accumulate,
                             cudaStream_t st);
 cudaError_t launch_loss_color(const float* rgb, const float* tgt, int64_t n, float* grad, float* loss, cudaStream_t st);

@@ -146,6 +146,7 @@ class Tracer:
         assert V.is_cuda and V.dtype == torch.float32 and V.is_contiguous() and V.shape[-1] == 3
         assert F.is_cuda and F.dtype == torch.int32 and F.is_contiguous() and F.shape[-1] == 3
         self._check(self._lib.dt_build_bvh(self.h, _ptr(V), V.shape[0], _ptr(F), F.shape[0], _stream(stream)), self.h)
+        self._nv_built = V.shape[0]
 
     def trace_forward(self, ds: DeviceScene, pixel_ids: Optional[torch.Tensor] = None, ior: Optional[float] = None,
                       max_depth: Optional[int] = None, cap_policy: Optional[int] = None, want_capped=False,
@@ -244,6 +245,18 @@ class Tracer:
                                                     float(lambda_vol), _ptr(grad_sigma), _ptr(loss),
                                                     _stream(stream)), self.h)
         return loss
+
+    def mesh_regularizers(self, lambda_edge: float, lambda_lap: float, grad_V: Optional[torch.Tensor] = None,
+                          loss: Optional[torch.Tensor] = None, stream=None):
+        """L_edge and L_lap of the last built mesh (P:451-457, NEXT-4): returns (loss[2], grad_V);
+        grad_V is accumulated into (a new zero tensor if None)."""
+        if grad_V is None:
+            grad_V = torch.zeros((self._nv_built, 3), dtype=torch.float32, device=self.device)
+        if loss is None:
+            loss = torch.empty(2, dtype=torch.float32, device=self.device)
+        self._check(self._lib.dt_mesh_regularizers(self.h, float(lambda_edge), float(lambda_lap), _ptr(grad_V),
+                                                   _ptr(loss), _stream(stream)), self.h)
+        return loss, grad_V
 
     def adam_step(self, param: torch.Tensor, grad: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: int,
                   lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0, uniform=False,

@@ -147,3 +147,30 @@ def test_ior_device_pointer_matches_scalar(tracer):
     assert torch.equal(out, ref)
     for a, b in zip(got_g, ref_g):                 # float atomics: summation order may differ
         assert rel_l2(a.cpu().numpy(), b.cpu().numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("mesh", ["ico3_noisy", "c2_cube_sphere"])
+def test_mesh_regularizers_match_oracle(tracer, mesh):
+    """NEXT-4 L_edge and L_lap (R31) and their vertex gradients."""
+    from oracle import mesh_reg as MR
+    g = np.random.default_rng(8)
+    if mesh == "ico3_noisy":
+        V, F = S.icosphere(3)
+        V = (V * (1 + 0.05 * g.normal(size=V.shape))).astype(np.float32)
+    else:
+        V, F = S.cube_sphere(65, 2)
+    Vd = torch.as_tensor(V, device="cuda:0")
+    Fd = torch.as_tensor(F.astype(np.int32), device="cuda:0")
+    tracer.build_bvh(Vd, Fd)
+    le, ll = 0.7, 1.3
+    loss, gV = tracer.mesh_regularizers(le, ll)
+    Le, ge = MR.loss_edge(V.astype(np.float64), F)
+    Ll, gl = MR.loss_lap(V.astype(np.float64), F)
+    l = loss.cpu().numpy()
+    assert abs(l[0] - Le) < 1e-4 * Le and abs(l[1] - Ll) < 1e-4 * Ll, (l, Le, Ll)
+    assert rel_l2(gV.cpu().numpy(), le * ge + ll * gl) < 1e-4
+    # accumulation into a caller buffer; deterministic (no atomics in the gradient)
+    loss2, gV2 = tracer.mesh_regularizers(le, ll, grad_V=gV.clone())
+    torch.testing.assert_close(gV2, 2 * gV, rtol=1e-5, atol=1e-6 * float(gV.abs().max()))
+    _, gV3 = tracer.mesh_regularizers(le, ll)
+    assert torch.equal(gV3, gV)
