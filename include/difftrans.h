@@ -255,6 +255,19 @@ DT_API dt_status dt_sigma_regularizers(dt_ctx* ctx, const dt_absorption* absorpt
 DT_API dt_status dt_mesh_regularizers(dt_ctx* ctx, float lambda_edge, float lambda_lap, float* grad_V, float* loss,
                                       void* stream);
 
+/* Mask regulariser (R32) of the current dt_build_bvh
+ * snapshot over full images: the rendered mask M^ (1 where the camera ray through the pixel
+ * centre hits the mesh), loss[0] = (1/N) sum |M^ - gt_mask| (N = n_views W H; gt_mask device
+ * float [n_views][H][W] in [0, 1]), and grad_V [nv][3] (device) += lambda d/dV of the
+ * area-coverage relaxation, estimated by silhouette-edge sampling: every projected silhouette
+ * edge (faces of opposite facing, or a boundary edge) is sampled every 0.5 px; a sample on the
+ * outer boundary (covered 0.02 px inside, not outside) pushes its edge's two vertices through
+ * the pinhole Jacobian by (1 - 2 gt(outside pixel)) / N per unit length.  mask_out (device
+ * float [n_views][H][W]) or NULL.  cams->pixel_ids must be NULL.  The per-vertex sums use float
+ * atomics (order-dependent at the ulp level). */
+DT_API dt_status dt_mask_loss(dt_ctx* ctx, const dt_cameras* cams, const float* gt_mask, float lambda, float* grad_V,
+                              float* loss, float* mask_out, void* stream);
+
 /* Adam (beta = (0.9, 0.999), weight decay 1e-6 added to the gradient as in
  * torch.optim.Adam) on n parameters, in place: m, v are [n] state buffers (zero at step 1).
  * uniform != 0: AdamUniform (Nicolet et al., cited at P:186) -- one second-moment statistic

@@ -94,6 +94,7 @@ SIGNATURES = {
                                         _P]),
     "dt_adam_step": (C.c_int, [_P, _P, _P, _P, _P, C.c_int64, C.POINTER(Adam), _P]),
     "dt_mesh_regularizers": (C.c_int, [_P, C.c_float, C.c_float, _P, _P, _P]),
+    "dt_mask_loss": (C.c_int, [_P, C.POINTER(Cameras), _P, C.c_float, _P, _P, _P, _P]),
     "dt_debug_closest_hit": (C.c_int, [_P, _P, C.c_int64, C.c_float, C.c_int32, _P, _P, _P]),
     "dt_debug_bvh_check": (C.c_int, [_P, C.POINTER(C.c_int64), _P]),
     "dt_debug_vertex_normals": (C.c_int, [_P, _P, _P]),

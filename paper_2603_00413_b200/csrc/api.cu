@@ -237,7 +237,7 @@ void dt_destroy(dt_ctx* c) {
                   c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, c->vstart, c->vcorner, c->scal,
                   c->iscal, c->rec.o, c->lvl, c->sigma_snap, c->gV, c->gN, c->gVn, c->gS, c->fe, c->gsig, c->gior,
                   c->counters, c->ranges, c->bdepth, c->wflag, c->widx, c->wbox, c->wdepth, c->scratch,
-                  c->nbr_start, c->nbr_cnt, c->nbr};
+                  c->nbr_start, c->nbr_cnt, c->nbr, c->nbr_owner};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
@@ -604,6 +604,22 @@ dt_status dt_mesh_regularizers(dt_ctx* c, float lambda_edge, float lambda_lap, f
   PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
   int nl = 0;
   DT_CU(launch_mesh_regularizers(c, lambda_edge, lambda_lap, grad_V, loss, (cudaStream_t)stream, &nl));
+  p.end(nl);
+  return DT_OK;
+}
+
+dt_status dt_mask_loss(dt_ctx* c, const dt_cameras* cams, const float* gt_mask, float lambda, float* grad_V,
+                       float* loss, float* mask_out, void* stream) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_mask_loss: call dt_build_bvh first");
+  DT_ARG(cams && gt_mask && grad_V && loss, "dt_mask_loss: NULL argument");
+  DT_ARG(cams->K && cams->c2w && cams->n_views > 0 && cams->width > 0 && cams->height > 0 && !cams->pixel_ids,
+         "dt_mask_loss: cams must describe full images (pixel_ids = NULL)");
+  DT_ARG(lambda >= 0.f, "dt_mask_loss: lambda must be >= 0");
+  PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
+  int nl = 0;
+  DT_CU(launch_mask_loss(c, cams, gt_mask, lambda, grad_V, loss, mask_out, (cudaStream_t)stream, &nl));
   p.end(nl);
   return DT_OK;
 }

@@ -134,6 +134,7 @@ struct dt_ctx {
   int* nbr_start = nullptr;   // [nv+1] vertex neighbour CSR (mesh regularisers)
   int* nbr_cnt = nullptr;     // [nv+1]
   int* nbr = nullptr;         // [<= 6 nf]
+  int* nbr_owner = nullptr;   // [<= 6 nf] vertex of each neighbour entry
   int nbr_cap_v = 0;
   int64_t nbr_cap = 0;
   float4* fe = nullptr;       // [2nf] per-face d/de1, d/de2
@@ -185,6 +186,9 @@ cudaError_t launch_backward_level(const BwdLaunch& a, int level, int sm_count, c
 cudaError_t launch_vertex_normal_backward(dt_ctx* c, cudaStream_t st);
 cudaError_t launch_mesh_regularizers(dt_ctx* c, float lambda_edge, float lambda_lap, float* grad_V, float* loss,
                                      cudaStream_t st, int* nl);
+cudaError_t launch_mask_loss(dt_ctx* c, const dt_cameras* cams, const float* gt, float lambda, float* grad_V,
+                             float* loss, float* mask_out, cudaStream_t st, int* nl);
+DevScene scene_from_ctx(const dt_ctx* c);
 cudaError_t launch_finalize(dt_ctx* c, float* grad_V, float* grad_ior, float* grad_sigma, int accumulate,
                             cudaStream_t st);
 cudaError_t launch_loss_color(const float* rgb, const float* tgt, int64_t n, float* grad, float* loss, cudaStream_t st);
@@ -193,7 +197,6 @@ cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64
 cudaError_t launch_bvh_check(dt_ctx* c, long long* out_dev, cudaStream_t st);
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, int res, bool pairs, cudaStream_t st);
-DevScene scene_from_ctx(const dt_ctx* c);
 cudaError_t launch_count_segments(const int* lvl, int max_depth, unsigned long long* seg, cudaStream_t st);
 // optim.cu
 cudaError_t launch_loss_rt(const float* rgb, const float* tgt, const float* mask, int64_t n, float lc, float lt,

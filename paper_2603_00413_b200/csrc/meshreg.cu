@@ -65,11 +65,15 @@ __global__ void k_nbr_scan(const int* __restrict__ cnt, int n, int* __restrict__
 }
 
 __global__ void k_nbr_fill(const int* __restrict__ vstart, const unsigned* __restrict__ corner,
-                           const int* __restrict__ F, int nv, const int* __restrict__ start, int* __restrict__ nbr) {
+                           const int* __restrict__ F, int nv, const int* __restrict__ start, int* __restrict__ nbr,
+                           int* __restrict__ owner) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
     int nb[kMaxValence];
     const int n = collect_neighbours(vstart, corner, F, v, nb);
-    for (int q = 0; q < n; ++q) nbr[start[v] + q] = nb[q];
+    for (int q = 0; q < n; ++q) {
+      nbr[start[v] + q] = nb[q];
+      owner[start[v] + q] = v;
+    }
   }
 }
 
@@ -144,10 +148,134 @@ __global__ void k_add_vec(const float4* __restrict__ src, int n, float* __restri
   }
 }
 
+// ----------------------------------------------------------------------------- L_mask (R32)
+constexpr int kMaskThreads = 128;
+
+DT_D void image_ray(const float* K, const float* c2w, int v, float u, float w, float3& o, float3& d) {
+  const float* k = K + 4 * v;
+  const float* m = c2w + 12 * v;
+  const float dx = (u - k[2]) / k[0], dy = (w - k[3]) / k[1];
+  const float3 r = f3(m[0] * dx + m[1] * dy + m[2], m[4] * dx + m[5] * dy + m[6], m[8] * dx + m[9] * dy + m[10]);
+  d = r * (1.0f / sqrtf(dot(r, r)));
+  o = f3(m[3], m[7], m[11]);
+}
+
+// the rendered mask (the camera ray through the pixel centre hits the mesh) and
+// sum |M^ - M| / N
+__global__ void __launch_bounds__(kMaskThreads) k_mask_render(DevScene s, const float* __restrict__ K,
+                                                              const float* __restrict__ c2w, int n_views, int W, int H,
+                                                              const float* __restrict__ gt, float inv_n,
+                                                              float* __restrict__ mask_out, float* __restrict__ loss) {
+  __shared__ int sstack[kStackShared * kMaskThreads];
+  int err = 0, visits = 0, tests = 0;
+  float acc = 0.f;
+  const int64_t n = (int64_t)n_views * W * H;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    float3 o, d;
+    camera_ray(K, c2w, W, H, p, o, d);
+    float t, u, v;
+    const float m = traverse(s, o, d, 0.0f, t, u, v, sstack + threadIdx.x, kMaskThreads, err, visits, tests) >= 0;
+    acc += fabsf(m - gt[p]);
+    if (mask_out) mask_out[p] = m;
+  }
+  acc = warp_sum(acc);
+  if (lane_id() == 0 && acc != 0.f) atomicAdd(loss, acc * inv_n);
+}
+
+DT_D bool covered(const DevScene& s, const float* K, const float* c2w, int v, float u, float w, int* sstack) {
+  float3 o, d;
+  image_ray(K, c2w, v, u, w, o, d);
+  float t, bu, bv;
+  int err = 0, visits = 0, tests = 0;
+  return traverse(s, o, d, 0.0f, t, bu, bv, sstack, kMaskThreads, err, visits, tests) >= 0;
+}
+
+// pinhole projection of X in view v: image point and d(u, w)/dX rows (OpenCV axes, R19)
+DT_D bool project(const float* K, const float* c2w, int v, float3 X, float2& p, float3& ju, float3& jw) {
+  const float* k = K + 4 * v;
+  const float* m = c2w + 12 * v;
+  const float3 q = X - f3(m[3], m[7], m[11]);
+  const float3 r0 = f3(m[0], m[4], m[8]), r1 = f3(m[1], m[5], m[9]), r2 = f3(m[2], m[6], m[10]);   // R columns
+  const float x = dot(r0, q), y = dot(r1, q), z = dot(r2, q);
+  if (!(z > 1e-6f)) return false;
+  p = make_float2(k[0] * x / z + k[2], k[1] * y / z + k[3]);
+  ju = (r0 * (1.0f / z) - r2 * (x / (z * z))) * k[0];
+  jw = (r1 * (1.0f / z) - r2 * (y / (z * z))) * k[1];
+  return true;
+}
+
+// silhouette-edge sampling of dL_mask/dV (R32): one thread per (view, directed neighbour
+// entry i -> j with i < j)
+__global__ void __launch_bounds__(kMaskThreads) k_mask_grad(
+    DevScene s, const float* __restrict__ K, const float* __restrict__ c2w, int n_views, int W, int H,
+    const float* __restrict__ gt, const int* __restrict__ nbr, const int* __restrict__ owner,
+    const int* __restrict__ nbr_total, int64_t n_ent, const int* __restrict__ vstart, const unsigned* __restrict__ vcorner, const int* __restrict__ F,
+    const float4* __restrict__ V, float scale, float spacing, float eps, float* __restrict__ grad_V) {
+  __shared__ int sstack[kStackShared * kMaskThreads];
+  const int64_t total = (int64_t)n_views * n_ent;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(id / n_ent);
+    const int64_t q = id - (int64_t)v * n_ent;
+    if (q >= *nbr_total) continue;                       // n_ent is the 6 nf bound
+    const int a = owner[q], b = nbr[q];
+    if (b <= a) continue;
+    int f1 = -1, f2 = -1;
+    for (int c = vstart[a]; c < vstart[a + 1]; ++c) {
+      const int f = (int)(vcorner[c] / 3u);
+      if (F[3 * f] == b || F[3 * f + 1] == b || F[3 * f + 2] == b) {
+        if (f1 < 0) f1 = f; else f2 = f;
+      }
+    }
+    const float* m = c2w + 12 * v;
+    const float3 cam = f3(m[3], m[7], m[11]);
+    auto front = [&](int f) {
+      const float3 p0 = f3(V[F[3 * f]]), p1 = f3(V[F[3 * f + 1]]), p2 = f3(V[F[3 * f + 2]]);
+      return dot(cam - p0, cross(p1 - p0, p2 - p0)) > 0.0f;
+    };
+    int fr = -1;
+    if (f2 < 0) {
+      if (f1 >= 0 && front(f1)) fr = f1;                       // boundary edge
+    } else {
+      const bool a1 = front(f1), a2 = front(f2);
+      if (a1 != a2) fr = a1 ? f1 : f2;
+    }
+    if (fr < 0) continue;
+    const int cv = F[3 * fr] != a && F[3 * fr] != b ? F[3 * fr] : (F[3 * fr + 1] != a && F[3 * fr + 1] != b ? F[3 * fr + 1]
+                                                                                                        : F[3 * fr + 2]);
+    float2 pa, pb, pc;
+    float3 jua, jwa, jub, jwb, t0, t1;
+    if (!project(K, c2w, v, f3(V[a]), pa, jua, jwa) || !project(K, c2w, v, f3(V[b]), pb, jub, jwb) ||
+        !project(K, c2w, v, f3(V[cv]), pc, t0, t1))
+      continue;
+    const float ex = pb.x - pa.x, ey = pb.y - pa.y, L = sqrtf(ex * ex + ey * ey);
+    if (!(L > 0.f)) continue;
+    float nx = -ey / L, ny = ex / L;
+    if (nx * (pc.x - pa.x) + ny * (pc.y - pa.y) > 0.f) { nx = -nx; ny = -ny; }   // outward: away from the face
+    const int Ks = min(4096, max(1, (int)ceilf(L / spacing)));
+    float ga = 0.f, gb = 0.f;
+    for (int k = 0; k < Ks; ++k) {
+      const float sk = ((float)k + 0.5f) / (float)Ks;
+      const float x = pa.x + sk * ex, y = pa.y + sk * ey;
+      const float xo = x + eps * nx, yo = y + eps * ny;
+      if (!(xo >= 0.f && xo < (float)W && yo >= 0.f && yo < (float)H)) continue;
+      if (covered(s, K, c2w, v, xo, yo, sstack + threadIdx.x)) continue;
+      if (!covered(s, K, c2w, v, x - eps * nx, y - eps * ny, sstack + threadIdx.x)) continue;
+      const float g = gt[((int64_t)v * H + (int)yo) * W + (int)xo];
+      const float w = (1.0f - 2.0f * g) * (L / (float)Ks);
+      ga += w * (1.0f - sk);
+      gb += w * sk;
+    }
+    if (ga == 0.f && gb == 0.f) continue;
+    const float3 da = (jua * nx + jwa * ny) * (ga * scale), db = (jub * nx + jwb * ny) * (gb * scale);
+    atomicAdd(grad_V + 3 * a, da.x); atomicAdd(grad_V + 3 * a + 1, da.y); atomicAdd(grad_V + 3 * a + 2, da.z);
+    atomicAdd(grad_V + 3 * b, db.x); atomicAdd(grad_V + 3 * b + 1, db.y); atomicAdd(grad_V + 3 * b + 2, db.z);
+  }
+}
+
 }  // namespace
 
-cudaError_t launch_mesh_regularizers(dt_ctx* c, float lambda_edge, float lambda_lap, float* grad_V, float* loss,
-                                     cudaStream_t st, int* nl) {
+// vertex neighbour CSR of the current snapshot (rebuilt per call: nv threads, cheap)
+cudaError_t build_neighbours(dt_ctx* c, cudaStream_t st, int* nl) {
   const int nv = c->nv, T = 256;
   const int g = std::max(1, std::min((nv + T - 1) / T, c->sm_count * 8));
   cudaError_t e;
@@ -161,20 +289,53 @@ cudaError_t launch_mesh_regularizers(dt_ctx* c, float lambda_edge, float lambda_
       return e;
     c->nbr_cap_v = nv + 1;
   }
-  // neighbour lists of the current snapshot; the total is bounded by the 2 * 3nf corner pairs
-  const int64_t nmax = (int64_t)6 * c->nf;
+  const int64_t nmax = (int64_t)6 * c->nf;   // bounded by the 2 * 3nf corner pairs
   if (c->nbr_cap < nmax) {
     cudaFree(c->nbr);
-    c->nbr = nullptr;
+    cudaFree(c->nbr_owner);
+    c->nbr = c->nbr_owner = nullptr;
     c->nbr_cap = 0;
-    if ((e = cudaMalloc(&c->nbr, (size_t)nmax * sizeof(int)))) return e;
+    if ((e = cudaMalloc(&c->nbr, (size_t)nmax * sizeof(int))) || (e = cudaMalloc(&c->nbr_owner, (size_t)nmax * sizeof(int))))
+      return e;
     c->nbr_cap = nmax;
   }
-  cudaMemsetAsync(loss, 0, 2 * sizeof(float), st);
   k_nbr_count<<<g, T, 0, st>>>(c->vstart, c->vcorner, c->F, nv, c->nbr_cnt);
   k_nbr_scan<<<1, 1024, 0, st>>>(c->nbr_cnt, nv, c->nbr_start);
-  k_nbr_fill<<<g, T, 0, st>>>(c->vstart, c->vcorner, c->F, nv, c->nbr_start, c->nbr);
-  int launches = 3;
+  k_nbr_fill<<<g, T, 0, st>>>(c->vstart, c->vcorner, c->F, nv, c->nbr_start, c->nbr, c->nbr_owner);
+  *nl += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mask_loss(dt_ctx* c, const dt_cameras* cams, const float* gt, float lambda, float* grad_V,
+                             float* loss, float* mask_out, cudaStream_t st, int* nl) {
+  cudaError_t e;
+  if ((e = build_neighbours(c, st, nl))) return e;
+  DevScene s = scene_from_ctx(c);
+  const int64_t npix = (int64_t)cams->n_views * cams->width * cams->height;
+  const float inv_n = 1.0f / (float)npix;
+  cudaMemsetAsync(loss, 0, sizeof(float), st);
+  int g = (int)std::min<int64_t>((npix + kMaskThreads - 1) / kMaskThreads, (int64_t)c->sm_count * 16);
+  k_mask_render<<<std::max(g, 1), kMaskThreads, 0, st>>>(s, cams->K, cams->c2w, cams->n_views, cams->width,
+                                                         cams->height, gt, inv_n, mask_out, loss);
+  // threads over the 6 nf bound of the neighbour entries; the real total is read on the device
+  const int64_t n_ent = 6 * (int64_t)c->nf;
+  g = (int)std::min<int64_t>((cams->n_views * n_ent + kMaskThreads - 1) / kMaskThreads, (int64_t)c->sm_count * 16);
+  k_mask_grad<<<std::max(g, 1), kMaskThreads, 0, st>>>(s, cams->K, cams->c2w, cams->n_views, cams->width, cams->height,
+                                                       gt, c->nbr, c->nbr_owner, c->nbr_start + c->nv, n_ent,
+                                                       c->vstart, c->vcorner, c->F,
+                                                       c->V, lambda * inv_n, 0.5f, 0.02f, grad_V);
+  *nl += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mesh_regularizers(dt_ctx* c, float lambda_edge, float lambda_lap, float* grad_V, float* loss,
+                                     cudaStream_t st, int* nl) {
+  const int nv = c->nv, T = 256;
+  const int g = std::max(1, std::min((nv + T - 1) / T, c->sm_count * 8));
+  cudaError_t e;
+  if ((e = build_neighbours(c, st, nl))) return e;
+  cudaMemsetAsync(loss, 0, 2 * sizeof(float), st);
+  int launches = 0;
   // L_edge through the vertex-normal chain: gN -> gVn, added to grad_V
   k_edge_reg<<<g, T, 0, st>>>(c->nrm, c->nbr_start, c->nbr, nv, lambda_edge, c->gN, loss);
   if ((e = launch_vertex_normal_backward(c, st))) return e;

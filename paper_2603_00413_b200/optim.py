@@ -5,6 +5,9 @@ One iteration, every arithmetic step in libdifftrans kern
   -> dt_trace_backward -> dt_sigma_regularizers (L_mat-smooth, L_vol; P:187-190, P:439-443)
   -> dt_adam_step on sigma ("material", lr 3e-3), IoR (lr 1e-4 while the geometry is
      frozen, then 1e-3) and, after the first k iterations, the vertices (AdamUniform, lr 1e-3).
+Every reg_every iterations of the joint stage (given ground-truth masks) the periodic mesh pass
+ runs reg_inner AdamUniform steps on L_mask + L_edge + L_lap (dt_mask_loss,
+dt_mesh_regularizers).
 Adam: beta = (0.9, 0.999), weight decay 1e-6.  Loss weights lambda_1 = 1,
 lambda_2 = 0.001, lambda_4 = 0.0005; lambda_3 is not given by the paper (SPEC
 default 0.01).  The IoR stays in [1, 3] and sigma >= 0 (projection after each update).
@@ -36,6 +39,14 @@ class RefineConfig:
     n_reg_points: int = 4096
     reg_sigma_perturb: float = 0.02         # xi ~ N(0, s^2) as a fraction of the sigma box
     ior_range: tuple = (1.0, 3.0)
+    # periodic mesh regularisation (NEXT-4): every reg_every iterations of the
+    # joint stage, reg_inner AdamUniform steps on the vertices of
+    # lambda_mask L_mask + lambda_edge L_edge + lambda_lap L_lap (weights unstated: R33)
+    reg_every: int = 100
+    reg_inner: int = 200
+    lambda_mask: float = 1.0
+    lambda_edge: float = 0.01
+    lambda_lap: float = 1.0
 
 
 @dataclass
@@ -77,7 +88,29 @@ class RefineOptimizer:
         xi = torch.randn((n, 3), generator=self.gen, device=dev) * (self.cfg.reg_sigma_perturb * (hi - lo))
         return pts.contiguous(), xi.contiguous()
 
-    def step(self, target: torch.Tensor, pixel_ids: Optional[torch.Tensor] = None, async_: bool = False) -> StepResult:
+    def regularize(self, gt_masks: torch.Tensor, iters: Optional[int] = None) -> torch.Tensor:
+        """The periodic mesh pass: `iters` (default cfg.reg_inner) AdamUniform steps
+        on the vertices of lambda_mask L_mask + lambda_edge L_edge + lambda_lap L_lap against the
+        ground-truth masks [n_views][H][W]; the LBVH is rebuilt before every step.  Returns the
+        last losses (L_mask, L_edge, L_lap) on the device."""
+        c, tr, ds = self.cfg, self.tr, self.ds
+        iters = c.reg_inner if iters is None else iters
+        m, v = torch.zeros_like(self.V), torch.zeros(1, device=self.V.device)
+        g = torch.zeros_like(self.V)
+        out = torch.zeros(3, dtype=torch.float32, device=self.V.device)
+        for t in range(1, iters + 1):
+            ds.set_vertices(self.V)
+            tr.build_bvh(ds.V, ds.F)
+            g.zero_()
+            lm, _, _ = tr.mask_loss(ds, gt_masks, c.lambda_mask, grad_V=g)
+            lr_, _ = tr.mesh_regularizers(c.lambda_edge, c.lambda_lap, grad_V=g)
+            tr.adam_step(self.V, g, m, v, t, c.lr_vertices, c.betas, c.eps, 0.0, uniform=True)
+            out[:1] = lm
+            out[1:] = lr_
+        return out
+
+    def step(self, target: torch.Tensor, pixel_ids: Optional[torch.Tensor] = None, async_: bool = False,
+             gt_masks: Optional[torch.Tensor] = None) -> StepResult:
         """One iteration, queued on the current stream.  async_: the forward does not wait for its
         arena-overflow check (an overflow surfaces as DT_ERR_RETRY on the next call; see
         Tracer.trace_forward) so consecutive steps queue back to back with no host stall."""
@@ -107,4 +140,6 @@ class RefineOptimizer:
                          c.weight_decay, uniform=True)
         self.loss[:2] = lrt
         self.loss[2:] = lreg
+        if gt_masks is not None and not frozen and c.reg_every > 0 and self.it % c.reg_every == 0:
+            self.regularize(gt_masks)
         return StepResult(self.loss, self.ior)

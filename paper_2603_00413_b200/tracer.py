@@ -258,6 +258,22 @@ class Tracer:
                                                    _ptr(loss), _stream(stream)), self.h)
         return loss, grad_V
 
+    def mask_loss(self, ds: DeviceScene, gt_mask: torch.Tensor, lam: float = 1.0, grad_V: Optional[torch.Tensor] = None,
+                  want_mask: bool = False, stream=None):
+        """L_mask of the last built mesh over ds's full images (NEXT-4, R32): returns
+        (loss[1], grad_V (accumulated; new zeros if None), rendered mask or None)."""
+        assert gt_mask.is_cuda and gt_mask.dtype == torch.float32 and gt_mask.is_contiguous()
+        assert gt_mask.numel() == ds.n_pixels
+        if grad_V is None:
+            grad_V = torch.zeros((self._nv_built, 3), dtype=torch.float32, device=self.device)
+        loss = torch.empty(1, dtype=torch.float32, device=self.device)
+        mask = torch.empty_like(gt_mask) if want_mask else None
+        cams = ds.cameras(None)
+        self._check(self._lib.dt_mask_loss(self.h, C.byref(cams), _ptr(gt_mask), float(lam), _ptr(grad_V), _ptr(loss),
+                                           _ptr(mask), _stream(stream)), self.h)
+        self._keep_mask = (ds, cams)
+        return loss, grad_V, mask
+
     def adam_step(self, param: torch.Tensor, grad: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: int,
                   lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0, uniform=False,
                   clamp=(-float("inf"), float("inf")), stream=None):
