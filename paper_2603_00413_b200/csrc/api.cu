@@ -237,7 +237,7 @@ void dt_destroy(dt_ctx* c) {
                   c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, c->vstart, c->vcorner, c->scal,
                   c->iscal, c->rec.o, c->lvl, c->sigma_snap, c->gV, c->gN, c->gVn, c->gS, c->fe, c->gsig, c->gior,
                   c->counters, c->ranges, c->bdepth, c->wflag, c->widx, c->wbox, c->wdepth, c->scratch,
-                  c->nbr_start, c->nbr_cnt, c->nbr, c->nbr_owner};
+                  c->nbr_start, c->nbr_cnt, c->nbr, c->nbr_owner, c->scan_part};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }

@@ -147,6 +147,69 @@ __global__ void k_scan(unsigned* __restrict__ h, int len) {
   for (int i = b; i < e; ++i) { unsigned x = h[i]; h[i] = run; run += x; }
 }
 
+// Multi-block exclusive scan (replaces the single-block k_scan on the build's long arrays):
+// per-chunk scan with the chunk totals in part[], a scan of part[], then the chunk offsets added.
+constexpr int kScanThreads = 256, kScanItems = 8, kScanChunk = kScanThreads * kScanItems;
+
+__global__ void k_scan_chunks(unsigned* __restrict__ h, int len, unsigned* __restrict__ part) {
+  __shared__ unsigned sv[kScanChunk];
+  __shared__ unsigned wsum[kScanThreads / 32];
+  const int base = blockIdx.x * kScanChunk, t = threadIdx.x;
+  for (int i = 0; i < kScanItems; ++i) {                 // coalesced load
+    const int idx = base + i * kScanThreads + t;
+    sv[i * kScanThreads + t] = idx < len ? h[idx] : 0u;
+  }
+  __syncthreads();
+  unsigned loc[kScanItems], s = 0;
+  for (int i = 0; i < kScanItems; ++i) { loc[i] = s; s += sv[t * kScanItems + i]; }
+  unsigned inc = s;                                      // warp-inclusive scan of thread sums
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(~0u, inc, o);
+    if ((t & 31) >= o) inc += y;
+  }
+  if ((t & 31) == 31) wsum[t >> 5] = inc;
+  __syncthreads();
+  if (t < 32) {
+    unsigned w = t < kScanThreads / 32 ? wsum[t] : 0u, wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(~0u, wi, o);
+      if (t >= o) wi += y;
+    }
+    if (t < kScanThreads / 32) wsum[t] = wi - w;         // exclusive warp offsets
+    if (t == kScanThreads / 32 - 1) part[blockIdx.x] = wi;
+  }
+  __syncthreads();
+  const unsigned off = wsum[t >> 5] + inc - s;
+  for (int i = 0; i < kScanItems; ++i) sv[t * kScanItems + i] = off + loc[i];
+  __syncthreads();
+  for (int i = 0; i < kScanItems; ++i) {
+    const int idx = base + i * kScanThreads + t;
+    if (idx < len) h[idx] = sv[i * kScanThreads + t];
+  }
+}
+
+__global__ void k_scan_add(unsigned* __restrict__ h, int len, const unsigned* __restrict__ part) {
+  const int base = blockIdx.x * kScanChunk;
+  const unsigned off = part[blockIdx.x];
+  for (int i = threadIdx.x; i < kScanChunk; i += blockDim.x)
+    if (base + i < len) h[base + i] += off;
+}
+
+// exclusive scan of h[0..len) in place; part: >= ceil(len / kScanChunk) scratch entries
+cudaError_t scan_exclusive(unsigned* h, int len, unsigned* part, cudaStream_t st, int* nl) {
+  const int nb = (len + kScanChunk - 1) / kScanChunk;
+  if (nb <= 1) {
+    k_scan<<<1, 1024, 0, st>>>(h, len);
+    *nl += 1;
+    return cudaGetLastError();
+  }
+  k_scan_chunks<<<nb, kScanThreads, 0, st>>>(h, len, part);
+  k_scan<<<1, 1024, 0, st>>>(part, nb);
+  k_scan_add<<<nb, kScanThreads, 0, st>>>(h, len, part);
+  *nl += 3;
+  return cudaGetLastError();
+}
+
 __global__ void k_scatter(const unsigned* __restrict__ kin, const unsigned* __restrict__ vin, unsigned* __restrict__ kout,
                           unsigned* __restrict__ vout, int n, int shift, const unsigned* __restrict__ hist) {
   __shared__ unsigned offs[256];
@@ -184,14 +247,15 @@ __global__ void k_scatter(const unsigned* __restrict__ kin, const unsigned* __re
 }
 
 cudaError_t radix_sort(unsigned* keys, unsigned* vals, unsigned* tk, unsigned* tv, int n, int bits, unsigned* hist,
-                       cudaStream_t st, bool& result_in_tmp) {
+                       unsigned* part, cudaStream_t st, bool& result_in_tmp, int* nl) {
   int nb = (n + kSortTile - 1) / kSortTile;
   result_in_tmp = false;
   unsigned *ki = keys, *vi = vals, *ko = tk, *vo = tv;
   for (int shift = 0; shift < bits; shift += 8) {
     k_hist<<<nb, kSortThreads, 0, st>>>(ki, n, shift, hist);
-    k_scan<<<1, 1024, 0, st>>>(hist, 256 * nb);
+    scan_exclusive(hist, 256 * nb, part, st, nl);
     k_scatter<<<nb, kSortThreads, 0, st>>>(ki, vi, ko, vo, n, shift, hist);
+    *nl += 2;
     std::swap(ki, ko);
     std::swap(vi, vo);
     result_in_tmp = !result_in_tmp;
@@ -520,6 +584,7 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   }
   size_t nb_needed = 256 * ((3 * (size_t)nf + kSortTile - 1) / kSortTile);
   if ((e = grow(c->hist, c->hist_cap, nb_needed))) return e;
+  if ((e = grow(c->scan_part, c->scan_part_cap, std::max(nb_needed, (size_t)nf) / kScanChunk + 16))) return e;
   if (!c->scal && (e = cudaMalloc(&c->scal, 16 * sizeof(float)))) return e;
   if (!c->iscal && (e = cudaMalloc(&c->iscal, 16 * sizeof(int)))) return e;
 
@@ -539,19 +604,19 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   int vbits = 8;
   while (vbits < 32 && (1u << vbits) < (unsigned)nv) vbits += 8;
   bool in_tmp;
-  if ((e = radix_sort(ka, va, kb, vb, 3 * nf, vbits, c->hist, st, in_tmp))) return e;
+  if ((e = radix_sort(ka, va, kb, vb, 3 * nf, vbits, c->hist, c->scan_part, st, in_tmp, &launches))) return e;
   unsigned* sk = in_tmp ? kb : ka;
   unsigned* sv = in_tmp ? vb : va;
   k_csr<<<gf3, T, 0, st>>>(sk, 3 * nf, nv, c->vstart);
   cudaMemcpyAsync(c->vcorner, sv, (size_t)3 * nf * sizeof(unsigned), cudaMemcpyDeviceToDevice, st);
   k_vertex_normals<<<gv, T, 0, st>>>(c->vstart, c->vcorner, c->fnrm, nv, c->nrm);
-  launches += 3 + 3 * (vbits / 8);
+  launches += 3;
   // LBVH: Morton codes, radix sort, Karras hierarchy, bottom-up refit
   k_morton<<<gf, T, 0, st>>>(c->V, c->F, nf, c->iscal, ka, va);
-  if ((e = radix_sort(ka, va, kb, vb, nf, 32, c->hist, st, in_tmp))) return e;
+  if ((e = radix_sort(ka, va, kb, vb, nf, 32, c->hist, c->scan_part, st, in_tmp, &launches))) return e;
   sk = in_tmp ? kb : ka;
   sv = in_tmp ? vb : va;
-  launches += 1 + 3 * 4;
+  launches += 1;
   if (nf > 1) {
     cudaMemsetAsync(c->rflags, 0, (size_t)(nf - 1) * sizeof(int), st);
     k_karras<<<gf, T, 0, st>>>(sk, nf, c->children, c->parent_int, c->parent_leaf, c->ranges);
@@ -563,8 +628,8 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   if (nf > 1) {
     k_bdepth<<<gf, T, 0, st>>>(c->parent_int, nf - 1, c->bdepth);
     k_wide_flags<<<gf, T, 0, st>>>(c->bdepth, c->ranges, nf - 1, c->wflag, c->widx, c->leaf_max);
-    k_scan<<<1, 1024, 0, st>>>(c->widx, nf - 1);
-    launches += 3;
+    if ((e = scan_exclusive(c->widx, nf - 1, c->scan_part, st, &launches))) return e;
+    launches += 2;
   }
   k_wide_build<<<gf, T, 0, st>>>(c->children, c->ranges, c->wflag, c->widx, c->bdepth, c->leafbox, c->nodebox, nf,
                                  c->iscal, reinterpret_cast<uint4*>(c->nodes), c->wbox, c->wdepth, c->iscal + 12, c->leaf_max);

@@ -96,6 +96,7 @@ struct dt_ctx {
   unsigned* keys = nullptr;   // [2 * max(nf, 3nf)] radix sort ping-pong
   unsigned* vals = nullptr;
   unsigned* hist = nullptr;
+  unsigned* scan_part = nullptr;   // multi-block scan chunk totals
   int2* children = nullptr;   // [nf-1]
   int* parent_int = nullptr;  // [nf-1]
   int* parent_leaf = nullptr; // [nf]
@@ -113,6 +114,7 @@ struct dt_ctx {
   float* scal = nullptr;      // device scalars: [0..5] root box, [6] bbox diagonal
   int* iscal = nullptr;       // device ints: ordered-int bounds
   size_t hist_cap = 0;
+  size_t scan_part_cap = 0;
   // record arena
   int64_t arena_cap = 0;
   bool arena_vol = false;       // arena carries the two volume-moment lanes (volumetric env)
