@@ -217,6 +217,7 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   if (const char* v = getenv("DT_TRAV_MODE")) c->trav_mode = std::max(0, std::min(3, atoi(v)));
   if (const char* v = getenv("DT_LEAF_VOTE")) c->leaf_vote = std::max(1, std::min(32, atoi(v)));
   if (const char* v = getenv("DT_TRAV_CHUNK")) c->trav_chunk = std::max(32, atoi(v));
+  if (const char* v = getenv("DT_WIDE_MODE")) c->wide_mode = std::max(0, std::min(1, atoi(v)));
   cudaError_t e;
   if ((e = cudaMalloc(&c->lvl, LV_INTS * sizeof(int))) || (e = cudaMallocHost(&c->host_lvl, LV_INTS * sizeof(int))) ||
       (e = cudaMalloc(&c->gior, 4 * sizeof(float))) || (e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long))) ||
@@ -237,7 +238,7 @@ void dt_destroy(dt_ctx* c) {
                   c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, c->vstart, c->vcorner, c->scal,
                   c->iscal, c->rec.o, c->lvl, c->sigma_snap, c->gV, c->gN, c->gVn, c->gS, c->fe, c->gsig, c->gior,
                   c->counters, c->ranges, c->bdepth, c->wflag, c->widx, c->wbox, c->wdepth, c->scratch,
-                  c->nbr_start, c->nbr_cnt, c->nbr, c->nbr_owner, c->scan_part};
+                  c->nbr_start, c->nbr_cnt, c->nbr, c->nbr_owner, c->scan_part, c->wqueue};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }

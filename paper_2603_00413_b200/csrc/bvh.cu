@@ -364,22 +364,87 @@ __global__ void k_wide_flags(const int* __restrict__ depth, const int2* __restri
   }
 }
 
+// Quantise and write wide node w: its entries ent[0..ne) (binary refs; internal entries carry
+// their own wide index in wref), boxes padded outward so the slab test stays conservative.
+DT_D void write_wide_node(int i, const int ent[4], const int wref[4], int ne, unsigned w, int wd, double pad,
+                          const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
+                          const int2* __restrict__ ranges, int leaf_max, uint4* __restrict__ wnodes,
+                          float4* __restrict__ wbox, int* __restrict__ wdepth) {
+  float3 ulo, uhi;
+  load_box(leafbox, nodebox, i, ulo, uhi);
+  double P[3] = {(double)__double2float_rd((double)ulo.x - pad), (double)__double2float_rd((double)ulo.y - pad),
+                 (double)__double2float_rd((double)ulo.z - pad)};
+  double hiU[3] = {(double)uhi.x + pad, (double)uhi.y + pad, (double)uhi.z + pad};
+  int ex[3];
+  double sc[3];
+  for (int a = 0; a < 3; ++a) {
+    double ext = hiU[a] - P[a];
+    int k = -126;
+    if (ext > 0.0) { frexp(ext / 255.0, &k); k = max(-126, min(127, k)); }
+    ex[a] = k + 127;
+    sc[a] = ldexp(1.0, k);
+  }
+  unsigned q[6] = {0, 0, 0, 0, 0, 0};
+  int refs[4];
+  for (int c = 0; c < 4; ++c) {
+    unsigned ql[3] = {255, 255, 255}, qh[3] = {0, 0, 0};
+    refs[c] = kEmptyRef;
+    if (c < ne) {
+      int e = ent[c];
+      float3 lo, hi;
+      load_box(leafbox, nodebox, e, lo, hi);
+      const float l3[3] = {lo.x, lo.y, lo.z}, h3[3] = {hi.x, hi.y, hi.z};
+      for (int a = 0; a < 3; ++a) {
+        double fl = floor(((double)l3[a] - pad - P[a]) / sc[a]);
+        double fh = ceil(((double)h3[a] + pad - P[a]) / sc[a]);
+        ql[a] = (unsigned)fmin(fmax(fl, 0.0), 255.0);
+        qh[a] = (unsigned)fmin(fmax(fh, 0.0), 255.0);
+      }
+      if (e >= 0 && bsize(ranges, e) > leaf_max) {
+        refs[c] = wref[c];
+      } else {
+        int first = e < 0 ? ~e : ranges[e].x;
+        int cnt = bsize(ranges, e);
+        refs[c] = -1 - ((first << 2) | (cnt - 1));
+      }
+    }
+    for (int a = 0; a < 3; ++a) {
+      q[a] |= ql[a] << (8 * c);
+      q[3 + a] |= qh[a] << (8 * c);
+    }
+  }
+  uint4* nd = wnodes + 4 * (size_t)w;
+  nd[0] = make_uint4(__float_as_uint((float)P[0]), __float_as_uint((float)P[1]), __float_as_uint((float)P[2]),
+                     (unsigned)ex[0] | ((unsigned)ex[1] << 8) | ((unsigned)ex[2] << 16));
+  nd[1] = make_uint4(q[0], q[1], q[2], q[3]);
+  nd[2] = make_uint4(q[4], q[5], (unsigned)refs[0], (unsigned)refs[1]);
+  nd[3] = make_uint4((unsigned)refs[2], (unsigned)refs[3], 0u, 0u);
+  wbox[2 * (size_t)w] = f4(ulo, 0.f);
+  wbox[2 * (size_t)w + 1] = f4(uhi, 0.f);
+  wdepth[w] = wd;
+}
+
+DT_D double wide_pad(const int* __restrict__ ibox) {
+  float m = fmaxf(fmaxf(fmaxf(fabsf(ord2f(ibox[0])), fabsf(ord2f(ibox[1]))), fmaxf(fabsf(ord2f(ibox[2])), fabsf(ord2f(ibox[3])))),
+                  fmaxf(fabsf(ord2f(ibox[4])), fabsf(ord2f(ibox[5]))));
+  return (double)m * 4e-6 + 1e-30;
+}
+
+// Collapse pattern 0: the wide roots are the binary nodes at even depth, each opening its
+// internal children once (2..4 entries).
 __global__ void k_wide_build(const int2* __restrict__ children, const int2* __restrict__ ranges,
                              const unsigned* __restrict__ flag, const unsigned* __restrict__ widx,
                              const int* __restrict__ depth, const float4* __restrict__ leafbox,
                              const float4* __restrict__ nodebox, int n, const int* __restrict__ ibox,
                              uint4* __restrict__ wnodes, float4* __restrict__ wbox, int* __restrict__ wdepth,
                              int* __restrict__ nwide, int leaf_max) {
-  float m = fmaxf(fmaxf(fmaxf(fabsf(ord2f(ibox[0])), fabsf(ord2f(ibox[1]))), fmaxf(fabsf(ord2f(ibox[2])), fabsf(ord2f(ibox[3])))),
-                  fmaxf(fabsf(ord2f(ibox[4])), fabsf(ord2f(ibox[5]))));
-  double pad = (double)m * 4e-6 + 1e-30;
+  const double pad = wide_pad(ibox);
   int n_int = n - 1;
   int total = max(n_int, 1);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     if (i == total - 1) *nwide = n_int == 0 ? 1 : (int)(widx[i] + flag[i]);
     if (n_int > 0 && !flag[i]) continue;
-    // entries of this wide node (binary refs)
-    int ent[4], ne = 0;
+    int ent[4], wref[4] = {0, 0, 0, 0}, ne = 0;
     if (n_int == 0) {
       ent[ne++] = ~0;                                   // single triangle
     } else {
@@ -396,61 +461,87 @@ __global__ void k_wide_build(const int2* __restrict__ children, const int2* __re
         }
       }
     }
-    float3 ulo, uhi;
-    if (n_int == 0) load_box(leafbox, nodebox, ~0, ulo, uhi);
-    else load_box(leafbox, nodebox, i, ulo, uhi);
-    double P[3] = {(double)__double2float_rd((double)ulo.x - pad), (double)__double2float_rd((double)ulo.y - pad),
-                   (double)__double2float_rd((double)ulo.z - pad)};
-    double hiU[3] = {(double)uhi.x + pad, (double)uhi.y + pad, (double)uhi.z + pad};
-    int ex[3];
-    double sc[3];
-    for (int a = 0; a < 3; ++a) {
-      double ext = hiU[a] - P[a];
-      int k = -126;
-      if (ext > 0.0) { frexp(ext / 255.0, &k); k = max(-126, min(127, k)); }
-      ex[a] = k + 127;
-      sc[a] = ldexp(1.0, k);
-    }
-    unsigned q[6] = {0, 0, 0, 0, 0, 0};
-    int refs[4];
-    for (int c = 0; c < 4; ++c) {
-      unsigned ql[3] = {255, 255, 255}, qh[3] = {0, 0, 0};
-      refs[c] = kEmptyRef;
-      if (c < ne) {
-        int e = ent[c];
-        float3 lo, hi;
-        load_box(leafbox, nodebox, e, lo, hi);
-        const float l3[3] = {lo.x, lo.y, lo.z}, h3[3] = {hi.x, hi.y, hi.z};
-        for (int a = 0; a < 3; ++a) {
-          double fl = floor(((double)l3[a] - pad - P[a]) / sc[a]);
-          double fh = ceil(((double)h3[a] + pad - P[a]) / sc[a]);
-          ql[a] = (unsigned)fmin(fmax(fl, 0.0), 255.0);
-          qh[a] = (unsigned)fmin(fmax(fh, 0.0), 255.0);
-        }
-        if (e >= 0 && bsize(ranges, e) > leaf_max) {
-          refs[c] = (int)widx[e];
-        } else {
-          int first = e < 0 ? ~e : ranges[e].x;
-          int cnt = bsize(ranges, e);
-          refs[c] = -1 - ((first << 2) | (cnt - 1));
-        }
-      }
-      for (int a = 0; a < 3; ++a) {
-        q[a] |= ql[a] << (8 * c);
-        q[3 + a] |= qh[a] << (8 * c);
-      }
-    }
-    unsigned w = n_int == 0 ? 0u : widx[i];
-    uint4* nd = wnodes + 4 * (size_t)w;
-    nd[0] = make_uint4(__float_as_uint((float)P[0]), __float_as_uint((float)P[1]), __float_as_uint((float)P[2]),
-                       (unsigned)ex[0] | ((unsigned)ex[1] << 8) | ((unsigned)ex[2] << 16));
-    nd[1] = make_uint4(q[0], q[1], q[2], q[3]);
-    nd[2] = make_uint4(q[4], q[5], (unsigned)refs[0], (unsigned)refs[1]);
-    nd[3] = make_uint4((unsigned)refs[2], (unsigned)refs[3], 0u, 0u);
-    wbox[2 * (size_t)w] = f4(ulo, 0.f);
-    wbox[2 * (size_t)w + 1] = f4(uhi, 0.f);
-    wdepth[w] = n_int == 0 ? 0 : depth[i] / 2;
+    for (int c = 0; c < ne; ++c)
+      if (ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max) wref[c] = (int)widx[ent[c]];
+    write_wide_node(n_int == 0 ? ~0 : i, ent, wref, ne, n_int == 0 ? 0u : widx[i], n_int == 0 ? 0 : depth[i] / 2,
+                    pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
   }
+}
+
+// Collapse pattern 1 (surface-area greedy): top down from the root, a wide node starts with
+// its binary node's two children and repeatedly opens the internal entry of largest surface
+// area until it has 4 entries (fuller nodes, larger boxes split first).  A work queue indexed
+// by wide node id: a node's unopened internal entries get fresh ids (atomic counter) and are
+// published into their queue slots; persistent threads claim slots in order and wait for
+// them; `pending` (published - finished) reaching 0 ends the pass.
+DT_D float box_area(const float4* __restrict__ nodebox, int e) {
+  const float4 a = __ldcg(nodebox + 2 * (size_t)e), b = __ldcg(nodebox + 2 * (size_t)e + 1);
+  const float dx = b.x - a.x, dy = b.y - a.y, dz = b.z - a.z;
+  return dx * dy + dy * dz + dz * dx;
+}
+
+__global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __restrict__ ranges,
+                               const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
+                               const int* __restrict__ ibox, uint4* __restrict__ wnodes, float4* __restrict__ wbox,
+                               int* __restrict__ wdepth, int* __restrict__ nwide, unsigned long long* queue,
+                               int* __restrict__ head, int* pending, int cap, int leaf_max) {
+  const double pad = wide_pad(ibox);
+  while (true) {
+    const int idx = atomicAdd(head, 1);
+    if (idx >= cap) return;
+    unsigned long long item;
+    for (int spin = 0;; ++spin) {                    // poll through L2 (no atomic traffic)
+      item = __ldcg(queue + idx);
+      if (item != ~0ull) break;
+      if (__ldcg(pending) == 0) return;              // no more work will be published
+      __nanosleep(spin < 8 ? 32 : 256);
+    }
+    __threadfence();                                   // acquire: the parent's writes before publishing
+    const int b = (int)(item & 0xffffffffu), w = (int)(item >> 32);
+    int ent[4], wref[4] = {0, 0, 0, 0}, ne = 2;
+    const int2 ch = children[b];
+    ent[0] = ch.x;
+    ent[1] = ch.y;
+    while (ne < 4) {
+      int best = -1;
+      float ba = -1.f;
+      for (int c = 0; c < ne; ++c) {
+        const int e = ent[c];
+        if (e >= 0 && bsize(ranges, e) > leaf_max) {
+          const float ar = box_area(nodebox, e);
+          if (ar > ba) { ba = ar; best = c; }
+        }
+      }
+      if (best < 0) break;
+      const int2 g = children[ent[best]];
+      ent[best] = g.x;
+      ent[ne++] = g.y;
+    }
+    int nin = 0;
+    for (int c = 0; c < ne; ++c) nin += ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max;
+    const int base = nin ? atomicAdd(nwide, nin) : 0;
+    const int wd = __ldcg(wdepth + w);                 // written by the parent before publishing w (L2)
+    for (int c = 0, k = 0; c < ne; ++c)
+      if (ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max) wref[c] = base + k++;
+    write_wide_node(b, ent, wref, ne, (unsigned)w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
+    for (int c = 0; c < ne; ++c) {
+      if (!(ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max)) continue;
+      wdepth[wref[c]] = wd + 1;
+      __threadfence();
+      atomicExch(queue + wref[c], ((unsigned long long)(unsigned)wref[c] << 32) | (unsigned)ent[c]);
+    }
+    __threadfence();
+    atomicAdd(pending, nin - 1);
+  }
+}
+
+__global__ void k_wide_topdown_init(unsigned long long* __restrict__ queue, int* __restrict__ head,
+                                    int* __restrict__ pending, int* __restrict__ nwide, int* __restrict__ wdepth) {
+  queue[0] = 0ull;                                      // binary root 0 -> wide node 0
+  *head = 0;
+  *pending = 1;
+  *nwide = 1;
+  wdepth[0] = 0;
 }
 
 __global__ void k_pack_tris(const float4* __restrict__ V, const int* __restrict__ F, const unsigned* __restrict__ order,
@@ -625,17 +716,42 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   k_refit<<<gf, T, 0, st>>>(c->V, c->F, sv, nf, c->children, c->parent_int, c->parent_leaf, c->rflags, c->leafbox,
                             c->nodebox);
   // collapse to the quantised 4-wide BVH
-  if (nf > 1) {
-    k_bdepth<<<gf, T, 0, st>>>(c->parent_int, nf - 1, c->bdepth);
-    k_wide_flags<<<gf, T, 0, st>>>(c->bdepth, c->ranges, nf - 1, c->wflag, c->widx, c->leaf_max);
-    if ((e = scan_exclusive(c->widx, nf - 1, c->scan_part, st, &launches))) return e;
+  if (nf > 1 && c->wide_mode == 1) {                    // surface-area greedy, top down
+    if (!c->wqueue || c->wqueue_cap < nf) {
+      cudaFree(c->wqueue);
+      c->wqueue = nullptr;
+      c->wqueue_cap = 0;
+      if ((e = cudaMalloc(&c->wqueue, (size_t)nf * sizeof(unsigned long long) + 16 * sizeof(int)))) return e;
+      c->wqueue_cap = nf;
+    }
+    int* ctr = reinterpret_cast<int*>(c->wqueue + c->wqueue_cap);
+    static int gq = 0;
+    if (!gq) {
+      int per = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_wide_topdown, T, 0);
+      gq = std::max(1, per) * c->sm_count;
+    }
+    cudaMemsetAsync(c->wqueue, 0xff, (size_t)nf * sizeof(unsigned long long), st);
+    k_wide_topdown_init<<<1, 1, 0, st>>>(c->wqueue, ctr, ctr + 1, c->iscal + 12, c->wdepth);
+    k_wide_topdown<<<gq, T, 0, st>>>(c->children, c->ranges, c->leafbox, c->nodebox, c->iscal,
+                                     reinterpret_cast<uint4*>(c->nodes), c->wbox, c->wdepth, c->iscal + 12, c->wqueue,
+                                     ctr, ctr + 1, nf - 1, c->leaf_max);
     launches += 2;
+  } else {
+    if (nf > 1) {
+      k_bdepth<<<gf, T, 0, st>>>(c->parent_int, nf - 1, c->bdepth);
+      k_wide_flags<<<gf, T, 0, st>>>(c->bdepth, c->ranges, nf - 1, c->wflag, c->widx, c->leaf_max);
+      if ((e = scan_exclusive(c->widx, nf - 1, c->scan_part, st, &launches))) return e;
+      launches += 2;
+    }
+    k_wide_build<<<gf, T, 0, st>>>(c->children, c->ranges, c->wflag, c->widx, c->bdepth, c->leafbox, c->nodebox, nf,
+                                   c->iscal, reinterpret_cast<uint4*>(c->nodes), c->wbox, c->wdepth, c->iscal + 12,
+                                   c->leaf_max);
+    launches += 1;
   }
-  k_wide_build<<<gf, T, 0, st>>>(c->children, c->ranges, c->wflag, c->widx, c->bdepth, c->leafbox, c->nodebox, nf,
-                                 c->iscal, reinterpret_cast<uint4*>(c->nodes), c->wbox, c->wdepth, c->iscal + 12, c->leaf_max);
   k_pack_tris<<<gf, T, 0, st>>>(c->V, c->F, sv, nf, c->tris);
   k_scalars<<<1, 1, 0, st>>>(c->iscal, c->scal);
-  launches += 4;
+  launches += 3;
   c->nv = nv;
   c->nf = nf;
   *nl += launches;

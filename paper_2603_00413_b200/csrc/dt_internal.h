@@ -97,6 +97,9 @@ struct dt_ctx {
   unsigned* vals = nullptr;
   unsigned* hist = nullptr;
   unsigned* scan_part = nullptr;   // multi-block scan chunk totals
+  unsigned long long* wqueue = nullptr;   // surface-area collapse work queue (+16 ints of counters)
+  int wqueue_cap = 0;
+  int wide_mode = 1;               // 0: even-depth collapse, 1: surface-area greedy (DT_WIDE_MODE)
   int2* children = nullptr;   // [nf-1]
   int* parent_int = nullptr;  // [nf-1]
   int* parent_leaf = nullptr; // [nf]
