@@ -416,6 +416,13 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    # functional check of the multi-rank path on a box with fewer GPUs than ranks (tests only;
+    # never used for a reported number): BENCH_SHARE_GPU=1 maps ranks onto the visible devices
+    # and BENCH_DIST_BACKEND picks the process-group backend (default nccl)
+    if os.environ.get("BENCH_SHARE_GPU") == "1":
+        import torch
+        local_rank %= max(torch.cuda.device_count(), 1)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":
@@ -425,7 +432,10 @@ def main():
             import torch
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+            else:
+                dist.init_process_group(backend)
         line = run_ours(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
