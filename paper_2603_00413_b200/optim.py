@@ -55,6 +55,46 @@ class StepResult:
     ior: torch.Tensor                       # [1] device: the IoR after this step's update
 
 
+class HostTargets:
+    """Double-buffered asynchronous upload of per-step targets from pinned host memory: the
+    copy of step i+1's target runs on a side stream (copy engine) while step i computes.
+
+        up = HostTargets(shape, device)
+        k = up.upload(host)                   # step 0's target
+        for i in range(n):
+            tgt = up.get(k)                   # current stream waits for that copy
+            k_next = up.upload(host_next)     # overlaps with the step below
+            opt.step(tgt); up.release(k)
+            k = k_next
+    """
+
+    def __init__(self, shape, device):
+        self.buf = [torch.empty(shape, dtype=torch.float32, device=device) for _ in range(2)]
+        self.done = [torch.cuda.Event() for _ in range(2)]
+        self.used = [None, None]
+        self.stream = torch.cuda.Stream(device)
+        self.i = 0
+
+    def upload(self, host: torch.Tensor) -> int:
+        k = self.i % 2
+        self.i += 1
+        if self.used[k] is not None:                  # the step that last read buffer k is done
+            self.stream.wait_event(self.used[k])
+        with torch.cuda.stream(self.stream):
+            self.buf[k].copy_(host, non_blocking=True)
+            self.done[k].record(self.stream)
+        return k
+
+    def get(self, k: int) -> torch.Tensor:
+        torch.cuda.current_stream().wait_event(self.done[k])
+        return self.buf[k]
+
+    def release(self, k: int):
+        e = torch.cuda.Event()
+        e.record(torch.cuda.current_stream())
+        self.used[k] = e
+
+
 class RefineOptimizer:
     """Jointly optimises vertices, IoR and absorption of a DeviceScene against target images."""
 
