@@ -93,15 +93,20 @@ DT_D void camera_ray(const float* K, const float* c2w, int W, int H, int64_t pid
 }
 
 // ----------------------------------------------------------------------------- intersection
-// Explicit round-to-nearest intrinsics: no FMA contraction, so the LBVH traversal, the
-// brute-force test and the backward replay produce bit-identical (t, u, v).
+// Explicit intrinsics (fixed fma / rounding, never re-contracted by the compiler), so the LBVH
+// traversal, the brute-force test and the backward replay produce bit-identical (t, u, v).
 DT_D float3 sub_rn(float3 a, float3 b) { return f3(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z)); }
 DT_D float dot_rn(float3 a, float3 b) {
-  return __fadd_rn(__fadd_rn(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)), __fmul_rn(a.z, b.z));
+  return __fmaf_rn(a.z, b.z, __fmaf_rn(a.y, b.y, __fmul_rn(a.x, b.x)));
 }
 DT_D float3 cross_rn(float3 a, float3 b) {
-  return f3(__fsub_rn(__fmul_rn(a.y, b.z), __fmul_rn(a.z, b.y)), __fsub_rn(__fmul_rn(a.z, b.x), __fmul_rn(a.x, b.z)),
-            __fsub_rn(__fmul_rn(a.x, b.y), __fmul_rn(a.y, b.x)));
+  return f3(__fmaf_rn(a.y, b.z, -__fmul_rn(a.z, b.y)), __fmaf_rn(a.z, b.x, -__fmul_rn(a.x, b.z)),
+            __fmaf_rn(a.x, b.y, -__fmul_rn(a.y, b.x)));
+}
+DT_D float rcp_approx(float x) {   // MUFU.RCP (~1 ulp): one instruction, same in every caller
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 // Moller-Trumbore (R15/R16): hit iff det != 0, u >= 0, v >= 0, u + v <= 1, t > t_lo.
@@ -110,7 +115,7 @@ DT_D bool intersect_tri(float3 o, float3 d, float3 v0, float3 e1, float3 e2, flo
   float3 p = cross_rn(d, e2);
   float det = dot_rn(e1, p);
   if (det == 0.0f) return false;
-  float inv = __frcp_rn(det);
+  float inv = rcp_approx(det);
   float3 s = sub_rn(o, v0);
   u = __fmul_rn(dot_rn(s, p), inv);
   if (!(u >= 0.0f)) return false;
