@@ -218,6 +218,7 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   if (const char* v = getenv("DT_LEAF_VOTE")) c->leaf_vote = std::max(1, std::min(32, atoi(v)));
   if (const char* v = getenv("DT_TRAV_CHUNK")) c->trav_chunk = std::max(32, atoi(v));
   if (const char* v = getenv("DT_WIDE_MODE")) c->wide_mode = std::max(0, std::min(1, atoi(v)));
+  if (const char* v = getenv("DT_PRIMARY_PACKET")) c->prim_packet = atoi(v) != 0;
   cudaError_t e;
   if ((e = cudaMalloc(&c->lvl, LV_INTS * sizeof(int))) || (e = cudaMallocHost(&c->host_lvl, LV_INTS * sizeof(int))) ||
       (e = cudaMalloc(&c->gior, 4 * sizeof(float))) || (e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long))) ||
@@ -364,6 +365,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.counters = c->counters;
   a.trav_mode = c->trav_mode;
   a.trav_chunk = c->trav_chunk;
+  a.prim_packet = c->prim_packet;
   a.leaf_vote = c->leaf_vote;
 
   // a previous asynchronous forward is checked first (its readback has long completed)

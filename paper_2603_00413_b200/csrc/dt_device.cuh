@@ -352,6 +352,97 @@ DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, 
   return T.best;
 }
 
+// Warp-packet closest hit for coherent rays (camera rays of an 8x4 pixel tile): the warp
+// walks one shared node sequence -- a child is entered if any lane's ray enters it (in the
+// order of the first active lane's entry distances), every lane tests its own ray against
+// the node boxes and leaf triangles, so each node is fetched once per warp (broadcast) and
+// the warp never diverges.  Same result as traverse() per ray: a lane's closest hit is found
+// because any box that lane enters is visited.  Must be called by all 32 lanes; inactive
+// lanes pass active = false.  wstack: this warp's shared-memory stack (kPacketStack entries).
+constexpr int kPacketStack = 96;
+DT_D int traverse_packet(const DevScene& s, float3 o, float3 d, bool active, float& bt, float& bu, float& bv,
+                         int* wstack, int& err, int& visits, int& tests) {
+  const float3 inv = safe_inv(d);
+  const unsigned amask = __ballot_sync(~0u, active);
+  int best = -1;
+  bt = kInf;
+  bu = bv = 0.f;
+  if (!amask) return -1;
+  const int leader = __ffs(amask) - 1;
+  const float tcap = active ? kInf : -1.0f;     // inactive lanes never enter a box
+  int sp = 0, cur = 0;
+  while (true) {
+    if (cur >= 0) {
+      const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)cur;
+      uint4 n0, n1, n2, n3;
+      ldg256(nd, n0, n1);
+      ldg256(nd + 2, n2, n3);
+      visits += active;
+      const int r[4] = {(int)n2.z, (int)n2.w, (int)n3.x, (int)n3.y};
+      const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
+                          exp_scale((n0.w >> 16) & 0xff) * inv.z);
+      const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
+                          (__uint_as_float(n0.z) - o.z) * inv.z);
+      float key[4];
+      unsigned hm[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int sh = 8 * c;
+        float tx0 = fmaf((float)((n1.x >> sh) & 0xff), A.x, B.x), tx1 = fmaf((float)((n1.w >> sh) & 0xff), A.x, B.x);
+        float ty0 = fmaf((float)((n1.y >> sh) & 0xff), A.y, B.y), ty1 = fmaf((float)((n2.x >> sh) & 0xff), A.y, B.y);
+        float tz0 = fmaf((float)((n1.z >> sh) & 0xff), A.z, B.z), tz1 = fmaf((float)((n2.y >> sh) & 0xff), A.z, B.z);
+        float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+        float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), fminf(bt, tcap)));
+        const bool h = tmin * 0.99999f <= tmax * 1.00001f && r[c] != kEmptyRef;
+        hm[c] = __ballot_sync(~0u, h);
+        // ordering key: the leader's entry distance; entered only by other lanes: after those;
+        // entered by nobody: +inf (dropped)
+        const float lk = __shfl_sync(~0u, h ? tmin : 3.0e38f, leader);
+        key[c] = hm[c] ? lk : kInf;
+      }
+      // warp-uniform: the entered children, nearest (leader's distance) first
+      int ord[4] = {0, 1, 2, 3};
+#pragma unroll
+      for (int i = 1; i < 4; ++i)
+#pragma unroll
+        for (int j = i; j > 0; --j)
+          if (key[ord[j]] < key[ord[j - 1]]) { int tmp = ord[j]; ord[j] = ord[j - 1]; ord[j - 1] = tmp; }
+      int list[4], ne = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (hm[ord[q]]) list[ne++] = r[ord[q]];
+      if (ne > 0) {
+        for (int q = ne - 1; q >= 1; --q) {          // farthest first: the nearest is on top
+          if (sp < kPacketStack) { if (lane_id() == 0) wstack[sp] = list[q]; } else err = 1;
+          ++sp;
+        }
+        __syncwarp();
+        cur = list[0];
+        continue;
+      }
+    } else {
+      int first, cnt;
+      leaf_range(cur, first, cnt);
+      for (int j = first; j < first + cnt; ++j) {
+        const float4* tr = s.tris + 3 * (size_t)j;
+        const float4 ta = __ldg(tr), tb = __ldg(tr + 1), tc = __ldg(tr + 2);
+        float t, u, v;
+        tests += active;
+        if (active && intersect_tri(o, d, f3(ta), f3(tb), f3(tc), 0.0f, t, u, v)) {
+          const int id = __float_as_int(ta.w);
+          if (t < bt || (t == bt && id < best)) { bt = t; bu = u; bv = v; best = id; }
+        }
+      }
+    }
+    if (sp == 0 || sp > kPacketStack) break;
+    --sp;
+    cur = wstack[sp];
+    __syncwarp();
+  }
+  if (!active) best = -1;
+  return best;
+}
+
 // triangle of ORIGINAL face f from the snapshot, with the same e1/e2 rounding as the leaves
 DT_D void face_tri(const DevScene& s, int f, int& i0, int& i1, int& i2, float3& v0, float3& e1, float3& e2) {
   i0 = __ldg(s.F + 3 * f); i1 = __ldg(s.F + 3 * f + 1); i2 = __ldg(s.F + 3 * f + 2);

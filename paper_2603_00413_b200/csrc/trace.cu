@@ -220,6 +220,8 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
 template <bool VOL>
 __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
   __shared__ int sstack[kStackShared * kTraceThreads];
+  __shared__ int pstack[(kTraceThreads / 32) * kPacketStack];
+  int* const wstack = pstack + (threadIdx.x >> 5) * kPacketStack;
   const DevScene& s = a.s;
   float3 blo = f3(s.scal[0], s.scal[1], s.scal[2]), bhi = f3(s.scal[3], s.scal[4], s.scal[5]);
   int err = 0, visits = 0, tests = 0, traced = 0;
@@ -248,14 +250,19 @@ __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
     float3 o = f3(0, 0, 0), d = f3(0, 0, 1);
     int face = -1;
     float t = 0.f, u = 0.f, v = 0.f;
+    bool inbox = false;
     if (valid) {
       camera_ray(a.K, a.c2w, a.W, a.H, pid, o, d);
       float tn;
-      bool inbox = slab(blo.x, bhi.x, blo.y, bhi.y, blo.z, bhi.z, o, safe_inv(d), kInf, tn);
-      if (inbox) {
-        ++traced;
-        face = traverse(s, o, d, 0.0f, t, u, v, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
-      }
+      inbox = slab(blo.x, bhi.x, blo.y, bhi.y, blo.z, bhi.z, o, safe_inv(d), kInf, tn);
+      traced += inbox;
+    }
+    if (a.prim_packet) {                // coherent camera rays: one node sequence per warp
+      face = traverse_packet(s, o, d, inbox, t, u, v, wstack, err, visits, tests);
+    } else if (inbox) {
+      face = traverse(s, o, d, 0.0f, t, u, v, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
+    }
+    if (valid) {
       if (face < 0) {
         float3 L = env_escape<VOL>(s, o, d, f3(0, 0, 0), nullptr, nullptr);
         a.rgb[3 * ray] = L.x; a.rgb[3 * ray + 1] = L.y; a.rgb[3 * ray + 2] = L.z;
