@@ -226,7 +226,7 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
       (e = cudaEventCreateWithFlags(&c->fwd_done, cudaEventDisableTiming)) ||
       (e = cudaMalloc(&c->scratch, 16 * sizeof(unsigned)))) {
     dt_destroy(c);
-    return DT_ERR_CUDA;
+    return e == cudaErrorMemoryAllocation ? DT_ERR_OOM : DT_ERR_CUDA;
   }
   *out = c;
   return DT_OK;
