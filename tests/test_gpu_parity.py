@@ -414,3 +414,23 @@ def test_loss_color_kernel(tracer):
     ref = (((x - c) * c) ** 2).sum() / 1000
     assert abs(float(loss) - float(ref)) < 1e-5 * float(ref)
     assert torch.allclose(g, 2 * (x - c) * c * c / 1000, atol=1e-7)
+
+
+def test_context_reuse_across_kinds(tracer):
+    """One context serving scenes of different absorption / env kinds in turn (arena lanes for
+    the volume moments appear on demand, the sigma snapshot is re-laid out) gives the same
+    results as fresh contexts."""
+    from paper_2603_00413_b200.tracer import Tracer
+    V, F = S.icosphere(2)
+    cams = T.one_view(24, 20, (0.5, 0.3, 2.7), fov_deg=55)
+    scenes = [T.scene(V, F, cams, env=T.small_grid_env(), D=3),
+              T.scene(V, F, cams, env=T.small_volume_env(), absorption=T.small_sigma_grid(V, 6), D=3),
+              T.scene(V, F, cams, env=T.lobe_env(), absorption=T.small_hash_grid(V, levels=3, log2_size=6), D=3),
+              T.scene(V, F, cams, env=T.small_grid_env(), D=3)]
+    pid = np.arange(scenes[0].n_pixels)
+    for sc in scenes:
+        g = S.upstream_grad(len(pid), 5)
+        shared = run_gpu(tracer, sc, pid, grad=g)
+        fresh = run_gpu(Tracer("cuda:0"), sc, pid, grad=g)
+        np.testing.assert_array_equal(shared["rgb"], fresh["rgb"])
+        assert rel_l2(shared["gV"], fresh["gV"]) < 1e-5 and rel_l2(shared["gsig"], fresh["gsig"]) < 1e-5
