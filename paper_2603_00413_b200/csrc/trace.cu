@@ -699,6 +699,14 @@ __global__ void __maxnreg__(DT_BWD_GRID_REGS)
     k_backward_level_grid(BwdLaunch a, int k, int max_depth, int64_t cap) {
   backward_level_body<1, VOL>(a, k, max_depth, cap);
 }
+// constant sigma, shell env: latency bound (dependent record -> child / vertex / gradient
+// fetches), so a register cap that buys occupancy pays (tools/sweep_regs.sh)
+#ifndef DT_BWD_CONST_REGS
+#define DT_BWD_CONST_REGS 80
+#endif
+__global__ void __maxnreg__(DT_BWD_CONST_REGS) k_backward_level_const(BwdLaunch a, int k, int max_depth, int64_t cap) {
+  backward_level_body<0, false>(a, k, max_depth, cap);
+}
 
 // Vertex-normal chain (reverse of P:170-173): dN -> d(sum of unit face normals) per vertex,
 // -> per face d/de1, d/de2 -> gathered back per vertex through the corner CSR.
@@ -897,7 +905,8 @@ void backward_dispatch(const BwdLaunch& a, int level, int sm_count, cudaStream_t
   static int g[2] = {0, 0};
   const bool vol = a.s.env_kind == 2;
   auto kern = ABS == 1 ? (vol ? k_backward_level_grid<true> : k_backward_level_grid<false>)
-                       : (vol ? k_backward_level<ABS, true> : k_backward_level<ABS, false>);
+               : ABS == 0 && !vol ? k_backward_level_const
+                                  : (vol ? k_backward_level<ABS, true> : k_backward_level<ABS, false>);
   if (!g[vol]) g[vol] = persistent_blocks((const void*)kern, kBwdThreads, sm_count);
   kern<<<g[vol], kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
 }
