@@ -365,12 +365,18 @@ def run_ours(args, rank, world, local_rank):
             continue
         if t.get("config") == args.config and t.get("kernel") == kname:
             traffic, traffic_src = float(t["dram_bytes_per_launch"]), os.path.relpath(f, ROOT)
+    l2 = None
+    try:                                      # L2 read bandwidth, tools/microbench/l2_bw.cu
+        l2 = float(json.load(open(os.path.join(ROOT, "profiles", "r01_l2_bandwidth.json")))["l2_read_gbs"])
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                 "note": "SURVEY 8(d) algorithmic bytes: ray in + hit out + counted node (64 B) and triangle "
                         "(48 B) fetches; the LBVH is L2-resident, so DRAM traffic (ncu, profiles/) is far lower",
                 "bytes_per_launch": int(bytes_per_launch), "ms_per_launch": round(ms_per_launch, 3),
+                "l2_read_peak_gbs": l2, "frac_of_l2": round(achieved / l2, 4) if l2 else None,
                 "share_of_step": round(ph[cls] / ms, 4)}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
