@@ -926,11 +926,12 @@ DT_D void group_transmittance_backward(const DevScene& s, const GridMap& m, floa
 
 // ----------------------------------------------------------------------------- environment
 DT_D float grid_coord(float p, float Re, int res, bool& clamped) {
-  float g = (p + Re) / (2.0f * Re) * (float)(res - 1);
-  clamped = false;
-  if (g < 0.0f) { clamped = true; return 0.0f; }
-  if (g > (float)(res - 1)) { clamped = true; return (float)(res - 1); }
-  return g;
+  // (p + Re) / (2 Re) * (res - 1), with the scale factored out (one division per texture,
+  // shared by every coordinate once inlined) and branch-free clamping
+  const float top = (float)(res - 1);
+  const float g = (p + Re) * (top / (2.0f * Re));
+  clamped = !(g >= 0.0f && g <= top);
+  return fminf(fmaxf(g, 0.0f), top);
 }
 
 DT_D float3 shell_point(const DevScene& s, float3 o, float3 dh, float& ts, float& sq) {

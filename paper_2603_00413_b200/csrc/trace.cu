@@ -707,6 +707,13 @@ __global__ void __maxnreg__(DT_BWD_GRID_REGS)
 __global__ void __maxnreg__(DT_BWD_CONST_REGS) k_backward_level_const(BwdLaunch a, int k, int max_depth, int64_t cap) {
   backward_level_body<0, false>(a, k, max_depth, cap);
 }
+// constant sigma, volumetric env: the per-sample texel Jacobians otherwise take 168 registers
+#ifndef DT_BWD_VOL_REGS
+#define DT_BWD_VOL_REGS 128
+#endif
+__global__ void __maxnreg__(DT_BWD_VOL_REGS) k_backward_level_vol(BwdLaunch a, int k, int max_depth, int64_t cap) {
+  backward_level_body<0, true>(a, k, max_depth, cap);
+}
 
 // Vertex-normal chain (reverse of P:170-173): dN -> d(sum of unit face normals) per vertex,
 // -> per face d/de1, d/de2 -> gathered back per vertex through the corner CSR.
@@ -905,8 +912,8 @@ void backward_dispatch(const BwdLaunch& a, int level, int sm_count, cudaStream_t
   static int g[2] = {0, 0};
   const bool vol = a.s.env_kind == 2;
   auto kern = ABS == 1 ? (vol ? k_backward_level_grid<true> : k_backward_level_grid<false>)
-               : ABS == 0 && !vol ? k_backward_level_const
-                                  : (vol ? k_backward_level<ABS, true> : k_backward_level<ABS, false>);
+               : ABS == 0 ? (vol ? k_backward_level_vol : k_backward_level_const)
+                          : (vol ? k_backward_level<ABS, true> : k_backward_level<ABS, false>);
   if (!g[vol]) g[vol] = persistent_blocks((const void*)kern, kBwdThreads, sm_count);
   kern<<<g[vol], kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
 }
