@@ -346,6 +346,12 @@ __global__ void __maxnreg__(DT_SHADE_GRID_REGS)
     k_shade_level_grid(FwdLaunch a, int k, int max_depth) {
   shade_level_body<1, VOL>(a, k, max_depth);
 }
+#ifndef DT_SHADE_VOL_REGS
+#define DT_SHADE_VOL_REGS 96
+#endif
+__global__ void __maxnreg__(DT_SHADE_VOL_REGS) k_shade_level_vol(FwdLaunch a, int k, int max_depth) {
+  shade_level_body<0, true>(a, k, max_depth);
+}
 
 // Traversal of level k >= 1 (K9): closest hit only, hit = (face, t, u, v) written back into
 // the record.  Lanes that finish their ray refill from the level's queue (one warp-aggregated
@@ -878,7 +884,8 @@ void shade_dispatch(const FwdLaunch& a, int level, int max_depth, int sm_count, 
   static int g[2] = {0, 0};
   const bool vol = a.s.env_kind == 2;
   auto kern = ABS == 1 ? (vol ? k_shade_level_grid<true> : k_shade_level_grid<false>)
-                       : (vol ? k_shade_level<ABS, true> : k_shade_level<ABS, false>);
+               : ABS == 0 && vol ? k_shade_level_vol
+                                 : (vol ? k_shade_level<ABS, true> : k_shade_level<ABS, false>);
   if (!g[vol]) g[vol] = persistent_blocks((const void*)kern, kTraceThreads, sm_count);
   kern<<<g[vol], kTraceThreads, 0, st>>>(a, level, max_depth);
 }
