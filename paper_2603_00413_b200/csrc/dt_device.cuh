@@ -25,8 +25,24 @@ constexpr int kWalkLanesBwd = DT_WALK_LANES_BWD;   // and backward (measured: to
 // lanes per segment walk of the hash texture, by absorption kind
 template <int ABS> struct WalkLanes { static constexpr int fwd = kWalkLanes, bwd = kWalkLanesBwd; };
 template <> struct WalkLanes<2> { static constexpr int fwd = DT_WALK_LANES_HASH, bwd = DT_WALK_LANES_HASH_BWD; };
-constexpr int kStackShared = 16;   // short stack entries per thread in shared memory
+#ifndef DT_STACK_SHARED
+#define DT_STACK_SHARED 16
+#endif
+// DT_STACK_KEYS = 1: every stack entry keeps the entry distance its parent measured, so a
+// popped node or leaf that starts beyond the current closest hit is dropped unfetched.
+#ifndef DT_STACK_KEYS
+#define DT_STACK_KEYS 0
+#endif
+// DT_PRMT_DECODE = 1: quantised box bytes become floats by a byte permute into 2^23 + q and
+// one exact subtraction (alu + fma pipes) instead of I2F.U8 (the conversion pipe)
+#ifndef DT_PRMT_DECODE
+#define DT_PRMT_DECODE 0
+#endif
+constexpr int kStackShared = DT_STACK_SHARED;   // short stack entries per thread in shared memory
 constexpr int kStackLocal = 112;   // spill entries per thread (local memory, L1-cached)
+constexpr int kStackKeys = DT_STACK_KEYS;
+constexpr int kStackWords = kStackShared * (1 + kStackKeys);   // shared ints per thread (refs, then keys)
+constexpr int kStackLocalWords = kStackLocal * (1 + kStackKeys);
 constexpr int kLeafMax = 3;        // triangles per wide-BVH leaf (a contiguous leaf-order range)
 constexpr int kEmptyRef = 0x7fffffff;
 
@@ -125,6 +141,15 @@ DT_D bool intersect_tri(float3 o, float3 d, float3 v0, float3 e1, float3 e2, flo
   t = __fmul_rn(dot_rn(e2, q), inv);
   return t > t_lo;
 }
+// The (u, v) intersect_tri computes for the same operands, bit for bit (same operation
+// sequence), for a hit whose face and t are already known (cooperative traversal).
+DT_D void tri_uv(float3 o, float3 d, float3 v0, float3 e1, float3 e2, float& u, float& v) {
+  float3 p = cross_rn(d, e2);
+  float inv = rcp_approx(dot_rn(e1, p));
+  float3 s = sub_rn(o, v0);
+  u = __fmul_rn(dot_rn(s, p), inv);
+  v = __fmul_rn(dot_rn(d, cross_rn(s, e1)), inv);
+}
 
 // ----------------------------------------------------------------------------- wide nodes
 // 64-B 4-wide node (layout in bvh.cu, k_wide_build): child c's box decodes to
@@ -199,6 +224,94 @@ DT_D void trav_init(Trav& T) {
     int tr = r##a; r##a = r##b; r##b = tr;                       \
   }
 
+// quantised plane byte c of word w as a float (exact, 0..255)
+DT_D float qbyte(unsigned w, int c) {
+#if DT_PRMT_DECODE
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | (unsigned)c)) - 8388608.0f;
+#else
+  return (float)((w >> (8 * c)) & 0xff);
+#endif
+}
+
+#ifndef DT_OCTANT
+#define DT_OCTANT 1
+#endif
+// Entry distances of the four child boxes of a 64-B wide node (kInf: missed or empty child).
+// Plane distance t = (p + q 2^e - o) / d = q * A + B with A = 2^e / d, B = (p - o) / d: one
+// FMA per plane; its rounding (~1 ulp of |p - o|) is far inside the box padding.
+// DT_OCTANT = 1: the near and far plane of each axis are picked once per node by the sign of
+// the ray direction (t is monotone in q), so a child needs one max and one min chain instead
+// of six pairwise min/max; the slab comparison tmin <= tmax * 1.000021 is the padded
+// tmin * 0.99999 <= tmax * 1.00001 with the two factors merged (slightly more permissive).
+DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, const int (&r)[4], float3 o, float3 inv, float bt,
+                    float (&key)[4]) {
+  const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
+                      exp_scale((n0.w >> 16) & 0xff) * inv.z);
+  const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
+                      (__uint_as_float(n0.z) - o.z) * inv.z);
+#if DT_OCTANT
+  const bool sx = inv.x < 0.0f, sy = inv.y < 0.0f, sz = inv.z < 0.0f;
+  const unsigned xn = sx ? n1.w : n1.x, xf = sx ? n1.x : n1.w;
+  const unsigned yn = sy ? n2.x : n1.y, yf = sy ? n1.y : n2.x;
+  const unsigned zn = sz ? n2.y : n1.z, zf = sz ? n1.z : n2.y;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float tmin = fmaxf(fmaxf(fmaf(qbyte(xn, c), A.x, B.x), fmaf(qbyte(yn, c), A.y, B.y)),
+                             fmaxf(fmaf(qbyte(zn, c), A.z, B.z), 0.0f));
+    const float tmax = fminf(fminf(fmaf(qbyte(xf, c), A.x, B.x), fmaf(qbyte(yf, c), A.y, B.y)),
+                             fminf(fmaf(qbyte(zf, c), A.z, B.z), bt));
+    key[c] = tmin <= tmax * 1.000021f && r[c] != kEmptyRef ? tmin : kInf;
+  }
+#else
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float tx0 = fmaf(qbyte(n1.x, c), A.x, B.x), tx1 = fmaf(qbyte(n1.w, c), A.x, B.x);
+    float ty0 = fmaf(qbyte(n1.y, c), A.y, B.y), ty1 = fmaf(qbyte(n2.x, c), A.y, B.y);
+    float tz0 = fmaf(qbyte(n1.z, c), A.z, B.z), tz1 = fmaf(qbyte(n2.y, c), A.z, B.z);
+    float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+    float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), bt));
+    key[c] = tmin * 0.99999f <= tmax * 1.00001f && r[c] != kEmptyRef ? tmin : kInf;   // symmetric in lo/hi
+  }
+#endif
+}
+
+// The traversal stack: entry i lives in this thread's shared column (sstack[i * stride],
+// its key at sstack[(kStackShared + i) * stride]) for i < kStackShared, else in lstack.
+DT_D void stack_push(Trav& T, int* sstack, int stride, int* lstack, int ref, float key, int& err) {
+  if (T.sp < kStackShared) {
+    sstack[T.sp * stride] = ref;
+    if (kStackKeys) sstack[(kStackShared + T.sp) * stride] = __float_as_int(key);
+  } else if (T.sp < kStackShared + kStackLocal) {
+    lstack[T.sp - kStackShared] = ref;
+    if (kStackKeys) lstack[kStackLocal + T.sp - kStackShared] = __float_as_int(key);
+  } else {
+    err = 1;
+  }
+  ++T.sp;
+}
+// Pops into T.cur the nearest remaining entry that can still hold a hit closer than T.bt (the
+// same conservative slab comparison the parent's visit made when it pushed the entry, now
+// against the current T.bt).  Returns false when the stack is exhausted.
+DT_D bool stack_pop(Trav& T, const int* sstack, int stride, const int* lstack) {
+  while (T.sp > 0) {
+    --T.sp;
+    int ref;
+    float key = 0.0f;
+    if (T.sp < kStackShared) {
+      ref = sstack[T.sp * stride];
+      if (kStackKeys) key = __int_as_float(sstack[(kStackShared + T.sp) * stride]);
+    } else {
+      ref = lstack[T.sp - kStackShared];
+      if (kStackKeys) key = __int_as_float(lstack[kStackLocal + T.sp - kStackShared]);
+    }
+    if (!kStackKeys || key * 0.99999f <= T.bt * 1.00001f) {
+      T.cur = ref;
+      return true;
+    }
+  }
+  return false;
+}
+
 // One traversal step: visit the current wide node (test its four child boxes, descend into
 // the nearest hit, push the others far-to-near) or the current leaf (test its triangles),
 // then pop when nothing was descended into.  Returns true when the ray is finished.
@@ -213,40 +326,17 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
     ldg256(nd, n0, n1);
     ldg256(nd + 2, n2, n3);
     ++visits;
-    float k0, k1, k2, k3;
     int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
-    // plane distance t = (p + q 2^e - o) / d = q * A + B with A = 2^e / d, B = (p - o) / d:
-    // one FMA per plane.  Its rounding (~1 ulp of |p - o|) is far inside the 4e-6 box pad.
-    const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
-                        exp_scale((n0.w >> 16) & 0xff) * inv.z);
-    const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
-                        (__uint_as_float(n0.z) - o.z) * inv.z);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int sh = 8 * c;
-      float tx0 = fmaf((float)((n1.x >> sh) & 0xff), A.x, B.x), tx1 = fmaf((float)((n1.w >> sh) & 0xff), A.x, B.x);
-      float ty0 = fmaf((float)((n1.y >> sh) & 0xff), A.y, B.y), ty1 = fmaf((float)((n2.x >> sh) & 0xff), A.y, B.y);
-      float tz0 = fmaf((float)((n1.z >> sh) & 0xff), A.z, B.z), tz1 = fmaf((float)((n2.y >> sh) & 0xff), A.z, B.z);
-      float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
-      float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), T.bt));
-      int rc = c == 0 ? r0 : c == 1 ? r1 : c == 2 ? r2 : r3;
-      bool h = tmin * 0.99999f <= tmax * 1.00001f && rc != kEmptyRef;   // slab test is symmetric in lo/hi
-      float key = h ? tmin : kInf;
-      if (c == 0) k0 = key; else if (c == 1) k1 = key; else if (c == 2) k2 = key; else k3 = key;
-    }
+    float key[4];
+    node_keys(n0, n1, n2, {r0, r1, r2, r3}, o, inv, T.bt, key);
+    float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
     DT_CX(0, 1) DT_CX(2, 3) DT_CX(0, 2) DT_CX(1, 3) DT_CX(1, 2)   // ascending by entry distance
     if (k0 < kInf) {
       int push[3] = {r3, r2, r1};
       float pk[3] = {k3, k2, k1};
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        if (pk[q] < kInf) {
-          if (T.sp < kStackShared) sstack[T.sp * stride] = push[q];
-          else if (T.sp < kStackShared + kStackLocal) lstack[T.sp - kStackShared] = push[q];
-          else err = 1;
-          ++T.sp;
-        }
-      }
+      for (int q = 0; q < 3; ++q)
+        if (pk[q] < kInf) stack_push(T, sstack, stride, lstack, push[q], pk[q], err);
       T.cur = r0;
       descended = true;
     }
@@ -264,11 +354,7 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
       }
     }
   }
-  if (!descended) {
-    if (T.sp == 0 || err) return true;
-    --T.sp;
-    T.cur = T.sp < kStackShared ? sstack[T.sp * stride] : lstack[T.sp - kStackShared];
-  }
+  if (!descended && (err || !stack_pop(T, sstack, stride, lstack))) return true;
   return false;
 }
 #undef DT_CX
@@ -288,37 +374,16 @@ DT_D void trav_node(const DevScene& s, float3 o, float3 inv, Trav& T, int* sstac
   ldg256(nd, n0, n1);
   ldg256(nd + 2, n2, n3);
   ++visits;
-  float k0, k1, k2, k3;
   int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
-  const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
-                      exp_scale((n0.w >> 16) & 0xff) * inv.z);
-  const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
-                      (__uint_as_float(n0.z) - o.z) * inv.z);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int sh = 8 * c;
-    float tx0 = fmaf((float)((n1.x >> sh) & 0xff), A.x, B.x), tx1 = fmaf((float)((n1.w >> sh) & 0xff), A.x, B.x);
-    float ty0 = fmaf((float)((n1.y >> sh) & 0xff), A.y, B.y), ty1 = fmaf((float)((n2.x >> sh) & 0xff), A.y, B.y);
-    float tz0 = fmaf((float)((n1.z >> sh) & 0xff), A.z, B.z), tz1 = fmaf((float)((n2.y >> sh) & 0xff), A.z, B.z);
-    float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
-    float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), T.bt));
-    int rc = c == 0 ? r0 : c == 1 ? r1 : c == 2 ? r2 : r3;
-    bool h = tmin * 0.99999f <= tmax * 1.00001f && rc != kEmptyRef;
-    float key = h ? tmin : kInf;
-    if (c == 0) k0 = key; else if (c == 1) k1 = key; else if (c == 2) k2 = key; else k3 = key;
-  }
+  float key[4];
+  node_keys(n0, n1, n2, {r0, r1, r2, r3}, o, inv, T.bt, key);
+  float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
   DT_CX2(0, 1) DT_CX2(2, 3) DT_CX2(0, 2) DT_CX2(1, 3) DT_CX2(1, 2)
   int push[3] = {r3, r2, r1};
   float pk[3] = {k3, k2, k1};
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    if (pk[q] < kInf) {
-      if (T.sp < kStackShared) sstack[T.sp * stride] = push[q];
-      else if (T.sp < kStackShared + kStackLocal) lstack[T.sp - kStackShared] = push[q];
-      else err = 1;
-      ++T.sp;
-    }
-  }
+  for (int q = 0; q < 3; ++q)
+    if (pk[q] < kInf) stack_push(T, sstack, stride, lstack, push[q], pk[q], err);
   T.cur = k0 < kInf ? r0 : kEmptyRef;
 }
 
@@ -341,7 +406,7 @@ DT_D void trav_leaf(const DevScene& s, float3 o, float3 d, float t_lo, int leaf,
 DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, float& bu, float& bv, int* sstack,
                   int stride, int& err, int& visits, int& tests) {
   float3 inv = safe_inv(d);
-  int lstack[kStackLocal];
+  int lstack[kStackLocalWords];
   Trav T;
   trav_init(T);
   while (!trav_step(s, o, d, inv, t_lo, T, sstack, stride, lstack, err, visits, tests)) {
@@ -387,10 +452,9 @@ DT_D int traverse_packet(const DevScene& s, float3 o, float3 d, bool active, flo
       unsigned hm[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int sh = 8 * c;
-        float tx0 = fmaf((float)((n1.x >> sh) & 0xff), A.x, B.x), tx1 = fmaf((float)((n1.w >> sh) & 0xff), A.x, B.x);
-        float ty0 = fmaf((float)((n1.y >> sh) & 0xff), A.y, B.y), ty1 = fmaf((float)((n2.x >> sh) & 0xff), A.y, B.y);
-        float tz0 = fmaf((float)((n1.z >> sh) & 0xff), A.z, B.z), tz1 = fmaf((float)((n2.y >> sh) & 0xff), A.z, B.z);
+        float tx0 = fmaf(qbyte(n1.x, c), A.x, B.x), tx1 = fmaf(qbyte(n1.w, c), A.x, B.x);
+        float ty0 = fmaf(qbyte(n1.y, c), A.y, B.y), ty1 = fmaf(qbyte(n2.x, c), A.y, B.y);
+        float tz0 = fmaf(qbyte(n1.z, c), A.z, B.z), tz1 = fmaf(qbyte(n2.y, c), A.z, B.z);
         float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
         float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), fminf(bt, tcap)));
         const bool h = tmin * 0.99999f <= tmax * 1.00001f && r[c] != kEmptyRef;
