@@ -218,6 +218,8 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   if (const char* v = getenv("DT_LEAF_VOTE")) c->leaf_vote = std::max(1, std::min(32, atoi(v)));
   if (const char* v = getenv("DT_TRAV_CHUNK")) c->trav_chunk = std::max(32, atoi(v));
   if (const char* v = getenv("DT_FLUSH_TASKS")) c->flush_tasks = std::max(1, std::min(32, atoi(v)));
+  if (const char* v = getenv("DT_REFILL_K")) c->refill_k = std::max(1, std::min(32, atoi(v)));
+  if (const char* v = getenv("DT_STEP_LOOP")) c->step_budget = std::max(1, atoi(v));
   if (const char* v = getenv("DT_WIDE_MODE")) c->wide_mode = std::max(0, std::min(1, atoi(v)));
   if (const char* v = getenv("DT_PRIMARY_PACKET")) c->prim_packet = atoi(v) != 0;
   cudaError_t e;
@@ -369,6 +371,8 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.prim_packet = c->prim_packet;
   a.leaf_vote = c->leaf_vote;
   a.flush_tasks = c->flush_tasks;
+  a.refill_k = c->refill_k;
+  a.step_budget = c->step_budget;
 
   // a previous asynchronous forward is checked first (its readback has long completed)
   dt_status prev = consume_async(c);

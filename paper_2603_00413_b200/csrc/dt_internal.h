@@ -62,6 +62,7 @@ struct FwdLaunch {
   unsigned long long* counters;   // [0] node visits, [1] triangle tests
   int trav_mode, trav_chunk, leaf_vote;
   int flush_tasks;      // mode 4: tasks that trigger a cooperative leaf flush (<= 32)
+  int refill_k, step_budget;   // mode 1: refill once refill_k lanes wait (32: after kStepBudget steps)
   int prim_packet;      // camera rays: warp-packet traversal (traverse_packet)
 };
 
@@ -156,6 +157,8 @@ struct dt_ctx {
   int trav_chunk = 256;       // rays per warp chunk (mode 2)
   int leaf_vote = 32;         // mode 3: lanes that must be ready before a warp leaf phase
   int flush_tasks = 32;       // mode 4: leaf tasks that trigger a warp-cooperative flush
+  int refill_k = 32;          // mode 1: lanes waiting for a ray that end the step loop early
+  int step_budget = 64;       // mode 1 with refill_k < 32: step loop length
   // profiling (dt_set_profiling / dt_get_profile)
   bool prof = false;
   double ph_ms[DT_PH_COUNT] = {};

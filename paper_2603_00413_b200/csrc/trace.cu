@@ -427,10 +427,19 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
       }
     }
     if (__all_sync(~0u, item >= n)) break;
-    if (item < 0 || item >= n) continue;
+    const bool live = item >= 0 && item < n;
     bool done = false;
-    for (int step = 0; step < kStepBudget && !done; ++step)
-      done = trav_step(s, o, d, inv, t_lo, T, sstack, kTraceThreads, lstack, err, visits, tests);
+    if (a.refill_k >= 32) {
+      if (live)
+        for (int step = 0; step < kStepBudget && !done; ++step)
+          done = trav_step(s, o, d, inv, t_lo, T, sstack, kTraceThreads, lstack, err, visits, tests);
+    } else {
+      // early refill: leave the step loop (warp-uniformly) once refill_k lanes wait for a ray
+      for (int step = 0; step < a.step_budget; ++step) {
+        if (live && !done) done = trav_step(s, o, d, inv, t_lo, T, sstack, kTraceThreads, lstack, err, visits, tests);
+        if (__popc(__ballot_sync(~0u, done || item < 0)) >= a.refill_k) break;
+      }
+    }
     if (done) {
       __stcs(a.r.hit + off + item, make_float4(__int_as_float(T.best), T.bt, T.bu, T.bv));
       item = -1;

@@ -16,3 +16,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sh
 echo "ncu shade rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_backward_level -s 16 -c 1 -o gpurun_out/${T}_bwd $B > gpurun_out/${T}_ncu3.log 2>&1
 echo "ncu bwd rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_trace_primary -s 4 -c 1 -o gpurun_out/${T}_primary $B > gpurun_out/${T}_ncu4.log 2>&1
+echo "ncu primary rc=$?"
