@@ -219,6 +219,7 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   if (const char* v = getenv("DT_TRAV_CHUNK")) c->trav_chunk = std::max(32, atoi(v));
   if (const char* v = getenv("DT_FLUSH_TASKS")) c->flush_tasks = std::max(1, std::min(32, atoi(v)));
   if (const char* v = getenv("DT_REFILL_K")) c->refill_k = std::max(1, std::min(32, atoi(v)));
+  if (const char* v = getenv("DT_SORT_LANES")) c->sort_lanes = atoi(v) != 0;
   if (const char* v = getenv("DT_STEP_LOOP")) c->step_budget = std::max(1, atoi(v));
   if (const char* v = getenv("DT_WIDE_MODE")) c->wide_mode = std::max(0, std::min(1, atoi(v)));
   if (const char* v = getenv("DT_PRIMARY_PACKET")) c->prim_packet = atoi(v) != 0;
@@ -372,6 +373,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.leaf_vote = c->leaf_vote;
   a.flush_tasks = c->flush_tasks;
   a.refill_k = c->refill_k;
+  a.sort_lanes = c->sort_lanes;
   a.step_budget = c->step_budget;
 
   // a previous asynchronous forward is checked first (its readback has long completed)
@@ -496,6 +498,7 @@ dt_status dt_trace_backward(dt_ctx* c, const float* grad_rgb, float* grad_V, flo
   DT_CU(cudaMemsetAsync(c->gior, 0, sizeof(float), st));
   BwdLaunch b{};
   b.s = c->fwd_scene;
+  b.sort_lanes = c->sort_lanes;
   b.r = c->rec;
   b.lvl = c->lvl;
   b.cap = c->arena_cap;

@@ -63,6 +63,7 @@ struct FwdLaunch {
   int trav_mode, trav_chunk, leaf_vote;
   int flush_tasks;      // mode 4: tasks that trigger a cooperative leaf flush (<= 32)
   int refill_k, step_budget;   // mode 1: refill once refill_k lanes wait (32: after kStepBudget steps)
+  int sort_lanes;       // shade: hit-first lane order over 64-record windows
   int prim_packet;      // camera rays: warp-packet traversal (traverse_packet)
 };
 
@@ -77,6 +78,7 @@ struct BwdLaunch {
   float4* dN;       // [nv] vertex-normal adjoints (atomics)
   float4* dsig;     // [1] or [R^3] (rgb + pad)
   float* dior;      // [1]
+  int sort_lanes;   // hit-first lane order over 64-record windows
 };
 
 }  // namespace dt
@@ -159,6 +161,7 @@ struct dt_ctx {
   int flush_tasks = 32;       // mode 4: leaf tasks that trigger a warp-cooperative flush
   int refill_k = 32;          // mode 1: lanes waiting for a ray that end the step loop early
   int step_budget = 64;       // mode 1 with refill_k < 32: step loop length
+  int sort_lanes = 1;         // shade / backward: hit-first lane order (DT_SORT_LANES)
   // profiling (dt_set_profiling / dt_get_profile)
   bool prof = false;
   double ph_ms[DT_PH_COUNT] = {};

@@ -68,6 +68,30 @@ DT_D int fetch_work(int* counter) {
   return __shfl_sync(~0u, base, 0);
 }
 
+// Hit-first lane order over a warp's window of 64 records (2 rounds of 32): records of class
+// 0 (a traced hit: interface path) first, then class 1 (a miss: environment path), then class 2
+// (nothing to do).  The per-record code has two long, disjoint paths, so warps that mix them
+// run both at half width; sorted, round 0 and round 1 are (nearly) uniform.  cA / cB: class of
+// window offsets lane and 32 + lane; returns the offsets this lane processes in the two rounds.
+// slot: the warp's 64 bytes of shared memory.
+DT_D void hit_first_order(int cA, int cB, unsigned char* slot, int& r0, int& r1) {
+  const unsigned lt = lanemask_lt();
+  const unsigned a0 = __ballot_sync(~0u, cA == 0), b0 = __ballot_sync(~0u, cB == 0);
+  const unsigned a1 = __ballot_sync(~0u, cA == 1), b1 = __ballot_sync(~0u, cB == 1);
+  const unsigned a2 = __ballot_sync(~0u, cA == 2), b2 = __ballot_sync(~0u, cB == 2);
+  const int n0 = __popc(a0) + __popc(b0), n1 = __popc(a1) + __popc(b1);
+  const int rA = cA == 0 ? __popc(a0 & lt) : cA == 1 ? n0 + __popc(a1 & lt) : n0 + n1 + __popc(a2 & lt);
+  const int rB = cB == 0 ? __popc(a0) + __popc(b0 & lt)
+               : cB == 1 ? n0 + __popc(a1) + __popc(b1 & lt)
+                         : n0 + n1 + __popc(a2) + __popc(b2 & lt);
+  slot[rA] = (unsigned char)lane_id();
+  slot[rB] = (unsigned char)(32 + lane_id());
+  __syncwarp();
+  r0 = slot[lane_id()];
+  r1 = slot[32 + lane_id()];
+  __syncwarp();
+}
+
 // first record index of level k >= 1
 DT_D int64_t level_base(const int* lvl, int k) {
   int64_t off = 0;
@@ -313,11 +337,26 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   constexpr bool kDyn = ABS != 0 || VOL;
   int* const ctr = a.lvl + LV_WORK_SHADE + k;
-  int64_t wbase = kDyn ? (int64_t)fetch_work(ctr) : blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31);
+  __shared__ unsigned char sslot[kTraceThreads * 2];
+  const bool sorted = !kDyn && a.sort_lanes;   // static striding over 64-record windows, hit-first
+  const int64_t wstep = sorted ? 2 * stride : stride;
+  int64_t wbase = kDyn ? (int64_t)fetch_work(ctr)
+                       : (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * (sorted ? 2 : 1);
+  int round = 0, ord0 = 0, ord1 = 0;
   while (wbase < n) {
     int next = 0;
     if (kDyn && lane_id() == 0) next = atomicAdd(ctr, 32);
-    const int64_t item = wbase + lane_id();
+    if (sorted && round == 0) {
+      int c[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t it = wbase + 32 * h + lane_id();
+        c[h] = 2;
+        if (it < n) c[h] = __float_as_int(a.r.hit[k == 0 ? a.cap - 1 - it : off + it].x) >= 0 ? 0 : 1;
+      }
+      hit_first_order(c[0], c[1], sslot + 2 * (threadIdx.x & ~31), ord0, ord1);
+    }
+    const int64_t item = wbase + (sorted ? (round == 0 ? ord0 : ord1) : lane_id());
     const bool valid = item < n;
     const int64_t idx = k == 0 ? a.cap - 1 - item : off + item;
     float3 o = f3(0, 0, 0), d = f3(0, 0, 1), thr = f3(0, 0, 0);
@@ -334,7 +373,12 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
       face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
     }
     shade_and_spawn<ABS, VOL>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
-    wbase = kDyn ? (int64_t)__shfl_sync(~0u, next, 0) : wbase + stride;
+    if (sorted) {
+      round ^= 1;
+      if (round == 0) wbase += wstep;
+    } else {
+      wbase = kDyn ? (int64_t)__shfl_sync(~0u, next, 0) : wbase + stride;
+    }
   }
 }
 
@@ -730,8 +774,26 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
   float gior = 0.0f;
   float3 gsc = f3(0, 0, 0);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t wbase = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); wbase < n; wbase += stride) {
-    const int64_t item = wbase + lane_id();
+  __shared__ unsigned char sslot[kBwdThreads * 2];
+  const bool sorted = a.sort_lanes;   // 64-record windows, interface (hit) records first
+  const int per = sorted ? 2 : 1;
+  for (int64_t wb = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * per; wb < n; wb += stride * per) {
+  int o0 = lane_id(), o1 = 32 + lane_id();
+  if (sorted) {
+    int c[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t it = wb + 32 * h + lane_id();
+      c[h] = 2;
+      if (it < n) {
+        const int f = __float_as_int(a.r.hit[k == 0 ? cap - 1 - it : off + it].w);
+        c[h] = (f & RF_MISS) ? 1 : ((f & RF_CAPPED) && s.cap_policy == 0 && !VOL) ? 2 : 0;
+      }
+    }
+    hit_first_order(c[0], c[1], sslot + 2 * (threadIdx.x & ~31), o0, o1);
+  }
+  for (int round = 0; round < per; ++round) {
+    const int64_t item = wb + (round == 0 ? o0 : o1);
     const bool valid = item < n;
     int64_t idx = 0;
     float3 o = f3(0, 0, 0), d = f3(0, 0, 1), x = o, gS = o;
@@ -841,6 +903,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
       a.r.go[idx] = f4(go, 0.f);
       a.r.gd[idx] = f4(gd, 0.f);
     }
+  }
   }
   // warp reductions of the scalar adjoints
   for (int o = 16; o > 0; o >>= 1) {
