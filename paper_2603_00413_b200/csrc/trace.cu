@@ -62,9 +62,9 @@ constexpr int kBwdThreads = 128;
 #define DT_BWD_GRID_REGS 128
 #endif
 
-DT_D int fetch_work(int* counter) {
+DT_D int fetch_work(int* counter, int chunk = 32) {
   int base = 0;
-  if (lane_id() == 0) base = atomicAdd(counter, 32);
+  if (lane_id() == 0) base = atomicAdd(counter, chunk);
   return __shfl_sync(~0u, base, 0);
 }
 
@@ -338,14 +338,14 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
   constexpr bool kDyn = ABS != 0 || VOL;
   int* const ctr = a.lvl + LV_WORK_SHADE + k;
   __shared__ unsigned char sslot[kTraceThreads * 2];
-  const bool sorted = !kDyn && a.sort_lanes;   // static striding over 64-record windows, hit-first
+  const bool sorted = a.sort_lanes;   // 64-record windows, hit-first (two rounds of 32)
+  const int chunk = sorted ? 64 : 32;
   const int64_t wstep = sorted ? 2 * stride : stride;
-  int64_t wbase = kDyn ? (int64_t)fetch_work(ctr)
+  int64_t wbase = kDyn ? (int64_t)fetch_work(ctr, chunk)
                        : (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * (sorted ? 2 : 1);
-  int round = 0, ord0 = 0, ord1 = 0;
+  int round = 0, ord0 = 0, ord1 = 0, next = 0;
   while (wbase < n) {
-    int next = 0;
-    if (kDyn && lane_id() == 0) next = atomicAdd(ctr, 32);
+    if (round == 0 && kDyn && lane_id() == 0) next = atomicAdd(ctr, chunk);
     if (sorted && round == 0) {
       int c[2];
 #pragma unroll
@@ -373,11 +373,11 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
       face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
     }
     shade_and_spawn<ABS, VOL>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
-    if (sorted) {
-      round ^= 1;
-      if (round == 0) wbase += wstep;
+    if (sorted && round == 0) {
+      round = 1;
     } else {
-      wbase = kDyn ? (int64_t)__shfl_sync(~0u, next, 0) : wbase + stride;
+      round = 0;
+      wbase = kDyn ? (int64_t)__shfl_sync(~0u, next, 0) : wbase + wstep;
     }
   }
 }
