@@ -242,6 +242,12 @@ DT_D float qbyte(unsigned w, int c) {
 #ifndef DT_FFMA2
 #define DT_FFMA2 0
 #endif
+// DT_TLO_CULL = 1: a child box the ray leaves before t_lo (R17) cannot hold a hit: its entry
+// distance is clamped at t_lo instead of 0 (secondary rays skip the thin boxes of the surface
+// they start on)
+#ifndef DT_TLO_CULL
+#define DT_TLO_CULL 1
+#endif
 // packed fp32 pairs (sm_100 FFMA2): per-element IEEE fma
 DT_D unsigned long long f2pack(float a, float b) {
   unsigned long long r;
@@ -257,12 +263,13 @@ DT_D unsigned long long ffma2(unsigned long long a, unsigned long long b, unsign
 // Entry distances of the four child boxes of a 64-B wide node (kInf: missed or empty child).
 // Plane distance t = (p + q 2^e - o) / d = q * A + B with A = 2^e / d, B = (p - o) / d: one
 // FMA per plane; its rounding (~1 ulp of |p - o|) is far inside the box padding.
+// tlo: entry distances are clamped at tlo (a box exited before tlo is missed).
 // DT_OCTANT = 1: the near and far plane of each axis are picked once per node by the sign of
 // the ray direction (t is monotone in q), so a child needs one max and one min chain instead
 // of six pairwise min/max; the slab comparison tmin <= tmax * 1.000021 is the padded
 // tmin * 0.99999 <= tmax * 1.00001 with the two factors merged (slightly more permissive).
 DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, const int (&r)[4], float3 o, float3 inv, float bt,
-                    float (&key)[4]) {
+                    float (&key)[4], float tlo = 0.0f) {
   const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
                       exp_scale((n0.w >> 16) & 0xff) * inv.z);
 #if DT_B_FMA
@@ -292,7 +299,7 @@ DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, const int (&r)[4], float3 o, f
     f2unpack(ffma2(f2pack(qbyte(xf, c), qbyte(xf, c + 1)), Ax, Bx), xf0, xf1);
     f2unpack(ffma2(f2pack(qbyte(yf, c), qbyte(yf, c + 1)), Ay, By), yf0, yf1);
     f2unpack(ffma2(f2pack(qbyte(zf, c), qbyte(zf, c + 1)), Az, Bz), zf0, zf1);
-    const float tmin0 = fmaxf(fmaxf(xn0, yn0), fmaxf(zn0, 0.0f)), tmin1 = fmaxf(fmaxf(xn1, yn1), fmaxf(zn1, 0.0f));
+    const float tmin0 = fmaxf(fmaxf(xn0, yn0), fmaxf(zn0, tlo)), tmin1 = fmaxf(fmaxf(xn1, yn1), fmaxf(zn1, tlo));
     const float tmax0 = fminf(fminf(xf0, yf0), fminf(zf0, bt)), tmax1 = fminf(fminf(xf1, yf1), fminf(zf1, bt));
     key[c] = tmin0 <= tmax0 * 1.000021f && r[c] != kEmptyRef ? tmin0 : kInf;
     key[c + 1] = tmin1 <= tmax1 * 1.000021f && r[c + 1] != kEmptyRef ? tmin1 : kInf;
@@ -301,7 +308,7 @@ DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, const int (&r)[4], float3 o, f
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const float tmin = fmaxf(fmaxf(fmaf(qbyte(xn, c), A.x, B.x), fmaf(qbyte(yn, c), A.y, B.y)),
-                             fmaxf(fmaf(qbyte(zn, c), A.z, B.z), 0.0f));
+                             fmaxf(fmaf(qbyte(zn, c), A.z, B.z), tlo));
     const float tmax = fminf(fminf(fmaf(qbyte(xf, c), A.x, B.x), fmaf(qbyte(yf, c), A.y, B.y)),
                              fminf(fmaf(qbyte(zf, c), A.z, B.z), bt));
     key[c] = tmin <= tmax * 1.000021f && r[c] != kEmptyRef ? tmin : kInf;
@@ -373,7 +380,7 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
     ++visits;
     int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
     float key[4];
-    node_keys(n0, n1, n2, {r0, r1, r2, r3}, o, inv, T.bt, key);
+    node_keys(n0, n1, n2, {r0, r1, r2, r3}, o, inv, T.bt, key, DT_TLO_CULL ? t_lo : 0.0f);
     float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
     DT_CX(0, 1) DT_CX(2, 3) DT_CX(0, 2) DT_CX(1, 3) DT_CX(1, 2)   // ascending by entry distance
     if (k0 < kInf) {
