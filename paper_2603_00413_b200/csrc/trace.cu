@@ -92,6 +92,22 @@ DT_D void hit_first_order(int cA, int cB, unsigned char* slot, int& r0, int& r1)
   __syncwarp();
 }
 
+// L2 prefetch (bulk, no registers) of a window of records [first, first + cnt) of level k:
+// the record lanes the next window's first pass reads.  Level 0 is stored reversed.
+#ifndef DT_PREFETCH
+#define DT_PREFETCH 0
+#endif
+DT_D void prefetch_l2(const float4* p, int cnt) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(cnt * 16) : "memory");
+}
+template <int NL>
+DT_D void prefetch_window(float4* const (&lanes)[NL], int k, int64_t cap, int64_t off, int64_t first, int n) {
+  if (!DT_PREFETCH || first >= n || lane_id() >= NL) return;
+  const int cnt = (int)(n - first < 64 ? n - first : 64);
+  const int64_t base = k == 0 ? cap - first - cnt : off + first;   // lowest record index of the window
+  prefetch_l2(lanes[lane_id()] + base, cnt);
+}
+
 // first record index of level k >= 1
 DT_D int64_t level_base(const int* lvl, int k) {
   int64_t off = 0;
@@ -347,6 +363,10 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
   while (wbase < n) {
     if (round == 0 && kDyn && lane_id() == 0) next = atomicAdd(ctr, chunk);
     if (sorted && round == 0) {
+      if (!kDyn) {
+        float4* const lanes[4] = {a.r.o, a.r.d, a.r.thr, a.r.hit};
+        prefetch_window<4>(lanes, k, a.cap, off, wbase + wstep, n);
+      }
       int c[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -780,6 +800,8 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
   for (int64_t wb = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * per; wb < n; wb += stride * per) {
   int o0 = lane_id(), o1 = 32 + lane_id();
   if (sorted) {
+    float4* const lanes[6] = {a.r.o, a.r.d, a.r.thr, a.r.hit, a.r.tau, a.r.lsub};
+    prefetch_window<6>(lanes, k, cap, off, wb + stride * per, n);
     int c[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
