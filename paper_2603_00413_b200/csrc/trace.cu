@@ -56,10 +56,10 @@ constexpr int kBwdThreads = 128;
 // register caps of the sigma-grid kernels (k_*_grid: their cooperative walks inflate the
 // allocation; measured: tools/sweep_regs.sh)
 #ifndef DT_SHADE_GRID_REGS
-#define DT_SHADE_GRID_REGS 96
+#define DT_SHADE_GRID_REGS 80
 #endif
 #ifndef DT_BWD_GRID_REGS
-#define DT_BWD_GRID_REGS 128
+#define DT_BWD_GRID_REGS 96
 #endif
 
 DT_D int fetch_work(int* counter, int chunk = 32) {
