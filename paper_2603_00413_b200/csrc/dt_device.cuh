@@ -119,9 +119,18 @@ DT_D float3 cross_rn(float3 a, float3 b) {
   return f3(__fmaf_rn(a.y, b.z, -__fmul_rn(a.z, b.y)), __fmaf_rn(a.z, b.x, -__fmul_rn(a.x, b.z)),
             __fmaf_rn(a.x, b.y, -__fmul_rn(a.y, b.x)));
 }
+#ifndef DT_RCP_FTZ
+#define DT_RCP_FTZ 1
+#endif
 DT_D float rcp_approx(float x) {   // MUFU.RCP (~1 ulp): one instruction, same in every caller
   float r;
+#if DT_RCP_FTZ
+  // a subnormal determinant (|det| < 2^-126) is flushed to 0: rcp = inf, the test then rejects
+  // (no degenerate triangle of the inputs comes near; saves the subnormal rescaling)
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+#else
   asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+#endif
   return r;
 }
 
@@ -395,8 +404,8 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
   } else {
     int first, cnt;
     leaf_range(T.cur, first, cnt);
-    for (int j = first; j < first + cnt; ++j) {
-      const float4* tr = s.tris + 3 * (size_t)j;
+    const float4* tr = s.tris + 3 * (size_t)first;
+    do {                                            // a leaf holds 1..kLeafMax triangles
       float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
       float t, u, v;
       ++tests;
@@ -404,7 +413,8 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
         int id = __float_as_int(a.w);
         if (t < T.bt || (t == T.bt && id < T.best)) { T.bt = t; T.bu = u; T.bv = v; T.best = id; }
       }
-    }
+      tr += 3;
+    } while (--cnt > 0);
   }
   if (!descended && (err || !stack_pop(T, sstack, stride, lstack))) return true;
   return false;
