@@ -257,6 +257,11 @@ DT_D float qbyte(unsigned w, int c) {
 #ifndef DT_TLO_CULL
 #define DT_TLO_CULL 1
 #endif
+// DT_PACKED_SORT = 1: trav_step orders the children on packed (distance bits | slot) keys with
+// integer min/max (2 instructions per compare-exchange instead of a compare and four selects)
+#ifndef DT_PACKED_SORT
+#define DT_PACKED_SORT 0
+#endif
 // packed fp32 pairs (sm_100 FFMA2): per-element IEEE fma
 DT_D unsigned long long f2pack(float a, float b) {
   unsigned long long r;
@@ -390,6 +395,26 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
     int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
     float key[4];
     node_keys(n0, n1, n2, {r0, r1, r2, r3}, o, inv, T.bt, key, DT_TLO_CULL ? t_lo : 0.0f);
+#if DT_PACKED_SORT
+    // ascending by entry distance on packed keys: the distance's bits with the child slot in the
+    // two low bits (keys are >= 0, so their bit patterns order like the floats; a miss is +inf
+    // = 0x7f800000 | slot), sorted with integer min/max; the ref is looked up by the slot
+    unsigned p0 = (__float_as_uint(key[0]) & ~3u), p1 = (__float_as_uint(key[1]) & ~3u) | 1u;
+    unsigned p2 = (__float_as_uint(key[2]) & ~3u) | 2u, p3 = (__float_as_uint(key[3]) & ~3u) | 3u;
+#define DT_UCX(a, b) { const unsigned lo_ = min(a, b), hi_ = max(a, b); a = lo_; b = hi_; }
+    DT_UCX(p0, p1) DT_UCX(p2, p3) DT_UCX(p0, p2) DT_UCX(p1, p3) DT_UCX(p1, p2)
+#undef DT_UCX
+    constexpr unsigned kMissKey = 0x7f800000u;
+    auto ref_of = [&](unsigned p) { return (p & 2u) ? ((p & 1u) ? r3 : r2) : ((p & 1u) ? r1 : r0); };
+    if (p0 < kMissKey) {
+      const unsigned pq[3] = {p3, p2, p1};
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (pq[q] < kMissKey) stack_push(T, sstack, stride, lstack, ref_of(pq[q]), __uint_as_float(pq[q] & ~3u), err);
+      T.cur = ref_of(p0);
+      descended = true;
+    }
+#else
     float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
     DT_CX(0, 1) DT_CX(2, 3) DT_CX(0, 2) DT_CX(1, 3) DT_CX(1, 2)   // ascending by entry distance
     if (k0 < kInf) {
@@ -401,6 +426,7 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
       T.cur = r0;
       descended = true;
     }
+#endif
   } else {
     int first, cnt;
     leaf_range(T.cur, first, cnt);
