@@ -262,6 +262,11 @@ DT_D float qbyte(unsigned w, int c) {
 #ifndef DT_PACKED_SORT
 #define DT_PACKED_SORT 0
 #endif
+// DT_NEAREST_ONLY = 1: trav_step only selects the nearest hit child (3 compares); the other hit
+// children are pushed in slot order instead of far-to-near
+#ifndef DT_NEAREST_ONLY
+#define DT_NEAREST_ONLY 0
+#endif
 // packed fp32 pairs (sm_100 FFMA2): per-element IEEE fma
 DT_D unsigned long long f2pack(float a, float b) {
   unsigned long long r;
@@ -395,7 +400,22 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
     int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
     float key[4];
     node_keys(n0, n1, n2, {r0, r1, r2, r3}, o, inv, T.bt, key, DT_TLO_CULL ? t_lo : 0.0f);
-#if DT_PACKED_SORT
+#if DT_NEAREST_ONLY
+    // descend into the nearest hit child; push the other hit children unsorted (slot order)
+    float kn = key[0];
+    int rn = r0, sn = 0;
+    if (key[1] < kn) { kn = key[1]; rn = r1; sn = 1; }
+    if (key[2] < kn) { kn = key[2]; rn = r2; sn = 2; }
+    if (key[3] < kn) { kn = key[3]; rn = r3; sn = 3; }
+    if (kn < kInf) {
+      const int rr[4] = {r0, r1, r2, r3};
+#pragma unroll
+      for (int q = 3; q >= 0; --q)
+        if (q != sn && key[q] < kInf) stack_push(T, sstack, stride, lstack, rr[q], key[q], err);
+      T.cur = rn;
+      descended = true;
+    }
+#elif DT_PACKED_SORT
     // ascending by entry distance on packed keys: the distance's bits with the child slot in the
     // two low bits (keys are >= 0, so their bit patterns order like the floats; a miss is +inf
     // = 0x7f800000 | slot), sorted with integer min/max; the ref is looked up by the slot
