@@ -9,7 +9,7 @@ namespace dt {
 
 constexpr float kInf = __builtin_huge_valf();
 #ifndef DT_WALK_LANES
-#define DT_WALK_LANES 8
+#define DT_WALK_LANES 4
 #endif
 #ifndef DT_WALK_LANES_BWD
 #define DT_WALK_LANES_BWD 4
