@@ -214,13 +214,10 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   cudaSetDevice(device);
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (const char* v = getenv("DT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(4, atoi(v)));
-  if (const char* v = getenv("DT_TRAV_MODE")) c->trav_mode = std::max(0, std::min(4, atoi(v)));
+  if (const char* v = getenv("DT_TRAV_MODE")) c->trav_mode = std::max(0, std::min(3, atoi(v)));
   if (const char* v = getenv("DT_LEAF_VOTE")) c->leaf_vote = std::max(1, std::min(32, atoi(v)));
   if (const char* v = getenv("DT_TRAV_CHUNK")) c->trav_chunk = std::max(32, atoi(v));
-  if (const char* v = getenv("DT_FLUSH_TASKS")) c->flush_tasks = std::max(1, std::min(32, atoi(v)));
-  if (const char* v = getenv("DT_REFILL_K")) c->refill_k = std::max(1, std::min(32, atoi(v)));
   if (const char* v = getenv("DT_SORT_LANES")) c->sort_lanes = atoi(v) != 0;
-  if (const char* v = getenv("DT_STEP_LOOP")) c->step_budget = std::max(1, atoi(v));
   if (const char* v = getenv("DT_WIDE_MODE")) c->wide_mode = std::max(0, std::min(1, atoi(v)));
   if (const char* v = getenv("DT_PRIMARY_PACKET")) c->prim_packet = atoi(v) != 0;
   cudaError_t e;
@@ -371,10 +368,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.trav_chunk = c->trav_chunk;
   a.prim_packet = c->prim_packet;
   a.leaf_vote = c->leaf_vote;
-  a.flush_tasks = c->flush_tasks;
-  a.refill_k = c->refill_k;
   a.sort_lanes = c->sort_lanes;
-  a.step_budget = c->step_budget;
 
   // a previous asynchronous forward is checked first (its readback has long completed)
   dt_status prev = consume_async(c);

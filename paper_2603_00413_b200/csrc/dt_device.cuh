@@ -25,24 +25,8 @@ constexpr int kWalkLanesBwd = DT_WALK_LANES_BWD;   // and backward (measured: to
 // lanes per segment walk of the hash texture, by absorption kind
 template <int ABS> struct WalkLanes { static constexpr int fwd = kWalkLanes, bwd = kWalkLanesBwd; };
 template <> struct WalkLanes<2> { static constexpr int fwd = DT_WALK_LANES_HASH, bwd = DT_WALK_LANES_HASH_BWD; };
-#ifndef DT_STACK_SHARED
-#define DT_STACK_SHARED 16
-#endif
-// DT_STACK_KEYS = 1: every stack entry keeps the entry distance its parent measured, so a
-// popped node or leaf that starts beyond the current closest hit is dropped unfetched.
-#ifndef DT_STACK_KEYS
-#define DT_STACK_KEYS 0
-#endif
-// DT_PRMT_DECODE = 1: quantised box bytes become floats by a byte permute into 2^23 + q and
-// one exact subtraction (alu + fma pipes) instead of I2F.U8 (the conversion pipe)
-#ifndef DT_PRMT_DECODE
-#define DT_PRMT_DECODE 0
-#endif
-constexpr int kStackShared = DT_STACK_SHARED;   // short stack entries per thread in shared memory
+constexpr int kStackShared = 16;   // short stack entries per thread in shared memory
 constexpr int kStackLocal = 112;   // spill entries per thread (local memory, L1-cached)
-constexpr int kStackKeys = DT_STACK_KEYS;
-constexpr int kStackWords = kStackShared * (1 + kStackKeys);   // shared ints per thread (refs, then keys)
-constexpr int kStackLocalWords = kStackLocal * (1 + kStackKeys);
 constexpr int kLeafMax = 3;        // triangles per wide-BVH leaf (a contiguous leaf-order range)
 constexpr int kEmptyRef = 0x7fffffff;
 
@@ -151,7 +135,7 @@ DT_D bool intersect_tri(float3 o, float3 d, float3 v0, float3 e1, float3 e2, flo
   return t > t_lo;
 }
 // The (u, v) intersect_tri computes for the same operands, bit for bit (same operation
-// sequence), for a hit whose face and t are already known (cooperative traversal).
+// sequence), for a hit whose face and t are already known (the shade pass).
 DT_D void tri_uv(float3 o, float3 d, float3 v0, float3 e1, float3 e2, float& u, float& v) {
   float3 p = cross_rn(d, e2);
   float inv = rcp_approx(dot_rn(e1, p));
@@ -233,97 +217,33 @@ DT_D void trav_init(Trav& T) {
     int tr = r##a; r##a = r##b; r##b = tr;                       \
   }
 
-// quantised plane byte c of word w as a float (exact, 0..255)
-DT_D float qbyte(unsigned w, int c) {
-#if DT_PRMT_DECODE
-  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | (unsigned)c)) - 8388608.0f;
-#else
-  return (float)((w >> (8 * c)) & 0xff);
-#endif
-}
+// quantised plane byte c of word w as a float (exact, 0..255; I2F.U8 with a byte select)
+DT_D float qbyte(unsigned w, int c) { return (float)((w >> (8 * c)) & 0xff); }
 
-#ifndef DT_OCTANT
-#define DT_OCTANT 1
-#endif
-#ifndef DT_B_FMA
-#define DT_B_FMA 0
-#endif
-#ifndef DT_FFMA2
-#define DT_FFMA2 0
-#endif
 // DT_TLO_CULL = 1: a child box the ray leaves before t_lo (R17) cannot hold a hit: its entry
 // distance is clamped at t_lo instead of 0 (secondary rays skip the thin boxes of the surface
 // they start on)
 #ifndef DT_TLO_CULL
 #define DT_TLO_CULL 1
 #endif
-// DT_PACKED_SORT = 1: trav_step orders the children on packed (distance bits | slot) keys with
-// integer min/max (2 instructions per compare-exchange instead of a compare and four selects)
-#ifndef DT_PACKED_SORT
-#define DT_PACKED_SORT 0
-#endif
-// DT_NEAREST_ONLY = 1: trav_step only selects the nearest hit child (3 compares); the other hit
-// children are pushed in slot order instead of far-to-near
-#ifndef DT_NEAREST_ONLY
-#define DT_NEAREST_ONLY 0
-#endif
-// packed fp32 pairs (sm_100 FFMA2): per-element IEEE fma
-DT_D unsigned long long f2pack(float a, float b) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-DT_D void f2unpack(unsigned long long v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
-DT_D unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-// Entry distances of the four child boxes of a 64-B wide node (kInf: missed or empty child).
-// Plane distance t = (p + q 2^e - o) / d = q * A + B with A = 2^e / d, B = (p - o) / d: one
-// FMA per plane; its rounding (~1 ulp of |p - o|) is far inside the box padding.
-// tlo: entry distances are clamped at tlo (a box exited before tlo is missed).
-// DT_OCTANT = 1: the near and far plane of each axis are picked once per node by the sign of
-// the ray direction (t is monotone in q), so a child needs one max and one min chain instead
-// of six pairwise min/max; the slab comparison tmin <= tmax * 1.000021 is the padded
-// tmin * 0.99999 <= tmax * 1.00001 with the two factors merged (slightly more permissive).
+// Entry distances of the four child boxes of a 64-B wide node (kInf: missed or empty child),
+// clamped below at tlo (a box exited before tlo is missed).  Plane distance
+// t = (p + q 2^e - o) / d = q * A + B with A = 2^e / d, B = (p - o) / d: one FMA per plane;
+// its rounding (~1 ulp of |p - o|) is far inside the box padding.  The near and far plane of
+// each axis are picked once per node by the sign of the ray direction (t is monotone in q),
+// so a child needs one max and one min chain; the slab comparison tmin <= tmax * 1.000021 is
+// the padded tmin * 0.99999 <= tmax * 1.00001 with the two factors merged (slightly more
+// permissive).  Variants measured against this one: profiles/r01_traversal_sweep.txt.
 DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, const int (&r)[4], float3 o, float3 inv, float bt,
                     float (&key)[4], float tlo = 0.0f) {
   const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
                       exp_scale((n0.w >> 16) & 0xff) * inv.z);
-#if DT_B_FMA
-  // B = p / d - o / d in one FMA per axis (o / d precomputed per ray as -oinv)
-  const float3 B = f3(fmaf(__uint_as_float(n0.x), inv.x, -o.x * inv.x), fmaf(__uint_as_float(n0.y), inv.y, -o.y * inv.y),
-                      fmaf(__uint_as_float(n0.z), inv.z, -o.z * inv.z));
-#else
   const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
                       (__uint_as_float(n0.z) - o.z) * inv.z);
-#endif
-#if DT_OCTANT
   const bool sx = inv.x < 0.0f, sy = inv.y < 0.0f, sz = inv.z < 0.0f;
   const unsigned xn = sx ? n1.w : n1.x, xf = sx ? n1.x : n1.w;
   const unsigned yn = sy ? n2.x : n1.y, yf = sy ? n1.y : n2.x;
   const unsigned zn = sz ? n2.y : n1.z, zf = sz ? n1.z : n2.y;
-#if DT_FFMA2
-  // children (0, 1) and (2, 3) share A and B: one packed FFMA2 per plane and child pair
-  // (per-element IEEE fma, bit-identical to fmaf)
-  const unsigned long long Ax = f2pack(A.x, A.x), Ay = f2pack(A.y, A.y), Az = f2pack(A.z, A.z);
-  const unsigned long long Bx = f2pack(B.x, B.x), By = f2pack(B.y, B.y), Bz = f2pack(B.z, B.z);
-#pragma unroll
-  for (int c = 0; c < 4; c += 2) {
-    float xn0, xn1, yn0, yn1, zn0, zn1, xf0, xf1, yf0, yf1, zf0, zf1;
-    f2unpack(ffma2(f2pack(qbyte(xn, c), qbyte(xn, c + 1)), Ax, Bx), xn0, xn1);
-    f2unpack(ffma2(f2pack(qbyte(yn, c), qbyte(yn, c + 1)), Ay, By), yn0, yn1);
-    f2unpack(ffma2(f2pack(qbyte(zn, c), qbyte(zn, c + 1)), Az, Bz), zn0, zn1);
-    f2unpack(ffma2(f2pack(qbyte(xf, c), qbyte(xf, c + 1)), Ax, Bx), xf0, xf1);
-    f2unpack(ffma2(f2pack(qbyte(yf, c), qbyte(yf, c + 1)), Ay, By), yf0, yf1);
-    f2unpack(ffma2(f2pack(qbyte(zf, c), qbyte(zf, c + 1)), Az, Bz), zf0, zf1);
-    const float tmin0 = fmaxf(fmaxf(xn0, yn0), fmaxf(zn0, tlo)), tmin1 = fmaxf(fmaxf(xn1, yn1), fmaxf(zn1, tlo));
-    const float tmax0 = fminf(fminf(xf0, yf0), fminf(zf0, bt)), tmax1 = fminf(fminf(xf1, yf1), fminf(zf1, bt));
-    key[c] = tmin0 <= tmax0 * 1.000021f && r[c] != kEmptyRef ? tmin0 : kInf;
-    key[c + 1] = tmin1 <= tmax1 * 1.000021f && r[c + 1] != kEmptyRef ? tmin1 : kInf;
-  }
-#else
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const float tmin = fmaxf(fmaxf(fmaf(qbyte(xn, c), A.x, B.x), fmaf(qbyte(yn, c), A.y, B.y)),
@@ -332,55 +252,22 @@ DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, const int (&r)[4], float3 o, f
                              fminf(fmaf(qbyte(zf, c), A.z, B.z), bt));
     key[c] = tmin <= tmax * 1.000021f && r[c] != kEmptyRef ? tmin : kInf;
   }
-#endif
-#else
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float tx0 = fmaf(qbyte(n1.x, c), A.x, B.x), tx1 = fmaf(qbyte(n1.w, c), A.x, B.x);
-    float ty0 = fmaf(qbyte(n1.y, c), A.y, B.y), ty1 = fmaf(qbyte(n2.x, c), A.y, B.y);
-    float tz0 = fmaf(qbyte(n1.z, c), A.z, B.z), tz1 = fmaf(qbyte(n2.y, c), A.z, B.z);
-    float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
-    float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), bt));
-    key[c] = tmin * 0.99999f <= tmax * 1.00001f && r[c] != kEmptyRef ? tmin : kInf;   // symmetric in lo/hi
-  }
-#endif
 }
 
-// The traversal stack: entry i lives in this thread's shared column (sstack[i * stride],
-// its key at sstack[(kStackShared + i) * stride]) for i < kStackShared, else in lstack.
-DT_D void stack_push(Trav& T, int* sstack, int stride, int* lstack, int ref, float key, int& err) {
-  if (T.sp < kStackShared) {
-    sstack[T.sp * stride] = ref;
-    if (kStackKeys) sstack[(kStackShared + T.sp) * stride] = __float_as_int(key);
-  } else if (T.sp < kStackShared + kStackLocal) {
-    lstack[T.sp - kStackShared] = ref;
-    if (kStackKeys) lstack[kStackLocal + T.sp - kStackShared] = __float_as_int(key);
-  } else {
-    err = 1;
-  }
+// The traversal stack: entry i lives in this thread's shared column (sstack[i * stride]) for
+// i < kStackShared, else in lstack (local memory).
+DT_D void stack_push(Trav& T, int* sstack, int stride, int* lstack, int ref, int& err) {
+  if (T.sp < kStackShared) sstack[T.sp * stride] = ref;
+  else if (T.sp < kStackShared + kStackLocal) lstack[T.sp - kStackShared] = ref;
+  else err = 1;
   ++T.sp;
 }
-// Pops into T.cur the nearest remaining entry that can still hold a hit closer than T.bt (the
-// same conservative slab comparison the parent's visit made when it pushed the entry, now
-// against the current T.bt).  Returns false when the stack is exhausted.
+// Pops the top entry into T.cur; false when the stack is empty.
 DT_D bool stack_pop(Trav& T, const int* sstack, int stride, const int* lstack) {
-  while (T.sp > 0) {
-    --T.sp;
-    int ref;
-    float key = 0.0f;
-    if (T.sp < kStackShared) {
-      ref = sstack[T.sp * stride];
-      if (kStackKeys) key = __int_as_float(sstack[(kStackShared + T.sp) * stride]);
-    } else {
-      ref = lstack[T.sp - kStackShared];
-      if (kStackKeys) key = __int_as_float(lstack[kStackLocal + T.sp - kStackShared]);
-    }
-    if (!kStackKeys || key * 0.99999f <= T.bt * 1.00001f) {
-      T.cur = ref;
-      return true;
-    }
-  }
-  return false;
+  if (T.sp == 0) return false;
+  --T.sp;
+  T.cur = T.sp < kStackShared ? sstack[T.sp * stride] : lstack[T.sp - kStackShared];
+  return true;
 }
 
 // One traversal step: visit the current wide node (test its four child boxes, descend into
@@ -400,41 +287,6 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
     int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
     float key[4];
     node_keys(n0, n1, n2, {r0, r1, r2, r3}, o, inv, T.bt, key, DT_TLO_CULL ? t_lo : 0.0f);
-#if DT_NEAREST_ONLY
-    // descend into the nearest hit child; push the other hit children unsorted (slot order)
-    float kn = key[0];
-    int rn = r0, sn = 0;
-    if (key[1] < kn) { kn = key[1]; rn = r1; sn = 1; }
-    if (key[2] < kn) { kn = key[2]; rn = r2; sn = 2; }
-    if (key[3] < kn) { kn = key[3]; rn = r3; sn = 3; }
-    if (kn < kInf) {
-      const int rr[4] = {r0, r1, r2, r3};
-#pragma unroll
-      for (int q = 3; q >= 0; --q)
-        if (q != sn && key[q] < kInf) stack_push(T, sstack, stride, lstack, rr[q], key[q], err);
-      T.cur = rn;
-      descended = true;
-    }
-#elif DT_PACKED_SORT
-    // ascending by entry distance on packed keys: the distance's bits with the child slot in the
-    // two low bits (keys are >= 0, so their bit patterns order like the floats; a miss is +inf
-    // = 0x7f800000 | slot), sorted with integer min/max; the ref is looked up by the slot
-    unsigned p0 = (__float_as_uint(key[0]) & ~3u), p1 = (__float_as_uint(key[1]) & ~3u) | 1u;
-    unsigned p2 = (__float_as_uint(key[2]) & ~3u) | 2u, p3 = (__float_as_uint(key[3]) & ~3u) | 3u;
-#define DT_UCX(a, b) { const unsigned lo_ = min(a, b), hi_ = max(a, b); a = lo_; b = hi_; }
-    DT_UCX(p0, p1) DT_UCX(p2, p3) DT_UCX(p0, p2) DT_UCX(p1, p3) DT_UCX(p1, p2)
-#undef DT_UCX
-    constexpr unsigned kMissKey = 0x7f800000u;
-    auto ref_of = [&](unsigned p) { return (p & 2u) ? ((p & 1u) ? r3 : r2) : ((p & 1u) ? r1 : r0); };
-    if (p0 < kMissKey) {
-      const unsigned pq[3] = {p3, p2, p1};
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        if (pq[q] < kMissKey) stack_push(T, sstack, stride, lstack, ref_of(pq[q]), __uint_as_float(pq[q] & ~3u), err);
-      T.cur = ref_of(p0);
-      descended = true;
-    }
-#else
     float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
     DT_CX(0, 1) DT_CX(2, 3) DT_CX(0, 2) DT_CX(1, 3) DT_CX(1, 2)   // ascending by entry distance
     if (k0 < kInf) {
@@ -442,11 +294,10 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
       float pk[3] = {k3, k2, k1};
 #pragma unroll
       for (int q = 0; q < 3; ++q)
-        if (pk[q] < kInf) stack_push(T, sstack, stride, lstack, push[q], pk[q], err);
+        if (pk[q] < kInf) stack_push(T, sstack, stride, lstack, push[q], err);
       T.cur = r0;
       descended = true;
     }
-#endif
   } else {
     int first, cnt;
     leaf_range(T.cur, first, cnt);
@@ -491,7 +342,7 @@ DT_D void trav_node(const DevScene& s, float3 o, float3 inv, Trav& T, int* sstac
   float pk[3] = {k3, k2, k1};
 #pragma unroll
   for (int q = 0; q < 3; ++q)
-    if (pk[q] < kInf) stack_push(T, sstack, stride, lstack, push[q], pk[q], err);
+    if (pk[q] < kInf) stack_push(T, sstack, stride, lstack, push[q], err);
   T.cur = k0 < kInf ? r0 : kEmptyRef;
 }
 
@@ -514,7 +365,7 @@ DT_D void trav_leaf(const DevScene& s, float3 o, float3 d, float t_lo, int leaf,
 DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, float& bu, float& bv, int* sstack,
                   int stride, int& err, int& visits, int& tests) {
   float3 inv = safe_inv(d);
-  int lstack[kStackLocalWords];
+  int lstack[kStackLocal];
   Trav T;
   trav_init(T);
   while (!trav_step(s, o, d, inv, t_lo, T, sstack, stride, lstack, err, visits, tests)) {

@@ -61,8 +61,6 @@ struct FwdLaunch {
   unsigned long long* sig_f;
   unsigned long long* counters;   // [0] node visits, [1] triangle tests
   int trav_mode, trav_chunk, leaf_vote;
-  int flush_tasks;      // mode 4: tasks that trigger a cooperative leaf flush (<= 32)
-  int refill_k, step_budget;   // mode 1: refill once refill_k lanes wait (32: after kStepBudget steps)
   int sort_lanes;       // shade: hit-first lane order over 64-record windows
   int prim_packet;      // camera rays: warp-packet traversal (traverse_packet)
 };
@@ -155,12 +153,9 @@ struct dt_ctx {
   int leaf_max = 1;           // triangles per wide-BVH leaf (sweep r01: 1 is fastest)
   int prim_packet = 0;        // camera rays as warp packets (DT_PRIMARY_PACKET=1): measured slower at C3
   int trav_mode = 1;          // 0: warp takes 32 rays; 1: per-lane global refill; 2: per-lane refill from a warp chunk;
-                              // 3: postponed leaves; 4: warp-cooperative leaf tests
+                              // 3: postponed leaves
   int trav_chunk = 256;       // rays per warp chunk (mode 2)
   int leaf_vote = 32;         // mode 3: lanes that must be ready before a warp leaf phase
-  int flush_tasks = 32;       // mode 4: leaf tasks that trigger a warp-cooperative flush
-  int refill_k = 32;          // mode 1: lanes waiting for a ray that end the step loop early
-  int step_budget = 64;       // mode 1 with refill_k < 32: step loop length
   int sort_lanes = 1;         // shade / backward: hit-first lane order (DT_SORT_LANES)
   // profiling (dt_set_profiling / dt_get_profile)
   bool prof = false;

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kMaskThreads) k_mask_render(DevScene s, const 
                                                               const float* __restrict__ c2w, int n_views, int W, int H,
                                                               const float* __restrict__ gt, float inv_n,
                                                               float* __restrict__ mask_out, float* __restrict__ loss) {
-  __shared__ int sstack[kStackWords * kMaskThreads];
+  __shared__ int sstack[kStackShared * kMaskThreads];
   int err = 0, visits = 0, tests = 0;
   float acc = 0.f;
   const int64_t n = (int64_t)n_views * W * H;
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kMaskThreads) k_mask_grad(
     const float* __restrict__ gt, const int* __restrict__ nbr, const int* __restrict__ owner,
     const int* __restrict__ nbr_total, int64_t n_ent, const int* __restrict__ vstart, const unsigned* __restrict__ vcorner, const int* __restrict__ F,
     const float4* __restrict__ V, float scale, float spacing, float eps, float* __restrict__ grad_V) {
-  __shared__ int sstack[kStackWords * kMaskThreads];
+  __shared__ int sstack[kStackShared * kMaskThreads];
   const int64_t total = (int64_t)n_views * n_ent;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
     const int v = (int)(id / n_ent);

@@ -92,22 +92,6 @@ DT_D void hit_first_order(int cA, int cB, unsigned char* slot, int& r0, int& r1)
   __syncwarp();
 }
 
-// L2 prefetch (bulk, no registers) of a window of records [first, first + cnt) of level k:
-// the record lanes the next window's first pass reads.  Level 0 is stored reversed.
-#ifndef DT_PREFETCH
-#define DT_PREFETCH 0
-#endif
-DT_D void prefetch_l2(const float4* p, int cnt) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(cnt * 16) : "memory");
-}
-template <int NL>
-DT_D void prefetch_window(float4* const (&lanes)[NL], int k, int64_t cap, int64_t off, int64_t first, int n) {
-  if (!DT_PREFETCH || first >= n || lane_id() >= NL) return;
-  const int cnt = (int)(n - first < 64 ? n - first : 64);
-  const int64_t base = k == 0 ? cap - first - cnt : off + first;   // lowest record index of the window
-  prefetch_l2(lanes[lane_id()] + base, cnt);
-}
-
 // first record index of level k >= 1
 DT_D int64_t level_base(const int* lvl, int k) {
   int64_t off = 0;
@@ -260,7 +244,7 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
 // only the hitting rays (misses write their env radiance straight to rgb).
 template <bool VOL>
 __global__ void DT_TRAV_LB k_trace_primary(FwdLaunch a, int max_depth) {
-  __shared__ int sstack[kStackWords * kTraceThreads];
+  __shared__ int sstack[kStackShared * kTraceThreads];
   __shared__ int pstack[(kTraceThreads / 32) * kPacketStack];
   int* const wstack = pstack + (threadIdx.x >> 5) * kPacketStack;
   const DevScene& s = a.s;
@@ -363,10 +347,6 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
   while (wbase < n) {
     if (round == 0 && kDyn && lane_id() == 0) next = atomicAdd(ctr, chunk);
     if (sorted && round == 0) {
-      if (!kDyn) {
-        float4* const lanes[4] = {a.r.o, a.r.d, a.r.thr, a.r.hit};
-        prefetch_window<4>(lanes, k, a.cap, off, wbase + wstep, n);
-      }
       int c[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -421,12 +401,9 @@ __global__ void __maxnreg__(DT_SHADE_VOL_REGS) k_shade_level_vol(FwdLaunch a, in
 // Traversal of level k >= 1 (K9): closest hit only, hit = (face, t, u, v) written back into
 // the record.  Lanes that finish their ray refill from the level's queue (one warp-aggregated
 // atomic per refill), so short reflected rays do not idle a warp behind long refracted ones.
-#ifndef DT_STEP_BUDGET
-#define DT_STEP_BUDGET 16
-#endif
-constexpr int kStepBudget = DT_STEP_BUDGET;   // traversal steps between refill votes
+constexpr int kStepBudget = 16;   // traversal steps between refill votes (swept: 8 / 16 / 32)
 __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
-  __shared__ int sstack_all[kStackWords * kTraceThreads];
+  __shared__ int sstack_all[kStackShared * kTraceThreads];
   const DevScene& s = a.s;
   if (a.lvl[LV_OVERFLOW]) return;
   const float t_lo = a.t_eps * s.scal[6];                                      // R17
@@ -434,7 +411,7 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
   const int64_t off = level_base(a.lvl, k);
   int* work = a.lvl + LV_WORK_TRACE + k;
   int* sstack = sstack_all + threadIdx.x;
-  int lstack[kStackLocalWords];
+  int lstack[kStackLocal];
   int err = 0, visits = 0, tests = 0;
   int item = -1;                       // -1: needs a ray; >= n: queue exhausted
   float3 o = f3(0, 0, 0), d = f3(0, 0, 1), inv = f3(0, 0, 0);
@@ -491,19 +468,10 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
       }
     }
     if (__all_sync(~0u, item >= n)) break;
-    const bool live = item >= 0 && item < n;
+    if (item < 0 || item >= n) continue;
     bool done = false;
-    if (a.refill_k >= 32) {
-      if (live)
-        for (int step = 0; step < kStepBudget && !done; ++step)
-          done = trav_step(s, o, d, inv, t_lo, T, sstack, kTraceThreads, lstack, err, visits, tests);
-    } else {
-      // early refill: leave the step loop (warp-uniformly) once refill_k lanes wait for a ray
-      for (int step = 0; step < a.step_budget; ++step) {
-        if (live && !done) done = trav_step(s, o, d, inv, t_lo, T, sstack, kTraceThreads, lstack, err, visits, tests);
-        if (__popc(__ballot_sync(~0u, done || item < 0)) >= a.refill_k) break;
-      }
-    }
+    for (int step = 0; step < kStepBudget && !done; ++step)
+      done = trav_step(s, o, d, inv, t_lo, T, sstack, kTraceThreads, lstack, err, visits, tests);
     if (done) {
       __stcs(a.r.hit + off + item, make_float4(__int_as_float(T.best), T.bt, T.bu, T.bv));
       item = -1;
@@ -518,7 +486,7 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
 // warp switches to a leaf phase -- all parked leaves tested together -- once at least
 // `leaf_vote` lanes have a parked leaf or no node left (Aila & Laine's postponed leaves).
 __global__ void DT_TRAV_LB k_traverse_level_ws(FwdLaunch a, int k) {
-  __shared__ int sstack_all[kStackWords * kTraceThreads];
+  __shared__ int sstack_all[kStackShared * kTraceThreads];
   const DevScene& s = a.s;
   if (a.lvl[LV_OVERFLOW]) return;
   const float t_lo = a.t_eps * s.scal[6];                                      // R17
@@ -526,7 +494,7 @@ __global__ void DT_TRAV_LB k_traverse_level_ws(FwdLaunch a, int k) {
   const int64_t off = level_base(a.lvl, k);
   int* work = a.lvl + LV_WORK_TRACE + k;
   int* sstack = sstack_all + threadIdx.x;
-  int lstack[kStackLocalWords];
+  int lstack[kStackLocal];
   int err = 0, visits = 0, tests = 0;
   int item = -1;
   float3 o = f3(0, 0, 0), d = f3(0, 0, 1), inv = f3(0, 0, 0);
@@ -592,158 +560,6 @@ __global__ void DT_TRAV_LB k_traverse_level_ws(FwdLaunch a, int k) {
   flush_counters(a.counters, visits, tests);
 }
 
-// Traversal of level k >= 1 with warp-cooperative leaf tests (trav_mode 4).  Lanes walk the
-// wide nodes on their own (per-lane refill as in k_traverse_level), but a leaf child that
-// passes its box test is not pushed: it goes into the warp's task list in shared memory.
-// When the list holds `flush_tasks` tasks, or `leaf_vote` lanes wait only for their tasks,
-// or no lane has a node left, all 32 lanes test the listed triangles against their owners'
-// rays and merge (t, original face id) into the owner's best hit with one 64-bit shared
-// atomicMin: for t > 0 the key order is exactly "smaller t, then lower original id" (R18).
-// The same leaves are tested as in k_traverse_level (every pushed leaf was tested there);
-// the triangle tests just run on full warps instead of the few lanes that sit at a leaf.
-// (u, v) are not stored: the shade pass recomputes them from the face (tri_uv, bit-exact).
-constexpr int kTaskCap = 32 + 4 * 32;   // below flush_tasks (<= 32) + 4 leaf children per lane
-constexpr unsigned long long kNoHitKey = (0x7f800000ull << 32) | 0xffffffffull;   // (inf, id -1)
-
-DT_D void coop_visit(const DevScene& s, float3 o, float3 inv, Trav& T, int* sstack, int* lstack, int& err,
-                     int& visits, unsigned (&word)[4], bool (&leaf)[4]) {
-  const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)T.cur;
-  uint4 n0, n1, n2, n3;
-  ldg256(nd, n0, n1);
-  ldg256(nd + 2, n2, n3);
-  ++visits;
-  int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
-  const int rr[4] = {r0, r1, r2, r3};
-  float key[4];
-  node_keys(n0, n1, n2, rr, o, inv, T.bt, key);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    // a hit leaf becomes a task (owner lane, first triangle, count - 1) instead of an entry
-    leaf[c] = key[c] < kInf && rr[c] < 0;
-    const unsigned x = ~(unsigned)rr[c];   // leaf ref = ~(first << 2 | cnt - 1)
-    word[c] = ((unsigned)lane_id() << 27) | ((x & 3u) << 25) | (x >> 2);
-    if (rr[c] < 0) key[c] = kInf;
-  }
-  float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
-#define DT_CX3(a, b)                                             \
-  if (k##b < k##a) {                                             \
-    float tk = k##a; k##a = k##b; k##b = tk;                     \
-    int tr = r##a; r##a = r##b; r##b = tr;                       \
-  }
-  DT_CX3(0, 1) DT_CX3(2, 3) DT_CX3(0, 2) DT_CX3(1, 3) DT_CX3(1, 2)
-#undef DT_CX3
-  if (k0 < kInf) {
-    int push[3] = {r3, r2, r1};
-    float pk[3] = {k3, k2, k1};
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-      if (pk[q] < kInf) stack_push(T, sstack, kTraceThreads, lstack, push[q], pk[q], err);
-    T.cur = r0;
-  } else if (err || !stack_pop(T, sstack, kTraceThreads, lstack)) {
-    T.cur = kEmptyRef;
-  }
-}
-
-__global__ void DT_TRAV_LB k_traverse_level_coop(FwdLaunch a, int k) {
-  constexpr int kWarps = kTraceThreads / 32;
-  __shared__ int sstack_all[kStackWords * kTraceThreads];
-  __shared__ float sray[kWarps][6][32];
-  __shared__ unsigned long long sbest[kTraceThreads];
-  __shared__ unsigned stask[kWarps][kTaskCap];
-  const DevScene& s = a.s;
-  if (a.lvl[LV_OVERFLOW]) return;
-  const float t_lo = a.t_eps * s.scal[6];                                      // R17
-  const int n = a.lvl[LV_CNT + k];
-  const int64_t off = level_base(a.lvl, k);
-  int* work = a.lvl + LV_WORK_TRACE + k;
-  int* sstack = sstack_all + threadIdx.x;
-  const int w = threadIdx.x >> 5, lane = lane_id();
-  float(*ray)[32] = sray[w];
-  unsigned* tasks = stask[w];
-  unsigned long long* best = sbest + (threadIdx.x & ~31);
-  const int flush_tasks = a.flush_tasks, wait_vote = a.leaf_vote;
-  int lstack[kStackLocalWords];
-  int err = 0, visits = 0, tests = 0;
-  int item = -1;                       // -1: needs a ray; >= n: queue exhausted
-  float3 o = f3(0, 0, 0), inv = f3(0, 0, 0);
-  Trav T;
-  trav_init(T);
-  bool pend = false;                   // this lane has tasks in the list
-  int count = 0;                       // tasks in the list (warp-uniform)
-  while (true) {
-    const unsigned need = __ballot_sync(~0u, item < 0);
-    if (need) {
-      const int leader = __ffs(need) - 1;
-      int base = 0;
-      if (lane == leader) base = atomicAdd(work, __popc(need));
-      base = __shfl_sync(~0u, base, leader);
-      if (item < 0) {
-        const int j = base + __popc(need & lanemask_lt());
-        if (j < n) {
-          item = j;
-          const float4 ro = __ldcs(a.r.o + off + j), rd = __ldcs(a.r.d + off + j);
-          o = f3(ro);
-          inv = safe_inv(f3(rd));
-          trav_init(T);
-          ray[0][lane] = ro.x; ray[1][lane] = ro.y; ray[2][lane] = ro.z;
-          ray[3][lane] = rd.x; ray[4][lane] = rd.y; ray[5][lane] = rd.z;
-          best[lane] = kNoHitKey;
-        } else {
-          item = n;
-        }
-      }
-      __syncwarp();
-    }
-    if (__all_sync(~0u, item >= n)) break;
-    for (int step = 0; step < kStepBudget; ++step) {
-      const bool live = item >= 0 && item < n;
-      unsigned word[4] = {0u, 0u, 0u, 0u};
-      bool leaf[4] = {false, false, false, false};
-      if (live && T.cur != kEmptyRef) coop_visit(s, o, inv, T, sstack, lstack, err, visits, word, leaf);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {            // append the leaf tasks (warp-ballot compaction)
-        const unsigned m = __ballot_sync(~0u, leaf[c]);
-        if (leaf[c]) tasks[count + __popc(m & lanemask_lt())] = word[c];
-        count += __popc(m);
-      }
-      pend = pend || leaf[0] || leaf[1] || leaf[2] || leaf[3];
-      const bool fin = live && T.cur == kEmptyRef;
-      const unsigned waiting = __ballot_sync(~0u, fin && pend);
-      const bool walking = __any_sync(~0u, live && T.cur != kEmptyRef);
-      if (count > 0 && (count >= flush_tasks || __popc(waiting) >= wait_vote || !walking)) {
-        __syncwarp();
-        for (int i = lane; i < count; i += 32) {
-          const unsigned wd = tasks[i];
-          const int ow = (int)(wd >> 27), first = (int)(wd & 0x1ffffffu), cnt = (int)((wd >> 25) & 3u) + 1;
-          const float3 ro = f3(ray[0][ow], ray[1][ow], ray[2][ow]), rd = f3(ray[3][ow], ray[4][ow], ray[5][ow]);
-          for (int j = first; j < first + cnt; ++j) {
-            const float4* tr = s.tris + 3 * (size_t)j;
-            const float4 ta = __ldg(tr), tb = __ldg(tr + 1), tc = __ldg(tr + 2);
-            float t, u, v;
-            ++tests;
-            if (intersect_tri(ro, rd, f3(ta), f3(tb), f3(tc), t_lo, t, u, v))
-              atomicMin(best + ow, ((unsigned long long)__float_as_uint(t) << 32) | __float_as_uint(ta.w));
-          }
-        }
-        __syncwarp();
-        count = 0;
-        if (pend) {
-          const unsigned long long b = best[lane];
-          T.bt = __uint_as_float((unsigned)(b >> 32));
-          T.best = (int)(unsigned)b;
-          pend = false;
-        }
-      }
-      if (fin && !pend) {
-        __stcs(a.r.hit + off + item, make_float4(__int_as_float(T.best), T.bt, 0.f, 0.f));
-        item = -1;
-      }
-    }
-  }
-  if (err) a.lvl[LV_STACKERR] = 1;
-  flush_counters(a.counters, visits, tests);
-}
-
 // Bottom-up radiance: L = tau * (R L_r + T L_t); level 0 writes the pixel.
 __global__ void k_gather(FwdLaunch a, int k) {
   if (a.lvl[LV_OVERFLOW]) return;
@@ -800,8 +616,6 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
   for (int64_t wb = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * per; wb < n; wb += stride * per) {
   int o0 = lane_id(), o1 = 32 + lane_id();
   if (sorted) {
-    float4* const lanes[6] = {a.r.o, a.r.d, a.r.thr, a.r.hit, a.r.tau, a.r.lsub};
-    prefetch_window<6>(lanes, k, cap, off, wb + stride * per, n);
     int c[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -1075,7 +889,7 @@ __global__ void k_check_finite(const float* __restrict__ x, int64_t n, int* flag
 __global__ void __launch_bounds__(kTraceThreads) k_debug_hit(DevScene s, const float* __restrict__ rays, int64_t n,
                                                              float t_lo, int brute, int* __restrict__ face,
                                                              float* __restrict__ tuv, int* err_flag) {
-  __shared__ int sstack[kStackWords * kTraceThreads];
+  __shared__ int sstack[kStackShared * kTraceThreads];
   int err = 0, visits = 0, tests = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float3 o = f3(rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]), d = f3(rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]);
@@ -1144,11 +958,8 @@ cudaError_t launch_shade_level(const FwdLaunch& a, int level, int max_depth, int
 }
 
 cudaError_t launch_traverse_level(const FwdLaunch& a, int level, int sm_count, cudaStream_t st) {
-  static int gl = 0, gw = 0, gc = 0;
-  if (a.trav_mode == 4 && a.s.nf < (1 << 25)) {   // task words hold a 25-bit triangle index
-    if (!gc) gc = persistent_blocks((const void*)k_traverse_level_coop, kTraceThreads, sm_count);
-    k_traverse_level_coop<<<gc, kTraceThreads, 0, st>>>(a, level);
-  } else if (a.trav_mode == 3) {
+  static int gl = 0, gw = 0;
+  if (a.trav_mode == 3) {
     if (!gw) gw = persistent_blocks((const void*)k_traverse_level_ws, kTraceThreads, sm_count);
     k_traverse_level_ws<<<gw, kTraceThreads, 0, st>>>(a, level);
   } else {
