@@ -457,3 +457,46 @@ def test_context_reuse_across_kinds(tracer):
         fresh = run_gpu(Tracer("cuda:0"), sc, pid, grad=g)
         np.testing.assert_array_equal(shared["rgb"], fresh["rgb"])
         assert rel_l2(shared["gV"], fresh["gV"]) < 1e-5 and rel_l2(shared["gsig"], fresh["gsig"]) < 1e-5
+
+
+def test_degenerate_method_cases(tracer):
+    """Degenerate cases of the method, each against the oracle: (a) eta = 1 and sigma = 0
+    (optical absence: R = 0 everywhere, the reflect child still spawned with weight 0, R5);
+    (b) zero-area faces in the mesh (a repeated vertex index and three collinear vertices:
+    no hit, no contribution to the vertex normals, R6, R16); (c) the camera inside the object
+    (every camera hit is an inside hit: refraction out or TIR, R8)."""
+    base = S.config_c1()
+    sc = T.scene(base.V, base.F, base.cams, env=base.env, ior=1.0, sigma=(0.0, 0.0, 0.0), D=3)
+    pid = np.arange(sc.n_pixels)
+    osc = O.OracleScene(sc)
+    orc = oracle_forward(O, osc, pid)
+    cmp = compare_forward(run_gpu(tracer, sc, pid)["rgb"], run_gpu(tracer, sc, pid)["sig"], orc)
+    assert_forward(cmp, "eta1")
+    # the exact vertex gradient is 0 here (the radiance no longer depends on the geometry), so
+    # rel-L2 has no denominator: the error is measured against the gradient scale of the same
+    # scene at eta = 1.5, sigma = 0 (same upstream gradient)
+    g = S.upstream_grad(len(pid), 11)
+    g[cmp["div_mask"] | cmp["flag_mask"]] = 0.0
+    gpu = run_gpu(tracer, sc, pid, grad=g)
+    gV, _, _ = O.backward(osc, g, pid)
+    ref = T.scene(base.V, base.F, base.cams, env=base.env, ior=1.5, sigma=(0.0, 0.0, 0.0), D=3)
+    gref, _, _ = O.backward(O.OracleScene(ref), g, pid)
+    assert np.linalg.norm(gV) <= 1e-9 * np.linalg.norm(gref)
+    assert np.linalg.norm(gpu["gV"] - gV) <= 1e-3 * np.linalg.norm(gref), np.linalg.norm(gpu["gV"] - gV)
+    V, F = S.icosphere(1)
+    # exactly collinear in float32 and float64 (A, 1.5 A, 2 A with dyadic A), so the face's cross
+    # product is 0 in both and its three vertices are isolated (normal (0, 0, 1), R6)
+    A = np.array([0.25, 0.125, 0.0625])
+    V = np.concatenate([V, [A, 1.5 * A, 2.0 * A]]).astype(np.float32)
+    nv = V.shape[0]
+    F = np.concatenate([F, [[0, 0, 5], [nv - 3, nv - 2, nv - 1]]]).astype(np.int32)
+    sc = T.scene(V, F, T.one_view(24, 20, (0.3, -0.4, 3.0)), env=T.lobe_env(), D=3)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "zero-area")
+    Vt, Ft = torch.as_tensor(V, device="cuda:0"), torch.as_tensor(F, device="cuda:0")
+    tracer.build_bvh(Vt, Ft)
+    n = tracer.vertex_normals(nv).cpu().numpy()
+    osc = O.OracleScene(sc)
+    np.testing.assert_allclose(n, O.vertex_normals(osc), atol=1e-5)   # the three extra vertices: (0, 0, 1)
+    V, F = S.icosphere(2)
+    sc = T.scene(V, F, T.one_view(20, 16, (0.0, 0.0, 0.3), fov_deg=70.0, target=(1.0, 0.2, 0.3)), env=T.lobe_env(), D=4)
+    parity_case(tracer, sc, np.arange(sc.n_pixels), "camera-inside")
