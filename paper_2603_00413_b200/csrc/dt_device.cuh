@@ -290,11 +290,20 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
     float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
     DT_CX(0, 1) DT_CX(2, 3) DT_CX(0, 2) DT_CX(1, 3) DT_CX(1, 2)   // ascending by entry distance
     if (k0 < kInf) {
-      int push[3] = {r3, r2, r1};
-      float pk[3] = {k3, k2, k1};
+      // the hit children are a prefix of the sorted order: push children 1..h far-to-near
+      const int h = (k1 < kInf) + (k2 < kInf) + (k3 < kInf);
+      if (T.sp + 3 <= kStackShared) {             // common case: all in the shared short stack
+        int* top = sstack + (T.sp + h - 1) * stride;
+        if (h > 0) top[0] = r1;
+        if (h > 1) top[-stride] = r2;
+        if (h > 2) top[-2 * stride] = r3;
+        T.sp += h;
+      } else {
+        const int push[3] = {r3, r2, r1};
 #pragma unroll
-      for (int q = 0; q < 3; ++q)
-        if (pk[q] < kInf) stack_push(T, sstack, stride, lstack, push[q], err);
+        for (int q = 0; q < 3; ++q)
+          if (q >= 3 - h) stack_push(T, sstack, stride, lstack, push[q], err);
+      }
       T.cur = r0;
       descended = true;
     }
