@@ -390,11 +390,7 @@ def run_ours(args, rank, world, local_rank):
         "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {sc.F.shape[0]} tris, {sc.cams.n_views} views "
-                               f"{sc.cams.width}x{sc.cams.height}, depth {sc.max_depth}, "
-                               f"{['const', 'grid', 'hash-grid'][sc.absorption.kind]} sigma, "
-                               f"{'analytic' if sc.env.kind == 0 else 'voxel+triplane'} env, "
-                               f"{'forward only' if infer else 'fwd+bwd+optimiser step'}",
+        "config": {"workload": workload_name(args.config, sc, infer),
                    "rays_per_step": int(n_rays) * world, "segments_per_step": int(segs / args.steps),
                    "segments_per_depth": last["segments_per_depth"], "parallelism": f"rays{world}",
                    "l2": "working set > L2: path-record arena "
@@ -407,6 +403,15 @@ def run_ours(args, rank, world, local_rank):
                               "tri_tests": prof["tri_tests"] // args.steps},
     }
     return line
+
+
+def workload_name(config, sc, infer):
+    """The config's `workload` string (identical on both arms)."""
+    return (f"{config}: {sc.F.shape[0]} tris, {sc.cams.n_views} views "
+            f"{sc.cams.width}x{sc.cams.height}, depth {sc.max_depth}, "
+            f"{['const', 'grid', 'hash-grid'][sc.absorption.kind]} sigma, "
+            f"{['analytic', 'voxel+triplane', 'volumetric voxel+triplane'][sc.env.kind]} env, "
+            f"{'forward only' if infer else 'fwd+bwd+optimiser step'}")
 
 
 def run_reference(args, rank, world):
@@ -427,10 +432,11 @@ def run_reference(args, rank, world):
     sample = (f"each step: {args.ref_pixels} object pixels of {args.config} (fp64 brute force "
               f"{'fwd+bwd' if bwd else 'fwd'}); "
               f"{tot_s} segments in {tot_t:.1f}s")
-    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    metric = METRIC if bwd else "Mrays·bounces/s forward-only (relighting / novel-view inference, D 8)"
+    return {"impl": "reference", "metric": metric, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config},
+            "config": {"workload": workload_name(args.config, sc, not bwd)},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
