@@ -414,11 +414,13 @@ DT_D void write_wide_node(int i, const int ent[4], const int wref[4], int ne, un
     }
   }
   uint4* nd = wnodes + 4 * (size_t)w;
+  // the three power-of-two scales as fp32 (x in word 3, y and z in words 14, 15), so the
+  // traversal reads them without decoding
   nd[0] = make_uint4(__float_as_uint((float)P[0]), __float_as_uint((float)P[1]), __float_as_uint((float)P[2]),
-                     (unsigned)ex[0] | ((unsigned)ex[1] << 8) | ((unsigned)ex[2] << 16));
+                     (unsigned)ex[0] << 23);
   nd[1] = make_uint4(q[0], q[1], q[2], q[3]);
   nd[2] = make_uint4(q[4], q[5], (unsigned)refs[0], (unsigned)refs[1]);
-  nd[3] = make_uint4((unsigned)refs[2], (unsigned)refs[3], 0u, 0u);
+  nd[3] = make_uint4((unsigned)refs[2], (unsigned)refs[3], (unsigned)ex[1] << 23, (unsigned)ex[2] << 23);
   wbox[2 * (size_t)w] = f4(ulo, 0.f);
   wbox[2 * (size_t)w + 1] = f4(uhi, 0.f);
   wdepth[w] = wd;
@@ -589,7 +591,7 @@ __global__ void k_bvh_check(const uint4* __restrict__ wnodes, const float4* __re
       int ref = wide_ref(n2, n3, c);
       if (ref == kEmptyRef) continue;
       float3 lo, hi;
-      decode_wide_child(n0, n1, n2, c, lo, hi);
+      decode_wide_child(n0, n1, n2, n3, c, lo, hi);
       float3 clo, chi;
       if (ref >= 0) {
         atomicAdd(wref + ref, 1);

@@ -145,9 +145,12 @@ DT_D void tri_uv(float3 o, float3 d, float3 v0, float3 e1, float3 e2, float& u, 
 }
 
 // ----------------------------------------------------------------------------- wide nodes
-// 64-B 4-wide node (layout in bvh.cu, k_wide_build): child c's box decodes to
-// lo = p + qlo * 2^(e-127), hi = p + qhi * 2^(e-127) (one fma per plane).
-DT_D float exp_scale(unsigned e) { return __uint_as_float(e << 23); }
+// 64-B 4-wide node (layout in bvh.cu, write_wide_node): child c's box decodes to
+// lo = p + qlo * s, hi = p + qhi * s with per-axis power-of-two scales s (one fma per plane).
+// per-axis power-of-two scales of a node: x in n0.w, y in n3.z, z in n3.w (fp32 bit patterns)
+DT_D float3 node_scale(uint4 n0, uint4 n3) {
+  return f3(__uint_as_float(n0.w), __uint_as_float(n3.z), __uint_as_float(n3.w));
+}
 // One 256-bit read-only load (sm_100: LDG.E.ENL2.256): a 64-B node is two instructions.
 DT_D void ldg256(const uint4* p, uint4& a, uint4& b) {
   asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -162,9 +165,10 @@ DT_D void ldg256f(const float4* p, float4& a, float4& b) {
 DT_D int wide_ref(uint4 n2, uint4 n3, int c) {
   return (int)(c == 0 ? n2.z : c == 1 ? n2.w : c == 2 ? n3.x : n3.y);
 }
-DT_D void decode_wide_child(uint4 n0, uint4 n1, uint4 n2, int c, float3& lo, float3& hi) {
+DT_D void decode_wide_child(uint4 n0, uint4 n1, uint4 n2, uint4 n3, int c, float3& lo, float3& hi) {
   float3 p = f3(__uint_as_float(n0.x), __uint_as_float(n0.y), __uint_as_float(n0.z));
-  float sx = exp_scale(n0.w & 0xff), sy = exp_scale((n0.w >> 8) & 0xff), sz = exp_scale((n0.w >> 16) & 0xff);
+  const float3 sc = node_scale(n0, n3);
+  const float sx = sc.x, sy = sc.y, sz = sc.z;
   int sh = 8 * c;
   lo = f3(fmaf((float)((n1.x >> sh) & 0xff), sx, p.x), fmaf((float)((n1.y >> sh) & 0xff), sy, p.y),
           fmaf((float)((n1.z >> sh) & 0xff), sz, p.z));
@@ -234,10 +238,10 @@ DT_D float qbyte(unsigned w, int c) { return (float)((w >> (8 * c)) & 0xff); }
 // so a child needs one max and one min chain; the slab comparison tmin <= tmax * 1.000021 is
 // the padded tmin * 0.99999 <= tmax * 1.00001 with the two factors merged (slightly more
 // permissive).  Variants measured against this one: profiles/r01_traversal_sweep.txt.
-DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, const int (&r)[4], float3 o, float3 inv, float bt,
+DT_D void node_keys(uint4 n0, uint4 n1, uint4 n2, uint4 n3, const int (&r)[4], float3 o, float3 inv, float bt,
                     float (&key)[4], float tlo = 0.0f) {
-  const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
-                      exp_scale((n0.w >> 16) & 0xff) * inv.z);
+  const float3 sc = node_scale(n0, n3);
+  const float3 A = f3(sc.x * inv.x, sc.y * inv.y, sc.z * inv.z);
   const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
                       (__uint_as_float(n0.z) - o.z) * inv.z);
   const bool sx = inv.x < 0.0f, sy = inv.y < 0.0f, sz = inv.z < 0.0f;
@@ -286,7 +290,7 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
     ++visits;
     int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
     float key[4];
-    node_keys(n0, n1, n2, {r0, r1, r2, r3}, o, inv, T.bt, key, DT_TLO_CULL ? t_lo : 0.0f);
+    node_keys(n0, n1, n2, n3, {r0, r1, r2, r3}, o, inv, T.bt, key, DT_TLO_CULL ? t_lo : 0.0f);
     float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
     DT_CX(0, 1) DT_CX(2, 3) DT_CX(0, 2) DT_CX(1, 3) DT_CX(1, 2)   // ascending by entry distance
     if (k0 < kInf) {
@@ -344,7 +348,7 @@ DT_D void trav_node(const DevScene& s, float3 o, float3 inv, Trav& T, int* sstac
   ++visits;
   int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
   float key[4];
-  node_keys(n0, n1, n2, {r0, r1, r2, r3}, o, inv, T.bt, key);
+  node_keys(n0, n1, n2, n3, {r0, r1, r2, r3}, o, inv, T.bt, key);
   float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
   DT_CX2(0, 1) DT_CX2(2, 3) DT_CX2(0, 2) DT_CX2(1, 3) DT_CX2(1, 2)
   int push[3] = {r3, r2, r1};
@@ -412,8 +416,8 @@ DT_D int traverse_packet(const DevScene& s, float3 o, float3 d, bool active, flo
       ldg256(nd + 2, n2, n3);
       visits += active;
       const int r[4] = {(int)n2.z, (int)n2.w, (int)n3.x, (int)n3.y};
-      const float3 A = f3(exp_scale(n0.w & 0xff) * inv.x, exp_scale((n0.w >> 8) & 0xff) * inv.y,
-                          exp_scale((n0.w >> 16) & 0xff) * inv.z);
+      const float3 sc = node_scale(n0, n3);
+      const float3 A = f3(sc.x * inv.x, sc.y * inv.y, sc.z * inv.z);
       const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
                           (__uint_as_float(n0.z) - o.z) * inv.z);
       float key[4];
