@@ -141,19 +141,20 @@ def target_scene(sc):
     return dataclasses.replace(sc, V=V, ior=1.45, absorption=ab)
 
 
-def oracle_sample(sc, n_pix: int, seed: int = 9, backward: bool = True):
-    """Bounded oracle run (forward [+ backward]) on n_pix object pixels: (seconds, segments, threads)."""
+def oracle_sample(sc, n_pix: int, seed: int = 9, backward: bool = True, nthreads: int = 0):
+    """Bounded oracle run (forward [+ backward]) on n_pix object pixels: (seconds, segments,
+    threads); nthreads = 0 uses every host core."""
     import oracle as O
     from paper_2603_00413_b200 import scenes as S
     osc = O.OracleScene(sc)
     pid = S.central_pixels(sc.cams, n_pix, seed)
     g = S.upstream_grad(len(pid), seed)
     t0 = time.perf_counter()
-    out = O.render(osc, pid)
+    out = O.render(osc, pid, nthreads=nthreads)
     if backward:
-        O.backward(osc, g, pid)
+        O.backward(osc, g, pid, nthreads=nthreads)
     dt = time.perf_counter() - t0
-    return dt, int(out["segments"].sum()), os.cpu_count()
+    return dt, int(out["segments"].sum()), nthreads or os.cpu_count()
 
 
 def algorithmic_bytes(stats, prof, steps: int):
@@ -381,7 +382,10 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         dt, osegs, cores = oracle_sample(sc, args.cpu_pixels, backward=not infer)
+        n1 = max(args.cpu_pixels // 32, 1)                  # also one thread
+        dt1, osegs1, _ = oracle_sample(sc, n1, seed=10, backward=not infer, nthreads=1)
         cpu = {"value": osegs / dt / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "value_1thread": osegs1 / dt1 / 1e6, "sample_1thread": f"{n1} object pixels, 1 thread",
                "sample": f"{args.cpu_pixels} object pixels of {args.config}, {'fwd' if infer else 'fwd+bwd'}, "
                          f"fp64 brute force, "
                          f"{osegs} segments in {dt:.1f}s"}
