@@ -482,6 +482,9 @@ DT_D float box_area(const float4* __restrict__ nodebox, int e) {
   return dx * dy + dy * dz + dz * dx;
 }
 
+#ifndef DT_WIDE_BLOCKS_PER_SM
+#define DT_WIDE_BLOCKS_PER_SM 1
+#endif
 __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __restrict__ ranges,
                                const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
                                const int* __restrict__ ibox, uint4* __restrict__ wnodes, float4* __restrict__ wbox,
@@ -496,7 +499,7 @@ __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __
       item = __ldcg(queue + idx);
       if (item != ~0ull) break;
       if (__ldcg(pending) == 0) return;              // no more work will be published
-      __nanosleep(spin < 8 ? 32 : 256);
+      __nanosleep(spin < 4 ? 64 : spin < 16 ? 256 : 1024);   // back off: every idle thread polls L2
     }
     __threadfence();                                   // acquire: the parent's writes before publishing
     const int b = (int)(item & 0xffffffffu), w = (int)(item >> 32);
@@ -731,7 +734,9 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
     if (!gq) {
       int per = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_wide_topdown, T, 0);
-      gq = std::max(1, per) * c->sm_count;
+      // fewer persistent threads than the occupancy allows: the queue is published top down, so
+      // most threads would only poll for unpublished entries
+      gq = std::max(1, std::min(per, DT_WIDE_BLOCKS_PER_SM)) * c->sm_count;
     }
     cudaMemsetAsync(c->wqueue, 0xff, (size_t)nf * sizeof(unsigned long long), st);
     k_wide_topdown_init<<<1, 1, 0, st>>>(c->wqueue, ctr, ctr + 1, c->iscal + 12, c->wdepth);
