@@ -8,6 +8,11 @@
  *     DESIGN.md), and a separate forward mode (dual numbers) used only to check it.
  * No blocking, fusion or reordering.  Shares no code with paper_2603_00413_b200/csrc.
  * Where the paper is silent or garbled the reading named R# in DESIGN.md §3 is followed.
+ * Parts that are our readings, with no value printed in the paper to pin them (DESIGN.md §2,
+ * "parity unpinned w.r.t. the paper"): the voxel + triplane shell env lookup (R14), the
+ * midpoint N_sigma quadrature (R10), the hash texture (R29) and the volume env (R30).  They are
+ * pinned by their own closed forms (constant / linear fields, one dense hash level == the
+ * vertex grid, zero density == the shell env) and by the FD and dot-product tests.
  */
 #include "oracle.h"
 
