@@ -88,7 +88,24 @@ inline uint64_t face_key(uint64_t pos, int ev, int face) {
   return pos | ((uint64_t)(uint32_t)(face + 1) << 20) | ((uint64_t)ev << 52);
 }
 
-const double BAND_BETA = 1e-4;   // edge band for the parity flags
+
+// ----------------------------------------------------------------------------- precision study
+// Built only with -DDTO_PRECISION_STUDY (tools/precision_study.py; never in liboracle.so):
+// rounds the value at one stage of the method to float32, to measure which stage's float32
+// rounding moves the radiance.  Stage bits: 1 camera ray, 2 hit point (child
+// origin), 4 child directions, 8 vertex normals, 16 shading normal, 32 env shell point,
+// 64 barycentrics (u, v) of the hit.
+#ifdef DTO_PRECISION_STUDY
+int g_study_mask = 0;
+inline void study_round(double& x, int bit) { if (g_study_mask & bit) x = (double)(float)x; }
+inline void study_round(Dual&, int) {}
+template <class S> inline void study_round(V3<S>& a, int bit) { study_round(a.x, bit); study_round(a.y, bit); study_round(a.z, bit); }
+#define DTO_STUDY(x, bit) study_round(x, bit)
+#else
+#define DTO_STUDY(x, bit) ((void)0)
+#endif
+
+const double BAND_BETA = 1e-5;   // edge band for the parity flags
 
 // ----------------------------------------------------------------------------- model
 template <class S> struct Model {
@@ -119,6 +136,7 @@ void vertex_normals(const std::vector<V3<S>>& V, const int32_t* F, int nf, std::
   for (auto& n : out) {
     S L = norm(n);
     n = val(L) > 0.0 ? scl(n, S(1.0) / L) : mk<S>(S(0.0), S(0.0), S(1.0));
+    DTO_STUDY(n, 8);
   }
 }
 
@@ -490,6 +508,7 @@ V3<S> env(const dto_scene* sc, V3<S> o, V3<S> d) {
     return L;
   }
   V3<S> p = shell_point(sc, o, dh);
+  DTO_STUDY(p, 32);
   return trilerp_vox(sc, p) + bilerp_plane(sc, 0, p.x, p.y) + bilerp_plane(sc, 1, p.x, p.z) +
          bilerp_plane(sc, 2, p.y, p.z);
 }
@@ -535,7 +554,10 @@ V3<S> trace(const Model<S>& m, V3<S> o, V3<S> d, int k, uint64_t pos, double w, 
   }
   const int32_t* F = sc->F + 3 * h.face;
   MT<S> r = moller_trumbore(o, d, m.V[F[0]], m.V[F[1]], m.V[F[2]]);  // differentiable (R15)
+  DTO_STUDY(r.u, 64);
+  DTO_STUDY(r.v, 64);
   V3<S> x = o + scl(d, r.t);
+  DTO_STUDY(x, 2);
   V3d gn = cross(m.Vd[F[1]] - m.Vd[F[0]], m.Vd[F[2]] - m.Vd[F[0]]);
   bool inside = dot(vald(d), gn) > 0.0;                             // R8
   if (k == sc->max_depth) {                                         // step 1 (R12, R13)
@@ -555,11 +577,14 @@ V3<S> trace(const Model<S>& m, V3<S> o, V3<S> d, int k, uint64_t pos, double w, 
   }
   bool fb;
   V3<S> ns = shading_normal(m, h.face, r.u, r.v, fb);
+  DTO_STUDY(ns, 16);
   V3<S> n = inside ? -ns : ns;
   S eta_i = inside ? m.ior : S(1.0), eta_t = inside ? S(1.0) : m.ior;
   Iface<S> I = interface(d, n, eta_i, eta_t);
   if (val(I.c_raw) < 1e-3) st.flags |= DTO_FLAG_GRAZING;
-  if (std::fabs(val(I.q)) < 1e-3) st.flags |= DTO_FLAG_NEARTIR;   // dR/dc_i ~ 1/sqrt(q) > 100 here
+  if (std::fabs(val(I.q)) < 1e-4) st.flags |= DTO_FLAG_NEARTIR;   // dR/dc_i ~ 1/sqrt(q)
+  DTO_STUDY(I.wr, 4);
+  DTO_STUDY(I.wt, 4);
   int ev = inside ? (I.tir ? EV_HIT_IN_TIR : EV_HIT_IN) : (I.tir ? EV_HIT_OUT_TIR : EV_HIT_OUT);
   st.sig_topo += mix64(topo_key(pos, ev));
   st.sig_face += mix64(face_key(pos, ev, h.face));
@@ -1046,6 +1071,8 @@ void get_ray(const dto_scene* sc, const int64_t* pid, const double* rays, int64_
   } else {
     camera_ray(sc, pid ? pid[i] : i, o, d);
   }
+  DTO_STUDY(o, 1);
+  DTO_STUDY(d, 1);
 }
 
 template <class Fn>
@@ -1157,6 +1184,10 @@ int dto_closest_hit(const dto_scene* s, const double* rays, int64_t n, double t_
   });
   return 0;
 }
+
+#ifdef DTO_PRECISION_STUDY
+void dto_study_set_mask(int mask) { g_study_mask = mask; }
+#endif
 
 int dto_camera_rays(const dto_scene* s, const int64_t* pixel_ids, int64_t n, double* rays) {
   for (int64_t i = 0; i < n; ++i) {

@@ -65,9 +65,9 @@ typedef struct {
 } dto_scene;
 
 /* Per-ray flag bits (parity protocol). */
-#define DTO_FLAG_EDGE    1  /* some node hit within BAND of an edge, near-missed a face, or tied */
+#define DTO_FLAG_EDGE    1  /* some node hit within 1e-5 (barycentric) of an edge, near-missed a face, or tied */
 #define DTO_FLAG_GRAZING 2  /* some node had cos(theta_i) < 1e-3 (incl. clamp)                   */
-#define DTO_FLAG_NEARTIR 4  /* some node had |eta^2 - sin^2| < 1e-3 (R depends on it like 1/sqrt)      */
+#define DTO_FLAG_NEARTIR 4  /* some node had |eta^2 - sin^2| < 1e-4 (R depends on it like 1/sqrt)      */
 
 /* Ray source for every entry point below: if `rays` != NULL it holds [n][6] =
  * (o.xyz, d.xyz) primary rays; else pixel ids view*H*W + y*W + x through the cameras. */

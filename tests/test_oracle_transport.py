@@ -231,3 +231,100 @@ def test_absorption_scales_inside_paths_only():
         Lb = O.env(osc, [0, 0, 0], [0, 0, 1.0])
         Lf = O.env(osc, [0, 0, 0], [0, 0, -1.0])
         np.testing.assert_allclose(out["rgb"][0], slab_expected(1.5, (sig,) * 3, 0.5, 4, Lf, Lb), atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- discriminating pins
+def test_vertex_normal_uniform_not_area_weighted():
+    """R6: n_v = normalize(sum of incident UNIT face normals).  The apex is shared
+    by a tiny face in the plane z = 0 (normal +z, area 2e-6) and a large face in the plane
+    x = 0 (normal +x, area 50): uniform weights give (1, 0, 1)/sqrt 2 exactly, area weights
+    (summing raw cross products) would give ~+x."""
+    V = np.array([[0, 0, 0], [1e-3, 0, 0], [0, 1e-3, 0], [0, 10, 0], [0, 0, 10]], np.float32)
+    F = np.array([[0, 1, 2], [0, 3, 4]], np.int32)
+    n = O.vertex_normals(O.OracleScene(T.scene(V, F, T.one_view(2, 2, (0, 0, 3)))))
+    np.testing.assert_allclose(n[0], [1 / math.sqrt(2), 0, 1 / math.sqrt(2)], atol=1e-15)
+    np.testing.assert_allclose(n[1:3], [[0, 0, 1.0]] * 2, atol=1e-15)
+    np.testing.assert_allclose(n[3:], [[1.0, 0, 0]] * 2, atol=1e-15)
+    # three unequal faces around a corner: still the normalised sum of the three axes
+    V = np.array([[0, 0, 0], [5, 0, 0], [0, 0.01, 0], [0, 0, 2]], np.float32)
+    F = np.array([[0, 2, 1], [0, 1, 3], [0, 3, 2]], np.int32)
+    n = O.vertex_normals(O.OracleScene(T.scene(V, F, T.one_view(2, 2, (0, 0, 3)))))
+    np.testing.assert_allclose(n[0], -np.ones(3) / math.sqrt(3), atol=1e-15)
+
+
+def triplane_linear_env(pres=5, radius=10.0, far_field=0):
+    """Zero voxel; each plane holds a distinct linear function of ITS OWN two axes, written
+    in the documented layout P_xy[y][x], P_xz[z][x], P_yz[z][y] (row index = second axis).
+    Per channel c: P_xy = A[c] (x, y), P_xz = B[c] (x, z), P_yz = C[c] (y, z)."""
+    ax = np.linspace(-radius, radius, pres)
+    row, col = np.meshgrid(ax, ax, indexing="ij")          # [row][col] coordinates
+    A = np.array([[1.0, 2.0], [0.5, -1.0], [3.0, 0.25]])    # (x, y) coefficients per channel
+    B = np.array([[-2.0, 0.75], [1.5, 4.0], [0.1, -3.0]])   # (x, z)
+    Cc = np.array([[0.3, -0.6], [-2.5, 1.0], [2.0, 5.0]])   # (y, z)
+    planes = np.zeros((3, pres, pres, 4), np.float32)
+    for c in range(3):
+        planes[0, :, :, c] = A[c, 0] * col + A[c, 1] * row   # P_xy[y][x]: col = x, row = y
+        planes[1, :, :, c] = B[c, 0] * col + B[c, 1] * row   # P_xz[z][x]: col = x, row = z
+        planes[2, :, :, c] = Cc[c, 0] * col + Cc[c, 1] * row  # P_yz[z][y]: col = y, row = z
+    vox = np.zeros((3, 3, 3, 4), np.float32)
+    env = S.Env(S.ENV_GRID, voxel=vox, planes=planes, radius=radius, far_field=far_field)
+
+    def expected(p):
+        x, y, z = p
+        return np.array([A[c, 0] * x + A[c, 1] * y + B[c, 0] * x + B[c, 1] * z + Cc[c, 0] * y + Cc[c, 1] * z
+                         for c in range(3)])
+    return env, expected
+
+
+def test_env_triplane_layout_and_far_field():
+    """R14 / P:91 triplane layout: every plane reproduces its own linear function exactly, so a
+    swapped row/column on any plane changes the value.  Far field (R14): the lookup point is
+    R_e d/|d| whatever the origin."""
+    V, F = S.icosphere(0)
+    cams = T.one_view(2, 2, (0, 0, 3))
+    g = np.random.default_rng(4)
+    for ff in (0, 1):
+        env, expected = triplane_linear_env(far_field=ff)
+        osc = O.OracleScene(T.scene(V, F, cams, env=env))
+        for _ in range(40):
+            o = g.uniform(-2, 2, 3)
+            d = g.normal(size=3)
+            dh = d / np.linalg.norm(d)
+            if ff:
+                p = 10.0 * dh
+            else:                                               # |o + t dh| = R_e, t > 0
+                b = o @ dh
+                p = o + (-b + math.sqrt(b * b - o @ o + 100.0)) * dh
+            np.testing.assert_allclose(O.env(osc, o, d), expected(p), atol=1e-11)
+    # far field with a linear voxel field: the value is R_e d^ for any origin
+    env = T.linear_grid_env()
+    env.far_field = 1
+    osc = O.OracleScene(T.scene(V, F, cams, env=env))
+    for _ in range(20):
+        o, d = g.uniform(-3, 3, 3), g.normal(size=3)
+        np.testing.assert_allclose(O.env(osc, o, d), 10.0 * d / np.linalg.norm(d), atol=1e-12)
+
+
+def test_camera_axes_opencv():
+    """R19: pinhole with OpenCV axes (+x right, +y down, +z forward) and +0.5 pixel centres.
+    A camera at the origin looking down +z (identity rotation) images the world point
+    (0.5, -0.25, 2) at column cx + fx*0.25 + ... (right of centre) and row above centre;
+    checked on the rays themselves and by rendering a small off-centre triangle."""
+    W, H, f = 40, 30, 30.0
+    K = np.array([[f, f, 19.5, 14.5]], np.float32)
+    c2w = np.zeros((1, 3, 4), np.float32)
+    c2w[0, :, :3] = np.eye(3)
+    cams = S.Cameras(W, H, K, c2w)
+    V = np.array([[0.45, -0.3, 2.0], [0.55, -0.3, 2.0], [0.5, -0.2, 2.0]], np.float32)
+    F = np.array([[0, 2, 1]], np.int32)
+    osc = O.OracleScene(T.scene(V, F, cams, env=T.lobe_env(), D=0, cap=S.CAP_ENV))
+    rays = O.camera_rays(osc, [0, W - 1, (H - 1) * W])
+    assert rays[0, 3] < 0 and rays[0, 4] < 0                     # top-left: -x, -y (up)
+    assert rays[1, 3] > 0 and rays[2, 4] > 0                     # top-right +x, bottom-left +y
+    # pixel centre (x + 0.5): pixel (19, 14) looks at ((19.5 - 19.5)/f, 0, 1) = +z exactly
+    r = O.camera_rays(osc, [14 * W + 19])
+    np.testing.assert_allclose(r[0, 3:], [0, 0, 1], atol=1e-15)
+    # the triangle around (0.5, -0.25, 2) projects to column 19.5 + 30*0.25 = 27, row 14.5 - 30*0.125 = 10.75
+    hit = O.render(osc, np.arange(W * H))["sig_topo"] != O.render(osc, [14 * W + 19])["sig_topo"][0]
+    ys, xs = np.divmod(np.flatnonzero(hit), W)
+    assert len(xs) > 0 and abs(xs.mean() + 0.5 - 27.0) < 1.0 and abs(ys.mean() + 0.5 - 10.75) < 1.0
