@@ -186,110 +186,6 @@ def camera_rays(osc: OracleScene, pixel_ids):
     return out
 
 
-FLAG_ILLCOND = 8
-F32_DIR_ERR = 1.2e-7     # ~2 ulp of a float32 unit direction component
-F32_POS_ERR = 1.2e-7     # ~2 ulp (relative to the mesh extent) of float32 geometry
-
-
-def ill_conditioned(osc: OracleScene, pixel_ids, tol: float = 5e-5, n_dirs: int = 2, nthreads: int = 0):
-    """Pixels whose radiance moves by more than `tol` when the camera ray direction moves by
-    the float32 rounding of its components (F32_DIR_ERR), or when the vertices move by the
-    float32 rounding of the mesh geometry (F32_POS_ERR): float32 arithmetic cannot hold them
-    to 1e-4 whatever the implementation.  Estimated with float64 central
-    differences along random tangents / displacements (eps = 1e-7, inside the smooth region)."""
-    rays = camera_rays(osc, pixel_ids)
-    n = rays.shape[0]
-    g = np.random.default_rng(1234)
-    sens = np.zeros(n)
-    eps = 1e-7
-    base_sig = None
-    for k in range(n_dirs):
-        u = g.normal(size=(n, 3))
-        d = rays[:, 3:]
-        u -= d * (u * d).sum(1, keepdims=True)
-        u /= np.linalg.norm(u, axis=1, keepdims=True)
-        rp = rays.copy(); rp[:, 3:] += eps * u
-        rm = rays.copy(); rm[:, 3:] -= eps * u
-        a = render(osc, rays=rp, nthreads=nthreads)
-        b = render(osc, rays=rm, nthreads=nthreads)
-        s = np.abs(a["rgb"] - b["rgb"]).max(1) / (2 * eps)
-        s[a["sig_topo"] != b["sig_topo"]] = np.inf
-        sens = np.maximum(sens, s)
-    ill = sens * F32_DIR_ERR > tol
-    # geometry: the device reads the same float32 vertices but derives edges, normals and hit
-    # points in float32 (~1-2 ulp of the mesh extent each); same estimate along random
-    # per-vertex displacements of that size
-    scale = float(np.abs(osc.V).max()) or 1.0
-    h = 1e-7 * scale
-    V0 = osc.V.astype(np.float64) if osc.V64 is None else osc.V64
-    old = osc.s.V64
-    sens_v = np.zeros(n)
-    try:
-        for k in range(n_dirs):
-            U = g.normal(size=V0.shape)
-            U /= np.linalg.norm(U, axis=1, keepdims=True)
-            Vp, Vm = np.ascontiguousarray(V0 + h * U), np.ascontiguousarray(V0 - h * U)
-            osc.s.V64 = _p(Vp)
-            a = render(osc, pixel_ids, nthreads=nthreads)
-            osc.s.V64 = _p(Vm)
-            b = render(osc, pixel_ids, nthreads=nthreads)
-            s = np.abs(a["rgb"] - b["rgb"]).max(1) / (2 * h)
-            s[a["sig_topo"] != b["sig_topo"]] = np.inf
-            sens_v = np.maximum(sens_v, s)
-    finally:
-        osc.s.V64 = old
-    return ill | (sens_v * F32_POS_ERR * scale > tol)
-
-
-def ill_conditioned_grad(osc: OracleScene, pixel_ids, grad_rgb, tol: float = 1e-2, n_dirs: int = 2,
-                         nthreads: int = 0, rays=None):
-    """Pixels whose reverse-mode result float32 cannot hold: the fp64 VJP of the pixel's own
-    upstream gradient (vertex block, or the IoR scalar) moves by more than `tol` relative when
-    the camera ray direction moves by its float32 rounding (F32_DIR_ERR along random tangents),
-    with the path topology unchanged.  The gradient analogue of ill_conditioned() (DESIGN.md
-    §4): e.g. near a grazing or near-TIR event the VJP moves by percents for a 2-ulp change of
-    the direction while the radiance moves by 1e-6.  One VJP per pixel and perturbation, run
-    in parallel threads (the library releases the GIL).  `rays` ([n, 6] o|d) replaces the
-    camera rays of `pixel_ids`."""
-    from concurrent.futures import ThreadPoolExecutor
-    rays = camera_rays(osc, pixel_ids) if rays is None else np.array(rays, np.float64).reshape(-1, 6)
-    g = np.ascontiguousarray(grad_rgb, np.float64).reshape(-1, 3)
-    n = rays.shape[0]
-
-    def vjp(i, r):
-        gV, gi, _ = backward(osc, g[i:i + 1], rays=r[None], nthreads=1)
-        v = gV.ravel()
-        idx = np.flatnonzero(v)
-        return idx, v[idx], gi, int(render(osc, rays=r[None], nthreads=1)["sig_topo"][0])
-
-    def rel(a, b):
-        u = np.union1d(a[0], b[0])
-        x = np.zeros(len(u))
-        y = np.zeros(len(u))
-        x[np.searchsorted(u, a[0])] = a[1]
-        y[np.searchsorted(u, b[0])] = b[1]
-        dv = np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)
-        di = abs(a[2] - b[2]) / max(abs(b[2]), 1e-300)
-        return np.inf if a[3] != b[3] else max(dv, di)
-
-    workers = nthreads or os.cpu_count() or 1
-    sens = np.zeros(n)
-    live = np.flatnonzero(np.abs(g).sum(1) > 0)
-    with ThreadPoolExecutor(workers) as ex:
-        base = dict(zip(live, ex.map(lambda i: vjp(i, rays[i]), live)))
-        rng = np.random.default_rng(4321)
-        for _ in range(n_dirs):
-            u = rng.normal(size=(n, 3))
-            d = rays[:, 3:]
-            u -= d * (u * d).sum(1, keepdims=True)
-            u /= np.linalg.norm(u, axis=1, keepdims=True)
-            rp = rays.copy()
-            rp[:, 3:] += F32_DIR_ERR * u
-            for i, r in zip(live, ex.map(lambda i: vjp(i, rp[i]), live)):
-                sens[i] = max(sens[i], rel(r, base[i]))
-    return sens > tol
-
-
 def vertex_normals(osc: OracleScene):
     out = np.zeros((osc.V.shape[0], 3))
     assert lib().dto_vertex_normals(osc.ref, _p(out)) == 0

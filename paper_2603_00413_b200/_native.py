@@ -101,17 +101,28 @@ SIGNATURES = {
 }
 
 _lib = None
+_lib_path = LIB_PATH
+
+
+def use_library(path: str) -> None:
+    """Tuning sweeps only (tools/bench_variant.py): load a variant build of libdifftrans.so
+    (same ABI, other compile-time constants) instead of the in-tree one.  Must be called
+    before the first lib()."""
+    global _lib_path
+    assert _lib is None, "libdifftrans already loaded"
+    _lib_path = path
 
 
 def lib():
     """Load libdifftrans.so (building it with nvcc first if it is absent)."""
     global _lib
     if _lib is None:
-        path = os.environ.get("DT_LIBDIFFTRANS", LIB_PATH)   # tuning variants (build.build(out=...))
+        path = _lib_path
         if not os.path.exists(path):
+            if path != LIB_PATH:
+                raise FileNotFoundError(path)
             from . import build as _build
             _build.build()
-            path = LIB_PATH
         _lib = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(_lib, name)

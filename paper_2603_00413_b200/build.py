@@ -28,7 +28,7 @@ def _stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, defines=(), out: str = None) -> str:
     """Build libdifftrans.so; `defines` (e.g. ["DT_BWD_MINB=6"]) and `out` build a tuning
-    variant elsewhere (selected at run time with DT_LIBDIFFTRANS=<path>)."""
+    variant elsewhere (tools/bench_variant.py loads it)."""
     lib = out or LIB
     if not force and not defines and out is None and not _stale():
         return LIB

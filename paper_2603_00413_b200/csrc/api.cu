@@ -41,21 +41,22 @@ cudaError_t alloc_arena(dt_ctx* c, int64_t cap) {
   if (c->rec.o) cudaFree(c->rec.o);
   c->rec = Records{};
   c->arena_cap = 0;
-  float4* base = nullptr;
-  const int lanes = kRecordBytes / 16 + (c->arena_vol ? 2 : 0);
-  cudaError_t e = cudaMalloc(&base, (size_t)cap * lanes * 16);
+  char* base = nullptr;
+  const size_t bytes = (size_t)cap * (kRecordBytes + (c->arena_vol ? 32 : 0));
+  cudaError_t e = cudaMalloc(&base, bytes);
   if (e != cudaSuccess) return e;
-  c->rec.o = base;
-  c->rec.d = base + cap;
-  c->rec.thr = base + 2 * cap;
-  c->rec.hit = base + 3 * cap;
-  c->rec.tau = base + 4 * cap;
-  c->rec.lsub = base + 5 * cap;
-  c->rec.go = base + 6 * cap;
-  c->rec.gd = base + 7 * cap;
+  c->rec.o = reinterpret_cast<Vec64*>(base);
+  c->rec.d = c->rec.o + cap;
+  float4* f = reinterpret_cast<float4*>(c->rec.d + cap);
+  c->rec.thr = f;
+  c->rec.hit = f + cap;
+  c->rec.tau = f + 2 * cap;
+  c->rec.lsub = f + 3 * cap;
+  c->rec.go = f + 4 * cap;
+  c->rec.gd = f + 5 * cap;
   if (c->arena_vol) {
-    c->rec.mq = base + 8 * cap;
-    c->rec.mg = base + 9 * cap;
+    c->rec.mq = f + 6 * cap;
+    c->rec.mg = f + 7 * cap;
   }
   c->arena_cap = cap;
   return cudaSuccess;
@@ -213,13 +214,6 @@ dt_status dt_create(int32_t device, dt_ctx** out) {
   c->device = device;
   cudaSetDevice(device);
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
-  if (const char* v = getenv("DT_LEAF_MAX")) c->leaf_max = std::max(1, std::min(4, atoi(v)));
-  if (const char* v = getenv("DT_TRAV_MODE")) c->trav_mode = std::max(0, std::min(3, atoi(v)));
-  if (const char* v = getenv("DT_LEAF_VOTE")) c->leaf_vote = std::max(1, std::min(32, atoi(v)));
-  if (const char* v = getenv("DT_TRAV_CHUNK")) c->trav_chunk = std::max(32, atoi(v));
-  if (const char* v = getenv("DT_SORT_LANES")) c->sort_lanes = atoi(v) != 0;
-  if (const char* v = getenv("DT_WIDE_MODE")) c->wide_mode = std::max(0, std::min(1, atoi(v)));
-  if (const char* v = getenv("DT_PRIMARY_PACKET")) c->prim_packet = atoi(v) != 0;
   cudaError_t e;
   if ((e = cudaMalloc(&c->lvl, LV_INTS * sizeof(int))) || (e = cudaMallocHost(&c->host_lvl, LV_INTS * sizeof(int))) ||
       (e = cudaMalloc(&c->gior, 4 * sizeof(float))) || (e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long))) ||
@@ -239,7 +233,7 @@ void dt_destroy(dt_ctx* c) {
   void* ptrs[] = {c->V, c->F, c->nrm, c->fnrm, c->nodes, c->tris, c->keys, c->vals, c->hist, c->children,
                   c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, c->vstart, c->vcorner, c->scal,
                   c->iscal, c->rec.o, c->lvl, c->sigma_snap, c->gV, c->gN, c->gVn, c->gS, c->fe, c->gsig, c->gior,
-                  c->counters, c->ranges, c->bdepth, c->wflag, c->widx, c->wbox, c->wdepth, c->scratch,
+                  c->counters, c->ranges, c->wbox, c->wdepth, c->scratch,
                   c->nbr_start, c->nbr_cnt, c->nbr, c->nbr_owner, c->scan_part, c->wqueue};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -364,11 +358,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.sig_t = (unsigned long long*)sig_topo;
   a.sig_f = (unsigned long long*)sig_face;
   a.counters = c->counters;
-  a.trav_mode = c->trav_mode;
-  a.trav_chunk = c->trav_chunk;
-  a.prim_packet = c->prim_packet;
-  a.leaf_vote = c->leaf_vote;
-  a.sort_lanes = c->sort_lanes;
+  a.grids = c->grid_cache;
 
   // a previous asynchronous forward is checked first (its readback has long completed)
   dt_status prev = consume_async(c);
@@ -492,7 +482,7 @@ dt_status dt_trace_backward(dt_ctx* c, const float* grad_rgb, float* grad_V, flo
   DT_CU(cudaMemsetAsync(c->gior, 0, sizeof(float), st));
   BwdLaunch b{};
   b.s = c->fwd_scene;
-  b.sort_lanes = c->sort_lanes;
+  b.grids = c->grid_cache;
   b.r = c->rec;
   b.lvl = c->lvl;
   b.cap = c->arena_cap;
@@ -667,7 +657,7 @@ dt_status dt_debug_vertex_normals(dt_ctx* c, float* out, void* stream) {
   cudaSetDevice(c->device);
   if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_debug_vertex_normals: call dt_build_bvh first");
   DT_ARG(out, "dt_debug_vertex_normals: out is NULL");
-  DT_CU(cudaMemcpy2DAsync(out, 12, c->nrm, 16, 12, c->nv, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  DT_CU(launch_normals_to_f32(c->nrm, c->nv, out, (cudaStream_t)stream));
   return DT_OK;
 }
 

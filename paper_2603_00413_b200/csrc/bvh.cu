@@ -38,15 +38,19 @@ __global__ void k_snapshot(const float* __restrict__ Vin, int nv, float4* __rest
   }
 }
 
-// unit face normals and centroid bounds (Morton quantisation)
-__global__ void k_faces(const float4* __restrict__ V, const int* __restrict__ F, int nf, float4* __restrict__ fn,
+// unit face normals (float64, the shading normals' inputs) and centroid bounds (Morton
+// quantisation)
+__global__ void k_faces(const float4* __restrict__ V, const int* __restrict__ F, int nf, D4* __restrict__ fn,
                         int* __restrict__ ibox) {
   float3 lo = f3(kInf, kInf, kInf), hi = -lo;
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x) {
     float3 a = f3(V[F[3 * f]]), b = f3(V[F[3 * f + 1]]), c = f3(V[F[3 * f + 2]]);
-    float3 n = cross(b - a, c - a);
-    float L = length(n);
-    fn[f] = L > 0.0f ? f4(n * (1.0f / L), L) : make_float4(0, 0, 0, 0);  // zero-area faces add 0 (R6)
+    const double3 a64 = d3(a);
+    const double3 n = cross(d3(b) - a64, d3(c) - a64);
+    const double L = length(n);
+    D4 o = {0.0, 0.0, 0.0, 0.0};                                         // zero-area faces add 0 (R6)
+    if (L > 0.0) o = D4{n.x / L, n.y / L, n.z / L, L};
+    fn[f] = o;
     float3 cen = (a + b + c) * (1.0f / 3.0f);
     lo = fminf3(lo, cen);
     hi = fmaxf3(hi, cen);
@@ -76,14 +80,15 @@ __global__ void k_csr(const unsigned* __restrict__ keys, int n3, int nv, int* __
   }
 }
 
-// n_v = normalize(sum of incident unit face normals), gathered in face order (deterministic)
+// n_v = normalize(sum of incident unit face normals) (R6), float64, gathered in face
+// order (deterministic)
 __global__ void k_vertex_normals(const int* __restrict__ vstart, const unsigned* __restrict__ corner,
-                                 const float4* __restrict__ fn, int nv, float4* __restrict__ nrm) {
+                                 const D4* __restrict__ fn, int nv, D4* __restrict__ nrm) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
-    float3 s = f3(0, 0, 0);
-    for (int j = vstart[v]; j < vstart[v + 1]; ++j) s += f3(fn[corner[j] / 3]);
-    float L = length(s);
-    nrm[v] = L > 0.0f ? f4(s * (1.0f / L), L) : make_float4(0, 0, 1, 0);
+    double3 s = d3(0, 0, 0);
+    for (int j = vstart[v]; j < vstart[v + 1]; ++j) s += xyz(fn[corner[j] / 3]);
+    const double L = length(s);
+    nrm[v] = L > 0.0 ? D4{s.x / L, s.y / L, s.z / L, L} : D4{0.0, 0.0, 1.0, 0.0};
   }
 }
 
@@ -347,23 +352,6 @@ __global__ void k_refit(const float4* __restrict__ V, const int* __restrict__ F,
 // unused slot (qlo = 255 > qhi = 0); otherwise leaf: ref = -1 - (first << 2 | (count - 1)).
 DT_D int bsize(const int2* __restrict__ ranges, int ref) { return ref < 0 ? 1 : ranges[ref].y - ranges[ref].x + 1; }
 
-__global__ void k_bdepth(const int* __restrict__ parent_int, int n_int, int* __restrict__ depth) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_int; i += gridDim.x * blockDim.x) {
-    int dd = 0;
-    for (int p = parent_int[i]; p >= 0; p = parent_int[p]) ++dd;
-    depth[i] = dd;
-  }
-}
-
-__global__ void k_wide_flags(const int* __restrict__ depth, const int2* __restrict__ ranges, int n_int,
-                             unsigned* __restrict__ flag, unsigned* __restrict__ scan_in, int leaf_max) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_int; i += gridDim.x * blockDim.x) {
-    unsigned f = (i == 0) || ((depth[i] & 1) == 0 && bsize(ranges, i) > leaf_max);
-    flag[i] = f;
-    scan_in[i] = f;
-  }
-}
-
 // Quantise and write wide node w: its entries ent[0..ne) (binary refs; internal entries carry
 // their own wide index in wref), boxes padded outward so the slab test stays conservative.
 DT_D void write_wide_node(int i, const int ent[4], const int wref[4], int ne, unsigned w, int wd, double pad,
@@ -432,45 +420,16 @@ DT_D double wide_pad(const int* __restrict__ ibox) {
   return (double)m * 4e-6 + 1e-30;
 }
 
-// Collapse pattern 0: the wide roots are the binary nodes at even depth, each opening its
-// internal children once (2..4 entries).
-__global__ void k_wide_build(const int2* __restrict__ children, const int2* __restrict__ ranges,
-                             const unsigned* __restrict__ flag, const unsigned* __restrict__ widx,
-                             const int* __restrict__ depth, const float4* __restrict__ leafbox,
-                             const float4* __restrict__ nodebox, int n, const int* __restrict__ ibox,
-                             uint4* __restrict__ wnodes, float4* __restrict__ wbox, int* __restrict__ wdepth,
-                             int* __restrict__ nwide, int leaf_max) {
-  const double pad = wide_pad(ibox);
-  int n_int = n - 1;
-  int total = max(n_int, 1);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    if (i == total - 1) *nwide = n_int == 0 ? 1 : (int)(widx[i] + flag[i]);
-    if (n_int > 0 && !flag[i]) continue;
-    int ent[4], wref[4] = {0, 0, 0, 0}, ne = 0;
-    if (n_int == 0) {
-      ent[ne++] = ~0;                                   // single triangle
-    } else {
-      int2 ch = children[i];
-      int cs[2] = {ch.x, ch.y};
-      for (int q = 0; q < 2; ++q) {
-        int c = cs[q];
-        if (c < 0 || bsize(ranges, c) <= leaf_max) {
-          ent[ne++] = c;
-        } else {
-          int2 g = children[c];
-          ent[ne++] = g.x;
-          ent[ne++] = g.y;
-        }
-      }
-    }
-    for (int c = 0; c < ne; ++c)
-      if (ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max) wref[c] = (int)widx[ent[c]];
-    write_wide_node(n_int == 0 ? ~0 : i, ent, wref, ne, n_int == 0 ? 0u : widx[i], n_int == 0 ? 0 : depth[i] / 2,
-                    pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
-  }
+// A one-triangle mesh: the root wide node holds the single leaf.
+__global__ void k_wide_single(const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
+                              const int2* __restrict__ ranges, const int* __restrict__ ibox, uint4* __restrict__ wnodes,
+                              float4* __restrict__ wbox, int* __restrict__ wdepth, int* __restrict__ nwide, int leaf_max) {
+  const int ent[4] = {~0, 0, 0, 0}, wref[4] = {0, 0, 0, 0};
+  *nwide = 1;
+  write_wide_node(~0, ent, wref, 1, 0u, 0, wide_pad(ibox), leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
 }
 
-// Collapse pattern 1 (surface-area greedy): top down from the root, a wide node starts with
+// Collapse to the 4-wide BVH (surface-area greedy): top down from the root, a wide node starts with
 // its binary node's two children and repeatedly opens the internal entry of largest surface
 // area until it has 4 entries (fuller nodes, larger boxes split first).  A work queue indexed
 // by wide node id: a node's unopened internal entries get fresh ids (atomic counter) and are
@@ -649,9 +608,10 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
     size_t cap = nv;
     cudaFree(c->V); cudaFree(c->nrm); cudaFree(c->gV); cudaFree(c->gN); cudaFree(c->gVn); cudaFree(c->gS);
     cudaFree(c->vstart);
-    c->V = c->nrm = c->gV = c->gN = c->gVn = c->gS = nullptr;
+    c->V = c->gV = c->gN = c->gVn = c->gS = nullptr;
+    c->nrm = nullptr;
     c->vstart = nullptr;
-    if ((e = cudaMalloc(&c->V, cap * 16)) || (e = cudaMalloc(&c->nrm, cap * 16)) || (e = cudaMalloc(&c->gV, cap * 16)) ||
+    if ((e = cudaMalloc(&c->V, cap * 16)) || (e = cudaMalloc(&c->nrm, cap * sizeof(D4))) || (e = cudaMalloc(&c->gV, cap * 16)) ||
         (e = cudaMalloc(&c->gN, cap * 16)) || (e = cudaMalloc(&c->gVn, cap * 16)) || (e = cudaMalloc(&c->gS, cap * 16)) ||
         (e = cudaMalloc(&c->vstart, (cap + 1) * sizeof(int))))
       return e;
@@ -660,20 +620,19 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   if ((size_t)nf > c->cap_nf) {
     size_t cap = nf;
     void* old[] = {c->F, c->fnrm, c->nodes, c->tris, c->keys, c->vals, c->children, c->parent_int, c->parent_leaf,
-                   c->rflags, c->nodebox, c->leafbox, c->vcorner, c->fe, c->ranges, c->bdepth, c->wflag, c->widx,
+                   c->rflags, c->nodebox, c->leafbox, c->vcorner, c->fe, c->ranges,
                    c->wbox, c->wdepth};
     for (void* p : old)
       if (p) cudaFree(p);
     size_t ks = 2 * 3 * cap;   // keys/vals ping-pong sized for the 3*nf corner sort
-    if ((e = cudaMalloc(&c->F, cap * 3 * sizeof(int))) || (e = cudaMalloc(&c->fnrm, cap * 16)) ||
+    if ((e = cudaMalloc(&c->F, cap * 3 * sizeof(int))) || (e = cudaMalloc(&c->fnrm, cap * sizeof(D4))) ||
         (e = cudaMalloc(&c->nodes, cap * 64)) || (e = cudaMalloc(&c->tris, cap * 48)) ||
         (e = cudaMalloc(&c->keys, ks * sizeof(unsigned))) || (e = cudaMalloc(&c->vals, ks * sizeof(unsigned))) ||
         (e = cudaMalloc(&c->children, cap * sizeof(int2))) || (e = cudaMalloc(&c->parent_int, cap * sizeof(int))) ||
         (e = cudaMalloc(&c->parent_leaf, cap * sizeof(int))) || (e = cudaMalloc(&c->rflags, cap * sizeof(int))) ||
         (e = cudaMalloc(&c->nodebox, cap * 32)) || (e = cudaMalloc(&c->leafbox, cap * 32)) ||
         (e = cudaMalloc(&c->vcorner, 3 * cap * sizeof(unsigned))) || (e = cudaMalloc(&c->fe, 2 * cap * 16)) ||
-        (e = cudaMalloc(&c->ranges, cap * sizeof(int2))) || (e = cudaMalloc(&c->bdepth, cap * sizeof(int))) ||
-        (e = cudaMalloc(&c->wflag, cap * sizeof(unsigned))) || (e = cudaMalloc(&c->widx, cap * sizeof(unsigned))) ||
+        (e = cudaMalloc(&c->ranges, cap * sizeof(int2))) ||
         (e = cudaMalloc(&c->wbox, cap * 32)) || (e = cudaMalloc(&c->wdepth, cap * sizeof(int))))
       return e;
     c->cap_nf = cap;
@@ -721,7 +680,7 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   k_refit<<<gf, T, 0, st>>>(c->V, c->F, sv, nf, c->children, c->parent_int, c->parent_leaf, c->rflags, c->leafbox,
                             c->nodebox);
   // collapse to the quantised 4-wide BVH
-  if (nf > 1 && c->wide_mode == 1) {                    // surface-area greedy, top down
+  if (nf > 1) {                                         // surface-area greedy, top down
     if (!c->wqueue || c->wqueue_cap < nf) {
       cudaFree(c->wqueue);
       c->wqueue = nullptr;
@@ -730,7 +689,7 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
       c->wqueue_cap = nf;
     }
     int* ctr = reinterpret_cast<int*>(c->wqueue + c->wqueue_cap);
-    static int gq = 0;
+    int& gq = c->grid_cache[kGridWide];                 // per context (device): occupancy x SMs
     if (!gq) {
       int per = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_wide_topdown, T, 0);
@@ -745,15 +704,8 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
                                      ctr, ctr + 1, nf - 1, c->leaf_max);
     launches += 2;
   } else {
-    if (nf > 1) {
-      k_bdepth<<<gf, T, 0, st>>>(c->parent_int, nf - 1, c->bdepth);
-      k_wide_flags<<<gf, T, 0, st>>>(c->bdepth, c->ranges, nf - 1, c->wflag, c->widx, c->leaf_max);
-      if ((e = scan_exclusive(c->widx, nf - 1, c->scan_part, st, &launches))) return e;
-      launches += 2;
-    }
-    k_wide_build<<<gf, T, 0, st>>>(c->children, c->ranges, c->wflag, c->widx, c->bdepth, c->leafbox, c->nodebox, nf,
-                                   c->iscal, reinterpret_cast<uint4*>(c->nodes), c->wbox, c->wdepth, c->iscal + 12,
-                                   c->leaf_max);
+    k_wide_single<<<1, 1, 0, st>>>(c->leafbox, c->nodebox, c->ranges, c->iscal, reinterpret_cast<uint4*>(c->nodes),
+                                   c->wbox, c->wdepth, c->iscal + 12, c->leaf_max);
     launches += 1;
   }
   k_pack_tris<<<gf, T, 0, st>>>(c->V, c->F, sv, nf, c->tris);

@@ -44,7 +44,7 @@ struct DevScene {
   // mesh snapshot (dt_build_bvh)
   const float4* V;      // [nv] xyz
   const int* F;         // [nf*3]
-  const float4* nrm;    // [nv] vertex normal xyz, |sum of unit face normals| in w
+  const D4* nrm;        // [nv] vertex normal xyz (float64), |sum of unit face normals| in w
   int nv, nf;
   // LBVH
   const float4* nodes;  // [(nf-1)*4] 64-B nodes: two child AABBs + child refs
@@ -92,6 +92,24 @@ DT_D void camera_ray(const float* K, const float* c2w, int W, int H, int64_t pid
   o = f3(m[3], m[7], m[11]);
 }
 
+// The same camera ray in float64: the tracer's geometric state.  Every product
+// term matches the float32 formula above; only the precision differs.
+DT_D void camera_ray64(const float* K, const float* c2w, int W, int H, int64_t pid, double3& o, double3& d) {
+  const int64_t hw = (int64_t)W * H;
+  const int view = (int)(pid / hw);
+  const int64_t rem = pid - (int64_t)view * hw;
+  const int y = (int)(rem / W), x = (int)(rem - (int64_t)y * W);
+  const float* k = K + 4 * view;
+  const float* m = c2w + 12 * view;
+  const double dx = ((double)x + 0.5 - (double)k[2]) * rcp64((double)k[0]);
+  const double dy = ((double)y + 0.5 - (double)k[3]) * rcp64((double)k[1]);
+  const double3 w = d3((double)m[0] * dx + (double)m[1] * dy + (double)m[2],
+                       (double)m[4] * dx + (double)m[5] * dy + (double)m[6],
+                       (double)m[8] * dx + (double)m[9] * dy + (double)m[10]);
+  d = w * rsqrt64(dot(w, w));
+  o = d3((double)m[3], (double)m[7], (double)m[11]);
+}
+
 // ----------------------------------------------------------------------------- intersection
 // Explicit intrinsics (fixed fma / rounding, never re-contracted by the compiler), so the LBVH
 // traversal, the brute-force test and the backward replay produce bit-identical (t, u, v).
@@ -134,16 +152,6 @@ DT_D bool intersect_tri(float3 o, float3 d, float3 v0, float3 e1, float3 e2, flo
   t = __fmul_rn(dot_rn(e2, q), inv);
   return t > t_lo;
 }
-// The (u, v) intersect_tri computes for the same operands, bit for bit (same operation
-// sequence), for a hit whose face and t are already known (the shade pass).
-DT_D void tri_uv(float3 o, float3 d, float3 v0, float3 e1, float3 e2, float& u, float& v) {
-  float3 p = cross_rn(d, e2);
-  float inv = rcp_approx(dot_rn(e1, p));
-  float3 s = sub_rn(o, v0);
-  u = __fmul_rn(dot_rn(s, p), inv);
-  v = __fmul_rn(dot_rn(d, cross_rn(s, e1)), inv);
-}
-
 // ----------------------------------------------------------------------------- wide nodes
 // 64-B 4-wide node (layout in bvh.cu, write_wide_node): child c's box decodes to
 // lo = p + qlo * s, hi = p + qhi * s with per-axis power-of-two scales s (one fma per plane).
@@ -330,49 +338,6 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
   return false;
 }
 #undef DT_CX
-#define DT_CX2(a, b)                                             \
-  if (k##b < k##a) {                                             \
-    float tk = k##a; k##a = k##b; k##b = tk;                     \
-    int tr = r##a; r##a = r##b; r##b = tr;                       \
-  }
-
-// Split halves of trav_step for the warp-synchronous traversal with postponed leaves
-// (k_traverse_level): trav_node visits the wide node T.cur and leaves the nearest hit child
-// (node or leaf) in T.cur, or kEmptyRef if none; trav_leaf tests one leaf's triangles.
-DT_D void trav_node(const DevScene& s, float3 o, float3 inv, Trav& T, int* sstack, int stride, int* lstack, int& err,
-                    int& visits) {
-  const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)T.cur;
-  uint4 n0, n1, n2, n3;
-  ldg256(nd, n0, n1);
-  ldg256(nd + 2, n2, n3);
-  ++visits;
-  int r0 = (int)n2.z, r1 = (int)n2.w, r2 = (int)n3.x, r3 = (int)n3.y;
-  float key[4];
-  node_keys(n0, n1, n2, n3, {r0, r1, r2, r3}, o, inv, T.bt, key);
-  float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
-  DT_CX2(0, 1) DT_CX2(2, 3) DT_CX2(0, 2) DT_CX2(1, 3) DT_CX2(1, 2)
-  int push[3] = {r3, r2, r1};
-  float pk[3] = {k3, k2, k1};
-#pragma unroll
-  for (int q = 0; q < 3; ++q)
-    if (pk[q] < kInf) stack_push(T, sstack, stride, lstack, push[q], err);
-  T.cur = k0 < kInf ? r0 : kEmptyRef;
-}
-
-DT_D void trav_leaf(const DevScene& s, float3 o, float3 d, float t_lo, int leaf, Trav& T, int& tests) {
-  int first, cnt;
-  leaf_range(leaf, first, cnt);
-  for (int j = first; j < first + cnt; ++j) {
-    const float4* tr = s.tris + 3 * (size_t)j;
-    float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
-    float t, u, v;
-    ++tests;
-    if (intersect_tri(o, d, f3(a), f3(b), f3(c), t_lo, t, u, v)) {
-      int id = __float_as_int(a.w);
-      if (t < T.bt || (t == T.bt && id < T.best)) { T.bt = t; T.bu = u; T.bv = v; T.best = id; }
-    }
-  }
-}
 
 // Closest hit (whole traversal).  Returns the original face id or -1.
 DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, float& bu, float& bv, int* sstack,
@@ -389,179 +354,127 @@ DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, 
   return T.best;
 }
 
-// Warp-packet closest hit for coherent rays (camera rays of an 8x4 pixel tile): the warp
-// walks one shared node sequence -- a child is entered if any lane's ray enters it (in the
-// order of the first active lane's entry distances), every lane tests its own ray against
-// the node boxes and leaf triangles, so each node is fetched once per warp (broadcast) and
-// the warp never diverges.  Same result as traverse() per ray: a lane's closest hit is found
-// because any box that lane enters is visited.  Must be called by all 32 lanes; inactive
-// lanes pass active = false.  wstack: this warp's shared-memory stack (kPacketStack entries).
-constexpr int kPacketStack = 96;
-DT_D int traverse_packet(const DevScene& s, float3 o, float3 d, bool active, float& bt, float& bu, float& bv,
-                         int* wstack, int& err, int& visits, int& tests) {
-  const float3 inv = safe_inv(d);
-  const unsigned amask = __ballot_sync(~0u, active);
-  int best = -1;
-  bt = kInf;
-  bu = bv = 0.f;
-  if (!amask) return -1;
-  const int leader = __ffs(amask) - 1;
-  const float tcap = active ? kInf : -1.0f;     // inactive lanes never enter a box
-  int sp = 0, cur = 0;
-  while (true) {
-    if (cur >= 0) {
-      const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)cur;
-      uint4 n0, n1, n2, n3;
-      ldg256(nd, n0, n1);
-      ldg256(nd + 2, n2, n3);
-      visits += active;
-      const int r[4] = {(int)n2.z, (int)n2.w, (int)n3.x, (int)n3.y};
-      const float3 sc = node_scale(n0, n3);
-      const float3 A = f3(sc.x * inv.x, sc.y * inv.y, sc.z * inv.z);
-      const float3 B = f3((__uint_as_float(n0.x) - o.x) * inv.x, (__uint_as_float(n0.y) - o.y) * inv.y,
-                          (__uint_as_float(n0.z) - o.z) * inv.z);
-      float key[4];
-      unsigned hm[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float tx0 = fmaf(qbyte(n1.x, c), A.x, B.x), tx1 = fmaf(qbyte(n1.w, c), A.x, B.x);
-        float ty0 = fmaf(qbyte(n1.y, c), A.y, B.y), ty1 = fmaf(qbyte(n2.x, c), A.y, B.y);
-        float tz0 = fmaf(qbyte(n1.z, c), A.z, B.z), tz1 = fmaf(qbyte(n2.y, c), A.z, B.z);
-        float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
-        float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), fminf(bt, tcap)));
-        const bool h = tmin * 0.99999f <= tmax * 1.00001f && r[c] != kEmptyRef;
-        hm[c] = __ballot_sync(~0u, h);
-        // ordering key: the leader's entry distance; entered only by other lanes: after those;
-        // entered by nobody: +inf (dropped)
-        const float lk = __shfl_sync(~0u, h ? tmin : 3.0e38f, leader);
-        key[c] = hm[c] ? lk : kInf;
-      }
-      // warp-uniform: the entered children, nearest (leader's distance) first
-      int ord[4] = {0, 1, 2, 3};
-#pragma unroll
-      for (int i = 1; i < 4; ++i)
-#pragma unroll
-        for (int j = i; j > 0; --j)
-          if (key[ord[j]] < key[ord[j - 1]]) { int tmp = ord[j]; ord[j] = ord[j - 1]; ord[j - 1] = tmp; }
-      int list[4], ne = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (hm[ord[q]]) list[ne++] = r[ord[q]];
-      if (ne > 0) {
-        for (int q = ne - 1; q >= 1; --q) {          // farthest first: the nearest is on top
-          if (sp < kPacketStack) { if (lane_id() == 0) wstack[sp] = list[q]; } else err = 1;
-          ++sp;
-        }
-        __syncwarp();
-        cur = list[0];
-        continue;
-      }
-    } else {
-      int first, cnt;
-      leaf_range(cur, first, cnt);
-      for (int j = first; j < first + cnt; ++j) {
-        const float4* tr = s.tris + 3 * (size_t)j;
-        const float4 ta = __ldg(tr), tb = __ldg(tr + 1), tc = __ldg(tr + 2);
-        float t, u, v;
-        tests += active;
-        if (active && intersect_tri(o, d, f3(ta), f3(tb), f3(tc), 0.0f, t, u, v)) {
-          const int id = __float_as_int(ta.w);
-          if (t < bt || (t == bt && id < best)) { bt = t; bu = u; bv = v; best = id; }
-        }
-      }
-    }
-    if (sp == 0 || sp > kPacketStack) break;
-    --sp;
-    cur = wstack[sp];
-    __syncwarp();
-  }
-  if (!active) best = -1;
-  return best;
+// Triangle of ORIGINAL face f from the snapshot, in float64: v0 and the edges v1 - v0, v2 - v0
+// (exact in float64 for float32 vertices).
+DT_D void face_tri64(const DevScene& s, int f, int& i0, int& i1, int& i2, double3& v0, double3& e1, double3& e2) {
+  i0 = __ldg(s.F + 3 * f); i1 = __ldg(s.F + 3 * f + 1); i2 = __ldg(s.F + 3 * f + 2);
+  v0 = d3(__ldg(s.V + i0));
+  e1 = d3(__ldg(s.V + i1)) - v0;
+  e2 = d3(__ldg(s.V + i2)) - v0;
 }
 
-// triangle of ORIGINAL face f from the snapshot, with the same e1/e2 rounding as the leaves
-DT_D void face_tri(const DevScene& s, int f, int& i0, int& i1, int& i2, float3& v0, float3& e1, float3& e2) {
-  i0 = __ldg(s.F + 3 * f); i1 = __ldg(s.F + 3 * f + 1); i2 = __ldg(s.F + 3 * f + 2);
-  v0 = f3(__ldg(s.V + i0));
-  e1 = sub_rn(f3(__ldg(s.V + i1)), v0);
-  e2 = sub_rn(f3(__ldg(s.V + i2)), v0);
+// Moller-Trumbore solve o + t d = v0 + u e1 + v e2 in float64 (R15, R16) for the face the
+// traversal selected (float32 candidate search, conservative boxes): the hit point, the
+// barycentrics and everything downstream use these values.
+// Returns 1 / det.
+DT_D double mt64(double3 o, double3 d, double3 v0, double3 e1, double3 e2, double& t, double& u, double& v) {
+  const double3 p = cross(d, e2);
+  const double inv = rcp64(dot(e1, p));
+  const double3 sv = o - v0;
+  u = dot(sv, p) * inv;
+  const double3 q = cross(sv, e1);
+  v = dot(d, q) * inv;
+  t = dot(e2, q) * inv;
+  return inv;
 }
 
 // ----------------------------------------------------------------------------- interface
-// One specular event (R1-R5, R7, R8).  Everything the reverse pass needs.
+// One specular event (R1-R5, R7, R8), float64.  Everything the reverse pass needs.
 struct Shade {
-  float3 n, ns, m, wi, wr, wt;
-  float Lm, sg, c_raw, ci, eta, eta_i, eta_t, q, ct, R, T;
-  float b0, b1, b2;
+  double3 n, wr, wt;            // oriented shading normal, reflect / refract directions
+  double Lm, ci, eta, eta_i, eta_t, q, ct, R, T;
+  double b0, b1, b2;
   bool inside, tir, clamped, degen, fb;
 };
 
-DT_D void shade_forward(const DevScene& s, float ior, int i0, int i1, int i2, float3 e1, float3 e2, float3 d, float u, float v,
-                        bool inside, Shade& S) {
+DT_D void shade_forward(const DevScene& s, double ior, int i0, int i1, int i2, double3 e1, double3 e2, double3 d,
+                        double u, double v, bool inside, Shade& S) {
   S.inside = inside;
-  S.b0 = 1.0f - u - v; S.b1 = u; S.b2 = v;
-  float3 n0 = f3(__ldg(s.nrm + i0)), n1 = f3(__ldg(s.nrm + i1)), n2 = f3(__ldg(s.nrm + i2));
-  S.m = n0 * S.b0 + n1 * S.b1 + n2 * S.b2;                 // n(x) = sum beta_i n_vi
-  S.Lm = length(S.m);
-  S.fb = !(S.Lm >= 1e-12f);
-  if (!S.fb) S.ns = S.m * (1.0f / S.Lm);
-  else { float3 c = cross(e1, e2); S.ns = c * (1.0f / length(c)); }
-  S.sg = inside ? -1.0f : 1.0f;
-  S.n = S.ns * S.sg;
-  S.eta_i = inside ? ior : 1.0f;
-  S.eta_t = inside ? 1.0f : ior;
-  S.wi = -d;
-  S.c_raw = dot(S.wi, S.n);
-  S.clamped = !(S.c_raw > 0.0f);
-  S.ci = S.clamped ? 0.0f : fminf(S.c_raw, 1.0f);
-  S.eta = S.eta_t / S.eta_i;
-  S.q = S.eta * S.eta - 1.0f + S.ci * S.ci;
-  S.wr = S.n * (2.0f * S.ci) - S.wi;
-  S.tir = S.q < 0.0f;
+  S.b0 = 1.0 - u - v; S.b1 = u; S.b2 = v;
+  const double3 n0 = xyz(ldg_d4(s.nrm + i0)), n1 = xyz(ldg_d4(s.nrm + i1)), n2 = xyz(ldg_d4(s.nrm + i2));
+  const double3 m = n0 * S.b0 + n1 * S.b1 + n2 * S.b2;       // n(x) = sum beta_i n_vi
+  const double mm = dot(m, m);
+  S.fb = !(mm >= 1e-24);                                      // |m| < 1e-12: geometric normal (R7)
+  double3 ns;
+  if (!S.fb) {
+    const double rl = rsqrt64(mm);
+    S.Lm = mm * rl;
+    ns = m * rl;
+  } else {
+    const double3 c = cross(e1, e2);
+    S.Lm = 0.0;
+    ns = c * rsqrt64(dot(c, c));
+  }
+  S.n = inside ? -ns : ns;
+  S.eta_i = inside ? ior : 1.0;
+  S.eta_t = inside ? 1.0 : ior;
+  const double c_raw = -dot(d, S.n);                          // omega_i . n, omega_i = -d
+  S.clamped = !(c_raw > 0.0);
+  S.ci = S.clamped ? 0.0 : fmin(c_raw, 1.0);
+  S.eta = S.eta_t * rcp64(S.eta_i);
+  S.q = S.eta * S.eta - 1.0 + S.ci * S.ci;
+  S.wr = S.n * (2.0 * S.ci) + d;
+  S.tir = S.q < 0.0;
   S.degen = false;
-  if (S.tir) { S.ct = 0.0f; S.R = 1.0f; S.T = 0.0f; S.wt = f3(0, 0, 0); return; }
-  S.ct = sqrtf(S.q) / S.eta;
-  S.wt = (S.wi - S.n * S.ci) * (-1.0f / S.eta) - S.n * S.ct;  // P:106-108 (R4)
-  if (S.ci == 0.0f && S.ct == 0.0f) { S.degen = true; S.R = 1.0f; S.T = 0.0f; return; }
-  float A = S.eta_i * S.ci, B = S.eta_t * S.ct, C = S.eta_i * S.ct, D = S.eta_t * S.ci;
-  float rs = (A - B) / (A + B), rp = (C - D) / (C + D);
-  S.R = 0.5f * (rs * rs + rp * rp);
-  S.T = 1.0f - S.R;
+  if (S.tir) { S.ct = 0.0; S.R = 1.0; S.T = 0.0; S.wt = d3(0, 0, 0); return; }
+  const double ie = rcp64(S.eta);
+  S.ct = sqrt64(S.q) * ie;
+  S.wt = (d + S.n * S.ci) * ie - S.n * S.ct;                  // P:106-108 (R4): -(omega_i - c n)/eta - ct n
+  if (S.ci == 0.0 && S.ct == 0.0) { S.degen = true; S.R = 1.0; S.T = 0.0; return; }
+  const double A = S.eta_i * S.ci, B = S.eta_t * S.ct, C = S.eta_i * S.ct, D = S.eta_t * S.ci;
+  const double rs = (A - B) * rcp64(A + B), rp = (C - D) * rcp64(C + D);
+  S.R = 0.5 * (rs * rs + rp * rp);
+  S.T = 1.0 - S.R;
+}
+
+// The interface state the reverse pass needs, rounded to float32 once it has been evaluated
+// in float64 (the reverse scales float32 adjoints by these Jacobian terms; the state itself,
+// where the float32 error would be amplified along the path, stays float64).
+struct ShadeF {
+  float3 n;
+  float Lm, ci, eta, eta_i, eta_t, q, ct, b0, b1, b2;
+  bool inside, tir, clamped, degen, fb;
+};
+DT_D ShadeF shade_f32(const Shade& S) {
+  ShadeF F;
+  F.n = f3(S.n);
+  F.Lm = (float)S.Lm; F.ci = (float)S.ci; F.eta = (float)S.eta; F.eta_i = (float)S.eta_i; F.eta_t = (float)S.eta_t;
+  F.q = (float)S.q; F.ct = (float)S.ct; F.b0 = (float)S.b0; F.b1 = (float)S.b1; F.b2 = (float)S.b2;
+  F.inside = S.inside; F.tir = S.tir; F.clamped = S.clamped; F.degen = S.degen; F.fb = S.fb;
+  return F;
 }
 
 // Reverse of shade_forward: given dL/dR (T = 1 - R folded in), dL/dwr, dL/dwt, returns
 // dL/dd (through omega_i = -d), dL/d(u, v) (through the shading normal), d/dn_vk and d/dior.
-DT_D void shade_backward(const Shade& S, float gR, float3 gwr, float3 gwt, float3 nv0, float3 nv1, float3 nv2,
+DT_D void shade_backward(const ShadeF& S, float3 d, float gR, float3 gwr, float3 gwt, float3 nv0, float3 nv1, float3 nv2,
                          float3& gd, float& gu, float& gv, float3 gN[3], float& gior) {
   float gci = 0.0f, geta = 0.0f, geta_i = 0.0f, geta_t = 0.0f;
   float3 gn = f3(0, 0, 0), gwi = f3(0, 0, 0);
-  if (!S.tir) {
-    if (!S.degen) {
-      float A = S.eta_i * S.ci, B = S.eta_t * S.ct, C = S.eta_i * S.ct, D = S.eta_t * S.ci;
-      float rs = (A - B) / (A + B), rp = (C - D) / (C + D);
-      float grs = gR * rs, grp = gR * rp;
-      float iab = 1.0f / ((A + B) * (A + B)), icd = 1.0f / ((C + D) * (C + D));
-      float gA = grs * 2.0f * B * iab, gB = -grs * 2.0f * A * iab;
-      float gC = grp * 2.0f * D * icd, gD = -grp * 2.0f * C * icd;
-      float gct = gB * S.eta_t + gC * S.eta_i;
-      gci += gA * S.eta_i + gD * S.eta_t;
-      geta_i += gA * S.ci + gC * S.ct;
-      geta_t += gB * S.ct + gD * S.ci;
-      // hand the gct through the transmitted direction and cos(theta_t) below
-      float ie = 1.0f / S.eta;
-      gwi -= gwt * ie;
-      gci += dot(gwt, S.n) * ie;
-      gn += gwt * (S.ci * ie) - gwt * S.ct;
-      geta += dot(gwt, S.wi - S.n * S.ci) * ie * ie;
-      gct -= dot(gwt, S.n);
-      float sq = sqrtf(S.q);
-      float gq = sq > 0.0f ? gct / (2.0f * S.eta * sq) : 0.0f;
-      geta += -gct * sq * ie * ie + gq * 2.0f * S.eta;
-      gci += gq * 2.0f * S.ci;
-    }
-    // degen (both cosines 0): R = 1, T = 0 constant; the refracted child carries zero
-    // adjoint, so gwt = 0 and nothing flows.
+  const float3 wi = -d;
+  if (!S.tir && !S.degen) {
+    float A = S.eta_i * S.ci, B = S.eta_t * S.ct, C = S.eta_i * S.ct, D = S.eta_t * S.ci;
+    float rs = (A - B) / (A + B), rp = (C - D) / (C + D);
+    float grs = gR * rs, grp = gR * rp;
+    float iab = 1.0f / ((A + B) * (A + B)), icd = 1.0f / ((C + D) * (C + D));
+    float gA = grs * 2.0f * B * iab, gB = -grs * 2.0f * A * iab;
+    float gC = grp * 2.0f * D * icd, gD = -grp * 2.0f * C * icd;
+    float gct = gB * S.eta_t + gC * S.eta_i;
+    gci += gA * S.eta_i + gD * S.eta_t;
+    geta_i += gA * S.ci + gC * S.ct;
+    geta_t += gB * S.ct + gD * S.ci;
+    // the transmitted direction omega_t = -(omega_i - ci n)/eta - ct n and cos(theta_t) below
+    float ie = 1.0f / S.eta;
+    gwi -= gwt * ie;
+    gci += dot(gwt, S.n) * ie;
+    gn += gwt * (S.ci * ie) - gwt * S.ct;
+    geta += dot(gwt, wi - S.n * S.ci) * ie * ie;
+    gct -= dot(gwt, S.n);
+    float sq = sqrtf(S.q);
+    float gq = sq > 0.0f ? gct / (2.0f * S.eta * sq) : 0.0f;
+    geta += -gct * sq * ie * ie + gq * 2.0f * S.eta;
+    gci += gq * 2.0f * S.ci;
   }
+  // degen (both cosines 0): R = 1, T = 0 constant; the refracted child carries zero adjoint.
   // omega_r = 2 ci n - omega_i
   gci += 2.0f * dot(gwr, S.n);
   gn += gwr * (2.0f * S.ci);
@@ -571,13 +484,13 @@ DT_D void shade_backward(const Shade& S, float gR, float3 gwr, float3 gwt, float
   geta_i -= geta * S.eta_t / (S.eta_i * S.eta_i);
   gior = S.inside ? geta_i : geta_t;
   // ci = clamp(omega_i . n): the lower clamp stops the gradient (R3)
-  if (!S.clamped) { gwi += S.n * gci; gn += S.wi * gci; }
+  if (!S.clamped) { gwi += S.n * gci; gn += wi * gci; }
   gd = -gwi;
   gu = gv = 0.0f;
   gN[0] = gN[1] = gN[2] = f3(0, 0, 0);
   if (!S.fb) {
-    float3 gns = gn * S.sg;
-    float3 gm = (gns - S.ns * dot(S.ns, gns)) * (1.0f / S.Lm);
+    const float3 gns = S.inside ? -gn : gn, ns = S.inside ? -S.n : S.n;
+    float3 gm = (gns - ns * dot(ns, gns)) * (1.0f / S.Lm);
     gN[0] = gm * S.b0; gN[1] = gm * S.b1; gN[2] = gm * S.b2;
     float g0 = dot(gm, nv0), g1 = dot(gm, nv1), g2 = dot(gm, nv2);
     gu = g1 - g0;
@@ -586,12 +499,12 @@ DT_D void shade_backward(const Shade& S, float gR, float3 gwr, float3 gwt, float
 }
 
 // Reverse of the Moller-Trumbore solve M [u v t]^T = o - v0 with M = [e1 e2 -d]:
-// lambda = M^-T (gu, gv, gt); go += lambda, gd += t lambda, gV_k = -beta_k lambda.
-DT_D void mt_backward(float3 d, float3 e1, float3 e2, float t, float u, float v, float gu, float gv, float gt,
-                      float3& go, float3& gd, float3 gV[3]) {
+// lambda = M^-T (gu, gv, gt); go += lambda, gd += t lambda, gV_k = -beta_k lambda.  The
+// determinant's reciprocal from the float64 geometry (idet), the rest float32.
+DT_D void mt_backward(float3 d, float3 e1, float3 e2, float idet, float t, float u, float v, float gu, float gv,
+                      float gt, float3& go, float3& gd, float3 gV[3]) {
   float3 de2 = cross(d, e2), e1d = cross(e1, d), e12 = cross(e1, e2);
-  float det = dot(e1, de2);
-  float3 lam = (de2 * gu + e1d * gv + e12 * gt) * (1.0f / det);
+  float3 lam = (de2 * gu + e1d * gv + e12 * gt) * idet;
   go += lam;
   gd += lam * t;
   gV[0] = lam * -(1.0f - u - v);
@@ -604,22 +517,21 @@ DT_D size_t cell_node(size_t base, int k, int R) {
   return base + ((size_t)(k >> 2) * R + ((k >> 1) & 1)) * R + (k & 1);
 }
 
-// Optical depth of a constant-sigma segment and its reverse (ABS = DT_ABS_CONST).
-DT_D float3 transmittance_const(const DevScene& s, float3 o, float3 x) {
-  const float3 S = f3(__ldg(s.sigma)) * length(x - o);
+// Optical depth of a constant-sigma segment and its reverse (ABS = DT_ABS_CONST); the chord
+// length from the float64 end points.
+DT_D float3 transmittance_const(const DevScene& s, double3 o, double3 x) {
+  const float3 S = f3(__ldg(s.sigma)) * (float)length(x - o);
   return f3(expf(-S.x), expf(-S.y), expf(-S.z));
 }
 
-DT_D void transmittance_const_backward(const DevScene& s, float3 o, float3 x, float3 gS, float3& gx, float3& go,
+// (the chord o -> x = o + t d: length t |d|, direction d / |d|)
+DT_D void transmittance_const_backward(const DevScene& s, float l, float3 dh, float3 gS, float3& gx, float3& go,
                                        float3& gsc) {
-  const float3 dx = x - o;
-  const float l = length(dx);
   gsc += gS * l;
   if (l > 0.0f) {
-    const float3 u = dx * (1.0f / l);
-    const float gl = dot(gS, f3(__ldg(s.sigma)));
-    gx += u * gl;
-    go -= u * gl;
+    const float3 u = dh * dot(gS, f3(__ldg(s.sigma)));
+    gx += u;
+    go -= u;
   }
 }
 
@@ -969,22 +881,33 @@ DT_D float grid_coord(float p, float Re, int res, bool& clamped) {
   clamped = !(g >= 0.0f && g <= top);
   return fminf(fmaxf(g, 0.0f), top);
 }
+// The same in float64 for the shell lookup (the lookup point comes from the float64 ray state);
+// returns the cell index and the fraction within it (float32: only a weight from here on).
+DT_D int grid_cell64(double p, double Re, int res, float& f, bool& clamped) {
+  const double top = (double)(res - 1);
+  double g = (p + Re) * (top * rcp64(2.0 * Re));
+  clamped = !(g >= 0.0 && g <= top);
+  g = fmin(fmax(g, 0.0), top);
+  const int i = min((int)floor(g), res - 2);
+  f = (float)(g - (double)i);
+  return i;
+}
 
-DT_D float3 shell_point(const DevScene& s, float3 o, float3 dh, float& ts, float& sq) {
-  if (s.far_field) { ts = s.radius; sq = 0.0f; return dh * s.radius; }
-  float b = dot(o, dh);
-  sq = sqrtf(fmaxf(b * b - dot(o, o) + s.radius * s.radius, 0.0f));
+DT_D double3 shell_point(const DevScene& s, double3 o, double3 dh, double& ts, double& sq) {
+  const double Re = (double)s.radius;
+  if (s.far_field) { ts = Re; sq = 0.0; return dh * Re; }
+  const double b = dot(o, dh);
+  sq = sqrt64(b * b - dot(o, o) + Re * Re);
   ts = -b + sq;
   return o + dh * ts;
 }
 
-DT_D float3 env_voxel(const DevScene& s, float3 p, float3 a, float3* gp) {
+DT_D float3 env_voxel(const DevScene& s, double3 p, float3 a, float3* gp) {
   bool c[3];
-  float g[3] = {grid_coord(p.x, s.radius, s.vres, c[0]), grid_coord(p.y, s.radius, s.vres, c[1]),
-                grid_coord(p.z, s.radius, s.vres, c[2])};
-  int R = s.vres, i0[3];
   float f[3];
-  for (int k = 0; k < 3; ++k) { i0[k] = min((int)floorf(g[k]), R - 2); f[k] = g[k] - (float)i0[k]; }
+  const int R = s.vres;
+  const int i0[3] = {grid_cell64(p.x, s.radius, R, f[0], c[0]), grid_cell64(p.y, s.radius, R, f[1], c[1]),
+                     grid_cell64(p.z, s.radius, R, f[2], c[2])};
   float3 out = f3(0, 0, 0), gg = f3(0, 0, 0);
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -1004,12 +927,11 @@ DT_D float3 env_voxel(const DevScene& s, float3 p, float3 a, float3* gp) {
   return out;
 }
 
-DT_D float3 env_plane(const DevScene& s, int k, float a_, float b_, float3 adj, float* ga, float* gb) {
+DT_D float3 env_plane(const DevScene& s, int k, double a_, double b_, float3 adj, float* ga, float* gb) {
   bool ca, cb;
-  int R = s.pres;
-  float g_a = grid_coord(a_, s.radius, R, ca), g_b = grid_coord(b_, s.radius, R, cb);
-  int ia = min((int)floorf(g_a), R - 2), ib = min((int)floorf(g_b), R - 2);
-  float fa = g_a - (float)ia, fb = g_b - (float)ib;
+  const int R = s.pres;
+  float fa, fb;
+  const int ia = grid_cell64(a_, s.radius, R, fa, ca), ib = grid_cell64(b_, s.radius, R, fb, cb);
   const float4* P = s.planes + (size_t)k * R * R;
   float4 t00 = __ldg(P + (size_t)ib * R + ia), t01 = __ldg(P + (size_t)ib * R + ia + 1);
   float4 t10 = __ldg(P + (size_t)(ib + 1) * R + ia), t11 = __ldg(P + (size_t)(ib + 1) * R + ia + 1);
@@ -1028,19 +950,19 @@ DT_D float3 env_plane(const DevScene& s, int k, float a_, float b_, float3 adj, 
 
 // Reverse of the shell point p = o + ts dh (or R_e dh in the far field): adds the adjoints
 // of o and dh for gp = dL/dp (ts, sq from shell_point).
-DT_D void shell_point_bwd(const DevScene& s, float3 o, float3 dh, float ts, float sq, float3 gp, float3& go,
-                          float3& gdh) {
+DT_D void shell_point_bwd(const DevScene& s, double3 o, double3 dh, double ts, double sq, double3 gp, double3& go,
+                          double3& gdh) {
   if (s.far_field) {
-    gdh += gp * s.radius;
+    gdh += gp * (double)s.radius;
     return;
   }
-  float b = dot(o, dh);
+  const double b = dot(o, dh);
   go += gp;
   gdh += gp * ts;
-  float gts = dot(gp, dh);
-  float gdisc = sq > 0.0f ? gts / (2.0f * sq) : 0.0f;
-  float gb = -gts + gdisc * 2.0f * b;
-  go -= o * (2.0f * gdisc);
+  const double gts = dot(gp, dh);
+  const double gdisc = sq > 0.0 ? gts * rcp64(2.0 * sq) : 0.0;
+  const double gb = -gts + gdisc * 2.0 * b;
+  go -= o * (2.0 * gdisc);
   go += dh * gb;
   gdh += o * gb;
 }
@@ -1226,57 +1148,60 @@ DT_D void env_volume_bwd(const DevScene& s, float3 o, float3 x, float3 aV, float
 }
 
 // Radiance of an escaping ray: the shell lookup (R14), preceded by the volume rendering of
-// the segment out to the shell for the volumetric env (R30).  Forward: Tn and mom (if given)
-// returned for the record.  Reverse (go/gd non-null): uses the recorded Tn, mom.
-DT_D float3 env_eval(const DevScene& s, float3 o, float3 d, float3 a, float3* go, float3* gd);
+// the segment out to the shell for the volumetric env (R30; its samples in float32).  Forward:
+// Tn and mom (if given) returned for the record.  Reverse (go/gd non-null, SET): uses the
+// recorded Tn, mom.
+DT_D float3 env_eval(const DevScene& s, double3 o, double3 d, float3 a, float3* go, float3* gd);
 template <bool VOL>
-DT_D float3 env_escape(const DevScene& s, float3 o, float3 d, float3 a, float3* go, float3* gd, float* Tn_io = nullptr,
-                       VolMom* mom_io = nullptr) {
+DT_D float3 env_escape(const DevScene& s, double3 o, double3 d, float3 a, float3* go, float3* gd,
+                       float* Tn_io = nullptr, VolMom* mom_io = nullptr) {
   if (!VOL) return env_eval(s, o, d, a, go, gd);
-  const float dn = length(d);
-  const float3 dh = d * (1.0f / dn);
-  float ts, sq;
-  const float3 ps = shell_point(s, o, dh, ts, sq);
+  const double rn = rsqrt64(dot(d, d));
+  const double3 dh = d * rn;
+  double ts, sq;
+  const double3 ps = shell_point(s, o, dh, ts, sq);
   if (!go) {                                   // forward
     float3 V;
     float Tn;
-    env_volume(s, o, ps, V, Tn, mom_io);
+    env_volume(s, f3(o), f3(ps), V, Tn, mom_io);
     if (Tn_io) *Tn_io = Tn;
     return V + env_eval(s, o, d, a, nullptr, nullptr) * Tn;
   }
   const float Tn = *Tn_io;                     // reverse, from the record
   const float3 E = env_eval(s, o, d, a * Tn, go, gd);
-  float3 gov = f3(0, 0, 0), gps = f3(0, 0, 0), gdh = f3(0, 0, 0);
-  env_volume_bwd(s, o, ps, a, dot(a, E), Tn, *mom_io, gov, gps);
-  shell_point_bwd(s, o, dh, ts, sq, gps, gov, gdh);
-  *go += gov;
-  *gd += (gdh - dh * dot(dh, gdh)) * (1.0f / dn);
+  float3 gov = f3(0, 0, 0), gps = f3(0, 0, 0);
+  env_volume_bwd(s, f3(o), f3(ps), a, dot(a, E), Tn, *mom_io, gov, gps);
+  double3 gdh = d3(0, 0, 0), go2 = d3(gov);
+  shell_point_bwd(s, o, dh, ts, sq, d3(gps), go2, gdh);
+  *go += f3(go2);
+  *gd += f3((gdh - dh * dot(dh, gdh)) * rn);
   return E;
 }
 
-// Env(o, d) (P:160 step 3).  If go/gd are non-null, also the reverse for adjoint a.
-DT_D float3 env_eval(const DevScene& s, float3 o, float3 d, float3 a, float3* go, float3* gd) {
-  float dn = length(d);
-  float3 dh = d * (1.0f / dn);
-  float3 L, gdh = f3(0, 0, 0);
+// Env(o, d) (P:160 step 3), the lookup point from the float64 ray.  If go/gd are non-null,
+// they are SET to the reverse for adjoint a.
+DT_D float3 env_eval(const DevScene& s, double3 o, double3 d, float3 a, float3* go, float3* gd) {
+  const double rn = rsqrt64(dot(d, d));
+  const double3 dh = d * rn;
+  float3 L;
+  double3 gdh = d3(0, 0, 0);
   if (s.env_kind == 0) {
     L = s.ambient;
     for (int j = 0; j < s.nlobes; ++j) {
       const float* lb = s.lobes + 7 * j;
-      float3 mu = f3(__ldg(lb), __ldg(lb + 1), __ldg(lb + 2));
-      float kap = __ldg(lb + 3);
-      float3 w = f3(__ldg(lb + 4), __ldg(lb + 5), __ldg(lb + 6));
-      float e = expf(kap * (dot(mu, dh) - 1.0f));
+      const double3 mu = d3(__ldg(lb), __ldg(lb + 1), __ldg(lb + 2));
+      const float kap = __ldg(lb + 3);
+      const float3 w = f3(__ldg(lb + 4), __ldg(lb + 5), __ldg(lb + 6));
+      const float e = expf((float)((double)kap * (dot(mu, dh) - 1.0)));
       L += w * e;
-      if (gd) gdh += mu * (dot(a, w) * e * kap);
+      if (gd) gdh += mu * (double)(dot(a, w) * e * kap);
     }
     if (go) *go = f3(0, 0, 0);
   } else {
-    float ts, sq;
-    float3 p = shell_point(s, o, dh, ts, sq);
+    double ts, sq;
+    const double3 p = shell_point(s, o, dh, ts, sq);
     float3 gp = f3(0, 0, 0);
-    float3* gpp = gd ? &gp : nullptr;
-    L = env_voxel(s, p, a, gpp);
+    L = env_voxel(s, p, a, gd ? &gp : nullptr);
     float g1 = 0, g2 = 0;
     L += env_plane(s, 0, p.x, p.y, a, gd ? &g1 : nullptr, &g2);
     if (gd) { gp.x += g1; gp.y += g2; }
@@ -1285,24 +1210,12 @@ DT_D float3 env_eval(const DevScene& s, float3 o, float3 d, float3 a, float3* go
     L += env_plane(s, 2, p.y, p.z, a, gd ? &g1 : nullptr, &g2);
     if (gd) { gp.y += g1; gp.z += g2; }
     if (gd) {
-      if (s.far_field) {
-        gdh = gp * s.radius;
-        *go = f3(0, 0, 0);
-      } else {
-        float b = dot(o, dh);
-        float3 g_o = gp;
-        gdh = gp * ts;
-        float gts = dot(gp, dh);
-        float gdisc = sq > 0.0f ? gts / (2.0f * sq) : 0.0f;
-        float gb = -gts + gdisc * 2.0f * b;
-        g_o -= o * (2.0f * gdisc);
-        g_o += dh * gb;
-        gdh += o * gb;
-        *go = g_o;
-      }
+      double3 g_o = d3(0, 0, 0);
+      shell_point_bwd(s, o, dh, ts, sq, d3(gp), g_o, gdh);
+      *go = f3(g_o);
     }
   }
-  if (gd) *gd = (gdh - dh * dot(dh, gdh)) * (1.0f / dn);
+  if (gd) *gd = f3((gdh - dh * dot(dh, gdh)) * rn);
   return L;
 }
 

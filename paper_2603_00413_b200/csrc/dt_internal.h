@@ -10,12 +10,12 @@
 
 namespace dt {
 
-// Path-record arena: one entry per traced segment, structure-of-arrays of 16-B lanes so
-// every kernel's loads/stores are coalesced float4 accesses.  Levels (depths) are
-// contiguous: level k occupies [off_k, off_k + cnt_k).
+// Path-record arena: one entry per traced segment, structure-of-arrays of 32-B (float64 ray
+// state) and 16-B lanes so every kernel's loads/stores are coalesced vector accesses.  Levels
+// (depths) are contiguous: level k occupies [off_k, off_k + cnt_k).
 struct Records {
-  float4* o;     // origin.xyz, ray index (int bits)
-  float4* d;     // direction.xyz, tree position (uint bits: root 1, reflect 2p, refract 2p+1)
+  Vec64* o;      // origin.xyz (float64), .i = ray index
+  Vec64* d;      // direction.xyz (float64), .u = tree position (root 1, reflect 2p, refract 2p+1)
   float4* thr;   // throughput into the node (product of ancestors' R/T and tau), scalar R/T weight
   float4* hit;   // face (int bits), t, R, flags (int bits, RF_*)
   float4* tau;   // interior transmittance of this segment (rgb), refract child index (int bits)
@@ -25,7 +25,7 @@ struct Records {
   float4* mq;    // volumetric env only (else null): the forward's volume moments Qc | od_M
   float4* mg;    //   and Go (env_volume), read by every backward of that forward
 };
-constexpr int kRecordBytes = 8 * 16;
+constexpr int kRecordBytes = 2 * 32 + 6 * 16;
 
 // device int block: per-level counts and work counters
 enum {
@@ -40,6 +40,11 @@ enum {
   LV_WORK_PRIMARY = 68,
   LV_INTS = 80
 };
+
+// slots of dt_ctx::grid_cache
+// (shade / backward: 6 slots each, by absorption kind x volumetric env)
+enum { kGridPrimary = 0, kGridPrimaryVol = 1, kGridTrav = 2, kGridWide = 3, kGridShade = 4, kGridBwd = 10,
+       kGridCount = 16 };
 
 struct FwdLaunch {
   DevScene s;
@@ -60,9 +65,7 @@ struct FwdLaunch {
   unsigned long long* sig_t;
   unsigned long long* sig_f;
   unsigned long long* counters;   // [0] node visits, [1] triangle tests
-  int trav_mode, trav_chunk, leaf_vote;
-  int sort_lanes;       // shade: hit-first lane order over 64-record windows
-  int prim_packet;      // camera rays: warp-packet traversal (traverse_packet)
+  int* grids;           // host: the context's persistent-grid cache (dt_ctx::grid_cache)
 };
 
 struct BwdLaunch {
@@ -76,7 +79,7 @@ struct BwdLaunch {
   float4* dN;       // [nv] vertex-normal adjoints (atomics)
   float4* dsig;     // [1] or [R^3] (rgb + pad)
   float* dior;      // [1]
-  int sort_lanes;   // hit-first lane order over 64-record windows
+  int* grids;       // host: the context's persistent-grid cache
 };
 
 }  // namespace dt
@@ -91,8 +94,8 @@ struct dt_ctx {
   size_t cap_nv = 0, cap_nf = 0;
   float4* V = nullptr;        // [nv]
   int* F = nullptr;           // [nf*3]
-  float4* nrm = nullptr;      // [nv]
-  float4* fnrm = nullptr;     // [nf] unit face normals
+  D4* nrm = nullptr;          // [nv] vertex normals (float64), |sum| in w
+  D4* fnrm = nullptr;         // [nf] unit face normals (float64), |e1 x e2| in w
   // LBVH
   float4* nodes = nullptr;    // [(nf-1)*4]
   float4* tris = nullptr;     // [nf*3]
@@ -102,7 +105,6 @@ struct dt_ctx {
   unsigned* scan_part = nullptr;   // multi-block scan chunk totals
   unsigned long long* wqueue = nullptr;   // surface-area collapse work queue (+16 ints of counters)
   int wqueue_cap = 0;
-  int wide_mode = 1;               // 0: even-depth collapse, 1: surface-area greedy (DT_WIDE_MODE)
   int2* children = nullptr;   // [nf-1]
   int* parent_int = nullptr;  // [nf-1]
   int* parent_leaf = nullptr; // [nf]
@@ -112,9 +114,6 @@ struct dt_ctx {
   int* vstart = nullptr;      // [nv+1] CSR of (vertex -> incident corners)
   unsigned* vcorner = nullptr;// [3nf] sorted corner ids (face*3 + k)
   int2* ranges = nullptr;     // [nf-1] leaf range of each binary node
-  int* bdepth = nullptr;      // [nf-1] binary depth
-  unsigned* wflag = nullptr;  // [nf-1] binary node starts a wide node
-  unsigned* widx = nullptr;   // [nf-1] its wide-node index (exclusive scan of wflag)
   float4* wbox = nullptr;     // [2 * n_wide] wide-node boxes (checks)
   int* wdepth = nullptr;      // [n_wide] wide-node depth (checks)
   float* scal = nullptr;      // device scalars: [0..5] root box, [6] bbox diagonal
@@ -149,14 +148,8 @@ struct dt_ctx {
   float4* gsig = nullptr;     // [1] or [R^3]: d/dsigma (rgb + pad)
   float* gior = nullptr;
   size_t gsig_cap = 0;
-  // tuning knobs (env DT_LEAF_MAX, DT_TRAV_MODE, DT_TRAV_CHUNK at dt_create)
-  int leaf_max = 1;           // triangles per wide-BVH leaf (sweep r01: 1 is fastest)
-  int prim_packet = 0;        // camera rays as warp packets (DT_PRIMARY_PACKET=1): measured slower at C3
-  int trav_mode = 1;          // 0: warp takes 32 rays; 1: per-lane global refill; 2: per-lane refill from a warp chunk;
-                              // 3: postponed leaves
-  int trav_chunk = 256;       // rays per warp chunk (mode 2)
-  int leaf_vote = 32;         // mode 3: lanes that must be ready before a warp leaf phase
-  int sort_lanes = 1;         // shade / backward: hit-first lane order (DT_SORT_LANES)
+  int leaf_max = 1;           // triangles per wide-BVH leaf (r01 sweep of 1..4: 1 is fastest)
+  int grid_cache[dt::kGridCount] = {};    // persistent-kernel grid sizes of this device (occupancy x SMs), by kGrid*
   // profiling (dt_set_profiling / dt_get_profile)
   bool prof = false;
   double ph_ms[DT_PH_COUNT] = {};
@@ -206,6 +199,7 @@ cudaError_t launch_loss_color(const float* rgb, const float* tgt, int64_t n, flo
 cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64_t n, float t_lo, int brute, int* face,
                                      float* tuv, int* err_flag, cudaStream_t st);
 cudaError_t launch_bvh_check(dt_ctx* c, long long* out_dev, cudaStream_t st);
+cudaError_t launch_normals_to_f32(const D4* nrm, int nv, float* out, cudaStream_t st);
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, int res, bool pairs, cudaStream_t st);
 cudaError_t launch_count_segments(const int* lvl, int max_depth, unsigned long long* seg, cudaStream_t st);

@@ -84,21 +84,21 @@ DT_D float warp_sum(float x) {
 
 // L_edge: loss over edges (i < j), and dL/dn_i = (1/|E|) sum_{j in N(i)} -2 (1 - n_i.n_j) n_j
 // written into gN (the vertex-normal chain then maps it to dV)
-__global__ void k_edge_reg(const float4* __restrict__ nrm, const int* __restrict__ start, const int* __restrict__ nbr,
+__global__ void k_edge_reg(const D4* __restrict__ nrm, const int* __restrict__ start, const int* __restrict__ nbr,
                            int nv, float lambda, float4* __restrict__ gN, float* __restrict__ loss) {
   const float inv_e = 2.0f / (float)max(start[nv], 1);     // |E| = (sum of valences) / 2
   float acc = 0.f;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
-    const float3 ni = f3(nrm[i]);
-    float3 g = f3(0, 0, 0);
+    const double3 ni = xyz(nrm[i]);
+    double3 g = d3(0, 0, 0);
     for (int q = start[i]; q < start[i + 1]; ++q) {
       const int j = nbr[q];
-      const float3 nj = f3(nrm[j]);
-      const float d = 1.0f - dot(ni, nj);
-      if (j > i) acc += d * d;
-      g += nj * (-2.0f * d);
+      const double3 nj = xyz(nrm[j]);
+      const double d = 1.0 - dot(ni, nj);                  // float64: near-parallel normals cancel
+      if (j > i) acc += (float)(d * d);
+      g += nj * (-2.0 * d);
     }
-    gN[i] = f4(g * (lambda * inv_e), 0.f);
+    gN[i] = f4(f3(g) * (lambda * inv_e), 0.f);
   }
   acc = warp_sum(acc);
   if (lane_id() == 0 && acc != 0.f) atomicAdd(loss, acc * inv_e);

@@ -42,9 +42,10 @@ constexpr int kBwdThreads = 128;
 #else
 #define DT_TRAV_LB __launch_bounds__(kTraceThreads)
 #endif
-// camera-ray kernel: 48 registers (10 blocks / SM) measured faster than its natural 64
+// camera-ray kernel: capped at 64 registers (8 blocks / SM; the float64 camera ray and env
+// lookup need ~64 without spilling)
 #ifndef DT_PRIM_MINB
-#define DT_PRIM_MINB 10
+#define DT_PRIM_MINB 8
 #endif
 #define DT_PRIM_LB __launch_bounds__(kTraceThreads, DT_PRIM_MINB)
 #if DT_SHADE_MINB > 1
@@ -122,15 +123,18 @@ DT_D void flush_counters(unsigned long long* c, int visits, int tests) {
 }
 
 // Shade one traced segment (record idx at level k) and spawn its children into level k+1.
+// The traversal chose the face (float32 candidate search); the hit point, barycentrics,
+// normals and the interface are recomputed here in float64 from the float64 ray state.
 // All 32 lanes of the warp must call this (the compaction is a warp collective).
 template <int ABS, bool VOL>
-DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int64_t lim, int k, int max_depth,
-                          bool valid, int64_t idx, float3 o, float3 d,
-                          int64_t ray, uint32_t pos, float3 thr, float w, int face, float t, float u, float v) {
+DT_D void shade_and_spawn(const FwdLaunch& a, double ior, int64_t child_off, int64_t lim, int k, int max_depth,
+                          bool valid, int64_t idx, double3 o, double3 d, int64_t ray, uint32_t pos, float3 thr, float w,
+                          int face) {
   const DevScene& s = a.s;
   bool is_hit = valid && face >= 0;
   bool spawn_r = false, spawn_t = false, need_tau = false, capped = false, volx = false;
-  float3 x = f3(0, 0, 0), wr = x, wt = x, tau = f3(1, 1, 1), capL = x, Vx = x;
+  double3 x = d3(0, 0, 0), wr = x, wt = x;
+  float3 tau = f3(1, 1, 1), capL = f3(0, 0, 0), Vx = capL;
   float Tx = 1.f;
   float R = 0.f, T = 0.f;
   if (valid) {
@@ -149,16 +153,17 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
       sig_add(a.sig_f, ray, face_key(pos, EV_MISS, -1));
     } else {
       int i0, i1, i2;
-      float3 v0, e1, e2;
-      face_tri(s, face, i0, i1, i2, v0, e1, e2);
-      tri_uv(o, d, v0, e1, e2, u, v);          // the traversal's (u, v), recomputed bit-exactly
-      bool inside = dot(d, cross(e1, e2)) > 0.0f;                             // R8
+      double3 v0, e1, e2;
+      double t, u, v;
+      face_tri64(s, face, i0, i1, i2, v0, e1, e2);
+      mt64(o, d, v0, e1, e2, t, u, v);                                        // R15, float64
+      const bool inside = dot(d, cross(e1, e2)) > 0.0;                        // R8
       x = o + d * t;
       need_tau = inside;
       volx = VOL && !inside;                                                  // exterior, volumetric env
       if (volx) {                                                             // R30
         VolMom mom;
-        env_volume(s, o, x, Vx, Tx, &mom);
+        env_volume(s, f3(o), f3(x), Vx, Tx, &mom);
         __stcs(a.r.mq + idx, f4(mom.Qc, mom.odM));                            // for the backward
         __stcs(a.r.mg + idx, f4(mom.Go, 0.f));
       }
@@ -166,7 +171,7 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
         capped = true;
         if (s.cap_policy == 1) capL = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);   // times tau below
         int fl = RF_CAPPED | (inside ? RF_INSIDE : 0);
-        __stcs(a.r.hit + idx, make_float4(__int_as_float(face), t, 0.f, __int_as_float(fl)));
+        __stcs(a.r.hit + idx, make_float4(__int_as_float(face), (float)t, 0.f, __int_as_float(fl)));
         int ev = inside ? EV_CAP_IN : EV_CAP_OUT;
         sig_add(a.sig_t, ray, topo_key(pos, ev));
         sig_add(a.sig_f, ray, face_key(pos, ev, face));
@@ -174,14 +179,14 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
       } else {
         Shade S;
         shade_forward(s, ior, i0, i1, i2, e1, e2, d, u, v, inside, S);
-        R = S.R;
-        T = S.T;
+        R = (float)S.R;
+        T = (float)S.T;
         wr = S.wr;
         wt = S.wt;
         spawn_r = true;                                                       // P:161 (R5)
         spawn_t = !S.tir;
         int fl = (inside ? RF_INSIDE : 0) | (S.tir ? RF_TIR : 0) | (S.degen ? RF_DEGEN : 0);
-        __stcs(a.r.hit + idx, make_float4(__int_as_float(face), t, R, __int_as_float(fl)));
+        __stcs(a.r.hit + idx, make_float4(__int_as_float(face), (float)t, R, __int_as_float(fl)));
         int ev = inside ? (S.tir ? EV_HIT_IN_TIR : EV_HIT_IN) : (S.tir ? EV_HIT_OUT_TIR : EV_HIT_OUT);
         sig_add(a.sig_t, ray, topo_key(pos, ev));
         sig_add(a.sig_f, ray, face_key(pos, ev, face));
@@ -193,11 +198,12 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
     if (need_tau) tau = transmittance_const(s, o, x);
   } else {
     const GridMap gm = grid_map(s);
+    const float3 of = f3(o), xf = f3(x);
     for (unsigned m = __ballot_sync(~0u, need_tau); m;) {                // cooperative walks
       int myq;
       constexpr int G = WalkLanes<ABS>::fwd;
       const int src = group_take<G>(m, myq), sl = max(src, 0);
-      const float3 Sd = group_optical_depth<G, ABS>(s, gm, shfl3(o, sl), shfl3(x, sl), src >= 0);
+      const float3 Sd = group_optical_depth<G, ABS>(s, gm, shfl3(of, sl), shfl3(xf, sl), src >= 0);
       const float3 mine = shfl3(Sd, max(myq, 0) * G);
       if (myq >= 0) tau = f3(expf(-mine.x), expf(-mine.y), expf(-mine.z));
     }
@@ -222,8 +228,8 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
     int64_t j = off + base + __popc(mr & lanemask_lt());
     if (j < lim) {
       cr = j;
-      __stcs(a.r.o + j, f4(x, __int_as_float((int)ray)));
-      __stcs(a.r.d + j, f4(wr, __uint_as_float(pos * 2u)));
+      stcs64(a.r.o + j, mk64(x, (int)ray, 0u));
+      stcs64(a.r.d + j, mk64(wr, 0, pos * 2u));
       __stcs(a.r.thr + j, f4(thr * tau * R, w * R));
     } else {
       a.lvl[LV_OVERFLOW] = 1;
@@ -232,8 +238,8 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
       j = off + base + nr + __popc(mt & lanemask_lt());
       if (j < lim) {
         ct = j;
-        __stcs(a.r.o + j, f4(x, __int_as_float((int)ray)));
-        __stcs(a.r.d + j, f4(wt, __uint_as_float(pos * 2u + 1u)));
+        stcs64(a.r.o + j, mk64(x, (int)ray, 0u));
+        stcs64(a.r.d + j, mk64(wt, 0, pos * 2u + 1u));
         __stcs(a.r.thr + j, f4(thr * tau * T, w * T));
       } else {
         a.lvl[LV_OVERFLOW] = 1;
@@ -245,13 +251,12 @@ DT_D void shade_and_spawn(const FwdLaunch& a, float ior, int64_t child_off, int6
 }
 
 // Level 0: camera rays.  Each warp takes 32 pixels of an 8x4 tile (or 32 consecutive
-// entries of the caller's pixel list), culls against the root box, traverses, and records
-// only the hitting rays (misses write their env radiance straight to rgb).
+// entries of the caller's pixel list), culls against the root box, traverses (float32
+// candidate search with the rounded ray), and records only the hitting rays, with their
+// float64 ray state (misses write their env radiance straight to rgb).
 template <bool VOL>
 __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
   __shared__ int sstack[kStackShared * kTraceThreads];
-  __shared__ int pstack[(kTraceThreads / 32) * kPacketStack];
-  int* const wstack = pstack + (threadIdx.x >> 5) * kPacketStack;
   const DevScene& s = a.s;
   float3 blo = f3(s.scal[0], s.scal[1], s.scal[2]), bhi = f3(s.scal[3], s.scal[4], s.scal[5]);
   int err = 0, visits = 0, tests = 0, traced = 0;
@@ -277,24 +282,20 @@ __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
       }
     }
     int64_t ray = a.pids ? item : pid;
-    float3 o = f3(0, 0, 0), d = f3(0, 0, 1);
+    double3 o64 = d3(0, 0, 0), d64 = d3(0, 0, 1);
     int face = -1;
     float t = 0.f, u = 0.f, v = 0.f;
     bool inbox = false;
     if (valid) {
-      camera_ray(a.K, a.c2w, a.W, a.H, pid, o, d);
+      camera_ray64(a.K, a.c2w, a.W, a.H, pid, o64, d64);
       float tn;
-      inbox = slab(blo.x, bhi.x, blo.y, bhi.y, blo.z, bhi.z, o, safe_inv(d), kInf, tn);
+      inbox = slab(blo.x, bhi.x, blo.y, bhi.y, blo.z, bhi.z, f3(o64), safe_inv(f3(d64)), kInf, tn);
       traced += inbox;
     }
-    if (a.prim_packet) {                // coherent camera rays: one node sequence per warp
-      face = traverse_packet(s, o, d, inbox, t, u, v, wstack, err, visits, tests);
-    } else if (inbox) {
-      face = traverse(s, o, d, 0.0f, t, u, v, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
-    }
+    if (inbox) face = traverse(s, f3(o64), f3(d64), 0.0f, t, u, v, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
     if (valid) {
       if (face < 0) {
-        float3 L = env_escape<VOL>(s, o, d, f3(0, 0, 0), nullptr, nullptr);
+        float3 L = env_escape<VOL>(s, o64, d64, f3(0, 0, 0), nullptr, nullptr);
         a.rgb[3 * ray] = L.x; a.rgb[3 * ray + 1] = L.y; a.rgb[3 * ray + 2] = L.z;
         sig_add(a.sig_t, ray, topo_key(1u, EV_MISS));
         sig_add(a.sig_f, ray, face_key(1u, EV_MISS, -1));
@@ -310,8 +311,8 @@ __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
     int64_t idx = a.cap - 1 - (rb + __popc(m & lanemask_lt()));
     if (rec && idx < 0) { a.lvl[LV_OVERFLOW] = 1; rec = false; }
     if (rec) {
-      __stcs(a.r.o + idx, f4(o, __int_as_float((int)ray)));
-      __stcs(a.r.d + idx, f4(d, __uint_as_float(1u)));
+      stcs64(a.r.o + idx, mk64(o64, (int)ray, 0u));
+      stcs64(a.r.d + idx, mk64(d64, 0, 1u));
       __stcs(a.r.thr + idx, make_float4(1.f, 1.f, 1.f, 1.f));
       __stcs(a.r.hit + idx, make_float4(__int_as_float(face), t, u, v));   // shaded by k_shade_level(0)
     }
@@ -326,14 +327,16 @@ __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
 // Shading of level k (K10): reads each record's ray and traversal result, evaluates the
 // event and spawns the children into level k+1 (warp-ballot compaction).  Level 0 needs
 // the final level-0 count, so it always runs after the traversal pass.
-// Work distribution: constant-sigma / non-volume levels cost about the same per record, so
-// warps stride statically; with a sigma grid or hash texture (cooperative interior walks) or
-// a volumetric env the cost varies a lot, so warps take 32-record chunks from the level's
-// counter, the next chunk's atomic in flight while the current one is shaded.
+// Each warp takes a window of 64 records and shades them in two rounds of 32 in hit-first
+// lane order (hit_first_order).  Work distribution: constant-sigma / non-volume levels cost
+// about the same per record, so warps stride statically; with a sigma grid or hash texture
+// (cooperative interior walks) or a volumetric env the cost varies a lot, so warps take
+// 64-record windows from the level's counter, the next window's atomic in flight while the
+// current one is shaded.
 template <int ABS, bool VOL>
 DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
   if (a.lvl[LV_OVERFLOW]) return;   // arena too small: the host grows it and re-runs
-  const float ior = a.s.ior_ptr ? __ldg(a.s.ior_ptr) : a.s.ior;
+  const double ior = a.s.ior_ptr ? (double)__ldg(a.s.ior_ptr) : (double)a.s.ior;
   // level offsets are fixed while this kernel runs (only level k+1's count grows): read once
   const int n = a.lvl[LV_CNT + k];
   const int64_t off = k == 0 ? 0 : level_base(a.lvl, k);
@@ -343,15 +346,11 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
   constexpr bool kDyn = ABS != 0 || VOL;
   int* const ctr = a.lvl + LV_WORK_SHADE + k;
   __shared__ unsigned char sslot[kTraceThreads * 2];
-  const bool sorted = a.sort_lanes;   // 64-record windows, hit-first (two rounds of 32)
-  const int chunk = sorted ? 64 : 32;
-  const int64_t wstep = sorted ? 2 * stride : stride;
-  int64_t wbase = kDyn ? (int64_t)fetch_work(ctr, chunk)
-                       : (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * (sorted ? 2 : 1);
+  int64_t wbase = kDyn ? (int64_t)fetch_work(ctr, 64) : (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 2;
   int round = 0, ord0 = 0, ord1 = 0, next = 0;
   while (wbase < n) {
-    if (round == 0 && kDyn && lane_id() == 0) next = atomicAdd(ctr, chunk);
-    if (sorted && round == 0) {
+    if (round == 0 && kDyn && lane_id() == 0) next = atomicAdd(ctr, 64);
+    if (round == 0) {
       int c[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -361,28 +360,29 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
       }
       hit_first_order(c[0], c[1], sslot + 2 * (threadIdx.x & ~31), ord0, ord1);
     }
-    const int64_t item = wbase + (sorted ? (round == 0 ? ord0 : ord1) : lane_id());
+    const int64_t item = wbase + (round == 0 ? ord0 : ord1);
     const bool valid = item < n;
     const int64_t idx = k == 0 ? a.cap - 1 - item : off + item;
-    float3 o = f3(0, 0, 0), d = f3(0, 0, 1), thr = f3(0, 0, 0);
+    double3 o = d3(0, 0, 0), d = d3(0, 0, 1);
+    float3 thr = f3(0, 0, 0);
     float w = 0.f;
     int64_t ray = 0;
     uint32_t pos = 0;
     int face = -1;
-    float t = 0, u = 0, v = 0;
     if (valid) {
-      float4 ro = __ldcs(a.r.o + idx), rd = __ldcs(a.r.d + idx), rt = __ldcs(a.r.thr + idx), h = __ldcs(a.r.hit + idx);
-      o = f3(ro); d = f3(rd); thr = f3(rt); w = rt.w;
-      ray = __float_as_int(ro.w);
-      pos = __float_as_uint(rd.w);
-      face = __float_as_int(h.x); t = h.y; u = h.z; v = h.w;
+      const Vec64 ro = ldcs64(a.r.o + idx), rd = ldcs64(a.r.d + idx);
+      const float4 rt = __ldcs(a.r.thr + idx), h = __ldcs(a.r.hit + idx);
+      o = xyz(ro); d = xyz(rd); thr = f3(rt); w = rt.w;
+      ray = ro.i;
+      pos = rd.u;
+      face = __float_as_int(h.x);
     }
-    shade_and_spawn<ABS, VOL>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, t, u, v);
-    if (sorted && round == 0) {
+    shade_and_spawn<ABS, VOL>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face);
+    if (round == 0) {
       round = 1;
     } else {
       round = 0;
-      wbase = kDyn ? (int64_t)__shfl_sync(~0u, next, 0) : wbase + wstep;
+      wbase = kDyn ? (int64_t)__shfl_sync(~0u, next, 0) : wbase + 2 * stride;
     }
   }
 }
@@ -404,8 +404,9 @@ __global__ void __maxnreg__(DT_SHADE_VOL_REGS) k_shade_level_vol(FwdLaunch a, in
 }
 
 // Traversal of level k >= 1 (K9): closest hit only, hit = (face, t, u, v) written back into
-// the record.  Lanes that finish their ray refill from the level's queue (one warp-aggregated
-// atomic per refill), so short reflected rays do not idle a warp behind long refracted ones.
+// the record (the float32 candidate search; shade recomputes the hit in float64).  Lanes that
+// finish their ray refill from the level's queue (one warp-aggregated atomic per refill), so
+// short reflected rays do not idle a warp behind long refracted ones.
 constexpr int kStepBudget = 16;   // traversal steps between refill votes (swept: 8 / 16 / 32)
 __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
   __shared__ int sstack_all[kStackShared * kTraceThreads];
@@ -422,49 +423,19 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
   float3 o = f3(0, 0, 0), d = f3(0, 0, 1), inv = f3(0, 0, 0);
   Trav T;
   trav_init(T);
-  int chunk_next = 0, chunk_end = 0;   // warp-uniform (mode 2)
-  const int mode = a.trav_mode;
   while (true) {
     unsigned need = __ballot_sync(~0u, item < 0);
-    // mode 0: the warp refills only when no lane is still traversing
-    if (mode == 0 && __ballot_sync(~0u, item < 0 || item >= n) != ~0u) need = 0;
-    while (need) {
-      int j = -1;
-      if (mode == 1 || mode == 0) {
-        // global queue: one warp-aggregated atomic
-        int leader = __ffs(need) - 1;
-        int base = 0;
-        if (lane_id() == leader) base = atomicAdd(work, __popc(need));
-        base = __shfl_sync(~0u, base, leader);
-        if ((need >> lane_id()) & 1) j = base + __popc(need & lanemask_lt());
-        need = 0;
-      } else {
-        // warp-private chunk of consecutive rays (keeps a warp's rays spatially coherent)
-        if (chunk_next >= chunk_end) {
-          int b = 0;
-          if (lane_id() == 0) b = atomicAdd(work, a.trav_chunk);
-          b = __shfl_sync(~0u, b, 0);
-          chunk_next = b;
-          chunk_end = min(b + a.trav_chunk, n);
-          if (b >= n) {
-            if (item < 0) item = n;
-            break;
-          }
-        }
-        int avail = chunk_end - chunk_next;
-        int r = __popc(need & lanemask_lt());
-        if (((need >> lane_id()) & 1) && r < avail) j = chunk_next + r;
-        int taken = min(__popc(need), avail);
-        chunk_next += taken;
-        unsigned served = __ballot_sync(~0u, j >= 0);
-        need &= ~served;
-      }
-      if (j >= 0) {
+    if (need) {                        // one warp-aggregated atomic on the level's queue
+      const int leader = __ffs(need) - 1;
+      int base = 0;
+      if (lane_id() == leader) base = atomicAdd(work, __popc(need));
+      base = __shfl_sync(~0u, base, leader);
+      if (item < 0) {
+        const int j = base + __popc(need & lanemask_lt());
         if (j < n) {
           item = j;
-          float4 ro = __ldcs(a.r.o + off + j), rd = __ldcs(a.r.d + off + j);
-          o = f3(ro);
-          d = f3(rd);
+          o = f3(xyz(ldcs64(a.r.o + off + j)));       // the float64 ray, rounded for the search
+          d = f3(xyz(ldcs64(a.r.d + off + j)));
           inv = safe_inv(d);
           trav_init(T);
         } else {
@@ -480,85 +451,6 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
     if (done) {
       __stcs(a.r.hit + off + item, make_float4(__int_as_float(T.best), T.bt, T.bu, T.bv));
       item = -1;
-    }
-  }
-  if (err) a.lvl[LV_STACKERR] = 1;
-  flush_counters(a.counters, visits, tests);
-}
-
-// Warp-synchronous variant of k_traverse_level (trav_mode 3): every lane runs the same step
-// loop; a lane that reaches a leaf parks it (one slot) and keeps descending nodes, and the
-// warp switches to a leaf phase -- all parked leaves tested together -- once at least
-// `leaf_vote` lanes have a parked leaf or no node left (Aila & Laine's postponed leaves).
-__global__ void DT_TRAV_LB k_traverse_level_ws(FwdLaunch a, int k) {
-  __shared__ int sstack_all[kStackShared * kTraceThreads];
-  const DevScene& s = a.s;
-  if (a.lvl[LV_OVERFLOW]) return;
-  const float t_lo = a.t_eps * s.scal[6];                                      // R17
-  const int n = a.lvl[LV_CNT + k];
-  const int64_t off = level_base(a.lvl, k);
-  int* work = a.lvl + LV_WORK_TRACE + k;
-  int* sstack = sstack_all + threadIdx.x;
-  int lstack[kStackLocal];
-  int err = 0, visits = 0, tests = 0;
-  int item = -1;
-  float3 o = f3(0, 0, 0), d = f3(0, 0, 1), inv = f3(0, 0, 0);
-  Trav T;
-  trav_init(T);
-  int leaf = kEmptyRef;
-  while (true) {
-    unsigned need = __ballot_sync(~0u, item < 0);
-    if (need) {
-      int leader = __ffs(need) - 1;
-      int base = 0;
-      if (lane_id() == leader) base = atomicAdd(work, __popc(need));
-      base = __shfl_sync(~0u, base, leader);
-      if (item < 0) {
-        int j = base + __popc(need & lanemask_lt());
-        if (j < n) {
-          item = j;
-          float4 ro = __ldcs(a.r.o + off + j), rd = __ldcs(a.r.d + off + j);
-          o = f3(ro);
-          d = f3(rd);
-          inv = safe_inv(d);
-          trav_init(T);
-          leaf = kEmptyRef;
-        } else {
-          item = n;
-        }
-      }
-    }
-    if (__all_sync(~0u, item >= n)) break;
-    for (int step = 0; step < kStepBudget; ++step) {
-      bool active = item >= 0 && item < n;
-      bool node_avail = active && T.cur >= 0 && T.cur != kEmptyRef;
-      bool has_leaf = active && leaf != kEmptyRef;
-      // ready = active with a parked leaf (an active lane without a node always has one)
-      unsigned act = __ballot_sync(~0u, active);
-      unsigned rdy = __ballot_sync(~0u, active && (has_leaf || !node_avail));
-      if (rdy != 0 && (rdy == act || __popc(rdy) >= a.leaf_vote)) {
-        if (has_leaf) {
-          trav_leaf(s, o, d, t_lo, leaf, T, tests);
-          leaf = kEmptyRef;
-        }
-      } else if (node_avail) {
-        trav_node(s, o, inv, T, sstack, kTraceThreads, lstack, err, visits);
-      }
-      if (active) {
-        while (true) {                 // park a leaf, pop until a node is current
-          if (T.cur == kEmptyRef && (err || !stack_pop(T, sstack, kTraceThreads, lstack))) break;
-          if (T.cur < 0 && leaf == kEmptyRef) {
-            leaf = T.cur;
-            T.cur = kEmptyRef;
-            continue;
-          }
-          break;
-        }
-        if (T.cur == kEmptyRef && leaf == kEmptyRef && (T.sp == 0 || err)) {
-          __stcs(a.r.hit + off + item, make_float4(__int_as_float(T.best), T.bt, T.bu, T.bv));
-          item = -1;
-        }
-      }
     }
   }
   if (err) a.lvl[LV_STACKERR] = 1;
@@ -588,7 +480,7 @@ __global__ void k_gather(FwdLaunch a, int k) {
       a.r.lsub[idx] = f4(L, ls.w);
     }
     if (k == 0) {
-      int64_t ray = __float_as_int(a.r.o[idx].w);
+      int64_t ray = a.r.o[idx].i;
       a.rgb[3 * ray] = L.x; a.rgb[3 * ray + 1] = L.y; a.rgb[3 * ray + 2] = L.z;
     }
   }
@@ -599,28 +491,30 @@ DT_D void atomic_add3(float4* p, float3 v) {
   atomicAdd(p, make_float4(v.x, v.y, v.z, 0.0f));
 }
 
-// Backward replay of level k (K12): per record, the local VJP at fixed topology.  Three
+// Backward replay of level k (K12): per record, the local VJP at fixed topology, evaluated at
+// the float64 ray state the forward used: the hit and the interface state are recomputed in
+// float64 exactly as the forward did, then rounded to float32 for the Jacobian-times-adjoint
+// arithmetic (the adjoints are float32; no state error propagates along the path).  Three
 // phases per warp-iteration so that the sigma-grid walks (ABS = grid) run warp-cooperatively:
 // (A) per lane: env / interface adjoints up to the interior segment's optical-depth adjoint
 // gS; (B) the transmittance adjoints of the warp's interior segments, one segment at a time
 // by the whole warp (or per lane for constant sigma); (C) per lane: x = o + t d and the
 // Moller-Trumbore reverse, vertex and normal atomics, parent-slot adjoints.
+// Each warp takes a window of 64 records in two rounds of 32, interface records first.
 template <int ABS, bool VOL>
 DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t cap) {
   const DevScene& s = a.s;
   if (a.lvl[LV_OVERFLOW]) return;   // an overflowed (asynchronous) forward: nothing valid to replay
-  const float ior = s.ior_ptr ? __ldg(s.ior_ptr) : s.ior;
+  const double ior = s.ior_ptr ? (double)__ldg(s.ior_ptr) : (double)s.ior;
   const int n = a.lvl[LV_CNT + k];
   const int64_t off = k == 0 ? 0 : level_base(a.lvl, k);
   float gior = 0.0f;
   float3 gsc = f3(0, 0, 0);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   __shared__ unsigned char sslot[kBwdThreads * 2];
-  const bool sorted = a.sort_lanes;   // 64-record windows, interface (hit) records first
-  const int per = sorted ? 2 : 1;
-  for (int64_t wb = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * per; wb < n; wb += stride * per) {
-  int o0 = lane_id(), o1 = 32 + lane_id();
-  if (sorted) {
+  for (int64_t wb = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 2; wb < n; wb += stride * 2) {
+  int o0, o1;
+  {
     int c[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -633,26 +527,25 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
     }
     hit_first_order(c[0], c[1], sslot + 2 * (threadIdx.x & ~31), o0, o1);
   }
-  for (int round = 0; round < per; ++round) {
+  for (int round = 0; round < 2; ++round) {
     const int64_t item = wb + (round == 0 ? o0 : o1);
     const bool valid = item < n;
     int64_t idx = 0;
-    float3 o = f3(0, 0, 0), d = f3(0, 0, 1), x = o, gS = o;
-    float3 go = f3(0, 0, 0), gd = f3(0, 0, 0), gx = f3(0, 0, 0);
-    float3 e1 = o, e2 = o, gNk[3];
-    float t = 0.f, u = 0.f, v = 0.f, gu = 0.f, gv = 0.f;
+    float3 go = f3(0, 0, 0), gd = go, gx = go, gS = go, gNk[3];
+    float3 of = go, xf = go, df = go, dhf = go, e1f = go, e2f = go;   // float32 copies for the reverse
+    float t = 0.f, u = 0.f, v = 0.f, gu = 0.f, gv = 0.f, idet = 0.f, lch = 0.f;
     int fl = 0, i0 = 0, i1 = 0, i2 = 0;
     bool geo = false, walk = false;
     // ---- (A)
     if (valid) {
       idx = k == 0 ? cap - 1 - item : off + item;
-      float4 ro = a.r.o[idx], rd = a.r.d[idx], rt = a.r.thr[idx], h = a.r.hit[idx];
-      o = f3(ro);
-      d = f3(rd);
-      int64_t ray = __float_as_int(ro.w);
+      const Vec64 ro = ldcs64(a.r.o + idx), rd = ldcs64(a.r.d + idx);
+      const float4 rt = a.r.thr[idx], h = a.r.hit[idx];
+      const double3 o = xyz(ro), d = xyz(rd);
+      const int64_t ray = ro.i;
       fl = __float_as_int(h.w);
       const float* g = a.grad_rgb + 3 * ray;
-      float3 adj = f3(__ldg(g), __ldg(g + 1), __ldg(g + 2)) * f3(rt);          // a_n = grad * throughput
+      const float3 adj = f3(__ldg(g), __ldg(g + 1), __ldg(g + 2)) * f3(rt);   // a_n = grad * throughput
       const bool volx = VOL && !(fl & (RF_MISS | RF_INSIDE));                 // exterior segment, R30
       VolMom mom;
       if (VOL && !(fl & RF_INSIDE)) {                                         // recorded by the forward
@@ -668,41 +561,55 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
         // capped branches return 0: no dependence
       } else {
         geo = true;
-        int face = __float_as_int(h.x);
-        float3 v0;
-        face_tri(s, face, i0, i1, i2, v0, e1, e2);
-        intersect_tri(o, d, v0, e1, e2, -kInf, t, u, v);                    // replay (bit-identical)
-        x = o + d * t;
-        bool inside = (fl & RF_INSIDE) != 0;
-        float4 tu = a.r.tau[idx];
-        float3 tau = f3(tu);
+        const int face = __float_as_int(h.x);
+        const bool inside = (fl & RF_INSIDE) != 0;
+        double3 v0, e1, e2;
+        double t64, u64, v64;
+        face_tri64(s, face, i0, i1, i2, v0, e1, e2);
+        idet = (float)mt64(o, d, v0, e1, e2, t64, u64, v64);                 // the forward's hit, replayed
+        const double3 x = o + d * t64;
+        of = f3(o); xf = f3(x); df = f3(d); e1f = f3(e1); e2f = f3(e2);
+        t = (float)t64; u = (float)u64; v = (float)v64;
+        lch = (float)length(x - o);
+        dhf = f3(d * rsqrt64(dot(d, d)));
+        const float4 tu = a.r.tau[idx];
+        const float3 tau = f3(tu);
         if (fl & RF_CAPPED) {                                                 // CAP_ENV leaf
           if (volx) {                                                         // V + Tn * (E or 0)
             float aT = 0.f;
             if (s.cap_policy == 1) aT = dot(adj, env_eval(s, o, d, adj * tau, &go, &gd));
-            env_volume_bwd(s, o, x, adj, aT, tau.x, mom, go, gx);
+            env_volume_bwd(s, of, xf, adj, aT, tau.x, mom, go, gx);
           } else {
-            float3 E = env_eval(s, o, d, adj * tau, &go, &gd);
+            const float3 E = env_eval(s, o, d, adj * tau, &go, &gd);
             if (inside) { walk = true; gS = -(adj * E * tau); }
           }
           gNk[0] = gNk[1] = gNk[2] = f3(0, 0, 0);
         } else {
-          Shade S;
-          shade_forward(s, ior, i0, i1, i2, e1, e2, d, u, v, inside, S);
-          float4 ls = a.r.lsub[idx];
-          int cr = __float_as_int(ls.w), ct = __float_as_int(tu.w);
-          float3 Lr = f3(0, 0, 0), Lt = f3(0, 0, 0), gwr = f3(0, 0, 0), gwt = f3(0, 0, 0);
+          ShadeF S;
+          {
+            Shade S64;
+            shade_forward(s, ior, i0, i1, i2, e1, e2, d, u64, v64, inside, S64);
+            S = shade_f32(S64);
+          }
+          const float4 ls = a.r.lsub[idx];
+          const int cr = __float_as_int(ls.w), ct = __float_as_int(tu.w);
+          float3 Lr = f3(0, 0, 0), Lt = f3(0, 0, 0);
+          float3 gwr = f3(0, 0, 0), gwt = f3(0, 0, 0);
           if (cr >= 0) { Lr = f3(a.r.lsub[cr]); gx += f3(a.r.go[cr]); gwr = f3(a.r.gd[cr]); }
           if (ct >= 0) { Lt = f3(a.r.lsub[ct]); gx += f3(a.r.go[ct]); gwt = f3(a.r.gd[ct]); }
-          float3 ap = adj * tau;
-          float3 Lc = Lr * S.R + Lt * S.T;
-          float gR = S.tir ? 0.0f : dot(ap, Lr - Lt);
+          const float3 ap = adj * tau;
+          const float Rf = h.z;                                               // R, as the forward stored it
+          const float3 Lc = Lr * Rf + Lt * (1.0f - Rf);
+          const float gR = S.tir ? 0.0f : dot(ap, Lr - Lt);
           if (inside) { walk = true; gS = -(adj * Lc * tau); }
-          if (volx) env_volume_bwd(s, o, x, adj, dot(adj, Lc), tau.x, mom, go, gx);   // V + Tn * Lc (R30)
+          if (volx) {                                                         // V + Tn * Lc (R30)
+            env_volume_bwd(s, of, xf, adj, dot(adj, Lc), tau.x, mom, go, gx);
+          }
           float3 gd_s;
           float gi;
-          float3 n0 = f3(__ldg(s.nrm + i0)), n1 = f3(__ldg(s.nrm + i1)), n2 = f3(__ldg(s.nrm + i2));
-          shade_backward(S, gR, gwr, gwt, n0, n1, n2, gd_s, gu, gv, gNk, gi);
+          const float3 n0 = f3(xyz(ldg_d4(s.nrm + i0))), n1 = f3(xyz(ldg_d4(s.nrm + i1))),
+                       n2 = f3(xyz(ldg_d4(s.nrm + i2)));
+          shade_backward(S, df, gR, gwr, gwt, n0, n1, n2, gd_s, gu, gv, gNk, gi);
           gd += gd_s;
           gior += gi;
         }
@@ -710,7 +617,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
     }
     // ---- (B) interior transmittance o -> x
     if (ABS == 0) {
-      if (walk) transmittance_const_backward(s, o, x, gS, gx, go, gsc);
+      if (walk) transmittance_const_backward(s, lch, dhf, gS, gx, go, gsc);
     } else {
       const GridMap gm = grid_map(s);
       for (unsigned m = __ballot_sync(~0u, walk); m;) {
@@ -718,7 +625,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
         constexpr int G = WalkLanes<ABS>::bwd;
         const int src = group_take<G>(m, myq), sl = max(src, 0);
         float3 wgx, wgo;
-        group_transmittance_backward<G, ABS>(s, gm, shfl3(o, sl), shfl3(x, sl), shfl3(gS, sl), src >= 0, a.dsig, wgx,
+        group_transmittance_backward<G, ABS>(s, gm, shfl3(of, sl), shfl3(xf, sl), shfl3(gS, sl), src >= 0, a.dsig, wgx,
                                              wgo);
         const float3 mx = shfl3(wgx, max(myq, 0) * G), mo = shfl3(wgo, max(myq, 0) * G);
         if (myq >= 0) { gx += mx; go += mo; }
@@ -728,9 +635,8 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
     if (geo) {
       go += gx;
       gd += gx * t;
-      float gt = dot(gx, d);
       float3 gVk[3];
-      mt_backward(d, e1, e2, t, u, v, gu, gv, gt, go, gd, gVk);
+      mt_backward(df, e1f, e2f, idet, t, u, v, gu, gv, dot(gx, df), go, gd, gVk);
       atomic_add3(a.dV + i0, gVk[0]);
       atomic_add3(a.dV + i1, gVk[1]);
       atomic_add3(a.dV + i2, gVk[2]);
@@ -773,7 +679,7 @@ __global__ void __maxnreg__(DT_BWD_GRID_REGS)
 // constant sigma, shell env: latency bound (dependent record -> child / vertex / gradient
 // fetches), so a register cap that buys occupancy pays (tools/sweep_regs.sh)
 #ifndef DT_BWD_CONST_REGS
-#define DT_BWD_CONST_REGS 80
+#define DT_BWD_CONST_REGS 96
 #endif
 __global__ void __maxnreg__(DT_BWD_CONST_REGS) k_backward_level_const(BwdLaunch a, int k, int max_depth, int64_t cap) {
   backward_level_body<0, false>(a, k, max_depth, cap);
@@ -788,27 +694,27 @@ __global__ void __maxnreg__(DT_BWD_VOL_REGS) k_backward_level_vol(BwdLaunch a, i
 
 // Vertex-normal chain (reverse of P:170-173): dN -> d(sum of unit face normals) per vertex,
 // -> per face d/de1, d/de2 -> gathered back per vertex through the corner CSR.
-__global__ void k_vn_bwd_vertex(const float4* __restrict__ dN, const float4* __restrict__ nrm, int nv, float4* __restrict__ gS) {
+__global__ void k_vn_bwd_vertex(const float4* __restrict__ dN, const D4* __restrict__ nrm, int nv, float4* __restrict__ gS) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
-    float4 n = nrm[v];
-    float3 g = f3(dN[v]), nn = f3(n);
-    gS[v] = n.w > 0.0f ? f4((g - nn * dot(nn, g)) * (1.0f / n.w), 0.f) : make_float4(0, 0, 0, 0);
+    const D4 n = nrm[v];
+    const double3 g = d3(dN[v]), nn = xyz(n);
+    gS[v] = n.w > 0.0 ? f4(f3((g - nn * dot(nn, g)) * (1.0 / n.w)), 0.f) : make_float4(0, 0, 0, 0);
   }
 }
 
-__global__ void k_vn_bwd_face(const float4* __restrict__ V, const int* __restrict__ F, const float4* __restrict__ fn,
+__global__ void k_vn_bwd_face(const float4* __restrict__ V, const int* __restrict__ F, const D4* __restrict__ fn,
                               const float4* __restrict__ gS, int nf, float4* __restrict__ fe) {
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x) {
-    float4 h4 = fn[f];
-    if (!(h4.w > 0.0f)) { fe[2 * f] = make_float4(0, 0, 0, 0); fe[2 * f + 1] = make_float4(0, 0, 0, 0); continue; }
+    const D4 h4 = fn[f];
+    if (!(h4.w > 0.0)) { fe[2 * f] = make_float4(0, 0, 0, 0); fe[2 * f + 1] = make_float4(0, 0, 0, 0); continue; }
     int i0 = F[3 * f], i1 = F[3 * f + 1], i2 = F[3 * f + 2];
-    float3 gh = f3(gS[i0]) + f3(gS[i1]) + f3(gS[i2]);
-    float3 h = f3(h4);
-    float3 gc = (gh - h * dot(h, gh)) * (1.0f / h4.w);
-    float3 a = f3(V[i0]);
-    float3 e1 = f3(V[i1]) - a, e2 = f3(V[i2]) - a;
-    fe[2 * f] = f4(cross(e2, gc), 0.f);      // d/de1 of c = e1 x e2
-    fe[2 * f + 1] = f4(cross(gc, e1), 0.f);  // d/de2
+    const double3 gh = d3(gS[i0]) + d3(gS[i1]) + d3(gS[i2]);
+    const double3 h = xyz(h4);
+    const double3 gc = (gh - h * dot(h, gh)) * (1.0 / h4.w);
+    const double3 a = d3(V[i0]);
+    const double3 e1 = d3(V[i1]) - a, e2 = d3(V[i2]) - a;
+    fe[2 * f] = f4(f3(cross(e2, gc)), 0.f);      // d/de1 of c = e1 x e2
+    fe[2 * f + 1] = f4(f3(cross(gc, e1)), 0.f);  // d/de2
   }
 }
 
@@ -886,6 +792,13 @@ __global__ void k_count_segments(const int* __restrict__ lvl, int D, unsigned lo
   *seg += s;
 }
 
+__global__ void k_normals_to_f32(const D4* __restrict__ nrm, int nv, float* __restrict__ out) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    const D4 n = nrm[v];
+    out[3 * v] = (float)n.x; out[3 * v + 1] = (float)n.y; out[3 * v + 2] = (float)n.z;
+  }
+}
+
 __global__ void k_check_finite(const float* __restrict__ x, int64_t n, int* flag) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (!isfinite(x[i])) *flag = 1;
@@ -929,16 +842,17 @@ int persistent_blocks(const void* fn, int threads, int sm_count) {
 
 }  // namespace
 
-template <class K>
-void launch_persistent(K kernel, int& grid, int threads, int sm_count, cudaStream_t st, const FwdLaunch& a, int x) {
-  if (!grid) grid = persistent_blocks((const void*)kernel, threads, sm_count);
-  kernel<<<grid, threads, 0, st>>>(a, x);
+// persistent grid of `kernel` on this context's device, cached per context (slot of grid_cache)
+int cached_grid(int* cache, int slot, const void* kernel, int threads, int sm_count) {
+  if (!cache[slot]) cache[slot] = persistent_blocks(kernel, threads, sm_count);
+  return cache[slot];
 }
 
 cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count, cudaStream_t st) {
-  static int g[2] = {0, 0};
-  if (a.s.env_kind == 2) launch_persistent(k_trace_primary<true>, g[1], kTraceThreads, sm_count, st, a, max_depth);
-  else launch_persistent(k_trace_primary<false>, g[0], kTraceThreads, sm_count, st, a, max_depth);
+  const bool vol = a.s.env_kind == 2;
+  auto kern = vol ? k_trace_primary<true> : k_trace_primary<false>;
+  const int g = cached_grid(a.grids, vol ? kGridPrimaryVol : kGridPrimary, (const void*)kern, kTraceThreads, sm_count);
+  kern<<<g, kTraceThreads, 0, st>>>(a, max_depth);
   return cudaGetLastError();
 }
 
@@ -946,13 +860,12 @@ cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count
 // variant carries only its own registers
 template <int ABS>
 void shade_dispatch(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
-  static int g[2] = {0, 0};
   const bool vol = a.s.env_kind == 2;
   auto kern = ABS == 1 ? (vol ? k_shade_level_grid<true> : k_shade_level_grid<false>)
                : ABS == 0 && vol ? k_shade_level_vol
                                  : (vol ? k_shade_level<ABS, true> : k_shade_level<ABS, false>);
-  if (!g[vol]) g[vol] = persistent_blocks((const void*)kern, kTraceThreads, sm_count);
-  kern<<<g[vol], kTraceThreads, 0, st>>>(a, level, max_depth);
+  const int g = cached_grid(a.grids, kGridShade + 2 * ABS + vol, (const void*)kern, kTraceThreads, sm_count);
+  kern<<<g, kTraceThreads, 0, st>>>(a, level, max_depth);
 }
 
 cudaError_t launch_shade_level(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
@@ -963,14 +876,8 @@ cudaError_t launch_shade_level(const FwdLaunch& a, int level, int max_depth, int
 }
 
 cudaError_t launch_traverse_level(const FwdLaunch& a, int level, int sm_count, cudaStream_t st) {
-  static int gl = 0, gw = 0;
-  if (a.trav_mode == 3) {
-    if (!gw) gw = persistent_blocks((const void*)k_traverse_level_ws, kTraceThreads, sm_count);
-    k_traverse_level_ws<<<gw, kTraceThreads, 0, st>>>(a, level);
-  } else {
-    if (!gl) gl = persistent_blocks((const void*)k_traverse_level, kTraceThreads, sm_count);
-    k_traverse_level<<<gl, kTraceThreads, 0, st>>>(a, level);
-  }
+  const int g = cached_grid(a.grids, kGridTrav, (const void*)k_traverse_level, kTraceThreads, sm_count);
+  k_traverse_level<<<g, kTraceThreads, 0, st>>>(a, level);
   return cudaGetLastError();
 }
 
@@ -981,13 +888,12 @@ cudaError_t launch_gather_level(const FwdLaunch& a, int level, int sm_count, cud
 
 template <int ABS>
 void backward_dispatch(const BwdLaunch& a, int level, int sm_count, cudaStream_t st) {
-  static int g[2] = {0, 0};
   const bool vol = a.s.env_kind == 2;
   auto kern = ABS == 1 ? (vol ? k_backward_level_grid<true> : k_backward_level_grid<false>)
                : ABS == 0 ? (vol ? k_backward_level_vol : k_backward_level_const)
                           : (vol ? k_backward_level<ABS, true> : k_backward_level<ABS, false>);
-  if (!g[vol]) g[vol] = persistent_blocks((const void*)kern, kBwdThreads, sm_count);
-  kern<<<g[vol], kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
+  const int g = cached_grid(a.grids, kGridBwd + 2 * ABS + vol, (const void*)kern, kBwdThreads, sm_count);
+  kern<<<g, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
 }
 
 cudaError_t launch_backward_level(const BwdLaunch& a, int level, int sm_count, cudaStream_t st) {
@@ -1040,6 +946,11 @@ cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, int r
 
 cudaError_t launch_count_segments(const int* lvl, int max_depth, unsigned long long* seg, cudaStream_t st) {
   k_count_segments<<<1, 1, 0, st>>>(lvl, max_depth, seg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_normals_to_f32(const D4* nrm, int nv, float* out, cudaStream_t st) {
+  k_normals_to_f32<<<std::max(1, std::min((nv + 255) / 256, 148 * 8)), 256, 0, st>>>(nrm, nv, out);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 import oracle as O
 from paper_2603_00413_b200 import scenes as S
 from tests import _scenes as T
-from tests._parity import GRAD_TOL, assert_forward, compare_forward, grad_upstream, oracle_forward, rel_l2
+from tests._parity import GRAD_TOL, assert_forward, compare_forward, grad_upstream, oracle_forward, rel_l2, report
 
 pytestmark = pytest.mark.gpu
 
@@ -45,13 +45,11 @@ def parity_case(tracer, sc, pixel_ids, label, grad_seed=11):
     gpu = run_gpu(tracer, sc, pixel_ids)
     cmp = compare_forward(gpu["rgb"], gpu["sig"], orc)
     assert_forward(cmp, label)
-    # capped weight (a diagnostic output): the ill-conditioning flag is computed on rgb only,
-    # so allow 1e-3 of the remaining pixels beyond 1e-4
-    ok = ~(cmp["div_mask"] | cmp["flag_mask"])
-    bad = np.abs(gpu["capw"][ok] - orc["capped_w"][ok]) > 1e-4
-    assert bad.sum() <= max(1, int(1e-3 * ok.sum())), (label, int(bad.sum()))
-    g = S.upstream_grad(len(pixel_ids), grad_seed)
-    g[cmp["div_mask"] | cmp["flag_mask"]] = 0.0
+    # capped weight (a diagnostic output: the sum of the capped branches' R/T path weights)
+    ok = ~cmp["div_mask"]
+    if ok.any():
+        assert np.abs(gpu["capw"][ok] - orc["capped_w"][ok]).max() <= 1e-4, label
+    g = grad_upstream(S.upstream_grad(len(pixel_ids), grad_seed), cmp)
     gpu = run_gpu(tracer, sc, pixel_ids, grad=g)
     gV, gi, gs = O.backward(osc, g, pixel_ids)
     errs = dict(V=rel_l2(gpu["gV"], gV), sigma=rel_l2(gpu["gsig"], gs))
@@ -60,6 +58,7 @@ def parity_case(tracer, sc, pixel_ids, label, grad_seed=11):
     errs["ior"], es = scalar_block_errors(tracer, osc, pixel_ids, g, sc.absorption.kind == S.ABS_CONST)
     if es is not None:
         errs["sigma_groups"] = es
+    report(label + " grad", {"n": len(pixel_ids)}, {k: float(e) for k, e in errs.items()})
     for k, e in errs.items():
         assert e <= GRAD_TOL, (label, k, errs)
     return cmp, errs, gpu["stats"]
@@ -183,14 +182,14 @@ def test_c2_full_launch_sampled_compare(tracer):
     cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
     assert_forward(cmp, "C2-full")
     gfull = np.zeros((sc.n_pixels, 3), np.float32)
-    g = S.upstream_grad(len(pid), 12)
-    g[cmp["div_mask"] | cmp["flag_mask"]] = 0
+    g = grad_upstream(S.upstream_grad(len(pid), 12), cmp)
     gfull[pid] = g
     gpu = run_gpu(tracer, sc, None, full_launch_grad=gfull)
     gV, gi, gs = O.backward(osc, g, pid)
-    assert rel_l2(gpu["gV"], gV) <= GRAD_TOL
+    e_v = rel_l2(gpu["gV"], gV)
     e_ior, e_sig = scalar_block_errors(tracer, osc, pid, g, True, n_full=sc.n_pixels)
-    assert e_ior <= GRAD_TOL and e_sig <= GRAD_TOL, (e_ior, e_sig)
+    report("C2-full grad", {"n": len(pid)}, {"V": e_v, "ior": e_ior, "sigma_groups": e_sig})
+    assert e_v <= GRAD_TOL and e_ior <= GRAD_TOL and e_sig <= GRAD_TOL, (e_v, e_ior, e_sig)
 
 
 def test_sigma_grid_and_far_field(tracer):
@@ -236,12 +235,13 @@ def test_c3v_volume_env_full_size_sampled(tracer):
     cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
     assert_forward(cmp, "C3V")
     gfull = np.zeros((sc.n_pixels, 3), np.float32)
-    g = S.upstream_grad(len(pid), 17)
-    g[cmp["div_mask"] | cmp["flag_mask"]] = 0
+    g = grad_upstream(S.upstream_grad(len(pid), 17), cmp)
     gfull[pid] = g
     gpu = run_gpu(tracer, sc, None, full_launch_grad=gfull)
     gV, gi, gs = O.backward(osc, g, pid)
-    assert rel_l2(gpu["gV"], gV) <= GRAD_TOL
+    e_v = rel_l2(gpu["gV"], gV)
+    report("C3V grad", {"n": len(pid)}, {"V": e_v})
+    assert e_v <= GRAD_TOL, e_v
 
 
 def test_hash_dense_level_equals_grid(tracer):
@@ -295,13 +295,14 @@ def test_c3_full_size_sampled(tracer):
     cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
     assert_forward(cmp, "C3")
     gfull = np.zeros((sc.n_pixels, 3), np.float32)
-    g, _ = grad_upstream(O, osc, pid, S.upstream_grad(len(pid), 13), cmp)
+    g = grad_upstream(S.upstream_grad(len(pid), 13), cmp)
     gfull[pid] = g
     gpu = run_gpu(tracer, sc, None, full_launch_grad=gfull)
     gV, gi, gs = O.backward(osc, g, pid)
-    assert rel_l2(gpu["gV"], gV) <= GRAD_TOL
+    e_v = rel_l2(gpu["gV"], gV)
     e_ior, e_sig = scalar_block_errors(tracer, osc, pid, g, True, n_full=sc.n_pixels)
-    assert e_ior <= GRAD_TOL and e_sig <= GRAD_TOL, (e_ior, e_sig)
+    report("C3 grad", {"n": len(pid)}, {"V": e_v, "ior": e_ior, "sigma_groups": e_sig})
+    assert e_v <= GRAD_TOL and e_ior <= GRAD_TOL and e_sig <= GRAD_TOL, (e_v, e_ior, e_sig)
 
 
 def test_c5_full_size_sampled(tracer):
@@ -316,14 +317,15 @@ def test_c5_full_size_sampled(tracer):
     cmp = compare_forward(gpu["rgb"][pid], gpu["sig"][pid], orc)
     assert_forward(cmp, "C5")
     gfull = np.zeros((sc.n_pixels, 3), np.float32)
-    g, _ = grad_upstream(O, osc, pid, S.upstream_grad(len(pid), 17), cmp)
+    g = grad_upstream(S.upstream_grad(len(pid), 17), cmp)
     gfull[pid] = g
     gpu = run_gpu(tracer, sc, None, full_launch_grad=gfull)
     del gfull
     gV, gi, gs = O.backward(osc, g, pid)
-    assert rel_l2(gpu["gV"], gV) <= GRAD_TOL
+    e_v = rel_l2(gpu["gV"], gV)
     e_ior, e_sig = scalar_block_errors(tracer, osc, pid, g, True, n_groups=8, n_full=sc.n_pixels)
-    assert e_ior <= GRAD_TOL and e_sig <= GRAD_TOL, (e_ior, e_sig)
+    report("C5 grad", {"n": len(pid)}, {"V": e_v, "ior": e_ior, "sigma_groups": e_sig})
+    assert e_v <= GRAD_TOL and e_ior <= GRAD_TOL and e_sig <= GRAD_TOL, (e_v, e_ior, e_sig)
 
 
 def test_c3r_relighting_depth8_full_size_sampled(tracer):
@@ -475,8 +477,7 @@ def test_degenerate_method_cases(tracer):
     # the exact vertex gradient is 0 here (the radiance no longer depends on the geometry), so
     # rel-L2 has no denominator: the error is measured against the gradient scale of the same
     # scene at eta = 1.5, sigma = 0 (same upstream gradient)
-    g = S.upstream_grad(len(pid), 11)
-    g[cmp["div_mask"] | cmp["flag_mask"]] = 0.0
+    g = grad_upstream(S.upstream_grad(len(pid), 11), cmp)
     gpu = run_gpu(tracer, sc, pid, grad=g)
     gV, _, _ = O.backward(osc, g, pid)
     ref = T.scene(base.V, base.F, base.cams, env=base.env, ior=1.5, sigma=(0.0, 0.0, 0.0), D=3)

@@ -150,27 +150,3 @@ def test_miss_and_no_absorption_gives_zero_gradients():
     osc = O.OracleScene(sc)
     gV, gi, gs = O.backward(osc, np.ones((1, 3)), [0])    # corner pixel misses the sphere
     assert np.abs(gV).max() == 0 and gi == 0 and np.abs(gs).max() == 0
-
-
-def test_gradient_conditioning_flag():
-    """oracle.ill_conditioned_grad: the C1 face-axis pixel (the slab series,
-    smooth in the direction) is not flagged; a pixel aimed within ~1e-7 rad of the critical
-    angle at the exit face (q ~ 1e-7: dR/dc ~ 1/sqrt(q)) is; a zero upstream gradient never is."""
-    sc = S.config_c1()
-    osc = O.OracleScene(sc)
-    pid = np.array([31 * 64 + 31, 31 * 64 + 30, 30 * 64 + 31])
-    g = S.upstream_grad(3, 3)
-    assert not O.ill_conditioned_grad(osc, pid, g).any()
-    g0 = np.zeros_like(g)
-    assert not O.ill_conditioned_grad(osc, pid, g0).any()
-    # a ray inside a slab (eta = 1.5, faces z = +-0.25) meeting the top face with sin(theta) =
-    # 1/1.5 - 1e-7 (1e-7 below the critical angle, q ~ 1.3e-7): the reverse mode there moves by
-    # far more than 1e-2 for a 2-ulp change of the direction, so it is flagged; the same ray at
-    # 30 degrees is not
-    V, F = S.slab(0.5, 4.0, 4)
-    osc = O.OracleScene(T.scene(V, F, T.one_view(2, 2, (0, 0, 3)), env=T.lobe_env(), sigma=(0.0, 0.0, 0.0), D=3))
-    rays = []
-    for s_t in (1.0 / 1.5 - 1e-7, 0.5):
-        rays.append([0.0, 0.0, 0.0, s_t, 0.0, math.sqrt(1.0 - s_t * s_t)])
-    flag = O.ill_conditioned_grad(osc, None, np.ones((2, 3)), rays=np.array(rays))
-    assert flag.tolist() == [True, False], flag

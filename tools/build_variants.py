@@ -1,6 +1,6 @@
 """Build tuning variants of libdifftrans.so in parallel:
    python tools/build_variants.py tag=DEF1,DEF2 tag2=DEF3 ...
--> paper_2603_00413_b200/variants/libdifftrans_<tag>.so (select with DT_LIBDIFFTRANS=...)."""
+-> paper_2603_00413_b200/variants/libdifftrans_<tag>.so (run with tools/bench_variant.py or tools/sweep.sh)."""
 import os
 import sys
 from concurrent.futures import ThreadPoolExecutor

@@ -1,13 +1,14 @@
 #!/bin/bash
-# traversal tuning sweep (C3 bench, no e2e/cpu baseline)
+# Variant sweep on the GPU box: tools/sweep.sh CONFIG tag1 tag2 ...  (variants built here with
+# tools/build_variants.py tag=DEF1,DEF2 ...); prints value, ms/step and the phase split.
+CFG=${1:-C3}; shift
 summ() {
 python -c "
 import json,sys; d=json.loads(sys.stdin.read()); p=d['phase_ms_per_step']; c=d['counters_per_step']
 print('$1', round(d['value']), d['ms_per_step'], 'trace0', p['trace0'], 'trace', p['trace'], 'shade', p['shade'], 'bwd', p['bwd'], 'visits', c['node_visits'], 'tris', c['tri_tests'])"
 }
-for lm in ${LEAVES:-1 2 3}; do for mode in ${MODES:-0 1 2}; do
-  DT_LEAF_MAX=$lm DT_TRAV_MODE=$mode timeout 120 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | summ "leaf=$lm mode=$mode"
-done; done
-for ch in ${CHUNKS:-64 128 512 1024}; do
-  DT_LEAF_MAX=${CLEAF:-2} DT_TRAV_MODE=2 DT_TRAV_CHUNK=$ch timeout 120 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | summ "chunk=$ch"
+export BENCH_NO_CLOCKS=1
+timeout 300 python bench.py --config $CFG --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | summ default
+for v in "$@"; do
+  timeout 300 python tools/bench_variant.py paper_2603_00413_b200/variants/libdifftrans_$v.so --config $CFG --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | summ "$v"
 done
