@@ -143,6 +143,10 @@ typedef struct {
                                 it by the kernels (forward and the matching backward) instead
                                 of the `ior` argument, so an on-device optimiser update needs
                                 no host round trip.  Must not change before the backward.    */
+  int32_t* seg_count;        /* optional device int32[n_rays], ACCUMULATED: += the number of
+                                segments traced for each ray (its ray tree's nodes at depth >= 1
+                                plus the camera segment if it passed the root-box test); the
+                                multi-GPU tile balancer's cost.  NULL: off.    */
 } dt_trace_opts;
 
 /* Host-side statistics filled by dt_trace_forward when requested. */
@@ -278,9 +282,19 @@ typedef struct {
   int32_t step;
   int32_t uniform;
   float clamp_lo, clamp_hi;  /* projection after the update (e.g. IoR in [1, 3], sigma >= 0) */
+  const int32_t* skip_if;    /* optional device int: when non-NULL and *skip_if != 0 at run time
+                                the update is skipped (param, m, v untouched).  Pass
+                                dt_forward_overflow_flag() so a step whose asynchronous forward
+                                overflowed the arena (its gradients are invalid) changes nothing. */
 } dt_adam;
 DT_API dt_status dt_adam_step(dt_ctx* ctx, float* param, const float* grad, float* m, float* v, int64_t n,
                               const dt_adam* cfg, void* stream);
+
+/* Device int32, nonzero iff the most recent dt_trace_forward on this context overflowed its
+ * record arena (its outputs and the following backward are invalid).  Reset by the next
+ * forward; valid for the context's lifetime (stream-ordered: read it in later kernels, e.g.
+ * dt_adam.skip_if).  NULL for a NULL context. */
+DT_API const int32_t* dt_forward_overflow_flag(const dt_ctx* ctx);
 
 /* Statistics of the last forward (waits for it if it ran with opts.async).  Returns
  * DT_ERR_RETRY if that asynchronous forward overflowed the arena. */

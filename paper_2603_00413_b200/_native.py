@@ -38,7 +38,8 @@ class Cameras(C.Structure):
 
 class TraceOpts(C.Structure):
     _fields_ = [("max_depth", C.c_int32), ("cap_policy", C.c_int32), ("t_eps", C.c_float),
-                ("check_finite", C.c_int32), ("async_", C.c_int32), ("ior_device", C.c_void_p)]
+                ("check_finite", C.c_int32), ("async_", C.c_int32), ("ior_device", C.c_void_p),
+                ("seg_count", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -56,7 +57,7 @@ class Stats(C.Structure):
 class Adam(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("weight_decay", C.c_float), ("step", C.c_int32), ("uniform", C.c_int32), ("clamp_lo", C.c_float),
-                ("clamp_hi", C.c_float)]
+                ("clamp_hi", C.c_float), ("skip_if", C.c_void_p)]
 
 
 PHASES = ["build", "trace0", "shade", "trace", "gather", "bwd", "normals_bwd", "loss"]
@@ -98,6 +99,7 @@ SIGNATURES = {
     "dt_debug_closest_hit": (C.c_int, [_P, _P, C.c_int64, C.c_float, C.c_int32, _P, _P, _P]),
     "dt_debug_bvh_check": (C.c_int, [_P, C.POINTER(C.c_int64), _P]),
     "dt_debug_vertex_normals": (C.c_int, [_P, _P, _P]),
+    "dt_forward_overflow_flag": (C.c_void_p, [_P]),
 }
 
 _lib = None

@@ -246,6 +246,8 @@ void dt_destroy(dt_ctx* c) {
 
 const char* dt_last_error(const dt_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+const int32_t* dt_forward_overflow_flag(const dt_ctx* c) { return c ? c->lvl + LV_OVERFLOW : nullptr; }
+
 dt_status dt_build_bvh(dt_ctx* c, const float* V, int32_t nv, const int32_t* F, int32_t nf, void* stream) {
   if (!c) return DT_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
@@ -359,6 +361,7 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.sig_f = (unsigned long long*)sig_face;
   a.counters = c->counters;
   a.grids = c->grid_cache;
+  a.segc = opts->seg_count;
 
   // a previous asynchronous forward is checked first (its readback has long completed)
   dt_status prev = consume_async(c);

@@ -66,6 +66,7 @@ struct FwdLaunch {
   unsigned long long* sig_f;
   unsigned long long* counters;   // [0] node visits, [1] triangle tests
   int* grids;           // host: the context's persistent-grid cache (dt_ctx::grid_cache)
+  int* segc;            // optional [n_rays] traced segments per ray (accumulated)
 };
 
 struct BwdLaunch {

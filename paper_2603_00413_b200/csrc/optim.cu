@@ -188,7 +188,8 @@ __global__ void k_sigma_reg_const(const float* __restrict__ sig, float lv, float
 
 __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
                        int64_t n, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
-                       const float* __restrict__ vshared, float lo, float hi) {
+                       const float* __restrict__ vshared, float lo, float hi, const int* __restrict__ skip) {
+  if (skip && *skip) return;                               // the step's forward overflowed: no update
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float gi = g[i] + wd * p[i];                           // torch.optim.Adam weight decay
     float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -215,7 +216,8 @@ __global__ void k_max_sq(const float* __restrict__ p, const float* __restrict__ 
   if (lane_id() == 0) atomicMax(out, __float_as_uint(mx));   // non-negative floats order as uints
 }
 
-__global__ void k_uniform_v(float* __restrict__ v, const unsigned* __restrict__ mx, float b2) {
+__global__ void k_uniform_v(float* __restrict__ v, const unsigned* __restrict__ mx, float b2, const int* __restrict__ skip) {
+  if (skip && *skip) return;
   v[0] = b2 * v[0] + (1.f - b2) * __uint_as_float(*mx);
 }
 
@@ -262,13 +264,13 @@ cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n,
   if (c->uniform) {
     cudaMemsetAsync(scratch, 0, sizeof(unsigned), st);
     k_max_sq<<<grid_for(n), 256, 0, st>>>(p, g, n, c->weight_decay, scratch);
-    k_uniform_v<<<1, 1, 0, st>>>(v, scratch, c->beta2);
+    k_uniform_v<<<1, 1, 0, st>>>(v, scratch, c->beta2, c->skip_if);
     k_adam<<<grid_for(n), 256, 0, st>>>(p, g, m, v, n, c->lr, c->beta1, c->beta2, c->eps, c->weight_decay, bc1, bc2, v,
-                                        c->clamp_lo, c->clamp_hi);
+                                        c->clamp_lo, c->clamp_hi, c->skip_if);
     *nl += 3;
   } else {
     k_adam<<<grid_for(n), 256, 0, st>>>(p, g, m, v, n, c->lr, c->beta1, c->beta2, c->eps, c->weight_decay, bc1, bc2,
-                                        nullptr, c->clamp_lo, c->clamp_hi);
+                                        nullptr, c->clamp_lo, c->clamp_hi, c->skip_if);
     *nl += 1;
   }
   return cudaGetLastError();

@@ -291,6 +291,7 @@ __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
       float tn;
       inbox = slab(blo.x, bhi.x, blo.y, bhi.y, blo.z, bhi.z, f3(o64), safe_inv(f3(d64)), kInf, tn);
       traced += inbox;
+      if (inbox && a.segc) a.segc[ray] += 1;          // one lane per ray: no atomic needed
     }
     if (inbox) face = traverse(s, f3(o64), f3(d64), 0.0f, t, u, v, sstack + threadIdx.x, kTraceThreads, err, visits, tests);
     if (valid) {
@@ -377,6 +378,7 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
       pos = rd.u;
       face = __float_as_int(h.x);
     }
+    if (valid && k > 0 && a.segc) atomicAdd(a.segc + ray, 1);
     shade_and_spawn<ABS, VOL>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face);
     if (round == 0) {
       round = 1;

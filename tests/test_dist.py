@@ -82,11 +82,59 @@ def test_gloo_allreduce_equals_single_process():
     assert np.abs(gs - rs).max() < 1e-4 * max(1.0, np.abs(rs).max())
 
 
-def test_flat_roundtrip():
-    gV = torch.randn(10, 3)
-    gi = torch.randn(1)
-    gs = torch.randn(4, 4, 4, 3)
-    f = DD.flat_grads(gV, gi, gs)
-    a, b, c = torch.zeros_like(gV), torch.zeros_like(gi), torch.zeros_like(gs)
-    DD.unflat_grads(f, a, b, c)
-    assert torch.equal(a, gV) and torch.equal(b, gi) and torch.equal(c, gs)
+def test_grad_buffer_views_and_allreduce_grads_roundtrip():
+    buf = DD.GradBuffer(10, (4, 4, 4, 3), "cpu")
+    buf.gV.copy_(torch.randn(10, 3))
+    buf.gI.fill_(2.5)
+    buf.gS.copy_(torch.randn(4, 4, 4, 3))
+    assert buf.flat.numel() == 30 + 1 + 192
+    assert torch.equal(buf.flat[:30], buf.gV.reshape(-1)) and float(buf.flat[30]) == 2.5
+    assert torch.equal(buf.flat[31:], buf.gS.reshape(-1))
+    # without a process group allreduce_grads is the identity
+    gV, gi, gs = buf.gV.clone(), buf.gI.clone(), buf.gS.clone()
+    DD.allreduce_grads(gV, gi, gs)
+    assert torch.equal(gV, buf.gV) and torch.equal(gi, buf.gI) and torch.equal(gs, buf.gS)
+
+
+def test_lpt_assign_properties():
+    """Greedy LPT: a partition of the tiles; loads within the largest tile of
+    each other and of the mean; the known optimum on a small case; a cyclic split of skewed
+    costs is worse."""
+    g = np.random.default_rng(3)
+    for world in (1, 2, 3, 8):
+        costs = g.pareto(1.5, size=500) * 100
+        parts = DD.lpt_assign(costs, world)
+        allt = np.concatenate(parts)
+        assert np.array_equal(np.sort(allt), np.arange(500))
+        loads = np.array([costs[p].sum() for p in parts])
+        assert loads.max() - loads.min() <= costs.max() + 1e-9
+        # greedy list scheduling: makespan <= mean load + largest job (and >= the mean load)
+        assert costs.sum() / world - 1e-9 <= loads.max() <= costs.sum() / world + costs.max() + 1e-9
+    # exact small cases: {7,6,5,4,3,2} on 2 ranks -> 14 / 13 (optimum 14 / 13); ties to lowest rank
+    parts = DD.lpt_assign([7, 6, 5, 4, 3, 2], 2)
+    assert [sorted(p.tolist()) for p in parts] == [[0, 3, 4], [1, 2, 5]]
+    # skewed costs: one heavy view -- cyclic splits it unevenly, LPT balances it
+    costs = np.ones(64)
+    costs[:16] = 20.0
+    cyc = [costs[np.arange(r, 64, 3)].sum() for r in range(3)]
+    lpt = [costs[p].sum() for p in DD.lpt_assign(costs, 3)]
+    assert max(lpt) < max(cyc) and max(lpt) - min(lpt) <= 20.0
+
+
+def test_tile_costs_and_tiles_pixel_ids():
+    n_views, W, H = 2, 70, 40
+    tx, ty = DD.tile_grid(W, H)
+    pid = DD.tiles_pixel_ids(np.arange(n_views * tx * ty), W, H)
+    assert np.array_equal(np.sort(pid), np.arange(n_views * W * H))
+    seg = (pid % 7).astype(np.int32)
+    costs = DD.tile_costs(pid, seg, n_views, W, H)
+    assert costs.shape == (n_views * tx * ty,) and costs.sum() == seg.sum()
+    # tile 0 of view 1: pixels x < 32, y < 32 of view 1
+    v1 = np.arange(W * H, 2 * W * H)
+    y, x = np.divmod(v1 - W * H, W)
+    m = (x < 32) & (y < 32)
+    assert costs[tx * ty] == (v1[m] % 7).sum()
+    # an LPT split's pixel lists partition the image
+    parts = DD.lpt_assign(costs, 3)
+    allp = np.concatenate([DD.tiles_pixel_ids(p, W, H) for p in parts])
+    assert np.array_equal(np.sort(allp), np.arange(n_views * W * H))

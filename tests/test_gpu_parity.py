@@ -129,7 +129,13 @@ def test_bvh_structure_and_bit_exact_vs_brute_force(tracer, cfg):
                                 T.one_view(2, 2, (0, 0, 3)), 2))
     f_o, tuv_o, fl = O.closest_hit(osc, rays[:m].astype(np.float64))
     f_g = f_bvh.cpu().numpy()[:m]
-    ok = fl == 0
+    # the candidate search is float32 (the shade pass then recomputes the chosen face's hit in
+    # float64): its barycentric rounding on these triangles (edges ~1e-2 of |o|) reaches ~1e-5,
+    # so rays within 1e-4 of an edge, or flagged by the oracle (near miss / tie), may pick the
+    # neighbouring face; every other ray must pick the oracle's face
+    mb = np.minimum(np.minimum(1 - tuv_o[:, 1] - tuv_o[:, 2], tuv_o[:, 1]), tuv_o[:, 2])
+    ok = (fl == 0) & ((f_o < 0) | (mb >= 1e-4))
+    assert ok.mean() > 0.97, ok.mean()
     assert (f_g[ok] == f_o[ok]).all(), int((f_g[ok] != f_o[ok]).sum())
     hit = ok & (f_o >= 0)
     np.testing.assert_allclose(tuv_bvh.cpu().numpy()[:m][hit, 0], tuv_o[hit, 0], rtol=2e-5, atol=2e-5)
