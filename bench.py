@@ -194,6 +194,18 @@ def run_ours(args, rank, world, local_rank):
     pid = None
     if world > 1:
         pid = torch.as_tensor(DD.tile_pixel_ids(sc.cams.n_views, sc.cams.width, sc.cams.height, rank, world), device=dev)
+        if args.balance == "lpt":
+            # tile balancing: one untimed forward of this rank's cyclic share
+            # counts the traced segments per ray; the per-tile costs of all ranks are summed into
+            # one vector and every rank runs the same greedy LPT assignment on it
+            tr.build_bvh(ds.V, ds.F)
+            segc = torch.zeros(pid.numel(), dtype=torch.int32, device=dev)
+            tr.trace_forward(ds, pid, seg_count=segc)
+            costs = torch.as_tensor(DD.tile_costs(pid.cpu().numpy(), segc.cpu().numpy(), sc.cams.n_views,
+                                                  sc.cams.width, sc.cams.height), device=dev)
+            dist.all_reduce(costs, op=dist.ReduceOp.SUM)
+            mine = DD.lpt_assign(costs.cpu().numpy(), world)[rank]
+            pid = torch.as_tensor(DD.tiles_pixel_ids(mine, sc.cams.width, sc.cams.height), device=dev)
     n_rays = ds.n_pixels if pid is None else pid.numel()
     infer = args.mode == "infer"
     rgb = torch.empty((n_rays, 3), dtype=torch.float32, device=dev)
@@ -215,9 +227,10 @@ def run_ours(args, rank, world, local_rank):
         # (AdamUniform), IoR and sigma all updated every step; gradients all-reduced across ranks
         # before the updates
         n_global = ds.n_pixels
-        hook = (lambda gV, gI, gS: DD.allreduce_grads(gV, gI, gS)) if world > 1 else None
+        hook = (lambda flat: DD.allreduce_flat(flat)) if world > 1 else None
+        bcast = (lambda t: dist.broadcast(t, 0)) if world > 1 else None
         opt = RefineOptimizer(tr, ds, RefineConfig(freeze_iters=0), seed=5, grad_hook=hook,
-                              loss_scale=n_rays / n_global)
+                              loss_scale=n_rays / n_global, rank=rank, broadcast=bcast)
 
         def step(async_=True):
             opt.step(target, pid, async_=async_)
@@ -396,7 +409,7 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(args.config, sc, infer),
                    "rays_per_step": int(n_rays) * world, "segments_per_step": int(segs / args.steps),
-                   "segments_per_depth": last["segments_per_depth"], "parallelism": f"rays{world}",
+                   "segments_per_depth": last["segments_per_depth"], "parallelism": f"rays{world}", "balance": args.balance if world > 1 else None,
                    "l2": "working set > L2: path-record arena "
                          f"{last['arena_capacity'] * 128 / 1e9:.1f} GB streamed every step; "
                          + ("LBVH built once (fixed mesh)" if infer else "LBVH rebuilt in-step")},
@@ -458,6 +471,8 @@ def main():
     ap.add_argument("--ref-pixels", type=int, default=192, help="oracle pixels per --impl reference step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--balance", default="lpt", choices=["lpt", "cyclic"],
+                    help="N > 1: tile assignment (greedy LPT on measured per-tile segments, or cyclic)")
     args = ap.parse_args()
     if args.config is None:
         args.config = "C3R" if args.mode == "infer" else "C3"

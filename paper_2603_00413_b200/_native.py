@@ -134,4 +134,8 @@ def lib():
 
 
 class DiffTransError(RuntimeError):
-    pass
+    """A non-DT_OK status; .status holds the dt_status code."""
+
+    def __init__(self, msg: str, status: int = -1):
+        super().__init__(msg)
+        self.status = status

@@ -19,6 +19,8 @@ from typing import Callable, Optional
 
 import torch
 
+from . import _native as N
+from .dist import GradBuffer
 from .tracer import DeviceScene, Tracer
 
 
@@ -96,16 +98,28 @@ class HostTargets:
 
 
 class RefineOptimizer:
-    """Jointly optimises vertices, IoR and absorption of a DeviceScene against target images."""
+    """Jointly optimises vertices, IoR and absorption of a DeviceScene against target images.
+
+    Data parallel (dist.py): every rank traces its own rays into one persistent
+    flat gradient buffer (dist.GradBuffer); the regularisers that do not depend on the rays
+    (L_mat-smooth / L_vol) are added on rank 0 only, before the gradient hook all-reduces the
+    buffer, so every rank applies the same summed gradient and the parameters stay identical
+    (the updates are deterministic); the periodic mesh pass runs on rank 0 and its vertices are
+    broadcast."""
 
     def __init__(self, tracer: Tracer, ds: DeviceScene, cfg: Optional[RefineConfig] = None, seed: int = 0,
-                 grad_hook: Optional[Callable] = None, loss_scale: float = 1.0):
-        """grad_hook(gV, g_ior, g_sigma): called on the ray-loss gradients before the
-        regularisers and the updates (data parallel: dist.allreduce_grads).  loss_scale scales
-        lambda_color / lambda_tone; with rays sharded over ranks, n_local / n_global makes the
-        summed gradient that of the global mean (loss_rt normalises by the local ray count)."""
+                 grad_hook: Optional[Callable] = None, loss_scale: float = 1.0, rank: int = 0,
+                 broadcast: Optional[Callable] = None):
+        """grad_hook(flat): called on the flat [dV | dIOR | dsigma] buffer (GradBuffer.flat) after the
+        ray-loss backward and rank 0's regularisers, before the updates (data parallel:
+        dist.allreduce_flat).  loss_scale scales lambda_color / lambda_tone; with rays sharded over
+        ranks, n_local / n_global makes the summed gradient that of the global mean (loss_rt
+        normalises by the local ray count).  rank: this process's rank (rank 0 adds the
+        ray-independent regularisers).  broadcast(tensor): rank 0's tensor to every rank (the
+        vertices after the periodic mesh pass)."""
         self.tr, self.ds, self.cfg = tracer, ds, cfg or RefineConfig()
         self.grad_hook, self.loss_scale = grad_hook, float(loss_scale)
+        self.rank, self.broadcast = int(rank), broadcast
         dev = ds.V.device
         self.V = ds.V.clone().contiguous()
         self.ior = torch.tensor([ds.ior], dtype=torch.float32, device=dev)
@@ -113,9 +127,11 @@ class RefineOptimizer:
         self.mV, self.vV = torch.zeros_like(self.V), torch.zeros(1, device=dev)          # AdamUniform: scalar v
         self.mI, self.vI = torch.zeros_like(self.ior), torch.zeros_like(self.ior)
         self.mS, self.vS = torch.zeros_like(self.sigma), torch.zeros_like(self.sigma)
+        self.grads = GradBuffer(self.V.shape[0], tuple(self.sigma.shape), dev)
         self.gen = torch.Generator(device=dev)
         self.gen.manual_seed(seed)
         self.it = 0
+        self.dropped = 0                      # asynchronous steps dropped by an arena overflow
         self.loss = torch.zeros(4, dtype=torch.float32, device=dev)
 
     def _reg_points(self):
@@ -149,37 +165,56 @@ class RefineOptimizer:
             out[1:] = lr_
         return out
 
+    def _forward(self, pixel_ids, async_):
+        """The step's forward.  An asynchronous forward's arena overflow is reported by the NEXT
+        call as DT_ERR_RETRY: that earlier step changed nothing (its updates were skipped on the
+        device through dt_adam.skip_if), so it is dropped -- its iteration count is taken back --
+        and this step's forward runs again on the grown arena."""
+        try:
+            return self.tr.trace_forward(self.ds, pixel_ids, ior_device=self.ior, async_=async_)
+        except N.DiffTransError as e:
+            if e.status != N.DT_ERR_RETRY:
+                raise
+            self.it -= 1
+            self.dropped += 1
+            return self.tr.trace_forward(self.ds, pixel_ids, ior_device=self.ior, async_=async_)
+
     def step(self, target: torch.Tensor, pixel_ids: Optional[torch.Tensor] = None, async_: bool = False,
              gt_masks: Optional[torch.Tensor] = None) -> StepResult:
         """One iteration, queued on the current stream.  async_: the forward does not wait for its
-        arena-overflow check (an overflow surfaces as DT_ERR_RETRY on the next call; see
-        Tracer.trace_forward) so consecutive steps queue back to back with no host stall."""
-        c, tr, ds = self.cfg, self.tr, self.ds
-        self.it += 1
+        arena-overflow check (an overflow surfaces as DT_ERR_RETRY on the next call, which then
+        drops that step; see _forward) so consecutive steps queue back to back with no host stall."""
+        c, tr, ds, G = self.cfg, self.tr, self.ds, self.grads
         ds.set_vertices(self.V)
         ds.set_sigma(self.sigma)
         tr.build_bvh(ds.V, ds.F)
         # the kernels read the IoR from self.ior (dt_trace_opts.ior_device): no host round trip
-        out = tr.trace_forward(ds, pixel_ids, ior_device=self.ior, async_=async_)
+        out = self._forward(pixel_ids, async_)
+        self.it += 1
         lrt, grad_rgb = tr.loss_rt(out.rgb, target, c.lambda_color * self.loss_scale, c.lambda_tone * self.loss_scale)
-        gV, gI, gS = tr.trace_backward(grad_rgb)
-        if self.grad_hook is not None:
-            self.grad_hook(gV, gI, gS)
+        tr.trace_backward(grad_rgb, grad_V=G.gV, grad_ior=G.gI, grad_sigma=G.gS)
         if ds.absorption.kind in (1, 2):          # grid / hash texture: sampled regularisers
             pts, xi = self._reg_points()
         else:
             pts = xi = None
-        lreg = tr.sigma_regularizers(ds, pts, xi, gS, c.lambda_smooth, c.lambda_vol)
+        w = 1.0 if self.rank == 0 else 0.0        # ray-independent: added once, on rank 0
+        lreg = tr.sigma_regularizers(ds, pts, xi, G.gS, c.lambda_smooth * w, c.lambda_vol * w)
+        if self.grad_hook is not None:
+            self.grad_hook(G.flat)
         frozen = self.it <= c.freeze_iters
-        tr.adam_step(self.sigma, gS, self.mS, self.vS, self.it, c.lr_material, c.betas, c.eps, c.weight_decay,
-                     clamp=(0.0, float("inf")))
-        tr.adam_step(self.ior, gI, self.mI, self.vI, self.it, c.lr_ior_frozen if frozen else c.lr_ior, c.betas, c.eps,
-                     c.weight_decay, clamp=c.ior_range)
+        skip = tr.overflow_flag()                 # an overflowed forward's gradients are invalid
+        tr.adam_step(self.sigma, G.gS, self.mS, self.vS, self.it, c.lr_material, c.betas, c.eps, c.weight_decay,
+                     clamp=(0.0, float("inf")), skip_if=skip)
+        tr.adam_step(self.ior, G.gI, self.mI, self.vI, self.it, c.lr_ior_frozen if frozen else c.lr_ior, c.betas, c.eps,
+                     c.weight_decay, clamp=c.ior_range, skip_if=skip)
         if not frozen:
-            tr.adam_step(self.V, gV, self.mV, self.vV, self.it - c.freeze_iters, c.lr_vertices, c.betas, c.eps,
-                         c.weight_decay, uniform=True)
+            tr.adam_step(self.V, G.gV, self.mV, self.vV, self.it - c.freeze_iters, c.lr_vertices, c.betas, c.eps,
+                         c.weight_decay, uniform=True, skip_if=skip)
         self.loss[:2] = lrt
         self.loss[2:] = lreg
         if gt_masks is not None and not frozen and c.reg_every > 0 and self.it % c.reg_every == 0:
-            self.regularize(gt_masks)
+            if self.rank == 0:                    # float atomics: one rank runs it, the others copy
+                self.regularize(gt_masks)
+            if self.broadcast is not None:
+                self.broadcast(self.V)
         return StepResult(self.loss, self.ior)

@@ -139,7 +139,7 @@ class Tracer:
     def _check(self, rc, h):
         if rc != N.DT_OK:
             msg = self._lib.dt_last_error(h).decode() if h else ""
-            raise N.DiffTransError(f"{N.STATUS.get(rc, rc)}: {msg}")
+            raise N.DiffTransError(f"{N.STATUS.get(rc, rc)}: {msg}", rc)
 
     # ------------------------------------------------------------------ path
     def build_bvh(self, V: torch.Tensor, F: torch.Tensor, stream=None):
@@ -152,11 +152,12 @@ class Tracer:
                       max_depth: Optional[int] = None, cap_policy: Optional[int] = None, want_capped=False,
                       want_sig=False, stats=False, check_finite=False, rgb: Optional[torch.Tensor] = None,
                       async_: bool = False, ior_device: Optional[torch.Tensor] = None,
-                      stream=None) -> ForwardOut:
+                      seg_count: Optional[torch.Tensor] = None, stream=None) -> ForwardOut:
         """async_: no end-of-call synchronisation (see dt_trace_opts.async); an arena overflow
         of this call is reported by the next call as DiffTransError('DT_ERR_RETRY ...').
         ior_device: a device float32[1] the kernels read the IoR from (no host round trip when an
-        on-device optimiser updates it); it must not change before the matching backward."""
+        on-device optimiser updates it); it must not change before the matching backward.
+        seg_count: optional device int32[n_rays], accumulated with each ray's traced segments."""
         cams = ds.cameras(pixel_ids)
         n = cams.n_rays
         dev = self.device
@@ -174,6 +175,9 @@ class Tracer:
         if ior_device is not None:
             assert ior_device.is_cuda and ior_device.dtype == torch.float32 and ior_device.numel() >= 1
             opts.ior_device = ior_device.data_ptr()
+        if seg_count is not None:
+            assert seg_count.is_cuda and seg_count.dtype == torch.int32 and seg_count.numel() == n
+            opts.seg_count = seg_count.data_ptr()
         ds.absorption.sigma = _ptr(ds.sigma)
         st_out = N.Stats() if stats else None
         rc = self._lib.dt_trace_forward(self.h, float(ds.ior if ior is None else ior), C.byref(ds.absorption),
@@ -274,16 +278,23 @@ class Tracer:
         self._keep_mask = (ds, cams)
         return loss, grad_V, mask
 
+    def overflow_flag(self) -> int:
+        """Device address of the int that is nonzero iff the last forward overflowed its record
+        arena (dt_forward_overflow_flag): pass as adam_step(skip_if=...)."""
+        return self._lib.dt_forward_overflow_flag(self.h)
+
     def adam_step(self, param: torch.Tensor, grad: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: int,
                   lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0, uniform=False,
-                  clamp=(-float("inf"), float("inf")), stream=None):
-        """In-place Adam / AdamUniform update of `param`."""
+                  clamp=(-float("inf"), float("inf")), skip_if: Optional[int] = None, stream=None):
+        """In-place Adam / AdamUniform update of `param`.  skip_if: device int
+        address (e.g. overflow_flag()); the update is skipped when it holds a nonzero value."""
         for t in (param, grad, m, v):
             assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
         cfg = N.Adam()
         cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay = lr, betas[0], betas[1], eps, weight_decay
         cfg.step, cfg.uniform = int(step), int(uniform)
         cfg.clamp_lo, cfg.clamp_hi = float(clamp[0]), float(clamp[1])
+        cfg.skip_if = skip_if
         self._check(self._lib.dt_adam_step(self.h, _ptr(param), _ptr(grad), _ptr(m), _ptr(v), param.numel(),
                                            C.byref(cfg), _stream(stream)), self.h)
 

@@ -220,3 +220,35 @@ def test_periodic_mesh_pass_fits_the_mask():
     assert last[0] < 0.5 * first, (first, last)
     r = np.linalg.norm(opt.V.cpu().numpy(), axis=1)
     assert r.max() > 1.05 and r.min() > 0.98, (r.min(), r.max())   # silhouette vertices moved out
+
+
+def test_overflowed_async_step_changes_nothing_and_is_dropped():
+    """ADVICE (api.cu:485): an asynchronous step whose forward overflows the record arena must not
+    update the parameters (dt_adam.skip_if = dt_forward_overflow_flag) and is dropped: the next
+    step takes its iteration count back and runs on the grown arena."""
+    from paper_2603_00413_b200.optim import RefineConfig, RefineOptimizer
+    from paper_2603_00413_b200.tracer import DeviceScene, Tracer
+    sc = S.config_c2()
+    sc = T.scene(sc.V, sc.F, sc.cams, env=sc.env, D=8)
+    dev = torch.device("cuda:0")
+    tr = Tracer(dev)
+    ds = DeviceScene(sc, dev)
+    tr.build_bvh(ds.V, ds.F)
+    target = tr.trace_forward(ds).rgb.clone() * 0.9
+    opt = RefineOptimizer(Tracer(dev), ds, RefineConfig(freeze_iters=0), seed=3)
+    full = opt.V.clone()
+    opt.V.copy_(full * 0.05)                   # a tiny object: the synchronous step measures a small need
+    opt.step(target)
+    opt.V.copy_(full)
+    before = (opt.V.clone(), opt.sigma.clone(), opt.ior.clone(), opt.mV.clone(), opt.vV.clone(), opt.mI.clone())
+    opt.step(target, async_=True)              # arena sized from the small need: overflows
+    torch.cuda.synchronize()
+    after = (opt.V, opt.sigma, opt.ior, opt.mV, opt.vV, opt.mI)
+    for x, y in zip(before, after):
+        assert torch.equal(x, y)
+    assert opt.it == 2
+    opt.step(target, async_=True)              # reports the overflow: that step is dropped, this one runs
+    torch.cuda.synchronize()
+    assert opt.dropped == 1 and opt.it == 2
+    assert not torch.equal(opt.V, before[0])
+    opt.tr.get_stats()                         # no further overflow pending
