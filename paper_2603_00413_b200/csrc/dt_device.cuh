@@ -282,14 +282,32 @@ DT_D bool stack_pop(Trav& T, const int* sstack, int stride, const int* lstack) {
   return true;
 }
 
+// Tests the triangles of leaf T.cur against the ray, keeping the closest hit (R18 ties).
+DT_D void leaf_test(const DevScene& s, float3 o, float3 d, float t_lo, Trav& T, int& tests) {
+  int first, cnt;
+  leaf_range(T.cur, first, cnt);
+  const float4* tr = s.tris + 3 * (size_t)first;
+  do {                                            // a leaf holds 1..kLeafMax triangles
+    float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
+    float t, u, v;
+    ++tests;
+    if (intersect_tri(o, d, f3(a), f3(b), f3(c), t_lo, t, u, v)) {
+      int id = __float_as_int(a.w);
+      if (t < T.bt || (t == T.bt && id < T.best)) { T.bt = t; T.bu = u; T.bv = v; T.best = id; }
+    }
+    tr += 3;
+  } while (--cnt > 0);
+}
+
 // One traversal step: visit the current wide node (test its four child boxes, descend into
-// the nearest hit, push the others far-to-near) or the current leaf (test its triangles),
-// then pop when nothing was descended into.  Returns true when the ray is finished.
-// sstack: this thread's column of the block's shared short stack (stride = blockDim.x);
-// entries beyond kStackShared spill to lstack (local memory).
+// the nearest hit, push the others far-to-near, or pop when none is hit); then, in the same
+// step, test the leaf it descended into or popped and pop again.  A warp whose lanes are split
+// between the node and the leaf code runs both halves every step anyway; fused, a lane does
+// both in one step (r02: C3 traversal 48.1 -> 46.6 ms, profiles/r02_traversal_sweep.txt).
+// Returns true when the ray is finished.  sstack: this thread's column of the block's shared
+// short stack (stride = blockDim.x); entries beyond kStackShared spill to lstack (local memory).
 DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_lo, Trav& T, int* sstack, int stride,
                     int* lstack, int& err, int& visits, int& tests) {
-  bool descended = false;
   if (T.cur >= 0) {
     const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)T.cur;
     uint4 n0, n1, n2, n3;
@@ -302,9 +320,8 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
     float k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
     DT_CX(0, 1) DT_CX(2, 3) DT_CX(0, 2) DT_CX(1, 3) DT_CX(1, 2)   // ascending by entry distance
     if (k0 < kInf) {
-      // the hit children are a prefix of the sorted order: push children 1..h far-to-near
       const int h = (k1 < kInf) + (k2 < kInf) + (k3 < kInf);
-      if (T.sp + 3 <= kStackShared) {             // common case: all in the shared short stack
+      if (T.sp + 3 <= kStackShared) {
         int* top = sstack + (T.sp + h - 1) * stride;
         if (h > 0) top[0] = r1;
         if (h > 1) top[-stride] = r2;
@@ -317,26 +334,17 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
           if (q >= 3 - h) stack_push(T, sstack, stride, lstack, push[q], err);
       }
       T.cur = r0;
-      descended = true;
+    } else if (err || !stack_pop(T, sstack, stride, lstack)) {
+      return true;
     }
-  } else {
-    int first, cnt;
-    leaf_range(T.cur, first, cnt);
-    const float4* tr = s.tris + 3 * (size_t)first;
-    do {                                            // a leaf holds 1..kLeafMax triangles
-      float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
-      float t, u, v;
-      ++tests;
-      if (intersect_tri(o, d, f3(a), f3(b), f3(c), t_lo, t, u, v)) {
-        int id = __float_as_int(a.w);
-        if (t < T.bt || (t == T.bt && id < T.best)) { T.bt = t; T.bu = u; T.bv = v; T.best = id; }
-      }
-      tr += 3;
-    } while (--cnt > 0);
   }
-  if (!descended && (err || !stack_pop(T, sstack, stride, lstack))) return true;
+  if (T.cur < 0) {
+    leaf_test(s, o, d, t_lo, T, tests);
+    if (err || !stack_pop(T, sstack, stride, lstack)) return true;
+  }
   return false;
 }
+
 #undef DT_CX
 
 // Closest hit (whole traversal).  Returns the original face id or -1.
