@@ -6,9 +6,9 @@ mkdir -p gpurun_out
 B="--config C3 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 SEC="--section SourceCounters --section LaunchStats --section Occupancy --section SchedulerStats --section WarpStateStats --section ComputeWorkloadAnalysis --section MemoryWorkloadAnalysis --section SpeedOfLight"
 export BENCH_NO_CLOCKS=1
-timeout 900 ncu $SEC --clock-control none --import-source on -k regex:$K -s $S -c 1 -f -o gpurun_out/nv_default python bench.py $B > gpurun_out/nv_default.log 2>&1
+timeout 900 ncu $SEC --clock-control none --import-source on -k regex:$K -s $S -c 1 -f -o gpurun_out/${P:-nv}_default python bench.py $B > gpurun_out/${P:-nv}_default.log 2>&1
 echo "default rc=$?"
 for v in "$@"; do
-  timeout 900 ncu $SEC --clock-control none --import-source on -k regex:$K -s $S -c 1 -f -o gpurun_out/nv_$v python tools/bench_variant.py paper_2603_00413_b200/variants/libdifftrans_$v.so $B > gpurun_out/nv_$v.log 2>&1
+  timeout 900 ncu $SEC --clock-control none --import-source on -k regex:$K -s $S -c 1 -f -o gpurun_out/${P:-nv}_$v python tools/bench_variant.py paper_2603_00413_b200/variants/libdifftrans_$v.so $B > gpurun_out/${P:-nv}_$v.log 2>&1
   echo "$v rc=$?"
 done
