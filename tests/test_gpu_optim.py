@@ -176,26 +176,39 @@ def test_mesh_regularizers_match_oracle(tracer, mesh):
     assert torch.equal(gV3, gV)
 
 
-def test_mask_loss_matches_oracle(tracer):
-    """NEXT-4 L_mask and its silhouette-edge-sampling gradient (R32) vs the oracle."""
+@pytest.mark.parametrize("case", ["ico2-1view", "ico3-3views"])
+def test_mask_loss_matches_oracle(tracer, case):
+    """NEXT-4 L_mask and its silhouette-edge-sampling gradient (R32) vs the oracle,
+    at the north_star gradient bar (rel-L2 <= 1e-3), the rendered mask identical and the loss
+    within 1e-6.  No sample is excluded.  tools/mask_diag.py found none of the 235 silhouette
+    samples of the 1-view case within 1e-4 px of a visibility change or of a ground-truth pixel
+    boundary, so float32 and float64 take the same sample decisions.  Measured rel-L2: 2.5e-7
+    (1 view) and 4.8e-7 (3 views); the round-1 tolerance of 2e-2 had no justification."""
     import oracle as O
     from oracle import mask as OM
     from paper_2603_00413_b200.tracer import DeviceScene
-    V, F = S.icosphere(2)
-    cams = T.one_view(48, 48, (0.3, 0.2, 3.0), fov_deg=50, up=(0.0, 1.0, 0.0))
+    if case == "ico2-1view":
+        V, F = S.icosphere(2)
+        cams = T.one_view(48, 48, (0.3, 0.2, 3.0), fov_deg=50, up=(0.0, 1.0, 0.0))
+    else:
+        V, F = S.icosphere(3)
+        cams = S.hemisphere_cameras(3, 40, 40, 3.0, 1.0, 7, fill=0.7)
     sc = T.scene(V, F, cams, D=0)
     osc = O.OracleScene(sc)
-    m = OM.rendered_mask(osc, cams, 0)
-    ys, xs = np.mgrid[0:48, 0:48]
-    gt = ((xs + 0.5 - 26) ** 2 + (ys + 0.5 - 22) ** 2 <= (0.8 * np.sqrt(m.sum() / np.pi)) ** 2).astype(np.float32)[None]
+    ms = np.stack([OM.rendered_mask(osc, cams, v) for v in range(cams.n_views)])
+    ys, xs = np.mgrid[0:cams.height, 0:cams.width]
+    gt = np.stack([((xs + 0.5 - 0.54 * cams.width) ** 2 + (ys + 0.5 - 0.46 * cams.height) ** 2
+                    <= (0.8 * np.sqrt(ms[v].sum() / np.pi)) ** 2) for v in range(cams.n_views)]).astype(np.float32)
     ds = DeviceScene(sc, torch.device("cuda:0"))
     tracer.build_bvh(ds.V, ds.F)
     loss, gV, mask = tracer.mask_loss(ds, torch.as_tensor(gt, device="cuda:0").contiguous(), 1.0, want_mask=True)
-    mg = mask.cpu().numpy()[0]
-    assert (mg != m).sum() <= 2                              # pixel centres on an edge may tie
-    assert abs(float(loss.cpu()[0]) - OM.loss(osc, cams, gt)) <= 2.0 / m.size
+    mg = mask.cpu().numpy().reshape(ms.shape)
+    assert (mg != ms).sum() == 0
+    assert abs(float(loss.cpu()[0]) - OM.loss(osc, cams, gt)) <= 1e-6
     go = OM.gradient(osc, sc, gt)
-    assert rel_l2(gV.cpu().numpy(), go) < 2e-2, rel_l2(gV.cpu().numpy(), go)
+    e = rel_l2(gV.cpu().numpy(), go)
+    print(f"mask gradient rel-L2 {e:.3e} ({case})")
+    assert e <= 1e-3, e
 
 
 def test_periodic_mesh_pass_fits_the_mask():
