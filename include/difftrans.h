@@ -315,6 +315,13 @@ DT_API dt_status dt_debug_bvh_check(dt_ctx* ctx, int64_t* out, void* stream);
 /* Test-only: copy the vertex normals of the last build to out (device float [nv][3]). */
 DT_API dt_status dt_debug_vertex_normals(dt_ctx* ctx, float* out, void* stream);
 
+/* Test-only: status of the bounds-checked build (compiled with -DDT_CHECKED=1; every kernel
+ * checks its record, node, triangle, vertex, texel and shared-slot indices).  Synchronises
+ * the device, then returns the source line of the first failed check in each translation
+ * unit (host out int32[5]: bvh.cu, trace.cu, optim.cu, meshreg.cu, api.cu; 0 = no failure)
+ * and clears them.  In the product build every entry is -1 (no checks compiled in). */
+DT_API dt_status dt_debug_check_status(int32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,7 +100,18 @@ SIGNATURES = {
     "dt_debug_bvh_check": (C.c_int, [_P, C.POINTER(C.c_int64), _P]),
     "dt_debug_vertex_normals": (C.c_int, [_P, _P, _P]),
     "dt_forward_overflow_flag": (C.c_void_p, [_P]),
+    "dt_debug_check_status": (C.c_int, [C.POINTER(C.c_int32)]),
 }
+
+
+def check_status():
+    """Bounds-checked build (DT_CHECKED): first failed check line per translation unit
+    (bvh, trace, optim, meshreg, api; 0 = none), cleared; all -1 in the product build."""
+    out = (C.c_int32 * 5)()
+    rc = lib().dt_debug_check_status(out)
+    if rc != 0:
+        raise DiffTransError(f"dt_debug_check_status failed ({rc})", rc)
+    return dict(zip(["bvh", "trace", "optim", "meshreg", "api"], list(out)))
 
 _lib = None
 _lib_path = LIB_PATH

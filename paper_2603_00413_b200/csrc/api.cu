@@ -185,6 +185,10 @@ void PhaseTimer::end(int n_launches) {
   }
 }
 
+namespace dt {
+DT_DEFINE_CHECK_READER(check_status_api)
+}  // namespace dt
+
 extern "C" {
 
 const char* dt_status_string(dt_status s) {
@@ -661,6 +665,17 @@ dt_status dt_debug_vertex_normals(dt_ctx* c, float* out, void* stream) {
   if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_debug_vertex_normals: call dt_build_bvh first");
   DT_ARG(out, "dt_debug_vertex_normals: out is NULL");
   DT_CU(launch_normals_to_f32(c->nrm, c->nv, out, (cudaStream_t)stream));
+  return DT_OK;
+}
+
+dt_status dt_debug_check_status(int32_t* out) {
+  if (!out) return DT_ERR_INVALID_ARG;
+  if (cudaDeviceSynchronize() != cudaSuccess) return DT_ERR_CUDA;
+  out[0] = dt::check_status_bvh();
+  out[1] = dt::check_status_trace();
+  out[2] = dt::check_status_optim();
+  out[3] = dt::check_status_meshreg();
+  out[4] = dt::check_status_api();
   return DT_OK;
 }
 

@@ -242,6 +242,7 @@ __global__ void k_scatter(const unsigned* __restrict__ kin, const unsigned* __re
     __syncthreads();
     if (valid) {
       unsigned pos = offs[dg] + wcnt[warp][dg] + rank;
+      DT_CHECK(pos < (unsigned)n);
       kout[pos] = k;
       vout[pos] = v;
     }
@@ -294,6 +295,7 @@ __global__ void k_karras(const unsigned* __restrict__ k, int n, int2* __restrict
       if (t <= 1) break;
     }
     int gamma = i + s * d + min(d, 0);
+    DT_CHECK(gamma >= 0 && gamma + 1 < n && min(i, j) >= 0 && max(i, j) < n);
     int left = min(i, j) == gamma ? ~gamma : gamma;
     int right = max(i, j) == gamma + 1 ? ~(gamma + 1) : gamma + 1;
     children[i] = make_int2(left, right);
@@ -325,7 +327,9 @@ __global__ void k_refit(const float4* __restrict__ V, const int* __restrict__ F,
     int p = parent_leaf[j];
     while (p >= 0) {
       __threadfence();
+      DT_CHECK(p < n - 1);
       if (atomicAdd(flags + p, 1) == 0) break;   // first arrival: the sibling finishes the node
+      __threadfence();                           // acquire: the sibling's box stores, fenced before its atomic
       int2 ch = children[p];
       float3 l0, h0, l1, h1;
       load_box(leafbox, nodebox, ch.x, l0, h0);
@@ -462,6 +466,7 @@ __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __
     }
     __threadfence();                                   // acquire: the parent's writes before publishing
     const int b = (int)(item & 0xffffffffu), w = (int)(item >> 32);
+    DT_CHECK(b >= 0 && w >= 0 && w < cap);
     int ent[4], wref[4] = {0, 0, 0, 0}, ne = 2;
     const int2 ch = children[b];
     ent[0] = ch.x;
@@ -487,6 +492,7 @@ __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __
     const int wd = __ldcg(wdepth + w);                 // written by the parent before publishing w (L2)
     for (int c = 0, k = 0; c < ne; ++c)
       if (ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max) wref[c] = base + k++;
+    DT_CHECK(base + nin <= cap);
     write_wide_node(b, ent, wref, ne, (unsigned)w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
     for (int c = 0; c < ne; ++c) {
       if (!(ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max)) continue;
@@ -749,5 +755,7 @@ DevScene scene_from_ctx(const dt_ctx* c) {
   s.scal = c->scal;
   return s;
 }
+
+DT_DEFINE_CHECK_READER(check_status_bvh)
 
 }  // namespace dt

@@ -286,6 +286,7 @@ DT_D bool stack_pop(Trav& T, const int* sstack, int stride, const int* lstack) {
 DT_D void leaf_test(const DevScene& s, float3 o, float3 d, float t_lo, Trav& T, int& tests) {
   int first, cnt;
   leaf_range(T.cur, first, cnt);
+  DT_CHECK(first >= 0 && first + cnt <= s.nf);
   const float4* tr = s.tris + 3 * (size_t)first;
   do {                                            // a leaf holds 1..kLeafMax triangles
     float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
@@ -309,6 +310,7 @@ DT_D void leaf_test(const DevScene& s, float3 o, float3 d, float t_lo, Trav& T, 
 DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_lo, Trav& T, int* sstack, int stride,
                     int* lstack, int& err, int& visits, int& tests) {
   if (T.cur >= 0) {
+    DT_CHECK(T.cur < max(s.nf - 1, 1));
     const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + 4 * (size_t)T.cur;
     uint4 n0, n1, n2, n3;
     ldg256(nd, n0, n1);
@@ -365,7 +367,9 @@ DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, 
 // Triangle of ORIGINAL face f from the snapshot, in float64: v0 and the edges v1 - v0, v2 - v0
 // (exact in float64 for float32 vertices).
 DT_D void face_tri64(const DevScene& s, int f, int& i0, int& i1, int& i2, double3& v0, double3& e1, double3& e2) {
+  DT_CHECK(f >= 0 && f < s.nf);
   i0 = __ldg(s.F + 3 * f); i1 = __ldg(s.F + 3 * f + 1); i2 = __ldg(s.F + 3 * f + 2);
+  DT_CHECK(i0 >= 0 && i0 < s.nv && i1 >= 0 && i1 < s.nv && i2 >= 0 && i2 < s.nv);
   v0 = d3(__ldg(s.V + i0));
   e1 = d3(__ldg(s.V + i1)) - v0;
   e2 = d3(__ldg(s.V + i2)) - v0;
@@ -570,6 +574,7 @@ DT_D uint32_t hash_index(const DevScene& s, int l, int N, int x, int y, int z) {
   const uint32_t T1 = (1u << s.hlog2) - 1u;
   if ((s.hdense >> l) & 1u) {
     const uint32_t n1 = (uint32_t)N + 1u;
+    DT_CHECK(x >= 0 && y >= 0 && z >= 0 && x <= N && y <= N && z <= N && n1 * n1 * n1 <= (1u << s.hlog2));
     return (uint32_t)x + n1 * ((uint32_t)y + n1 * (uint32_t)z);
   }
   return ((uint32_t)x ^ ((uint32_t)y * 2654435761u) ^ ((uint32_t)z * 805459861u)) & T1;
@@ -612,6 +617,7 @@ DT_D void grid_corners(const DevScene& s, const GridMap& m, int base, float3 c[8
 #pragma unroll
   for (int yz = 0; yz < 4; ++yz) {
     float4 p, q;
+    DT_CHECK(base >= 0 && cell_node((size_t)base, yz << 1, m.R) < (size_t)m.R * m.R * m.R);
     ldg256f(s.sigma + 2 * cell_node((size_t)base, yz << 1, m.R), p, q);
     c[yz << 1] = f3(p.x, p.y, p.z);
     c[(yz << 1) | 1] = f3(p.w, q.x, q.y);
@@ -921,6 +927,7 @@ DT_D float3 env_voxel(const DevScene& s, double3 p, float3 a, float3* gp) {
   for (int k = 0; k < 8; ++k) {
     int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
     float wx = dx ? f[0] : 1 - f[0], wy = dy ? f[1] : 1 - f[1], wz = dz ? f[2] : 1 - f[2];
+    DT_CHECK(i0[0] >= 0 && i0[1] >= 0 && i0[2] >= 0 && i0[0] + dx < R && i0[1] + dy < R && i0[2] + dz < R);
     float4 t = __ldg(s.voxel + ((size_t)(i0[2] + dz) * R + (i0[1] + dy)) * R + (i0[0] + dx));
     out += f3(t) * (wx * wy * wz);
     if (gp) {
@@ -941,6 +948,7 @@ DT_D float3 env_plane(const DevScene& s, int k, double a_, double b_, float3 adj
   float fa, fb;
   const int ia = grid_cell64(a_, s.radius, R, fa, ca), ib = grid_cell64(b_, s.radius, R, fb, cb);
   const float4* P = s.planes + (size_t)k * R * R;
+  DT_CHECK(k >= 0 && k < 3 && ia >= 0 && ib >= 0 && ia + 1 < R && ib + 1 < R);
   float4 t00 = __ldg(P + (size_t)ib * R + ia), t01 = __ldg(P + (size_t)ib * R + ia + 1);
   float4 t10 = __ldg(P + (size_t)(ib + 1) * R + ia), t11 = __ldg(P + (size_t)(ib + 1) * R + ia + 1);
   float3 out = f3(t00) * ((1 - fa) * (1 - fb)) + f3(t01) * (fa * (1 - fb)) + f3(t10) * ((1 - fa) * fb) +

@@ -201,6 +201,11 @@ cudaError_t launch_debug_closest_hit(const DevScene& s, const float* rays, int64
                                      float* tuv, int* err_flag, cudaStream_t st);
 cudaError_t launch_bvh_check(dt_ctx* c, long long* out_dev, cudaStream_t st);
 cudaError_t launch_normals_to_f32(const D4* nrm, int nv, float* out, cudaStream_t st);
+// bounds-checked build (DT_CHECKED): first failed check line per translation unit, cleared
+int check_status_bvh();
+int check_status_trace();
+int check_status_optim();
+int check_status_meshreg();
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 cudaError_t launch_pack_sigma(const float* in, float4* out, int64_t nodes, int res, bool pairs, cudaStream_t st);
 cudaError_t launch_count_segments(const int* lvl, int max_depth, unsigned long long* seg, cudaStream_t st);

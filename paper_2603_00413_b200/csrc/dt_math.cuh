@@ -7,6 +7,40 @@
 #define DT_HD __host__ __device__ __forceinline__
 #define DT_D __device__ __forceinline__
 
+// Bounds-checked build (-DDT_CHECKED=1, tools/checked_build.sh): DT_CHECK(c) records the
+// source line of the first failed check in a per-translation-unit device word, read back by
+// dt_check_status() (compute-sanitizer is not available on the GPU pool, so the index
+// arithmetic of every kernel family is checked by the kernels themselves).  In the product
+// build it compiles to nothing.
+#ifndef DT_CHECKED
+#define DT_CHECKED 0
+#endif
+#if DT_CHECKED
+namespace dt {
+namespace {
+__device__ int g_dt_check_line;
+}
+}  // namespace dt
+#define DT_CHECK(c)                                                   \
+  do {                                                                \
+    if (!(c)) atomicCAS(&::dt::g_dt_check_line, 0, __LINE__);        \
+  } while (0)
+// host: first failed line of this translation unit (0: none); clears it
+#define DT_DEFINE_CHECK_READER(name)                                  \
+  int name() {                                                        \
+    int v = 0, z = 0;                                                 \
+    cudaMemcpyFromSymbol(&v, ::dt::g_dt_check_line, sizeof(int));     \
+    cudaMemcpyToSymbol(::dt::g_dt_check_line, &z, sizeof(int));       \
+    return v;                                                         \
+  }
+#else
+#define DT_CHECK(c) \
+  do {              \
+  } while (0)
+#define DT_DEFINE_CHECK_READER(name) \
+  int name() { return -1; }
+#endif
+
 DT_HD float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
 DT_HD float3 f3(float4 a) { return make_float3(a.x, a.y, a.z); }
 DT_HD float4 f4(float3 a, float w) { return make_float4(a.x, a.y, a.z, w); }

@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kMaskThreads) k_mask_grad(
     const int64_t q = id - (int64_t)v * n_ent;
     if (q >= *nbr_total) continue;                       // n_ent is the 6 nf bound
     const int a = owner[q], b = nbr[q];
+    DT_CHECK(a >= 0 && b >= 0 && a < s.nv && b < s.nv);
     if (b <= a) continue;
     int f1 = -1, f2 = -1;
     for (int c = vstart[a]; c < vstart[a + 1]; ++c) {
@@ -348,5 +349,7 @@ cudaError_t launch_mesh_regularizers(dt_ctx* c, float lambda_edge, float lambda_
   *nl += launches;
   return cudaGetLastError();
 }
+
+DT_DEFINE_CHECK_READER(check_status_meshreg)
 
 }  // namespace dt

@@ -276,4 +276,6 @@ cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n,
   return cudaGetLastError();
 }
 
+DT_DEFINE_CHECK_READER(check_status_optim)
+
 }  // namespace dt

@@ -90,6 +90,7 @@ DT_D void hit_first_order(int cA, int cB, unsigned char* slot, int& r0, int& r1)
   const int rB = cB == 0 ? __popc(a0) + __popc(b0 & lt)
                : cB == 1 ? n0 + __popc(a1) + __popc(b1 & lt)
                          : n0 + n1 + __popc(a2) + __popc(b2 & lt);
+  DT_CHECK(rA >= 0 && rA < 64 && rB >= 0 && rB < 64);
   slot[rA] = (unsigned char)lane_id();
   slot[rB] = (unsigned char)(32 + lane_id());
   __syncwarp();
@@ -371,6 +372,7 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
     uint32_t pos = 0;
     int face = -1;
     if (valid) {
+      DT_CHECK(idx >= 0 && idx < a.cap);
       const Vec64 ro = ldcs64(a.r.o + idx), rd = ldcs64(a.r.d + idx);
       const float4 rt = __ldcs(a.r.thr + idx), h = __ldcs(a.r.hit + idx);
       o = xyz(ro); d = xyz(rd); thr = f3(rt); w = rt.w;
@@ -436,6 +438,7 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
         const int j = base + __popc(need & lanemask_lt());
         if (j < n) {
           item = j;
+          DT_CHECK(off + j < a.cap);
           o = f3(xyz(ldcs64(a.r.o + off + j)));       // the float64 ray, rounded for the search
           d = f3(xyz(ldcs64(a.r.d + off + j)));
           inv = safe_inv(d);
@@ -462,10 +465,14 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
 // Bottom-up radiance: L = tau * (R L_r + T L_t); level 0 writes the pixel.
 __global__ void k_gather(FwdLaunch a, int k) {
   if (a.lvl[LV_OVERFLOW]) return;
+#ifdef DT_CHECK_SELFTEST
+  DT_CHECK(false);                     // tools/checked_build.sh: the check plumbing reports a failure
+#endif
   const int n = a.lvl[LV_CNT + k];
   const int64_t off = k == 0 ? 0 : level_base(a.lvl, k);
   for (int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; item < n; item += (int64_t)gridDim.x * blockDim.x) {
     const int64_t idx = k == 0 ? a.cap - 1 - item : off + item;
+    DT_CHECK(idx >= 0 && idx < a.cap);
     float4 h = a.r.hit[idx];
     int fl = __float_as_int(h.w);
     float4 ls = a.r.lsub[idx];
@@ -476,6 +483,7 @@ __global__ void k_gather(FwdLaunch a, int k) {
       float4 tu = a.r.tau[idx];
       int cr = __float_as_int(ls.w), ct = __float_as_int(tu.w);
       float R = h.z;
+      DT_CHECK(cr < a.cap && ct < a.cap);
       float3 Lr = cr >= 0 ? f3(a.r.lsub[cr]) : f3(0, 0, 0);
       float3 Lt = ct >= 0 ? f3(a.r.lsub[ct]) : f3(0, 0, 0);
       L = f3(ls) + f3(tu) * (Lr * R + Lt * (1.0f - R));   // own emission (R30; 0 otherwise) + tau * children
@@ -541,6 +549,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
     // ---- (A)
     if (valid) {
       idx = k == 0 ? cap - 1 - item : off + item;
+      DT_CHECK(idx >= 0 && idx < cap);
       const Vec64 ro = ldcs64(a.r.o + idx), rd = ldcs64(a.r.d + idx);
       const float4 rt = a.r.thr[idx], h = a.r.hit[idx];
       const double3 o = xyz(ro), d = xyz(rd);
@@ -595,6 +604,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
           }
           const float4 ls = a.r.lsub[idx];
           const int cr = __float_as_int(ls.w), ct = __float_as_int(tu.w);
+          DT_CHECK(cr < cap && ct < cap && (cr < 0 || cr > idx - (k == 0 ? cap : 0)));
           float3 Lr = f3(0, 0, 0), Lt = f3(0, 0, 0);
           float3 gwr = f3(0, 0, 0), gwt = f3(0, 0, 0);
           if (cr >= 0) { Lr = f3(a.r.lsub[cr]); gx += f3(a.r.go[cr]); gwr = f3(a.r.gd[cr]); }
@@ -961,5 +971,7 @@ cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream
   k_check_finite<<<std::max(g, 1), 256, 0, st>>>(x, n, flag);
   return cudaGetLastError();
 }
+
+DT_DEFINE_CHECK_READER(check_status_trace)
 
 }  // namespace dt

@@ -25,3 +25,15 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _checked_build_status(request):
+    """DT_CHECKED_RUN=1 (tools/checked_build.sh, on the GPU box, with libdifftrans built with
+    -DDT_CHECKED=1): after every GPU test, every in-kernel bounds check must have held."""
+    yield
+    if os.environ.get("DT_CHECKED_RUN") != "1" or "gpu" not in request.keywords:
+        return
+    from paper_2603_00413_b200 import _native
+    st = _native.check_status()
+    assert all(v == 0 for v in st.values()), f"in-kernel bounds check failed (source lines): {st}"
