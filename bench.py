@@ -163,18 +163,37 @@ def algorithmic_bytes(stats, prof, steps: int):
     and triangles (48 B) the rays fetch, counted on the device (most are served by L2)."""
     seg = stats["segments_per_depth"]
     D = len(seg) - 1
-    # traversal (k >= 1): ray in (o, d: 32 B), hit out (16 B), node and triangle fetches
+    # traversal (k >= 1): float64 ray in (o, d: 64 B), hit out (16 B), node and triangle fetches
     nodes = (prof["node_visits"] - prof["node_visits_primary"]) / steps
     tris = (prof["tri_tests"] - prof["tri_tests_primary"]) / steps
-    trace = sum(seg[k] * 48 for k in range(1, D + 1)) + nodes * 64 + tris * 48
-    # shading (all levels): record in (o, d, thr, hit: 64 B), hit/tau/lsub out (48 B),
-    # vertex gather (3 ids + 3 positions + 3 normals: 108 B), children out (48 B each)
-    shade = sum(seg[k] * (64 + 48 + 108) + (seg[k + 1] if k < D else 0) * 48 for k in range(0, D + 1))
-    # backward: record in (96 B) + grad_rgb (12 B) + slots out (32 B) + gather (108 B) +
-    # 6 float4 atomics RMW (192 B) + children's slots/radiance in (48 B each)
-    bwd = sum(seg[k] * (96 + 12 + 32 + 108 + 192) + (seg[k + 1] if k < D else 0) * 48 for k in range(0, D + 1))
+    trace = sum(seg[k] * 80 for k in range(1, D + 1)) + nodes * 64 + tris * 48
+    # shading (all levels): record in (o, d float64 64 B + thr, hit 32 B), hit/tau/lsub out
+    # (48 B), vertex gather (3 ids 12 B + 3 positions 48 B + 3 float64 normals 96 B), children
+    # out (o, d, thr: 80 B each)
+    shade = sum(seg[k] * (96 + 48 + 156) + (seg[k + 1] if k < D else 0) * 80 for k in range(0, D + 1))
+    # backward: record in (o, d, thr, hit, tau, lsub: 128 B) + grad_rgb (12 B) + slots out
+    # (32 B) + gather (156 B) + 6 float4 atomics RMW (192 B) + children's slots/radiance in
+    # (48 B each)
+    bwd = sum(seg[k] * (128 + 12 + 32 + 156 + 192) + (seg[k + 1] if k < D else 0) * 48 for k in range(0, D + 1))
+    # traversal lane operations (DESIGN.md §5): 130 per 4-wide node visit (15 setup + 4 x 21
+    # child slab test + 25 ordering + 6 push / pop), 37 per Moller-Trumbore triangle test
+    ops = nodes * OPS_PER_VISIT + tris * OPS_PER_TEST
     return {"trace": trace, "shade": shade, "bwd": bwd, "trace_launches": D, "shade_launches": D + 1,
-            "bwd_launches": D + 1}
+            "bwd_launches": D + 1, "trace_ops": ops}
+
+
+OPS_PER_VISIT, OPS_PER_TEST = 130, 37
+
+
+def alu_peak(sm_count: int):
+    """SIMT lane-operation issue peak (B200_PROFILING.md / B300_MICROARCH.md unit counts): 4
+    schedulers x 32 lanes per SM issue one operation per clock at the max SM clock."""
+    try:
+        mhz = float(json.load(open(PEAKS))["sm_max_mhz"])
+        src = "derived: SMs x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json)"
+    except Exception:
+        mhz, src = 1965.0, "derived: SMs x 128 lanes x 1965 MHz (fallback)"
+    return sm_count * 128 * mhz * 1e6 / 1e12, src
 
 
 def run_ours(args, rank, world, local_rank):
@@ -384,14 +403,40 @@ def run_ours(args, rank, world, local_rank):
         l2 = float(json.load(open(os.path.join(ROOT, "profiles", "r01_l2_bandwidth.json")))["l2_read_gbs"])
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": kname,
-                "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
-                "note": "SURVEY 8(d) algorithmic bytes: ray in + hit out + counted node (64 B) and triangle "
-                        "(48 B) fetches; the LBVH is L2-resident, so DRAM traffic (ncu, profiles/) is far lower",
-                "bytes_per_launch": int(bytes_per_launch), "ms_per_launch": round(ms_per_launch, 3),
-                "l2_read_peak_gbs": l2, "frac_of_l2": round(achieved / l2, 4) if l2 else None,
-                "share_of_step": round(ph[cls] / ms, 4)}
+    hbm_view = {"unit": "GB/s", "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src,
+                "frac": round(achieved / peak, 4), "bytes_per_launch": int(bytes_per_launch),
+                "l2_read_peak_gbs": l2, "frac_of_l2": round(achieved / l2, 4) if l2 else None}
+    ncu = {}
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*traffic*.json"))):
+        try:
+            t = json.load(open(f))
+        except Exception:
+            continue
+        if t.get("config") == args.config and t.get("kernel") == kname:
+            ncu = t
+    if cls == "trace":
+        # the traversal is bound by instruction issue (ncu: IPC ~3.2 of 4, ~17 of 32 lanes
+        # active, L2-resident LBVH, DRAM at a few % of peak): its roofline is lane operations
+        # against the SIMT issue peak; the algorithmic-bytes view is kept alongside
+        apk, apk_src = alu_peak(torch.cuda.get_device_properties(dev).multi_processor_count)
+        ops_launch = ab["trace_ops"] / max(ab["trace_launches"], 1)
+        a_ops = ops_launch / (ms_per_launch / 1e3) / 1e12
+        roofline = {"bound": "alu", "kernel": kname, "achieved": round(a_ops, 3), "peak": round(apk, 2),
+                    "peak_source": apk_src, "unit": "Tlane-op/s", "frac": round(a_ops / apk, 4),
+                    "ops_per_node_visit": OPS_PER_VISIT, "ops_per_triangle_test": OPS_PER_TEST,
+                    "ops_per_launch": int(ops_launch)}
+    else:
+        roofline = {"bound": "hbm", "kernel": kname, **{k: v for k, v in hbm_view.items() if k != "bytes_per_launch"},
+                    "bytes_per_launch": int(bytes_per_launch)}
+    roofline.update({"traffic": traffic, "traffic_source": traffic_src, "ms_per_launch": round(ms_per_launch, 3),
+                     "share_of_step": round(ph[cls] / ms, 4)})
+    if traffic is not None:
+        roofline["dram_frac"] = round(traffic / (ms_per_launch / 1e3) / 1e9 / peak, 4)
+    for key in ("l2_hit_pct", "l1_hit_pct", "lanes_per_inst", "ipc", "issue_active_pct"):
+        if key in ncu:
+            roofline[key] = ncu[key]
+    if cls == "trace":
+        roofline["hbm_view"] = hbm_view
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         dt, osegs, cores = oracle_sample(sc, args.cpu_pixels, backward=not infer)

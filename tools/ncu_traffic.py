@@ -19,10 +19,24 @@ for r in rows[2:]:
     rd = float(r[h.index("dram__bytes_read.sum")]) * scale[u[h.index("dram__bytes_read.sum")]]
     wr = float(r[h.index("dram__bytes_write.sum")]) * scale[u[h.index("dram__bytes_write.sum")]]
     ms = float(r[h.index("gpu__time_duration.sum")]) * tscale[u[h.index("gpu__time_duration.sum")]]
+    def g(name):
+        return float(r[h.index(name)]) if name in h and r[h.index(name)] not in ("", "n/a") else None
     launches.append({"dram_read": rd, "dram_write": wr, "ms_cold_serialised": ms,
-                     "l2_hit_pct": float(r[h.index("lts__t_sector_hit_rate.pct")])})
+                     "l2_hit_pct": g("lts__t_sector_hit_rate.pct"), "l1_hit_pct": g("l1tex__t_sector_hit_rate.pct"),
+                     "lanes_per_inst": g("smsp__thread_inst_executed_per_inst_executed.ratio"),
+                     "ipc": g("sm__inst_executed.avg.per_cycle_active"),
+                     "issue_active_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active")})
 avg = sum(x["dram_read"] + x["dram_write"] for x in launches) / max(len(launches), 1)
+
+
+def mean(k):
+    v = [x[k] for x in launches if x[k] is not None]
+    return round(sum(v) / len(v), 3) if v else None
+
+
 json.dump({"config": config, "kernel": kernel, "source": rep.split("/")[-1],
            "capture": "ncu --set full --clock-control none, the timed step's launches of the kernel",
-           "dram_bytes_per_launch": avg, "launches": launches}, open(out, "w"), indent=1)
+           "dram_bytes_per_launch": avg, **{k: mean(k) for k in ("l2_hit_pct", "l1_hit_pct", "lanes_per_inst", "ipc",
+                                                                  "issue_active_pct")},
+           "launches": launches}, open(out, "w"), indent=1)
 print(f"{len(launches)} launches, {avg / 1e9:.3f} GB per launch")
