@@ -271,12 +271,14 @@ def test_hash_dense_level_equals_grid(tracer):
     assert np.abs(rb["gsig"][0, R ** 3:]).max() == 0.0
 
 
-def test_c4h_hash_texture_full_mesh_sampled(tracer):
-    """NEXT-2 workload: C4's knot + gems with the 16-level hash texture; 128 sampled pixels
-    (table 2^16 per level here to keep the oracle's per-thread adjoint small)."""
-    sc = S.config_c4h(log2_size=16)
-    pid = S.central_pixels(sc.cams, 128, 7)
-    parity_case(tracer, sc, pid, "C4H")
+@pytest.mark.parametrize("log2_size,n_pix", [(16, 128), (19, 48)])
+def test_c4h_hash_texture_full_mesh_sampled(tracer, log2_size, n_pix):
+    """NEXT-2 workload: C4's knot + gems with the 16-level hash texture, sampled pixels; the
+    2^19-entry table is the bench's (fewer pixels: the oracle keeps a per-thread float64
+    adjoint of the whole table)."""
+    sc = S.config_c4h(log2_size=log2_size)
+    pid = S.central_pixels(sc.cams, n_pix, 7)
+    parity_case(tracer, sc, pid, f"C4H-2^{log2_size}")
 
 
 def test_flat_facets_and_tir(tracer):
