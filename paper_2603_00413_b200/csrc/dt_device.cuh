@@ -366,6 +366,23 @@ DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, 
 
 // Triangle of ORIGINAL face f from the snapshot, in float64: v0 and the edges v1 - v0, v2 - v0
 // (exact in float64 for float32 vertices).
+// The same from the face's vertex indices (handed over in the hit record by the traversal).
+DT_D void tri64(const DevScene& s, int i0, int i1, int i2, double3& v0, double3& e1, double3& e2) {
+  DT_CHECK(i0 >= 0 && i0 < s.nv && i1 >= 0 && i1 < s.nv && i2 >= 0 && i2 < s.nv);
+  v0 = d3(__ldg(s.V + i0));
+  e1 = d3(__ldg(s.V + i1)) - v0;
+  e2 = d3(__ldg(s.V + i2)) - v0;
+}
+// Traversal output record: (face, i0, i1, i2) as int bits; the indices are fetched once per
+// ray when its traversal ends, so the shade's first dependent fetch is the vertices.
+DT_D float4 hit_record(const DevScene& s, int face) {
+  int i0 = 0, i1 = 0, i2 = 0;
+  if (face >= 0) {
+    DT_CHECK(face < s.nf);
+    i0 = __ldg(s.F + 3 * face); i1 = __ldg(s.F + 3 * face + 1); i2 = __ldg(s.F + 3 * face + 2);
+  }
+  return make_float4(__int_as_float(face), __int_as_float(i0), __int_as_float(i1), __int_as_float(i2));
+}
 DT_D void face_tri64(const DevScene& s, int f, int& i0, int& i1, int& i2, double3& v0, double3& e1, double3& e2) {
   DT_CHECK(f >= 0 && f < s.nf);
   i0 = __ldg(s.F + 3 * f); i1 = __ldg(s.F + 3 * f + 1); i2 = __ldg(s.F + 3 * f + 2);

@@ -17,7 +17,9 @@ struct Records {
   Vec64* o;      // origin.xyz (float64), .i = ray index
   Vec64* d;      // direction.xyz (float64), .u = tree position (root 1, reflect 2p, refract 2p+1)
   float4* thr;   // throughput into the node (product of ancestors' R/T and tau), scalar R/T weight
-  float4* hit;   // face (int bits), t, R, flags (int bits, RF_*)
+                 //   (after the shade of a hit: the face's vertex index i2 in w)
+  float4* hit;   // traversal: face, vertex indices i0 i1 i2 (int bits); after the shade:
+                 //   i0, i1 (int bits), R, flags (int bits, RF_*); a miss: -1, 0, 0, RF_MISS
   float4* tau;   // interior transmittance of this segment (rgb), refract child index (int bits)
   float4* lsub;  // radiance returned by the subtree (rgb), reflect child index (int bits)
   float4* go;    // backward: dL/d(origin) of this segment, for the parent

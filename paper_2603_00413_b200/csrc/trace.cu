@@ -130,7 +130,7 @@ DT_D void flush_counters(unsigned long long* c, int visits, int tests) {
 template <int ABS, bool VOL>
 DT_D void shade_and_spawn(const FwdLaunch& a, double ior, int64_t child_off, int64_t lim, int k, int max_depth,
                           bool valid, int64_t idx, double3 o, double3 d, int64_t ray, uint32_t pos, float3 thr, float w,
-                          int face) {
+                          int face, int i0, int i1, int i2) {
   const DevScene& s = a.s;
   bool is_hit = valid && face >= 0;
   bool spawn_r = false, spawn_t = false, need_tau = false, capped = false, volx = false;
@@ -153,10 +153,9 @@ DT_D void shade_and_spawn(const FwdLaunch& a, double ior, int64_t child_off, int
       sig_add(a.sig_t, ray, topo_key(pos, EV_MISS));
       sig_add(a.sig_f, ray, face_key(pos, EV_MISS, -1));
     } else {
-      int i0, i1, i2;
       double3 v0, e1, e2;
       double t, u, v;
-      face_tri64(s, face, i0, i1, i2, v0, e1, e2);
+      tri64(s, i0, i1, i2, v0, e1, e2);
       mt64(o, d, v0, e1, e2, t, u, v);                                        // R15, float64
       const bool inside = dot(d, cross(e1, e2)) > 0.0;                        // R8
       x = o + d * t;
@@ -172,7 +171,8 @@ DT_D void shade_and_spawn(const FwdLaunch& a, double ior, int64_t child_off, int
         capped = true;
         if (s.cap_policy == 1) capL = env_eval(s, o, d, f3(0, 0, 0), nullptr, nullptr);   // times tau below
         int fl = RF_CAPPED | (inside ? RF_INSIDE : 0);
-        __stcs(a.r.hit + idx, make_float4(__int_as_float(face), (float)t, 0.f, __int_as_float(fl)));
+        __stcs(a.r.hit + idx, make_float4(__int_as_float(i0), __int_as_float(i1), 0.f, __int_as_float(fl)));
+        __stcs(a.r.thr + idx, f4(thr, __int_as_float(i2)));
         int ev = inside ? EV_CAP_IN : EV_CAP_OUT;
         sig_add(a.sig_t, ray, topo_key(pos, ev));
         sig_add(a.sig_f, ray, face_key(pos, ev, face));
@@ -187,7 +187,8 @@ DT_D void shade_and_spawn(const FwdLaunch& a, double ior, int64_t child_off, int
         spawn_r = true;                                                       // P:161 (R5)
         spawn_t = !S.tir;
         int fl = (inside ? RF_INSIDE : 0) | (S.tir ? RF_TIR : 0) | (S.degen ? RF_DEGEN : 0);
-        __stcs(a.r.hit + idx, make_float4(__int_as_float(face), (float)t, R, __int_as_float(fl)));
+        __stcs(a.r.hit + idx, make_float4(__int_as_float(i0), __int_as_float(i1), R, __int_as_float(fl)));
+        __stcs(a.r.thr + idx, f4(thr, __int_as_float(i2)));
         int ev = inside ? (S.tir ? EV_HIT_IN_TIR : EV_HIT_IN) : (S.tir ? EV_HIT_OUT_TIR : EV_HIT_OUT);
         sig_add(a.sig_t, ray, topo_key(pos, ev));
         sig_add(a.sig_f, ray, face_key(pos, ev, face));
@@ -316,7 +317,7 @@ __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
       stcs64(a.r.o + idx, mk64(o64, (int)ray, 0u));
       stcs64(a.r.d + idx, mk64(d64, 0, 1u));
       __stcs(a.r.thr + idx, make_float4(1.f, 1.f, 1.f, 1.f));
-      __stcs(a.r.hit + idx, make_float4(__int_as_float(face), t, u, v));   // shaded by k_shade_level(0)
+      __stcs(a.r.hit + idx, hit_record(s, face));   // shaded by k_shade_level(0)
     }
     base = __shfl_sync(~0u, next, 0);
   }
@@ -370,7 +371,7 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
     float w = 0.f;
     int64_t ray = 0;
     uint32_t pos = 0;
-    int face = -1;
+    int face = -1, i0 = 0, i1 = 0, i2 = 0;
     if (valid) {
       DT_CHECK(idx >= 0 && idx < a.cap);
       const Vec64 ro = ldcs64(a.r.o + idx), rd = ldcs64(a.r.d + idx);
@@ -379,9 +380,11 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
       ray = ro.i;
       pos = rd.u;
       face = __float_as_int(h.x);
+      i0 = __float_as_int(h.y); i1 = __float_as_int(h.z); i2 = __float_as_int(h.w);
     }
     if (valid && k > 0 && a.segc) atomicAdd(a.segc + ray, 1);
-    shade_and_spawn<ABS, VOL>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face);
+    shade_and_spawn<ABS, VOL>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, i0, i1,
+                              i2);
     if (round == 0) {
       round = 1;
     } else {
@@ -424,6 +427,8 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
   int lstack[kStackLocal];
   int err = 0, visits = 0, tests = 0;
   int item = -1;                       // -1: needs a ray; >= n: queue exhausted
+  int pend = -1;                       // finished ray whose hit record is stored next round
+  float4 ph = make_float4(0.f, 0.f, 0.f, 0.f);
   float3 o = f3(0, 0, 0), d = f3(0, 0, 1), inv = f3(0, 0, 0);
   Trav T;
   trav_init(T);
@@ -449,15 +454,24 @@ __global__ void DT_TRAV_LB k_traverse_level(FwdLaunch a, int k) {
       }
     }
     if (__all_sync(~0u, item >= n)) break;
-    if (item < 0 || item >= n) continue;
     bool done = false;
-    for (int step = 0; step < kStepBudget && !done; ++step)
-      done = trav_step(s, o, d, inv, t_lo, T, sstack, kTraceThreads, lstack, err, visits, tests);
+    if (item >= 0 && item < n) {
+      for (int step = 0; step < kStepBudget && !done; ++step)
+        done = trav_step(s, o, d, inv, t_lo, T, sstack, kTraceThreads, lstack, err, visits, tests);
+    }
+    // the hit record of a ray finished one round earlier: its face's vertex indices were
+    // fetched then and have arrived during this round's steps
+    if (pend >= 0) {
+      __stcs(a.r.hit + off + pend, ph);
+      pend = -1;
+    }
     if (done) {
-      __stcs(a.r.hit + off + item, make_float4(__int_as_float(T.best), T.bt, T.bu, T.bv));
+      ph = hit_record(s, T.best);
+      pend = item;
       item = -1;
     }
   }
+  if (pend >= 0) __stcs(a.r.hit + off + pend, ph);
   if (err) a.lvl[LV_STACKERR] = 1;
   flush_counters(a.counters, visits, tests);
 }
@@ -572,11 +586,11 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
         // capped branches return 0: no dependence
       } else {
         geo = true;
-        const int face = __float_as_int(h.x);
+        i0 = __float_as_int(h.x); i1 = __float_as_int(h.y); i2 = __float_as_int(rt.w);   // from the shade
         const bool inside = (fl & RF_INSIDE) != 0;
         double3 v0, e1, e2;
         double t64, u64, v64;
-        face_tri64(s, face, i0, i1, i2, v0, e1, e2);
+        tri64(s, i0, i1, i2, v0, e1, e2);
         idet = (float)mt64(o, d, v0, e1, e2, t64, u64, v64);                 // the forward's hit, replayed
         const double3 x = o + d * t64;
         of = f3(o); xf = f3(x); df = f3(d); e1f = f3(e1); e2f = f3(e2);
