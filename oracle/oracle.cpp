@@ -82,7 +82,7 @@ inline uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 enum Event { EV_MISS = 0, EV_HIT_OUT = 1, EV_HIT_IN = 2, EV_HIT_OUT_TIR = 3, EV_HIT_IN_TIR = 4,
-             EV_CAP_OUT = 5, EV_CAP_IN = 6 };
+             EV_CAP_OUT = 5, EV_CAP_IN = 6, EV_CAP_DROP = 7 };
 inline uint64_t topo_key(uint64_t pos, int ev) { return pos | ((uint64_t)ev << 32); }
 inline uint64_t face_key(uint64_t pos, int ev, int face) {
   return pos | ((uint64_t)(uint32_t)(face + 1) << 20) | ((uint64_t)ev << 52);
@@ -561,6 +561,12 @@ V3<S> trace(const Model<S>& m, V3<S> o, V3<S> d, int k, uint64_t pos, double w, 
   V3d gn = cross(m.Vd[F[1]] - m.Vd[F[0]], m.Vd[F[2]] - m.Vd[F[0]]);
   bool inside = dot(vald(d), gn) > 0.0;                             // R8
   if (k == sc->max_depth) {                                         // step 1 (R12, R13)
+    if (sc->cap_policy == 0 && sc->env_kind != 2) {                 // discarded branch (R13, R34)
+      st.sig_topo += mix64(topo_key(pos, EV_CAP_DROP));
+      st.sig_face += mix64(face_key(pos, EV_CAP_DROP, -1));
+      st.capped_w += w;
+      return zero3<S>();
+    }
     int ev = inside ? EV_CAP_IN : EV_CAP_OUT;
     st.sig_topo += mix64(topo_key(pos, ev));
     st.sig_face += mix64(face_key(pos, ev, h.face));

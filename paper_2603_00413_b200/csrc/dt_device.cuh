@@ -31,7 +31,8 @@ constexpr int kLeafMax = 3;        // triangles per wide-BVH leaf (a contiguous 
 constexpr int kEmptyRef = 0x7fffffff;
 
 // per-record event codes (the protocol numbering, shared only as a spec)
-enum { EV_MISS = 0, EV_HIT_OUT = 1, EV_HIT_IN = 2, EV_HIT_OUT_TIR = 3, EV_HIT_IN_TIR = 4, EV_CAP_OUT = 5, EV_CAP_IN = 6 };
+enum { EV_MISS = 0, EV_HIT_OUT = 1, EV_HIT_IN = 2, EV_HIT_OUT_TIR = 3, EV_HIT_IN_TIR = 4, EV_CAP_OUT = 5, EV_CAP_IN = 6,
+       EV_CAP_DROP = 7 };   // EV_CAP_DROP: a hit at D_max discarded under CAP_ZERO (R13, R34)
 // record flag bits (hit.w)
 enum { RF_MISS = 1, RF_CAPPED = 2, RF_INSIDE = 4, RF_TIR = 8, RF_DEGEN = 16, RF_CULLED = 32 };
 

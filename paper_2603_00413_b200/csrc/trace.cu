@@ -152,6 +152,15 @@ DT_D void shade_and_spawn(const FwdLaunch& a, double ior, int64_t child_off, int
       }
       sig_add(a.sig_t, ray, topo_key(pos, EV_MISS));
       sig_add(a.sig_f, ray, face_key(pos, EV_MISS, -1));
+    } else if (k == max_depth && s.cap_policy == 0 && !VOL) {
+      // a hit at D_max under CAP_ZERO (R13, R34): the branch is discarded -- radiance and
+      // gradient are zero whichever face or side was hit, so only "it hit" is recorded: no
+      // vertex fetch, no interface, no interior transmittance (a sigma-grid walk at C4)
+      capped = true;
+      __stcs(a.r.hit + idx, make_float4(0.f, 0.f, 0.f, __int_as_float(RF_CAPPED)));
+      sig_add(a.sig_t, ray, topo_key(pos, EV_CAP_DROP));
+      sig_add(a.sig_f, ray, face_key(pos, EV_CAP_DROP, -1));
+      if (a.capw) atomicAdd(a.capw + ray, w);
     } else {
       double3 v0, e1, e2;
       double t, u, v;
