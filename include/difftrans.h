@@ -286,6 +286,11 @@ typedef struct {
                                 the update is skipped (param, m, v untouched).  Pass
                                 dt_forward_overflow_flag() so a step whose asynchronous forward
                                 overflowed the arena (its gradients are invalid) changes nothing. */
+  int32_t* step_device;      /* optional device int (CUDA-graph replays): when non-NULL the step
+                                t is read from it at run time instead of `step` (which is then
+                                ignored; *step_device must hold t >= 1) and, unless the update was
+                                skipped, incremented by 1 after the update, so one captured step
+                                replays with the right bias correction every time. */
 } dt_adam;
 DT_API dt_status dt_adam_step(dt_ctx* ctx, float* param, const float* grad, float* m, float* v, int64_t n,
                               const dt_adam* cfg, void* stream);
@@ -297,7 +302,15 @@ DT_API dt_status dt_adam_step(dt_ctx* ctx, float* param, const float* grad, floa
 DT_API const int32_t* dt_forward_overflow_flag(const dt_ctx* ctx);
 
 /* Statistics of the last forward (waits for it if it ran with opts.async).  Returns
- * DT_ERR_RETRY if that asynchronous forward overflowed the arena. */
+ * DT_ERR_RETRY if that asynchronous forward overflowed the arena.
+ * CUDA graphs: dt_trace_forward may be captured into a graph (stream capture on `stream`)
+ * once an asynchronous forward of the same ray count has run on the context and been checked
+ * (dt_get_stats) and profiling is off; the captured forward copies its level counts to host
+ * memory on every replay, so after the replays have completed (the caller synchronises the
+ * replay stream) dt_get_stats reports the last replay's statistics, or DT_ERR_RETRY if it
+ * overflowed the arena (the arena is grown: the graph must be captured again).  Capture
+ * never allocates: a forward that would need to grow the arena fails with
+ * DT_ERR_INVALID_ARG instead. */
 DT_API dt_status dt_get_stats(dt_ctx* ctx, dt_stats* out);
 DT_API dt_status dt_set_profiling(dt_ctx* ctx, int32_t enable);
 DT_API dt_status dt_get_profile(dt_ctx* ctx, dt_profile* out, int32_t reset);

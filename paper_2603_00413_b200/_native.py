@@ -57,7 +57,7 @@ class Stats(C.Structure):
 class Adam(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("weight_decay", C.c_float), ("step", C.c_int32), ("uniform", C.c_int32), ("clamp_lo", C.c_float),
-                ("clamp_hi", C.c_float), ("skip_if", C.c_void_p)]
+                ("clamp_hi", C.c_float), ("skip_if", C.c_void_p), ("step_device", C.c_void_p)]
 
 
 PHASES = ["build", "trace0", "shade", "trace", "gather", "bwd", "normals_bwd", "loss"]

@@ -149,10 +149,13 @@ void fill_stats(dt_ctx* c, dt_stats* st) {
 // Check a pending asynchronous forward: wait for its readback, record its need, and report
 // an overflow (growing the arena for the next step).
 dt_status consume_async(dt_ctx* c) {
-  if (!c->async_pending) return DT_OK;
+  if (!c->async_pending && !c->graph_fwd) return DT_OK;
+  if (c->async_pending) {
+    cudaError_t e = cudaEventSynchronize(c->fwd_done);
+    if (e != cudaSuccess) return fail(c, DT_ERR_CUDA, "async forward: %s", cudaGetErrorString(e));
+  }
+  // (graph replays: the caller has synchronised the replay stream; host_lvl is the last replay's)
   c->async_pending = false;
-  cudaError_t e = cudaEventSynchronize(c->fwd_done);
-  if (e != cudaSuccess) return fail(c, DT_ERR_CUDA, "async forward: %s", cudaGetErrorString(e));
   if (c->prof) resolve_profile(c, false);
   int64_t need = level_need(c->host_lvl, c->last_D);
   c->last_need = need;
@@ -293,8 +296,24 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   int64_t npix = (int64_t)cams->n_views * cams->width * cams->height;
   int64_t n_rays = cams->pixel_ids ? cams->n_rays : npix;
   DT_ARG(n_rays >= 0 && n_rays < (1ll << 31), "dt_trace_forward: n_rays=%lld out of range", (long long)n_rays);
-  DT_ARG(rgb || n_rays == 0, "dt_trace_forward: rgb must be a device pointer");  cudaStream_t st = (cudaStream_t)stream;
+  DT_ARG(rgb || n_rays == 0, "dt_trace_forward: rgb must be a device pointer");
+  cudaStream_t st = (cudaStream_t)stream;
   const int D = opts->max_depth;
+  // CUDA-graph capture (see dt_get_stats): no host synchronisation and no allocation allowed
+  cudaStreamCaptureStatus cap_state = cudaStreamCaptureStatusNone;
+  DT_CU(cudaStreamIsCapturing(st, &cap_state));
+  const bool capturing = cap_state != cudaStreamCaptureStatusNone;
+  if (capturing) {
+    DT_ARG(!c->async_pending, "dt_trace_forward (capture): check the previous asynchronous forward (dt_get_stats) "
+           "before capturing");
+    DT_ARG(!c->prof, "dt_trace_forward (capture): profiling must be off");
+    DT_ARG(opts->async && !stats && !opts->check_finite,
+           "dt_trace_forward (capture): the forward must be asynchronous, without stats / check_finite");
+    DT_ARG(c->last_need > 0 && c->last_rays == n_rays && c->arena_cap >= c->last_need + c->last_need / 4 &&
+               abs_nodes(ab) <= c->sigma_cap && (env->kind != DT_ENV_VOLUME || c->arena_vol),
+           "dt_trace_forward (capture): warm up first (an asynchronous forward of the same %lld rays, checked)",
+           (long long)n_rays);
+  }
 
   // absorption snapshot (the backward differentiates w.r.t. these values)
   size_t nodes = abs_nodes(ab);
@@ -368,7 +387,8 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.segc = opts->seg_count;
 
   // a previous asynchronous forward is checked first (its readback has long completed)
-  dt_status prev = consume_async(c);
+  dt_status prev = capturing ? DT_OK : consume_async(c);
+  if (!capturing) c->graph_fwd = false;   // an eager forward replaces the captured one's state
   if (prev != DT_OK) return prev;
   int64_t limit = 0;   // HBM budget, queried (cudaMemGetInfo) only when the arena must grow
   if (env->kind == DT_ENV_VOLUME && !c->arena_vol) {   // the volume needs two more record lanes
@@ -429,8 +449,12 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
     c->last_rays = n_rays;
     c->last_retries = retries;
     if (async) {
-      DT_CU(cudaEventRecord(c->fwd_done, st));
-      c->async_pending = true;
+      if (capturing) {
+        c->graph_fwd = true;           // host_lvl refreshed by every replay (the copy above)
+      } else {
+        DT_CU(cudaEventRecord(c->fwd_done, st));
+        c->async_pending = true;
+      }
       break;
     }
     DT_CU(cudaStreamSynchronize(st));
@@ -587,7 +611,7 @@ dt_status dt_adam_step(dt_ctx* c, float* param, const float* grad, float* m, flo
   if (!c) return DT_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
   DT_ARG(cfg && param && grad && m && v, "dt_adam_step: NULL argument");
-  DT_ARG(n > 0 && cfg->step >= 1 && cfg->lr >= 0.f && cfg->beta1 >= 0.f && cfg->beta1 < 1.f && cfg->beta2 >= 0.f &&
+  DT_ARG(n > 0 && (cfg->step >= 1 || cfg->step_device) && cfg->lr >= 0.f && cfg->beta1 >= 0.f && cfg->beta1 < 1.f && cfg->beta2 >= 0.f &&
              cfg->beta2 < 1.f && cfg->eps > 0.f,
          "dt_adam_step: bad configuration (n=%lld step=%d)", (long long)n, cfg->step);
   PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);

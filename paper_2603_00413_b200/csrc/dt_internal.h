@@ -164,6 +164,8 @@ struct dt_ctx {
   int last_D = 0, last_retries = 0;
   int64_t last_rays = 0, last_need = 0;
   bool async_pending = false;
+  bool graph_fwd = false;        // the last forward was captured into a CUDA graph: host_lvl is
+                                 // refreshed by each replay (read after the caller synchronises)
   cudaEvent_t fwd_done = nullptr;
   unsigned* scratch = nullptr;                  // device [16] (AdamUniform max)
   struct Pending { int ph; cudaEvent_t a, b; };

@@ -188,8 +188,14 @@ __global__ void k_sigma_reg_const(const float* __restrict__ sig, float lv, float
 
 __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
                        int64_t n, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
-                       const float* __restrict__ vshared, float lo, float hi, const int* __restrict__ skip) {
+                       const float* __restrict__ vshared, float lo, float hi, const int* __restrict__ skip,
+                       const int* __restrict__ tdev) {
   if (skip && *skip) return;                               // the step's forward overflowed: no update
+  if (tdev) {                                              // the step count lives on the device (graphs)
+    const float t = (float)*tdev;
+    bc1 = 1.0f - powf(b1, t);
+    bc2 = 1.0f - powf(b2, t);
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float gi = g[i] + wd * p[i];                           // torch.optim.Adam weight decay
     float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -219,6 +225,10 @@ __global__ void k_max_sq(const float* __restrict__ p, const float* __restrict__ 
 __global__ void k_uniform_v(float* __restrict__ v, const unsigned* __restrict__ mx, float b2, const int* __restrict__ skip) {
   if (skip && *skip) return;
   v[0] = b2 * v[0] + (1.f - b2) * __uint_as_float(*mx);
+}
+
+__global__ void k_step_bump(int* __restrict__ t, const int* __restrict__ skip) {
+  if (!(skip && *skip)) *t += 1;
 }
 
 int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
@@ -260,17 +270,22 @@ cudaError_t launch_sigma_reg(const dt_absorption* ab, const float* pts, const fl
 
 cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n, const dt_adam* c, unsigned* scratch,
                         cudaStream_t st, int* nl) {
-  float bc1 = 1.0f - powf(c->beta1, (float)c->step), bc2 = 1.0f - powf(c->beta2, (float)c->step);
+  const int t = c->step_device ? 1 : c->step;            // (device step: read by the kernel)
+  float bc1 = 1.0f - powf(c->beta1, (float)t), bc2 = 1.0f - powf(c->beta2, (float)t);
   if (c->uniform) {
     cudaMemsetAsync(scratch, 0, sizeof(unsigned), st);
     k_max_sq<<<grid_for(n), 256, 0, st>>>(p, g, n, c->weight_decay, scratch);
     k_uniform_v<<<1, 1, 0, st>>>(v, scratch, c->beta2, c->skip_if);
     k_adam<<<grid_for(n), 256, 0, st>>>(p, g, m, v, n, c->lr, c->beta1, c->beta2, c->eps, c->weight_decay, bc1, bc2, v,
-                                        c->clamp_lo, c->clamp_hi, c->skip_if);
+                                        c->clamp_lo, c->clamp_hi, c->skip_if, c->step_device);
     *nl += 3;
   } else {
     k_adam<<<grid_for(n), 256, 0, st>>>(p, g, m, v, n, c->lr, c->beta1, c->beta2, c->eps, c->weight_decay, bc1, bc2,
-                                        nullptr, c->clamp_lo, c->clamp_hi, c->skip_if);
+                                        nullptr, c->clamp_lo, c->clamp_hi, c->skip_if, c->step_device);
+    *nl += 1;
+  }
+  if (c->step_device) {
+    k_step_bump<<<1, 1, 0, st>>>(c->step_device, c->skip_if);
     *nl += 1;
   }
   return cudaGetLastError();

@@ -132,6 +132,7 @@ class RefineOptimizer:
         self.gen.manual_seed(seed)
         self.it = 0
         self.dropped = 0                      # asynchronous steps dropped by an arena overflow
+        self.t_dev = None                     # device Adam step counts [sigma, IoR, V] (CUDA graphs)
         self.loss = torch.zeros(4, dtype=torch.float32, device=dev)
 
     def _reg_points(self):
@@ -203,13 +204,14 @@ class RefineOptimizer:
             self.grad_hook(G.flat)
         frozen = self.it <= c.freeze_iters
         skip = tr.overflow_flag()                 # an overflowed forward's gradients are invalid
+        td = [None, None, None] if self.t_dev is None else [self.t_dev[i:i + 1] for i in range(3)]
         tr.adam_step(self.sigma, G.gS, self.mS, self.vS, self.it, c.lr_material, c.betas, c.eps, c.weight_decay,
-                     clamp=(0.0, float("inf")), skip_if=skip)
+                     clamp=(0.0, float("inf")), skip_if=skip, step_device=td[0])
         tr.adam_step(self.ior, G.gI, self.mI, self.vI, self.it, c.lr_ior_frozen if frozen else c.lr_ior, c.betas, c.eps,
-                     c.weight_decay, clamp=c.ior_range, skip_if=skip)
+                     c.weight_decay, clamp=c.ior_range, skip_if=skip, step_device=td[1])
         if not frozen:
             tr.adam_step(self.V, G.gV, self.mV, self.vV, self.it - c.freeze_iters, c.lr_vertices, c.betas, c.eps,
-                         c.weight_decay, uniform=True, skip_if=skip)
+                         c.weight_decay, uniform=True, skip_if=skip, step_device=td[2])
         self.loss[:2] = lrt
         self.loss[2:] = lreg
         if gt_masks is not None and not frozen and c.reg_every > 0 and self.it % c.reg_every == 0:
@@ -218,3 +220,43 @@ class RefineOptimizer:
             if self.broadcast is not None:
                 self.broadcast(self.V)
         return StepResult(self.loss, self.ior)
+
+    def capture_step(self, target: torch.Tensor, pixel_ids: Optional[torch.Tensor] = None,
+                     prepare: Optional[Callable] = None) -> torch.cuda.CUDAGraph:
+        """One post-freeze optimisation step (LBVH rebuild, forward, loss, backward, regularisers,
+        gradient hook, Adam) captured into a CUDA graph: each replay runs the whole step with no
+        host work and no launch overhead (the launch-bound regime of the paper's 5,000-ray batches,
+        P:531).  The Adam step counts move to the device (dt_adam.step_device) so every replay
+        applies the right bias correction; `self.it` stops advancing (see sync_steps).
+        prepare(): optional work captured before the step (e.g. drawing this replay's random
+        pixel batch into `pixel_ids` / `target`, whose addresses must stay fixed).  The periodic
+        mesh pass is not captured (host-driven, every reg_every steps).  After replays,
+        synchronise and call self.tr.get_stats(): DT_ERR_RETRY means a replay overflowed the
+        record arena (its updates were skipped on the device; capture again)."""
+        c = self.cfg
+        assert self.it >= c.freeze_iters, "capture the post-freeze phase (the schedule is host logic)"
+        dev = self.V.device
+        self.t_dev = torch.tensor([self.it + 1, self.it + 1, self.it + 1 - c.freeze_iters], dtype=torch.int32,
+                                  device=dev)
+
+        def one():
+            if prepare is not None:
+                prepare()
+            self.step(target, pixel_ids, async_=True)
+
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):          # warm-up (allocations, persistent grids, arena size)
+            for _ in range(2):
+                one()
+                self.tr.get_stats()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            one()
+        return g
+
+    def sync_steps(self) -> None:
+        """After CUDA-graph replays: the host step count from the device counters."""
+        if self.t_dev is not None:
+            self.it = int(self.t_dev[0].item()) - 1

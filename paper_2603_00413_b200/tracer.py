@@ -285,9 +285,12 @@ class Tracer:
 
     def adam_step(self, param: torch.Tensor, grad: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: int,
                   lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0, uniform=False,
-                  clamp=(-float("inf"), float("inf")), skip_if: Optional[int] = None, stream=None):
+                  clamp=(-float("inf"), float("inf")), skip_if: Optional[int] = None,
+                  step_device: Optional[torch.Tensor] = None, stream=None):
         """In-place Adam / AdamUniform update of `param`.  skip_if: device int
-        address (e.g. overflow_flag()); the update is skipped when it holds a nonzero value."""
+        address (e.g. overflow_flag()); the update is skipped when it holds a nonzero value.
+        step_device: device int32[1] holding t, read at run time and incremented after the update
+        (CUDA-graph replays); `step` is then ignored."""
         for t in (param, grad, m, v):
             assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
         cfg = N.Adam()
@@ -295,6 +298,9 @@ class Tracer:
         cfg.step, cfg.uniform = int(step), int(uniform)
         cfg.clamp_lo, cfg.clamp_hi = float(clamp[0]), float(clamp[1])
         cfg.skip_if = skip_if
+        if step_device is not None:
+            assert step_device.is_cuda and step_device.dtype == torch.int32
+            cfg.step_device = step_device.data_ptr()
         self._check(self._lib.dt_adam_step(self.h, _ptr(param), _ptr(grad), _ptr(m), _ptr(v), param.numel(),
                                            C.byref(cfg), _stream(stream)), self.h)
 

@@ -1,5 +1,7 @@
 """GPU parity of the optimisation-step kernels (NEXT-1) against oracle/optim.py, and an
 end-to-end desk-scale recovery check of the whole refine loop (Table 2 analog)."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -265,3 +267,44 @@ def test_overflowed_async_step_changes_nothing_and_is_dropped():
     assert opt.dropped == 1 and opt.it == 2
     assert not torch.equal(opt.V, before[0])
     opt.tr.get_stats()                         # no further overflow pending
+
+
+def test_cuda_graph_step_matches_eager():
+    """RefineOptimizer.capture_step: a CUDA graph of one step (LBVH rebuild, async forward, loss,
+    backward, regularisers, Adam with device step counts) replayed 3 times reaches the same
+    parameters as 5 eager steps (the capture runs 2 eager warm-up steps first), up to the float
+    atomics' summation order; the device step counters advance once per replay."""
+    from paper_2603_00413_b200.optim import RefineConfig, RefineOptimizer
+    from paper_2603_00413_b200.tracer import DeviceScene, Tracer
+    sc = S.config_c2(n_views=2, res=96)
+    dev = torch.device("cuda:0")
+    tr0 = Tracer(dev)
+    ds0 = DeviceScene(dataclasses.replace(sc, ior=1.45), dev)
+    tr0.build_bvh(ds0.V, ds0.F)
+    pid = torch.as_tensor(S.central_pixels(sc.cams, 3000, 9), device=dev)
+    target = tr0.trace_forward(ds0, pid).rgb.clone()
+    res = []
+    for graph in (False, True):
+        tr = Tracer(dev)
+        ds = DeviceScene(sc, dev)
+        opt = RefineOptimizer(tr, ds, RefineConfig(freeze_iters=0), seed=4)
+        opt.step(target, pid)                       # synchronous first step sizes the arena
+        tr.get_stats()
+        if graph:
+            g = opt.capture_step(target, pid)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            tr.get_stats()
+            assert opt.t_dev.tolist() == [7, 7, 7]
+            opt.sync_steps()
+        else:
+            for _ in range(5):
+                opt.step(target, pid, async_=True)
+            torch.cuda.synchronize()
+            tr.get_stats()
+        assert opt.it == 6
+        res.append((opt.V.clone(), opt.ior.clone(), opt.sigma.clone()))
+    (Va, ia, sa), (Vb, ib, sb) = res
+    assert rel_l2(Vb.cpu().numpy(), Va.cpu().numpy()) < 1e-5
+    assert abs(float(ib) - float(ia)) < 1e-5 and rel_l2(sb.cpu().numpy(), sa.cpu().numpy()) < 1e-5
