@@ -355,13 +355,18 @@ __global__ void k_refit(const float4* __restrict__ V, const int* __restrict__ F,
 // q* hold one byte per child (child c in bits 8c..8c+7).  ref >= 0: wide node; ref = EMPTY:
 // unused slot (qlo = 255 > qhi = 0); otherwise leaf: ref = -1 - (first << 2 | (count - 1)).
 DT_D int bsize(const int2* __restrict__ ranges, int ref) { return ref < 0 ? 1 : ranges[ref].y - ranges[ref].x + 1; }
+// entry e of a wide node is itself a wide node (else a leaf: <= leaf_max triangles, or an
+// SAH-chosen leaf, bit 9 of the collapse DP's decisions)
+DT_D bool wide_entry(const int2* __restrict__ ranges, const int* __restrict__ dec, int e, int leaf_max) {
+  return e >= 0 && bsize(ranges, e) > leaf_max && !(dec && ((__ldcg(dec + e) >> 9) & 1));
+}
 
 // Quantise and write wide node w: its entries ent[0..ne) (binary refs; internal entries carry
 // their own wide index in wref), boxes padded outward so the slab test stays conservative.
 DT_D void write_wide_node(int i, const int ent[4], const int wref[4], int ne, unsigned w, int wd, double pad,
                           const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
                           const int2* __restrict__ ranges, int leaf_max, uint4* __restrict__ wnodes,
-                          float4* __restrict__ wbox, int* __restrict__ wdepth) {
+                          float4* __restrict__ wbox, int* __restrict__ wdepth, const int* __restrict__ dec = nullptr) {
   float3 ulo, uhi;
   load_box(leafbox, nodebox, i, ulo, uhi);
   double P[3] = {(double)__double2float_rd((double)ulo.x - pad), (double)__double2float_rd((double)ulo.y - pad),
@@ -392,7 +397,7 @@ DT_D void write_wide_node(int i, const int ent[4], const int wref[4], int ne, un
         ql[a] = (unsigned)fmin(fmax(fl, 0.0), 255.0);
         qh[a] = (unsigned)fmin(fmax(fh, 0.0), 255.0);
       }
-      if (e >= 0 && bsize(ranges, e) > leaf_max) {
+      if (wide_entry(ranges, dec, e, leaf_max)) {
         refs[c] = wref[c];
       } else {
         int first = e < 0 ? ~e : ranges[e].x;
@@ -448,11 +453,124 @@ DT_D float box_area(const float4* __restrict__ nodebox, int e) {
 #ifndef DT_WIDE_BLOCKS_PER_SM
 #define DT_WIDE_BLOCKS_PER_SM 1
 #endif
+
+// ----------------------------------------------------------------------------- SAH collapse
+// DT_WIDE_SAH = 1: the collapse takes the SAH-optimal set of entries per wide node (the
+// dynamic program of Ylitie, Karras & Laine 2017 for wide BVHs, at width 4) instead of the
+// greedy largest-area opening.  Bottom up over the binary tree (atomic-flag climb like the
+// refit), C(n, i) = the least expected cost of representing binary subtree n by at most i
+// entries of its parent wide node:
+//   C(leaf, i)  = A(leaf) c_tri                          (one triangle, any i)
+//   C(n, 1)     = A(n) c_node + min_{a+b=4} C(l, a) + C(r, b)      (n becomes a wide node)
+//   C(n, i > 1) = min(C(n, i - 1), min_{a+b=i} C(l, a) + C(r, b))   (n opened into i entries)
+// with A the box surface area and c_node / c_tri the costs of a 4-box node visit and a
+// triangle test (130 : 37 lane operations).  dec[n] holds the argmins: bits
+// 2(j-2)..+1 = a - 1 of the best split for j = 2..4, bit 6 + (i - 2) = "C(n, i) opens n".
+#ifndef DT_WIDE_SAH
+#define DT_WIDE_SAH 1
+#endif
+#ifndef DT_COST_NODE
+#define DT_COST_NODE (130.f / 37.f)
+#endif
+// DT_SAH_LEAF > 1: a subtree of up to that many triangles may become one leaf entry when
+// its SAH cost A(n) c_tri |n| beats the node (bit 9 of dec)
+#ifndef DT_SAH_LEAF
+#define DT_SAH_LEAF 1
+#endif
+constexpr float kCostNode = DT_COST_NODE, kCostTri = 1.f;
+
+DT_D float box_area2(const float4* __restrict__ leafbox, const float4* __restrict__ nodebox, int ref) {
+  float3 lo, hi;
+  load_box(leafbox, nodebox, ref, lo, hi);
+  const float dx = hi.x - lo.x, dy = hi.y - lo.y, dz = hi.z - lo.z;
+  return dx * dy + dy * dz + dz * dx;
+}
+
+__global__ void k_wide_cost(const int2* __restrict__ children, const int2* __restrict__ ranges, const int* __restrict__ parent_int,
+                            const int* __restrict__ parent_leaf, int* __restrict__ flags, const float4* __restrict__ leafbox,
+                            const float4* __restrict__ nodebox, int n, float4* __restrict__ cost, int* __restrict__ dec) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    int p = parent_leaf[j];
+    while (p >= 0) {
+      __threadfence();
+      if (atomicAdd(flags + p, 1) == 0) break;   // the second arrival evaluates the node
+      __threadfence();
+      const int2 ch = children[p];
+      float Cl[4], Cr[4];
+      const int cc[2] = {ch.x, ch.y};
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        float* C = s2 == 0 ? Cl : Cr;
+        if (cc[s2] < 0) {
+          const float c = box_area2(leafbox, nodebox, cc[s2]) * kCostTri;
+          C[0] = C[1] = C[2] = C[3] = c;
+        } else {
+          const float4 q = __ldcg(cost + cc[s2]);
+          C[0] = q.x; C[1] = q.y; C[2] = q.z; C[3] = q.w;
+        }
+      }
+      float best[5];                              // best[j] = min_{a+b=j} Cl[a-1] + Cr[b-1]
+      int d = 0;
+#pragma unroll
+      for (int jj = 2; jj <= 4; ++jj) {
+        float bv = kInf;
+        int ba = 1;
+        for (int a = 1; a < jj; ++a) {
+          const float v = Cl[a - 1] + Cr[jj - a - 1];
+          if (v < bv) { bv = v; ba = a; }
+        }
+        best[jj] = bv;
+        d |= (ba - 1) << (2 * (jj - 2));
+      }
+      float C[4];
+      const float Ap = box_area2(leafbox, nodebox, p);
+      C[0] = Ap * kCostNode + best[4];
+      const int cnt = ranges[p].y - ranges[p].x + 1;
+      if (DT_SAH_LEAF > 1 && cnt <= DT_SAH_LEAF && Ap * kCostTri * (float)cnt < C[0]) {
+        C[0] = Ap * kCostTri * (float)cnt;
+        d |= 1 << 9;
+      }
+#pragma unroll
+      for (int i = 2; i <= 4; ++i) {
+        if (best[i] < C[i - 2]) { C[i - 1] = best[i]; d |= 1 << (6 + i - 2); }
+        else C[i - 1] = C[i - 2];
+      }
+      __stcg(cost + p, make_float4(C[0], C[1], C[2], C[3]));
+      __stcg(dec + p, d);
+      p = parent_int[p];
+    }
+  }
+}
+
+// Entries of the wide node at binary node b from the DP decisions (at most 4).
+DT_D int sah_entries(const int2* __restrict__ children, const int* __restrict__ dec, const int2* __restrict__ ranges,
+                     int b, int leaf_max, int ent[4]) {
+  int sx[8], sk[8], sp = 0, ne = 0;
+  {
+    const int2 ch = children[b];
+    const int a = ((__ldcg(dec + b) >> 4) & 3) + 1;   // split of the budget 4
+    sx[sp] = ch.y; sk[sp++] = 4 - a;
+    sx[sp] = ch.x; sk[sp++] = a;
+  }
+  while (sp > 0) {
+    const int x = sx[--sp];
+    int k = sk[sp];
+    if (x < 0 || bsize(ranges, x) <= leaf_max || k == 1) { ent[ne++] = x; continue; }
+    const int d = __ldcg(dec + x);
+    while (k > 1 && !((d >> (6 + k - 2)) & 1)) --k;  // the best representation with <= k entries
+    if (k == 1) { ent[ne++] = x; continue; }
+    const int a = ((d >> (2 * (k - 2))) & 3) + 1;
+    const int2 ch = children[x];
+    sx[sp] = ch.y; sk[sp++] = k - a;
+    sx[sp] = ch.x; sk[sp++] = a;
+  }
+  return ne;
+}
 __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __restrict__ ranges,
                                const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
                                const int* __restrict__ ibox, uint4* __restrict__ wnodes, float4* __restrict__ wbox,
                                int* __restrict__ wdepth, int* __restrict__ nwide, unsigned long long* queue,
-                               int* __restrict__ head, int* pending, int cap, int leaf_max) {
+                               int* __restrict__ head, int* pending, int cap, int leaf_max, const int* __restrict__ dec) {
   const double pad = wide_pad(ibox);
   while (true) {
     const int idx = atomicAdd(head, 1);
@@ -471,7 +589,8 @@ __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __
     const int2 ch = children[b];
     ent[0] = ch.x;
     ent[1] = ch.y;
-    while (ne < 4) {
+    if (dec) ne = sah_entries(children, dec, ranges, b, leaf_max, ent);
+    while (!dec && ne < 4) {
       int best = -1;
       float ba = -1.f;
       for (int c = 0; c < ne; ++c) {
@@ -487,15 +606,15 @@ __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __
       ent[ne++] = g.y;
     }
     int nin = 0;
-    for (int c = 0; c < ne; ++c) nin += ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max;
+    for (int c = 0; c < ne; ++c) nin += wide_entry(ranges, dec, ent[c], leaf_max);
     const int base = nin ? atomicAdd(nwide, nin) : 0;
     const int wd = __ldcg(wdepth + w);                 // written by the parent before publishing w (L2)
     for (int c = 0, k = 0; c < ne; ++c)
-      if (ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max) wref[c] = base + k++;
+      if (wide_entry(ranges, dec, ent[c], leaf_max)) wref[c] = base + k++;
     DT_CHECK(base + nin <= cap);
-    write_wide_node(b, ent, wref, ne, (unsigned)w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
+    write_wide_node(b, ent, wref, ne, (unsigned)w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth, dec);
     for (int c = 0; c < ne; ++c) {
-      if (!(ent[c] >= 0 && bsize(ranges, ent[c]) > leaf_max)) continue;
+      if (!wide_entry(ranges, dec, ent[c], leaf_max)) continue;
       wdepth[wref[c]] = wd + 1;
       __threadfence();
       atomicExch(queue + wref[c], ((unsigned long long)(unsigned)wref[c] << 32) | (unsigned)ent[c]);
@@ -703,11 +822,24 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
       // most threads would only poll for unpublished entries
       gq = std::max(1, std::min(per, DT_WIDE_BLOCKS_PER_SM)) * c->sm_count;
     }
+    int* dec = nullptr;
+#if DT_WIDE_SAH
+    // the DP's per-node costs and decisions live in scratch the collapse does not otherwise
+    // use at this point: the sort keys (float4 per node = 4 words, 3nf words available in
+    // keys + vals) -- cost in keys/vals [0, 4(nf-1)) needs 4(nf-1) <= 6nf words: the corner
+    // sort's key/value buffers hold 2 x 3nf words each
+    float4* cost = reinterpret_cast<float4*>(c->keys);
+    dec = reinterpret_cast<int*>(c->keys + 4 * (size_t)(nf - 1));
+    cudaMemsetAsync(c->rflags, 0, (size_t)(nf - 1) * sizeof(int), st);
+    k_wide_cost<<<gf, T, 0, st>>>(c->children, c->ranges, c->parent_int, c->parent_leaf, c->rflags, c->leafbox, c->nodebox, nf,
+                                  cost, dec);
+    launches += 1;
+#endif
     cudaMemsetAsync(c->wqueue, 0xff, (size_t)nf * sizeof(unsigned long long), st);
     k_wide_topdown_init<<<1, 1, 0, st>>>(c->wqueue, ctr, ctr + 1, c->iscal + 12, c->wdepth);
     k_wide_topdown<<<gq, T, 0, st>>>(c->children, c->ranges, c->leafbox, c->nodebox, c->iscal,
                                      reinterpret_cast<uint4*>(c->nodes), c->wbox, c->wdepth, c->iscal + 12, c->wqueue,
-                                     ctr, ctr + 1, nf - 1, c->leaf_max);
+                                     ctr, ctr + 1, nf - 1, c->leaf_max, dec);
     launches += 2;
   } else {
     k_wide_single<<<1, 1, 0, st>>>(c->leafbox, c->nodebox, c->ranges, c->iscal, reinterpret_cast<uint4*>(c->nodes),
