@@ -212,20 +212,29 @@ def run_ours(args, rank, world, local_rank):
     tr = Tracer(dev)
     pid = None
     if world > 1:
-        pid = torch.as_tensor(DD.tile_pixel_ids(sc.cams.n_views, sc.cams.width, sc.cams.height, rank, world), device=dev)
-        if args.balance == "lpt":
+        from paper_2603_00413_b200.tracer import TileShard
+        W, H, nvw = sc.cams.width, sc.cams.height, sc.cams.n_views
+        # the rank's (view, 32x32 tile) shard goes to the kernels as dt_cameras.tile (no pixel
+        # list: the kernels enumerate the tiles' pixels); ragged images fall back to pixel lists
+        tiled = W % 32 == 0 and H % 32 == 0
+        pid = TileShard(32, rank, world) if tiled else \
+            torch.as_tensor(DD.tile_pixel_ids(nvw, W, H, rank, world), device=dev)
+        if args.balance == "lpt" and tiled:
             # tile balancing: one untimed forward of this rank's cyclic share
             # counts the traced segments per ray; the per-tile costs of all ranks are summed into
             # one vector and every rank runs the same greedy LPT assignment on it
             tr.build_bvh(ds.V, ds.F)
-            segc = torch.zeros(pid.numel(), dtype=torch.int32, device=dev)
+            nr = pid.n_rays(nvw, W, H)
+            segc = torch.zeros(nr, dtype=torch.int32, device=dev)
             tr.trace_forward(ds, pid, seg_count=segc)
-            costs = torch.as_tensor(DD.tile_costs(pid.cpu().numpy(), segc.cpu().numpy(), sc.cams.n_views,
-                                                  sc.cams.width, sc.cams.height), device=dev)
+            total = nvw * (W // 32) * (H // 32)
+            costs = torch.as_tensor(DD.shard_tile_costs(DD.shard_tiles(nvw, W, H, rank, world), segc.cpu().numpy(),
+                                                        total), device=dev)
             dist.all_reduce(costs, op=dist.ReduceOp.SUM)
             mine = DD.lpt_assign(costs.cpu().numpy(), world)[rank]
-            pid = torch.as_tensor(DD.tiles_pixel_ids(mine, sc.cams.width, sc.cams.height), device=dev)
-    n_rays = ds.n_pixels if pid is None else pid.numel()
+            pid = TileShard(32, tile_ids=torch.as_tensor(mine, dtype=torch.int32, device=dev))
+    n_rays = ds.n_pixels if pid is None else (pid.numel() if torch.is_tensor(pid) else
+                                             pid.n_rays(sc.cams.n_views, sc.cams.width, sc.cams.height))
     infer = args.mode == "infer"
     rgb = torch.empty((n_rays, 3), dtype=torch.float32, device=dev)
     if infer:

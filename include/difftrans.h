@@ -113,15 +113,28 @@ typedef struct {
 /* Pinhole cameras, OpenCV axes (R19): d_cam = ((x+0.5-cx)/fx, (y+0.5-cy)/fy, 1),
  * d = normalize(R d_cam), o = camera centre.  K -> float [n_views][4] = fx, fy, cx, cy;
  * c2w -> float [n_views][3][4] row-major.
- * Rays: if pixel_ids != NULL, ray r is pixel pixel_ids[r] (= view*H*W + y*W + x) for
- * r < n_rays; else every pixel of every view, ray r = pixel id r, n_rays ignored.
- * K, c2w and pixel_ids are read during dt_trace_forward only. */
+ * Rays, in order of precedence:
+ *  - pixel_ids != NULL: ray r is pixel pixel_ids[r] (= view*H*W + y*W + x) for r < n_rays;
+ *  - tile > 0 (data-parallel shard, SURVEY 8(b) / DESIGN.md §6): the image plane is cut into
+ *    tile x tile pixel tiles numbered view-major, then tile row, then tile column
+ *    (tiles_x = width / tile per row); this shard holds the tiles listed in tile_ids (device
+ *    int32 [n_tiles], e.g. a longest-processing-time assignment) or, when tile_ids is NULL,
+ *    every tile with id % shard_count == shard_rank.  Ray r is pixel (r mod tile^2) of the
+ *    shard's tile r / tile^2, with a tile's pixels in 8 x 4 micro-tiles in row-major order
+ *    (a warp's 32 rays are one screen-space block); n_rays is ignored (= tiles x tile^2).
+ *    width and height must be multiples of tile, and tile a multiple of 8;
+ *  - else every pixel of every view, ray r = pixel id r, n_rays ignored.
+ * K, c2w, pixel_ids and tile_ids are read during dt_trace_forward only. */
 typedef struct {
   int32_t n_views, width, height;
   const float* K;
   const float* c2w;
   const int64_t* pixel_ids;
   int64_t n_rays;
+  int32_t tile;
+  int32_t shard_rank, shard_count;
+  const int32_t* tile_ids;
+  int32_t n_tiles;
 } dt_cameras;
 
 /* max_depth = D_max (R12): segments at depth 0..D_max are intersection-tested; a

@@ -33,7 +33,9 @@ class Env(C.Structure):
 
 class Cameras(C.Structure):
     _fields_ = [("n_views", C.c_int32), ("width", C.c_int32), ("height", C.c_int32), ("K", C.c_void_p),
-                ("c2w", C.c_void_p), ("pixel_ids", C.c_void_p), ("n_rays", C.c_int64)]
+                ("c2w", C.c_void_p), ("pixel_ids", C.c_void_p), ("n_rays", C.c_int64), ("tile", C.c_int32),
+                ("shard_rank", C.c_int32), ("shard_count", C.c_int32), ("tile_ids", C.c_void_p),
+                ("n_tiles", C.c_int32)]
 
 
 class TraceOpts(C.Structure):

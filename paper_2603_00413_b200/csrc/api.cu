@@ -294,7 +294,24 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
               (env->kind == DT_ENV_GRID || (env->n_samples >= 1 && !env->far_field))),
          "dt_trace_forward: env (kind=%d) invalid", env->kind);
   int64_t npix = (int64_t)cams->n_views * cams->width * cams->height;
+  const bool tiled = !cams->pixel_ids && cams->tile > 0;
   int64_t n_rays = cams->pixel_ids ? cams->n_rays : npix;
+  if (tiled) {
+    DT_ARG(cams->tile % 8 == 0 && cams->width % cams->tile == 0 && cams->height % cams->tile == 0,
+           "dt_trace_forward: tile=%d must be a multiple of 8 dividing width %d and height %d", cams->tile,
+           cams->width, cams->height);
+    const int64_t total = npix / ((int64_t)cams->tile * cams->tile);
+    int64_t nt;
+    if (cams->tile_ids) {
+      DT_ARG(cams->n_tiles >= 0, "dt_trace_forward: n_tiles < 0");
+      nt = cams->n_tiles;
+    } else {
+      DT_ARG(cams->shard_count >= 1 && cams->shard_rank >= 0 && cams->shard_rank < cams->shard_count,
+             "dt_trace_forward: shard_rank %d / shard_count %d invalid", cams->shard_rank, cams->shard_count);
+      nt = total > cams->shard_rank ? (total - cams->shard_rank + cams->shard_count - 1) / cams->shard_count : 0;
+    }
+    n_rays = nt * cams->tile * cams->tile;
+  }
   DT_ARG(n_rays >= 0 && n_rays < (1ll << 31), "dt_trace_forward: n_rays=%lld out of range", (long long)n_rays);
   DT_ARG(rgb || n_rays == 0, "dt_trace_forward: rgb must be a device pointer");
   cudaStream_t st = (cudaStream_t)stream;
@@ -377,7 +394,15 @@ dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const 
   a.pids = cams->pixel_ids;
   a.tiles_x = (cams->width + 7) / 8;
   a.tiles_per_view = a.tiles_x * ((cams->height + 3) / 4);
-  a.n_items = cams->pixel_ids ? n_rays : (int64_t)a.tiles_per_view * cams->n_views * 32;
+  a.n_items = cams->pixel_ids || tiled ? n_rays : (int64_t)a.tiles_per_view * cams->n_views * 32;
+  a.shard_tile = tiled ? cams->tile : 0;
+  if (tiled) {
+    a.stiles_x = cams->width / cams->tile;
+    a.stiles_per_view = a.stiles_x * (cams->height / cams->tile);
+    a.shard_rank = cams->shard_rank;
+    a.shard_count = std::max(cams->shard_count, 1);
+    a.tile_ids = cams->tile_ids;
+  }
   a.rgb = rgb;
   a.capw = capped_w;
   a.sig_t = (unsigned long long*)sig_topo;
@@ -641,8 +666,9 @@ dt_status dt_mask_loss(dt_ctx* c, const dt_cameras* cams, const float* gt_mask, 
   cudaSetDevice(c->device);
   if (!c->built) return fail(c, DT_ERR_NOT_BUILT, "dt_mask_loss: call dt_build_bvh first");
   DT_ARG(cams && gt_mask && grad_V && loss, "dt_mask_loss: NULL argument");
-  DT_ARG(cams->K && cams->c2w && cams->n_views > 0 && cams->width > 0 && cams->height > 0 && !cams->pixel_ids,
-         "dt_mask_loss: cams must describe full images (pixel_ids = NULL)");
+  DT_ARG(cams->K && cams->c2w && cams->n_views > 0 && cams->width > 0 && cams->height > 0 && !cams->pixel_ids &&
+             cams->tile <= 0,
+         "dt_mask_loss: cams must describe full images (pixel_ids = NULL, tile = 0)");
   DT_ARG(lambda >= 0.f, "dt_mask_loss: lambda must be >= 0");
   PhaseTimer p(c, DT_PH_LOSS, (cudaStream_t)stream);
   int nl = 0;

@@ -61,6 +61,9 @@ struct FwdLaunch {
   const int64_t* pids;
   int64_t n_items;      // work items for level 0
   int tiles_x, tiles_per_view;
+  // tile shards (dt_cameras.tile > 0): tile side, tiles per row / per view, cyclic rule or list
+  int shard_tile, stiles_x, stiles_per_view, shard_rank, shard_count;
+  const int* tile_ids;
   // outputs
   float* rgb;
   float* capw;

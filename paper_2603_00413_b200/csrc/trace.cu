@@ -281,6 +281,18 @@ __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
     if (valid) {
       if (a.pids) {
         pid = a.pids[item];
+      } else if (a.shard_tile > 0) {   // tile shard: slot item / T^2, 8x4 micro-tiles inside the tile
+        const int T = a.shard_tile, T2 = T * T;
+        const int64_t slot = item / T2;
+        const int w = (int)(item - slot * T2);
+        const int64_t tid = a.tile_ids ? (int64_t)a.tile_ids[slot] : a.shard_rank + slot * a.shard_count;
+        const int view = (int)(tid / a.stiles_per_view);
+        const int tv = (int)(tid - (int64_t)view * a.stiles_per_view);
+        const int ty = tv / a.stiles_x, tx = tv - ty * a.stiles_x;
+        const int mt = w >> 5, l = w & 31, mpr = T >> 3;
+        const int px = tx * T + (mt % mpr) * 8 + (l & 7), py = ty * T + (mt / mpr) * 4 + (l >> 3);
+        DT_CHECK(view >= 0 && view < a.n_views && px < a.W && py < a.H);
+        pid = ((int64_t)view * a.H + py) * a.W + px;
       } else {
         int64_t tile = item >> 5;
         int l = (int)(item & 31);
@@ -292,7 +304,7 @@ __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
         pid = ((int64_t)view * a.H + py) * a.W + px;
       }
     }
-    int64_t ray = a.pids ? item : pid;
+    int64_t ray = a.pids || a.shard_tile > 0 ? item : pid;
     double3 o64 = d3(0, 0, 0), d64 = d3(0, 0, 1);
     int face = -1;
     float t = 0.f, u = 0.f, v = 0.f;

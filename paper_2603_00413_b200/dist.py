@@ -72,6 +72,20 @@ def tile_costs(pixel_ids: np.ndarray, seg_count: np.ndarray, n_views: int, W: in
     return np.bincount(t, weights=np.asarray(seg_count, np.float64), minlength=n_views * tx * ty)
 
 
+def shard_tiles(n_views: int, W: int, H: int, rank: int, world: int, tile: int = 32) -> np.ndarray:
+    """The global tile ids of the cyclic tile shard (rank, world) in ray order (TileShard)."""
+    return cyclic_tiles(n_views, W, H, rank, world, tile)
+
+
+def shard_tile_costs(tiles: np.ndarray, seg_count: np.ndarray, n_tiles_total: int, tile: int = 32) -> np.ndarray:
+    """Per-tile cost from per-ray segment counts of a TileShard forward (rays tile by tile,
+    tile^2 per tile): float64 [n_tiles_total], zero for tiles of other shards."""
+    seg = np.asarray(seg_count, np.float64).reshape(len(tiles), tile * tile).sum(1)
+    out = np.zeros(n_tiles_total, np.float64)
+    out[np.asarray(tiles, np.int64)] = seg
+    return out
+
+
 def lpt_assign(costs: Sequence[float], world: int) -> list:
     """Greedy longest-processing-time assignment: tiles in decreasing cost order, each to the
     currently least-loaded rank (ties: lowest rank; equal costs: lowest tile id first).  Returns

@@ -90,10 +90,19 @@ class DeviceScene:
         assert sigma.numel() == self.sigma.numel()
         self.sigma = sigma.to(self.device, torch.float32).contiguous()
 
-    def cameras(self, pixel_ids: Optional[torch.Tensor] = None) -> N.Cameras:
+    def cameras(self, pixel_ids=None) -> N.Cameras:
+        """pixel_ids: None (every pixel), a device int64 tensor of pixel ids, or a TileShard."""
         c = N.Cameras()
         c.n_views, c.width, c.height = self.n_views, self.width, self.height
         c.K, c.c2w = _ptr(self.K), _ptr(self.c2w)
+        if isinstance(pixel_ids, TileShard):
+            sh = pixel_ids
+            c.tile, c.shard_rank, c.shard_count = sh.tile, sh.rank, sh.count
+            if sh.tile_ids is not None:
+                assert sh.tile_ids.is_cuda and sh.tile_ids.dtype == torch.int32 and sh.tile_ids.is_contiguous()
+                c.tile_ids, c.n_tiles = _ptr(sh.tile_ids), sh.tile_ids.numel()
+            c.n_rays = sh.n_rays(self.n_views, self.width, self.height)
+            return c
         if pixel_ids is not None:
             assert pixel_ids.dtype == torch.int64 and pixel_ids.is_cuda and pixel_ids.is_contiguous()
             if pixel_ids.numel() == 0:       # an empty list is not "all pixels" (NULL)
@@ -105,6 +114,27 @@ class DeviceScene:
         else:
             c.pixel_ids, c.n_rays = None, self.n_pixels
         return c
+
+
+@dataclass
+class TileShard:
+    """A data-parallel shard of the image plane (dt_cameras.tile): the tile x tile
+    pixel tiles listed in tile_ids (device int32, e.g. dist.lpt_assign) or, when None, every tile
+    with id % count == rank; rays in tile order, 8 x 4 micro-tiles inside a tile (the order of
+    dist.tiles_pixel_ids).  Width and height must be multiples of tile."""
+    tile: int = 32
+    rank: int = 0
+    count: int = 1
+    tile_ids: Optional[torch.Tensor] = None
+
+    def n_tiles(self, n_views: int, W: int, H: int) -> int:
+        if self.tile_ids is not None:
+            return int(self.tile_ids.numel())
+        total = n_views * (W // self.tile) * (H // self.tile)
+        return max(0, (total - self.rank + self.count - 1) // self.count)
+
+    def n_rays(self, n_views: int, W: int, H: int) -> int:
+        return self.n_tiles(n_views, W, H) * self.tile * self.tile
 
 
 @dataclass

@@ -138,3 +138,21 @@ def test_tile_costs_and_tiles_pixel_ids():
     parts = DD.lpt_assign(costs, 3)
     allp = np.concatenate([DD.tiles_pixel_ids(p, W, H) for p in parts])
     assert np.array_equal(np.sort(allp), np.arange(n_views * W * H))
+
+
+def test_tile_shard_order_and_costs():
+    """TileShard (dt_cameras.tile): the cyclic shard's tiles and ray count match the pixel-id
+    path's, and per-ray segment counts fold back into per-tile costs."""
+    from paper_2603_00413_b200.tracer import TileShard
+    n_views, W, H, world = 3, 64, 96, 4
+    total = n_views * (W // 32) * (H // 32)
+    for r in range(world):
+        sh = TileShard(32, r, world)
+        tiles = DD.shard_tiles(n_views, W, H, r, world)
+        assert sh.n_tiles(n_views, W, H) == len(tiles)
+        assert sh.n_rays(n_views, W, H) == len(DD.tile_pixel_ids(n_views, W, H, r, world))
+        seg = np.arange(len(tiles) * 1024) % 7
+        c = DD.shard_tile_costs(tiles, seg, total)
+        assert c.sum() == seg.sum() and np.all(c[np.setdiff1d(np.arange(total), tiles)] == 0)
+        np.testing.assert_array_equal(
+            c, DD.tile_costs(DD.tile_pixel_ids(n_views, W, H, r, world), seg, n_views, W, H))
