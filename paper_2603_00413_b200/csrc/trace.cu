@@ -67,6 +67,14 @@ constexpr int kBwdThreads = 128;
 #ifndef DT_BWD_GRID_REGS
 #define DT_BWD_GRID_REGS 96
 #endif
+// the same for the hash texture (uncapped they take 158 / 168 registers: 12 warps per SM on
+// a walk bound by the latency of its table fetches)
+#ifndef DT_SHADE_HASH_REGS
+#define DT_SHADE_HASH_REGS 128
+#endif
+#ifndef DT_BWD_HASH_REGS
+#define DT_BWD_HASH_REGS 96
+#endif
 
 DT_D int fetch_work(int* counter, int chunk = 32) {
   int base = 0;
@@ -424,6 +432,11 @@ __global__ void __maxnreg__(DT_SHADE_GRID_REGS)
     k_shade_level_grid(FwdLaunch a, int k, int max_depth) {
   shade_level_body<1, VOL>(a, k, max_depth);
 }
+template <bool VOL>
+__global__ void __maxnreg__(DT_SHADE_HASH_REGS)
+    k_shade_level_hash(FwdLaunch a, int k, int max_depth) {
+  shade_level_body<2, VOL>(a, k, max_depth);
+}
 #ifndef DT_SHADE_VOL_REGS
 #define DT_SHADE_VOL_REGS 96
 #endif
@@ -723,6 +736,11 @@ __global__ void __maxnreg__(DT_BWD_GRID_REGS)
     k_backward_level_grid(BwdLaunch a, int k, int max_depth, int64_t cap) {
   backward_level_body<1, VOL>(a, k, max_depth, cap);
 }
+template <bool VOL>
+__global__ void __maxnreg__(DT_BWD_HASH_REGS)
+    k_backward_level_hash(BwdLaunch a, int k, int max_depth, int64_t cap) {
+  backward_level_body<2, VOL>(a, k, max_depth, cap);
+}
 // constant sigma, shell env: latency bound (dependent record -> child / vertex / gradient
 // fetches), so a register cap that buys occupancy pays (tools/sweep_regs.sh)
 #ifndef DT_BWD_CONST_REGS
@@ -908,9 +926,10 @@ cudaError_t launch_trace_primary(const FwdLaunch& a, int max_depth, int sm_count
 template <int ABS>
 void shade_dispatch(const FwdLaunch& a, int level, int max_depth, int sm_count, cudaStream_t st) {
   const bool vol = a.s.env_kind == 2;
-  auto kern = ABS == 1 ? (vol ? k_shade_level_grid<true> : k_shade_level_grid<false>)
-               : ABS == 0 && vol ? k_shade_level_vol
-                                 : (vol ? k_shade_level<ABS, true> : k_shade_level<ABS, false>);
+  auto kern = ABS == 1   ? (vol ? k_shade_level_grid<true> : k_shade_level_grid<false>)
+              : ABS == 2 ? (vol ? k_shade_level_hash<true> : k_shade_level_hash<false>)
+              : vol      ? k_shade_level_vol
+                         : k_shade_level<0, false>;
   const int g = cached_grid(a.grids, kGridShade + 2 * ABS + vol, (const void*)kern, kTraceThreads, sm_count);
   kern<<<g, kTraceThreads, 0, st>>>(a, level, max_depth);
 }
@@ -937,8 +956,8 @@ template <int ABS>
 void backward_dispatch(const BwdLaunch& a, int level, int sm_count, cudaStream_t st) {
   const bool vol = a.s.env_kind == 2;
   auto kern = ABS == 1 ? (vol ? k_backward_level_grid<true> : k_backward_level_grid<false>)
-               : ABS == 0 ? (vol ? k_backward_level_vol : k_backward_level_const)
-                          : (vol ? k_backward_level<ABS, true> : k_backward_level<ABS, false>);
+               : ABS == 2 ? (vol ? k_backward_level_hash<true> : k_backward_level_hash<false>)
+                          : (vol ? k_backward_level_vol : k_backward_level_const);
   const int g = cached_grid(a.grids, kGridBwd + 2 * ABS + vol, (const void*)kern, kBwdThreads, sm_count);
   kern<<<g, kBwdThreads, 0, st>>>(a, level, a.s.max_depth, a.cap);
 }
