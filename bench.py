@@ -289,6 +289,45 @@ def run_ours(args, rank, world, local_rank):
     tr.set_profiling(False)
     prof = tr.profile(reset=True)
     segs = prof["segments"]         # counted on the device by every timed forward
+    eager = None
+    ms_eager = ms
+    if world == 1 and args.graph:
+        # the same step captured once into a CUDA graph and replayed (no per-kernel launch gaps,
+        # no profiling events); the eager run above supplies the phase split and launch counts
+        eager = {"ms_per_step": round(ms / args.steps, 3), "value": round(segs / (ms / 1e3) / 1e6, 3),
+                 "note": "same step launched kernel by kernel, with per-phase profiling events"}
+        if infer:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                for _ in range(2):
+                    step()
+                    tr.get_stats()
+            torch.cuda.current_stream(dev).wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+        else:
+            graph = opt.capture_step(target, pid)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        tr.get_stats()
+        tr.profile(reset=True)
+        clocks = ClockSampler(local_rank)
+        if os.environ.get("BENCH_NO_CLOCKS") is None:
+            clocks.start()
+        e0.record()
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        clk = clocks.stop()
+        tr.get_stats()              # raises DT_ERR_RETRY if a replay overflowed the arena
+        segs = tr.profile(reset=True)["segments"]
+        if not infer:
+            opt.sync_steps()
     if world > 1:
         dist.barrier()
         t = torch.tensor([ms, float(segs)], dtype=torch.float64, device=dev)
@@ -438,7 +477,7 @@ def run_ours(args, rank, world, local_rank):
         roofline = {"bound": "hbm", "kernel": kname, **{k: v for k, v in hbm_view.items() if k != "bytes_per_launch"},
                     "bytes_per_launch": int(bytes_per_launch)}
     roofline.update({"traffic": traffic, "traffic_source": traffic_src, "ms_per_launch": round(ms_per_launch, 3),
-                     "share_of_step": round(ph[cls] / ms, 4)})
+                     "share_of_step": round(ph[cls] / ms_eager, 4)})
     if traffic is not None:
         roofline["dram_frac"] = round(traffic / (ms_per_launch / 1e3) / 1e9 / peak, 4)
     for key in ("l2_hit_pct", "l1_hit_pct", "lanes_per_inst", "ipc", "issue_active_pct"):
@@ -468,6 +507,7 @@ def run_ours(args, rank, world, local_rank):
                          f"{last['arena_capacity'] * 128 / 1e9:.1f} GB streamed every step; "
                          + ("LBVH built once (fixed mesh)" if infer else "LBVH rebuilt in-step")},
         "clocks": clk, "e2e": e2e, "gpu_launches": int(prof["kernel_launches"]), "roofline": roofline,
+        "cuda_graph": eager is not None, "eager": eager,
         "cpu_baseline": cpu,
         "phase_ms_per_step": {k: round(v / args.steps, 3) for k, v in ph.items()},
         "counters_per_step": {"node_visits": prof["node_visits"] // args.steps,
@@ -620,6 +660,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--balance", default="lpt", choices=["lpt", "cyclic"],
                     help="N > 1: tile assignment (greedy LPT on measured per-tile segments, or cyclic)")
+    ap.add_argument("--graph", action="store_true",
+                    help="N = 1: also capture the full-image step into a CUDA graph and time its replays (measured: "
+                         "no gain at C3, the kernels are long enough to hide launch gaps; default off)")
     ap.add_argument("--batch", type=int, default=0,
                     help="> 0: the paper's training iteration with this many random rays per step (P:531: 5000), "
                          "captured into a CUDA graph; 0: full images (default)")

@@ -240,7 +240,7 @@ void dt_destroy(dt_ctx* c) {
   void* ptrs[] = {c->V, c->F, c->nrm, c->fnrm, c->nodes, c->tris, c->keys, c->vals, c->hist, c->children,
                   c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, c->vstart, c->vcorner, c->scal,
                   c->iscal, c->rec.o, c->lvl, c->sigma_snap, c->gV, c->gN, c->gVn, c->gS, c->fe, c->gsig, c->gior,
-                  c->counters, c->ranges, c->wbox, c->wdepth, c->scratch,
+                  c->counters, c->ranges, c->wbox, c->wdepth, c->went, c->scratch,
                   c->nbr_start, c->nbr_cnt, c->nbr, c->nbr_owner, c->scan_part, c->wqueue};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -355,10 +355,9 @@ __global__ void k_refit(const float4* __restrict__ V, const int* __restrict__ F,
 // q* hold one byte per child (child c in bits 8c..8c+7).  ref >= 0: wide node; ref = EMPTY:
 // unused slot (qlo = 255 > qhi = 0); otherwise leaf: ref = -1 - (first << 2 | (count - 1)).
 DT_D int bsize(const int2* __restrict__ ranges, int ref) { return ref < 0 ? 1 : ranges[ref].y - ranges[ref].x + 1; }
-// entry e of a wide node is itself a wide node (else a leaf: <= leaf_max triangles, or an
-// SAH-chosen leaf, bit 9 of the collapse DP's decisions)
-DT_D bool wide_entry(const int2* __restrict__ ranges, const int* __restrict__ dec, int e, int leaf_max) {
-  return e >= 0 && bsize(ranges, e) > leaf_max && !(dec && ((__ldcg(dec + e) >> 9) & 1));
+// entry e of a wide node is itself a wide node (else a leaf of <= leaf_max triangles)
+DT_D bool wide_entry(const int2* __restrict__ ranges, int e, int leaf_max) {
+  return e >= 0 && bsize(ranges, e) > leaf_max;
 }
 
 // Quantise and write wide node w: its entries ent[0..ne) (binary refs; internal entries carry
@@ -366,7 +365,7 @@ DT_D bool wide_entry(const int2* __restrict__ ranges, const int* __restrict__ de
 DT_D void write_wide_node(int i, const int ent[4], const int wref[4], int ne, unsigned w, int wd, double pad,
                           const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
                           const int2* __restrict__ ranges, int leaf_max, uint4* __restrict__ wnodes,
-                          float4* __restrict__ wbox, int* __restrict__ wdepth, const int* __restrict__ dec = nullptr) {
+                          float4* __restrict__ wbox, int* __restrict__ wdepth) {
   float3 ulo, uhi;
   load_box(leafbox, nodebox, i, ulo, uhi);
   double P[3] = {(double)__double2float_rd((double)ulo.x - pad), (double)__double2float_rd((double)ulo.y - pad),
@@ -397,7 +396,7 @@ DT_D void write_wide_node(int i, const int ent[4], const int wref[4], int ne, un
         ql[a] = (unsigned)fmin(fmax(fl, 0.0), 255.0);
         qh[a] = (unsigned)fmin(fmax(fh, 0.0), 255.0);
       }
-      if (wide_entry(ranges, dec, e, leaf_max)) {
+      if (wide_entry(ranges, e, leaf_max)) {
         refs[c] = wref[c];
       } else {
         int first = e < 0 ? ~e : ranges[e].x;
@@ -464,18 +463,14 @@ DT_D float box_area(const float4* __restrict__ nodebox, int e) {
 //   C(n, 1)     = A(n) c_node + min_{a+b=4} C(l, a) + C(r, b)      (n becomes a wide node)
 //   C(n, i > 1) = min(C(n, i - 1), min_{a+b=i} C(l, a) + C(r, b))   (n opened into i entries)
 // with A the box surface area and c_node / c_tri the costs of a 4-box node visit and a
-// triangle test (130 : 37 lane operations).  dec[n] holds the argmins: bits
-// 2(j-2)..+1 = a - 1 of the best split for j = 2..4, bit 6 + (i - 2) = "C(n, i) opens n".
+// triangle test (130 : 37 lane operations).  The same pass records the entry
+// lists the argmins select (went: E(n, 2), E(n, 3) and n's own wide node W(n)), so the top-down
+// pass reads a wide node's entries with one load instead of walking the decisions.
 #ifndef DT_WIDE_SAH
 #define DT_WIDE_SAH 1
 #endif
 #ifndef DT_COST_NODE
 #define DT_COST_NODE (130.f / 37.f)
-#endif
-// DT_SAH_LEAF > 1: a subtree of up to that many triangles may become one leaf entry when
-// its SAH cost A(n) c_tri |n| beats the node (bit 9 of dec)
-#ifndef DT_SAH_LEAF
-#define DT_SAH_LEAF 1
 #endif
 constexpr float kCostNode = DT_COST_NODE, kCostTri = 1.f;
 
@@ -486,9 +481,23 @@ DT_D float box_area2(const float4* __restrict__ leafbox, const float4* __restric
   return dx * dy + dy * dz + dz * dx;
 }
 
+// Entries E(x, k) of the best representation of binary subtree x by at most k <= 3 entries
+// (went: per internal node 3 int4 = E(x,2)[2] | E(x,3)[3] | W(x)[4], kEmptyRef-padded; W(x) is
+// the entry list of the wide node made of x: its budget of 4 split between its children).
+DT_D int get_entries(const int4* __restrict__ went, int x, int k, int out[4]) {
+  if (x < 0 || k <= 1) { out[0] = x; return 1; }
+  const int4 w0 = __ldcg(went + 3 * (size_t)x), w1 = __ldcg(went + 3 * (size_t)x + 1);
+  const int e[5] = {w0.x, w0.y, w0.z, w0.w, w1.x};
+  const int o = k == 2 ? 0 : 2, cnt = k == 2 ? 2 : 3;
+  int n = 0;
+  for (int q = 0; q < cnt; ++q)
+    if (e[o + q] != kEmptyRef) out[n++] = e[o + q];
+  return n;
+}
+
 __global__ void k_wide_cost(const int2* __restrict__ children, const int2* __restrict__ ranges, const int* __restrict__ parent_int,
                             const int* __restrict__ parent_leaf, int* __restrict__ flags, const float4* __restrict__ leafbox,
-                            const float4* __restrict__ nodebox, int n, float4* __restrict__ cost, int* __restrict__ dec) {
+                            const float4* __restrict__ nodebox, int n, float4* __restrict__ cost, int4* __restrict__ went) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     int p = parent_leaf[j];
     while (p >= 0) {
@@ -510,7 +519,7 @@ __global__ void k_wide_cost(const int2* __restrict__ children, const int2* __res
         }
       }
       float best[5];                              // best[j] = min_{a+b=j} Cl[a-1] + Cr[b-1]
-      int d = 0;
+      int split[5];
 #pragma unroll
       for (int jj = 2; jj <= 4; ++jj) {
         float bv = kInf;
@@ -520,57 +529,62 @@ __global__ void k_wide_cost(const int2* __restrict__ children, const int2* __res
           if (v < bv) { bv = v; ba = a; }
         }
         best[jj] = bv;
-        d |= (ba - 1) << (2 * (jj - 2));
+        split[jj] = ba;
       }
       float C[4];
-      const float Ap = box_area2(leafbox, nodebox, p);
-      C[0] = Ap * kCostNode + best[4];
-      const int cnt = ranges[p].y - ranges[p].x + 1;
-      if (DT_SAH_LEAF > 1 && cnt <= DT_SAH_LEAF && Ap * kCostTri * (float)cnt < C[0]) {
-        C[0] = Ap * kCostTri * (float)cnt;
-        d |= 1 << 9;
-      }
+      bool open[5];
+      C[0] = box_area2(leafbox, nodebox, p) * kCostNode + best[4];
 #pragma unroll
       for (int i = 2; i <= 4; ++i) {
-        if (best[i] < C[i - 2]) { C[i - 1] = best[i]; d |= 1 << (6 + i - 2); }
-        else C[i - 1] = C[i - 2];
+        open[i] = best[i] < C[i - 2];
+        C[i - 1] = open[i] ? best[i] : C[i - 2];
+      }
+      // entry lists: E(p, 2), E(p, 3) (for the parent's budget split) and W(p) (p's own wide node)
+      int L[3][4];
+      int nl[3];
+#pragma unroll
+      for (int i = 2; i <= 4; ++i) {
+        int* out = L[i - 2];
+        int cnt = 0;
+        if (i == 4 || open[i]) {
+          int a[4], b[4];
+          const int na = get_entries(went, ch.x, split[i], a), nb = get_entries(went, ch.y, i - split[i], b);
+          for (int q = 0; q < na; ++q) out[cnt++] = a[q];
+          for (int q = 0; q < nb; ++q) out[cnt++] = b[q];
+        } else if (i == 2) {
+          out[cnt++] = p;                          // E(p, 1)
+        } else {
+          for (int q = 0; q < nl[i - 3]; ++q) out[cnt++] = L[i - 3][q];
+        }
+        nl[i - 2] = cnt;
+        for (int q = cnt; q < 4; ++q) out[q] = kEmptyRef;
       }
       __stcg(cost + p, make_float4(C[0], C[1], C[2], C[3]));
-      __stcg(dec + p, d);
+      __stcg(went + 3 * (size_t)p, make_int4(L[0][0], L[0][1], L[1][0], L[1][1]));
+      __stcg(went + 3 * (size_t)p + 1, make_int4(L[1][2], L[2][0], L[2][1], L[2][2]));
+      __stcg(went + 3 * (size_t)p + 2, make_int4(L[2][3], kEmptyRef, kEmptyRef, kEmptyRef));
       p = parent_int[p];
     }
   }
 }
 
-// Entries of the wide node at binary node b from the DP decisions (at most 4).
-DT_D int sah_entries(const int2* __restrict__ children, const int* __restrict__ dec, const int2* __restrict__ ranges,
-                     int b, int leaf_max, int ent[4]) {
-  int sx[8], sk[8], sp = 0, ne = 0;
-  {
-    const int2 ch = children[b];
-    const int a = ((__ldcg(dec + b) >> 4) & 3) + 1;   // split of the budget 4
-    sx[sp] = ch.y; sk[sp++] = 4 - a;
-    sx[sp] = ch.x; sk[sp++] = a;
-  }
-  while (sp > 0) {
-    const int x = sx[--sp];
-    int k = sk[sp];
-    if (x < 0 || bsize(ranges, x) <= leaf_max || k == 1) { ent[ne++] = x; continue; }
-    const int d = __ldcg(dec + x);
-    while (k > 1 && !((d >> (6 + k - 2)) & 1)) --k;  // the best representation with <= k entries
-    if (k == 1) { ent[ne++] = x; continue; }
-    const int a = ((d >> (2 * (k - 2))) & 3) + 1;
-    const int2 ch = children[x];
-    sx[sp] = ch.y; sk[sp++] = k - a;
-    sx[sp] = ch.x; sk[sp++] = a;
-  }
+// Entries of the wide node made of binary node b (at most 4): W(b) from the DP.
+DT_D int sah_entries(const int4* __restrict__ went, int b, int ent[4]) {
+  const int4 w1 = __ldcg(went + 3 * (size_t)b + 1), w2 = __ldcg(went + 3 * (size_t)b + 2);
+  const int e[4] = {w1.y, w1.z, w1.w, w2.x};
+  int ne = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (e[q] != kEmptyRef) ent[ne++] = e[q];
   return ne;
 }
+
 __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __restrict__ ranges,
                                const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
                                const int* __restrict__ ibox, uint4* __restrict__ wnodes, float4* __restrict__ wbox,
                                int* __restrict__ wdepth, int* __restrict__ nwide, unsigned long long* queue,
-                               int* __restrict__ head, int* pending, int cap, int leaf_max, const int* __restrict__ dec) {
+                               int* __restrict__ head, int* pending, int cap, int leaf_max,
+                               const int4* __restrict__ went) {
   const double pad = wide_pad(ibox);
   while (true) {
     const int idx = atomicAdd(head, 1);
@@ -589,8 +603,8 @@ __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __
     const int2 ch = children[b];
     ent[0] = ch.x;
     ent[1] = ch.y;
-    if (dec) ne = sah_entries(children, dec, ranges, b, leaf_max, ent);
-    while (!dec && ne < 4) {
+    if (went) ne = sah_entries(went, b, ent);
+    while (!went && ne < 4) {
       int best = -1;
       float ba = -1.f;
       for (int c = 0; c < ne; ++c) {
@@ -606,15 +620,15 @@ __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __
       ent[ne++] = g.y;
     }
     int nin = 0;
-    for (int c = 0; c < ne; ++c) nin += wide_entry(ranges, dec, ent[c], leaf_max);
+    for (int c = 0; c < ne; ++c) nin += wide_entry(ranges, ent[c], leaf_max);
     const int base = nin ? atomicAdd(nwide, nin) : 0;
     const int wd = __ldcg(wdepth + w);                 // written by the parent before publishing w (L2)
     for (int c = 0, k = 0; c < ne; ++c)
-      if (wide_entry(ranges, dec, ent[c], leaf_max)) wref[c] = base + k++;
+      if (wide_entry(ranges, ent[c], leaf_max)) wref[c] = base + k++;
     DT_CHECK(base + nin <= cap);
-    write_wide_node(b, ent, wref, ne, (unsigned)w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth, dec);
+    write_wide_node(b, ent, wref, ne, (unsigned)w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
     for (int c = 0; c < ne; ++c) {
-      if (!wide_entry(ranges, dec, ent[c], leaf_max)) continue;
+      if (!wide_entry(ranges, ent[c], leaf_max)) continue;
       wdepth[wref[c]] = wd + 1;
       __threadfence();
       atomicExch(queue + wref[c], ((unsigned long long)(unsigned)wref[c] << 32) | (unsigned)ent[c]);
@@ -746,7 +760,7 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
     size_t cap = nf;
     void* old[] = {c->F, c->fnrm, c->nodes, c->tris, c->keys, c->vals, c->children, c->parent_int, c->parent_leaf,
                    c->rflags, c->nodebox, c->leafbox, c->vcorner, c->fe, c->ranges,
-                   c->wbox, c->wdepth};
+                   c->wbox, c->wdepth, c->went};
     for (void* p : old)
       if (p) cudaFree(p);
     size_t ks = 2 * 3 * cap;   // keys/vals ping-pong sized for the 3*nf corner sort
@@ -757,7 +771,7 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
         (e = cudaMalloc(&c->parent_leaf, cap * sizeof(int))) || (e = cudaMalloc(&c->rflags, cap * sizeof(int))) ||
         (e = cudaMalloc(&c->nodebox, cap * 32)) || (e = cudaMalloc(&c->leafbox, cap * 32)) ||
         (e = cudaMalloc(&c->vcorner, 3 * cap * sizeof(unsigned))) || (e = cudaMalloc(&c->fe, 2 * cap * 16)) ||
-        (e = cudaMalloc(&c->ranges, cap * sizeof(int2))) ||
+        (e = cudaMalloc(&c->ranges, cap * sizeof(int2))) || (e = cudaMalloc(&c->went, cap * 3 * sizeof(int4))) ||
         (e = cudaMalloc(&c->wbox, cap * 32)) || (e = cudaMalloc(&c->wdepth, cap * sizeof(int))))
       return e;
     c->cap_nf = cap;
@@ -822,24 +836,22 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
       // most threads would only poll for unpublished entries
       gq = std::max(1, std::min(per, DT_WIDE_BLOCKS_PER_SM)) * c->sm_count;
     }
-    int* dec = nullptr;
+    int4* went = nullptr;
 #if DT_WIDE_SAH
-    // the DP's per-node costs and decisions live in scratch the collapse does not otherwise
-    // use at this point: the sort keys (float4 per node = 4 words, 3nf words available in
-    // keys + vals) -- cost in keys/vals [0, 4(nf-1)) needs 4(nf-1) <= 6nf words: the corner
-    // sort's key/value buffers hold 2 x 3nf words each
+    // the DP's per-node costs live in scratch the collapse does not otherwise use at this
+    // point (the sort keys: 4 words per node of the 6 nf available); its entry lists in went
     float4* cost = reinterpret_cast<float4*>(c->keys);
-    dec = reinterpret_cast<int*>(c->keys + 4 * (size_t)(nf - 1));
+    went = c->went;
     cudaMemsetAsync(c->rflags, 0, (size_t)(nf - 1) * sizeof(int), st);
-    k_wide_cost<<<gf, T, 0, st>>>(c->children, c->ranges, c->parent_int, c->parent_leaf, c->rflags, c->leafbox, c->nodebox, nf,
-                                  cost, dec);
+    k_wide_cost<<<gf, T, 0, st>>>(c->children, c->ranges, c->parent_int, c->parent_leaf, c->rflags, c->leafbox,
+                                  c->nodebox, nf, cost, went);
     launches += 1;
 #endif
     cudaMemsetAsync(c->wqueue, 0xff, (size_t)nf * sizeof(unsigned long long), st);
     k_wide_topdown_init<<<1, 1, 0, st>>>(c->wqueue, ctr, ctr + 1, c->iscal + 12, c->wdepth);
     k_wide_topdown<<<gq, T, 0, st>>>(c->children, c->ranges, c->leafbox, c->nodebox, c->iscal,
                                      reinterpret_cast<uint4*>(c->nodes), c->wbox, c->wdepth, c->iscal + 12, c->wqueue,
-                                     ctr, ctr + 1, nf - 1, c->leaf_max, dec);
+                                     ctr, ctr + 1, nf - 1, c->leaf_max, went);
     launches += 2;
   } else {
     k_wide_single<<<1, 1, 0, st>>>(c->leafbox, c->nodebox, c->ranges, c->iscal, reinterpret_cast<uint4*>(c->nodes),

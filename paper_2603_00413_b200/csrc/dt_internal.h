@@ -122,6 +122,7 @@ struct dt_ctx {
   int2* ranges = nullptr;     // [nf-1] leaf range of each binary node
   float4* wbox = nullptr;     // [2 * n_wide] wide-node boxes (checks)
   int* wdepth = nullptr;      // [n_wide] wide-node depth (checks)
+  int4* went = nullptr;       // [3 (nf-1)] SAH collapse entry lists per binary node (bvh.cu)
   float* scal = nullptr;      // device scalars: [0..5] root box, [6] bbox diagonal
   int* iscal = nullptr;       // device ints: ordered-int bounds
   size_t hist_cap = 0;
