@@ -308,3 +308,37 @@ def test_cuda_graph_step_matches_eager():
     (Va, ia, sa), (Vb, ib, sb) = res
     assert rel_l2(Vb.cpu().numpy(), Va.cpu().numpy()) < 1e-5
     assert abs(float(ib) - float(ia)) < 1e-5 and rel_l2(sb.cpu().numpy(), sa.cpu().numpy()) < 1e-5
+
+
+def test_cuda_graph_replay_overflow_is_reported_and_changes_nothing():
+    """A replay whose forward overflows the record arena (the arena was sized when the graph
+    was captured) skips its updates on the device (dt_adam.skip_if) and is reported by
+    dt_get_stats as DT_ERR_RETRY after the replays."""
+    from paper_2603_00413_b200 import _native as N
+    from paper_2603_00413_b200.optim import RefineConfig, RefineOptimizer
+    from paper_2603_00413_b200.tracer import DeviceScene, Tracer
+    sc = S.config_c2(n_views=2, res=96)
+    sc = T.scene(sc.V, sc.F, sc.cams, env=sc.env, D=8)
+    dev = torch.device("cuda:0")
+    tr = Tracer(dev)
+    ds = DeviceScene(sc, dev)
+    tr.build_bvh(ds.V, ds.F)
+    target = tr.trace_forward(ds).rgb.clone() * 0.9
+    tr = Tracer(dev)                           # a fresh context: its arena is sized by the tiny object
+    opt = RefineOptimizer(tr, ds, RefineConfig(freeze_iters=0), seed=3)
+    full = opt.V.clone()
+    opt.V.copy_(full * 0.05)                   # a tiny object: the arena is sized for few segments
+    opt.step(target)
+    tr.get_stats()
+    g = opt.capture_step(target)
+    torch.cuda.synchronize()
+    tr.get_stats()
+    opt.V.copy_(full)                          # the captured build reads opt.V: now far more segments
+    before = [t.clone() for t in (opt.V, opt.sigma, opt.ior, opt.mV, opt.vV, opt.t_dev)]
+    g.replay()
+    torch.cuda.synchronize()
+    with pytest.raises(N.DiffTransError) as e:
+        tr.get_stats()
+    assert e.value.status == N.DT_ERR_RETRY
+    for x, y in zip(before, (opt.V, opt.sigma, opt.ior, opt.mV, opt.vV, opt.t_dev)):
+        assert torch.equal(x, y)
