@@ -330,11 +330,13 @@ def run_ours(args, rank, world, local_rank):
             opt.sync_steps()
     if world > 1:
         dist.barrier()
-        t = torch.tensor([ms, float(segs)], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, float(segs), float(n_rays)], dtype=torch.float64, device=dev)
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        ms, segs = float(mx[0]), float(t[1])
+        ms, segs, rays_total = float(mx[0]), float(t[1]), int(t[2])
+    else:
+        rays_total = int(n_rays)
     value = segs / (ms / 1e3) / 1e6
 
     # ---- end-to-end through the public API with host buffers (pinned), same metric
@@ -501,7 +503,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(args.config, sc, infer),
-                   "rays_per_step": int(n_rays) * world, "segments_per_step": int(segs / args.steps),
+                   "rays_per_step": rays_total, "segments_per_step": int(segs / args.steps),
                    "segments_per_depth": last["segments_per_depth"], "parallelism": f"rays{world}", "balance": args.balance if world > 1 else None,
                    "l2": "working set > L2: path-record arena "
                          f"{last['arena_capacity'] * 128 / 1e9:.1f} GB streamed every step; "

@@ -34,12 +34,15 @@ def test_single_gpu_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
 
 
-def test_two_ranks_functional():
+@pytest.mark.parametrize("balance,port", [("lpt", 29517), ("cyclic", 29518)])
+def test_two_ranks_functional(balance, port):
+    """Both tile assignments (cyclic tile shards, LPT tile lists), with the end-to-end leg."""
     d = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-             "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2", "--config", "C2", "--steps", "3",
-             "--warmup", "3", "--no-e2e"], env={"BENCH_SHARE_GPU": "1", "BENCH_DIST_BACKEND": "gloo"})
+             "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--config", "C2", "--steps", "3",
+             "--warmup", "3", "--balance", balance], env={"BENCH_SHARE_GPU": "1", "BENCH_DIST_BACKEND": "gloo"})
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "rays2"
-    assert d["cpu_baseline"] is None
+    assert d["config"]["balance"] == balance and d["config"]["rays_per_step"] == 8 * 256 * 256
+    assert d["e2e"]["value"] > 0 and d["cpu_baseline"] is None
 
 
 def test_reference_arm():
