@@ -506,7 +506,7 @@ def run_ours(args, rank, world, local_rank):
                    "rays_per_step": rays_total, "segments_per_step": int(segs / args.steps),
                    "segments_per_depth": last["segments_per_depth"], "parallelism": f"rays{world}", "balance": args.balance if world > 1 else None,
                    "l2": "working set > L2: path-record arena "
-                         f"{last['arena_capacity'] * 128 / 1e9:.1f} GB streamed every step; "
+                         f"{last['arena_capacity'] * 160 / 1e9:.1f} GB streamed every step; "
                          + ("LBVH built once (fixed mesh)" if infer else "LBVH rebuilt in-step")},
         "clocks": clk, "e2e": e2e, "gpu_launches": int(prof["kernel_launches"]), "roofline": roofline,
         "cuda_graph": eager is not None, "eager": eager,
