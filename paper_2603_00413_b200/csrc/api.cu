@@ -536,6 +536,7 @@ dt_status dt_trace_backward(dt_ctx* c, const float* grad_rgb, float* grad_V, flo
   DT_CU(cudaMemsetAsync(c->gN, 0, (size_t)c->nv * 16, st));
   DT_CU(cudaMemsetAsync(c->gsig, 0, (c->sigma_len / 3) * sizeof(float4), st));
   DT_CU(cudaMemsetAsync(c->gior, 0, sizeof(float), st));
+  DT_CU(cudaMemsetAsync(c->lvl + LV_WORK_BWD, 0, 16 * sizeof(int), st));
   BwdLaunch b{};
   b.s = c->fwd_scene;
   b.grids = c->grid_cache;

@@ -33,7 +33,7 @@ constexpr int kRecordBytes = 2 * 32 + 6 * 16;
 enum {
   LV_CNT = 0,            // [16] records per level
   LV_WORK_TRACE = 16,    // [16]
-  LV_WORK_GATHER = 32,   // [16]
+  LV_WORK_BWD = 32,      // [16] backward window counters (reset by every dt_trace_backward)
   LV_WORK_SHADE = 48,    // [16]
   LV_OVERFLOW = 64,
   LV_STACKERR = 65,

@@ -375,7 +375,10 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
   const int64_t child_off = level_base(a.lvl, k + 1);
   const int64_t lim = a.cap - a.lvl[LV_CNT + 0];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  constexpr bool kDyn = ABS != 0 || VOL;
+#ifndef DT_SHADE_DYN
+#define DT_SHADE_DYN 1
+#endif
+  constexpr bool kDyn = ABS != 0 || VOL || DT_SHADE_DYN;
   int* const ctr = a.lvl + LV_WORK_SHADE + k;
   __shared__ unsigned char sslot[kTraceThreads * 2];
   int64_t wbase = kDyn ? (int64_t)fetch_work(ctr, 64) : (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 2;
@@ -568,9 +571,15 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
   const int64_t off = k == 0 ? 0 : level_base(a.lvl, k);
   float gior = 0.0f;
   float3 gsc = f3(0, 0, 0);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   __shared__ unsigned char sslot[kBwdThreads * 2];
-  for (int64_t wb = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 2; wb < n; wb += stride * 2) {
+  // 64-record windows taken from the level's counter (the next window's atomic in flight while
+  // this one is replayed): window costs vary with the hit / miss mix, so a static stride leaves
+  // a tail
+  int* const ctr = a.lvl + LV_WORK_BWD + k;
+  int64_t wb = fetch_work(ctr, 64);
+  int nx = 0;
+  if (lane_id() == 0) nx = atomicAdd(ctr, 64);
+  while (wb < n) {
   int o0, o1;
   {
     int c[2];
@@ -711,6 +720,8 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
       a.r.gd[idx] = f4(gd, 0.f);
     }
   }
+  wb = __shfl_sync(~0u, nx, 0);
+  if (lane_id() == 0) nx = atomicAdd(ctr, 64);
   }
   // warp reductions of the scalar adjoints
   for (int o = 16; o > 0; o >>= 1) {
