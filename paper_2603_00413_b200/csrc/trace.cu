@@ -360,11 +360,11 @@ __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
 // event and spawns the children into level k+1 (warp-ballot compaction).  Level 0 needs
 // the final level-0 count, so it always runs after the traversal pass.
 // Each warp takes a window of 64 records and shades them in two rounds of 32 in hit-first
-// lane order (hit_first_order).  Work distribution: constant-sigma / non-volume levels cost
-// about the same per record, so warps stride statically; with a sigma grid or hash texture
-// (cooperative interior walks) or a volumetric env the cost varies a lot, so warps take
-// 64-record windows from the level's counter, the next window's atomic in flight while the
-// current one is shaded.
+// lane order (hit_first_order).  Work distribution: warps take 64-record windows from the
+// level's counter, the next window's atomic in flight while the current one is shaded -- a
+// window's cost varies with its hit / miss mix (and with the interior walks of a sigma grid,
+// a hash texture or a volumetric env), so a static stride left a tail (r02: constant-sigma C3
+// shade 9.45 -> 8.92 ms; DT_SHADE_DYN=0 restores the static stride).
 template <int ABS, bool VOL>
 DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
   if (a.lvl[LV_OVERFLOW]) return;   // arena too small: the host grows it and re-runs
