@@ -755,7 +755,7 @@ __global__ void __maxnreg__(DT_BWD_HASH_REGS)
 // constant sigma, shell env: latency bound (dependent record -> child / vertex / gradient
 // fetches), so a register cap that buys occupancy pays (tools/sweep_regs.sh)
 #ifndef DT_BWD_CONST_REGS
-#define DT_BWD_CONST_REGS 96
+#define DT_BWD_CONST_REGS 88
 #endif
 __global__ void __maxnreg__(DT_BWD_CONST_REGS) k_backward_level_const(BwdLaunch a, int k, int max_depth, int64_t cap) {
   backward_level_body<0, false>(a, k, max_depth, cap);
