@@ -49,3 +49,10 @@ def test_reference_arm():
     d = run([sys.executable, "bench.py", "--impl", "reference", "--config", "C2", "--steps", "1", "--warmup", "1",
              "--ref-pixels", "16"])
     assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_batch_mode_cuda_graph():
+    """--batch: the paper's random-ray training iteration, captured into a CUDA graph."""
+    d = run([sys.executable, "bench.py", "--config", "C2", "--batch", "500", "--steps", "5", "--warmup", "3"])
+    assert d["value"] > 0 and d["config"]["batch"] == 500 and d["config"]["cuda_graph"] is True
+    assert d["eager"]["value"] > 0 and d["iterations_per_s"] > 0 and d["gpu_launches"] > 0
