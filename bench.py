@@ -576,6 +576,8 @@ def run_batch(args, rank, world, local_rank):
     tr.build_bvh(dt_.V, dt_.F)
     target_full = tr.trace_forward(dt_).rgb.clone()
     del dt_
+    # a build serves only B rays here: the plain Karras hierarchy (no treelet passes) is cheaper
+    tr.set_bvh_quality(0)
     B, npix = args.batch, ds.n_pixels
     torch.manual_seed(11 + rank)
     pid = torch.empty(B, dtype=torch.int64, device=dev)

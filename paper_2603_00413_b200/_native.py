@@ -88,6 +88,7 @@ SIGNATURES = {
     "dt_last_error": (C.c_char_p, [_P]),
     "dt_status_string": (C.c_char_p, [C.c_int]),
     "dt_build_bvh": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int32, _P]),
+    "dt_set_bvh_quality": (C.c_int, [_P, C.c_int32]),
     "dt_trace_forward": (C.c_int, [_P, C.c_float, C.POINTER(Absorption), C.POINTER(Env), C.POINTER(Cameras),
                                    C.POINTER(TraceOpts), _P, _P, _P, _P, C.POINTER(Stats), _P]),
     "dt_trace_backward": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, _P]),

@@ -271,6 +271,14 @@ dt_status dt_build_bvh(dt_ctx* c, const float* V, int32_t nv, const int32_t* F, 
   return DT_OK;
 }
 
+dt_status dt_set_bvh_quality(dt_ctx* c, int32_t treelet_passes) {
+  if (!c) return DT_ERR_INVALID_ARG;
+  DT_ARG(treelet_passes >= 0 && treelet_passes <= 4, "dt_set_bvh_quality: treelet_passes=%d not in [0, 4]",
+         treelet_passes);
+  c->treelet_passes = treelet_passes;
+  return DT_OK;
+}
+
 dt_status dt_trace_forward(dt_ctx* c, float ior, const dt_absorption* ab, const dt_env* env, const dt_cameras* cams,
                            const dt_trace_opts* opts, float* rgb, float* capped_w, uint64_t* sig_topo,
                            uint64_t* sig_face, dt_stats* stats, void* stream) {

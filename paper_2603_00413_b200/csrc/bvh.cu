@@ -343,6 +343,144 @@ __global__ void k_refit(const float4* __restrict__ V, const int* __restrict__ F,
   }
 }
 
+// ----------------------------------------------------------------------------- treelets
+// Treelet restructuring (Karras & Aila 2013) improves the Karras hierarchy before the collapse
+// (dt_set_bvh_quality: passes, default 2).  Bottom up (atomic-flag climb, like the refit),
+// every node with >= N triangles below becomes the root of a treelet: its two children, then
+// repeatedly the treelet leaf of largest box area replaced by its own two children, until N = 5
+// treelet leaves (4 internal nodes).  A dynamic program over the 31 subsets of the leaves finds
+// the binary topology of least SAH cost, C(S) = A(S) c_i + min_{P u Q = S} C(P) + C(Q) (leaves:
+// their subtree costs), and the treelet's internal nodes are rewired to it when it is cheaper.
+// The leaf boxes and every ancestor's box are unchanged; the triangle order (leaf indices) too.
+// After a pass, ranges[n] holds (0, count - 1): only the triangle count of a subtree stays
+// meaningful (the collapse uses it for leaf_max = 1 only).  r02 sweep (C3, ms/step): N = 4 /
+// 5 / 6 at 2 passes: 78.6 / 78.5 / 79.7 (6 costs 1.5 ms per pass); 5 at 1 / 2 / 3 passes: 78.9 /
+// 78.5 / 78.7; none 81.1.  Node visits -6.6% at N = 5, 2 passes.
+#ifndef DT_TREELET_N
+#define DT_TREELET_N 5                 // treelet leaves (DP over 2^N - 1 subsets)
+#endif
+constexpr float kTreeletCi = 1.2f, kTreeletCt = 1.0f;
+
+DT_D float box_area3(float3 lo, float3 hi) {
+  const float dx = hi.x - lo.x, dy = hi.y - lo.y, dz = hi.z - lo.z;
+  return dx * dy + dy * dz + dz * dx;
+}
+
+__global__ void k_treelet(int2* children, int* parent_int, int* parent_leaf, int* flags, float4* nodebox,
+                          const float4* __restrict__ leafbox, float* cost, int2* ranges, float* narea, int n) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    int p = parent_leaf[j];
+    while (p >= 0) {
+      __threadfence();
+      if (atomicAdd(flags + p, 1) == 0) break;   // the second arrival processes p
+      __threadfence();
+      const int2 ch = __ldcg(children + p);
+      auto cnt_of = [&](int r) { if (r < 0) return 1; const int2 g = __ldcg(ranges + r); return g.y - g.x + 1; };
+      auto cost_of = [&](int r) {
+        if (r < 0) { float3 lo, hi; load_box(leafbox, nodebox, r, lo, hi); return box_area3(lo, hi) * kTreeletCt; }
+        return __ldcg(cost + r);
+      };
+      const int cnt = cnt_of(ch.x) + cnt_of(ch.y);
+      float3 plo, phi;
+      load_box(leafbox, nodebox, p, plo, phi);
+      const float ap = box_area3(plo, phi);
+      float cp = ap * kTreeletCi + cost_of(ch.x) + cost_of(ch.y);
+      if (cnt >= DT_TREELET_N) {
+        int L[DT_TREELET_N], I[DT_TREELET_N - 1], nl = 2, ni = 1;
+        L[0] = ch.x; L[1] = ch.y; I[0] = p;
+        while (nl < DT_TREELET_N) {                       // grow: open the treelet leaf of largest area
+          int bi = -1;
+          float ba = -1.f;
+          for (int i = 0; i < nl; ++i) {
+            if (L[i] < 0) continue;
+            const float ar = __ldcg(narea + L[i]);    // processed below p: its area is recorded
+            if (ar > ba) { ba = ar; bi = i; }
+          }
+          if (bi < 0) break;
+          const int x = L[bi];
+          const int2 cx = __ldcg(children + x);
+          I[ni++] = x;
+          L[bi] = cx.x;
+          L[nl++] = cx.y;
+        }
+        float3 lo[DT_TREELET_N], hi[DT_TREELET_N];
+        float cl[DT_TREELET_N];
+        int cn[DT_TREELET_N];
+        for (int i = 0; i < nl; ++i) {
+          load_box(leafbox, nodebox, L[i], lo[i], hi[i]);
+          cl[i] = cost_of(L[i]);
+          cn[i] = cnt_of(L[i]);
+        }
+        // (nl == DT_TREELET_N here: a subtree of >= N triangles always grows to N leaves.)  Every
+        // subset index is a compile-time constant once the loops unroll, so the DP lives in
+        // registers.
+        constexpr int NS = 1 << DT_TREELET_N, full = NS - 1;
+        float copt[NS];
+        unsigned char part[NS];
+#pragma unroll
+        for (int S = 1; S < NS; ++S) {
+          if ((S & (S - 1)) == 0) {
+#pragma unroll
+            for (int i = 0; i < DT_TREELET_N; ++i)
+              if (S == (1 << i)) copt[S] = cl[i];
+            part[S] = 0;
+            continue;
+          }
+          float3 ulo = f3(kInf, kInf, kInf), uhi = f3(-kInf, -kInf, -kInf);
+#pragma unroll
+          for (int i = 0; i < DT_TREELET_N; ++i)
+            if (S >> i & 1) { ulo = fminf3(ulo, lo[i]); uhi = fmaxf3(uhi, hi[i]); }
+          const int low = S & -S;
+          float best = kInf;
+          int bp = low;
+#pragma unroll
+          for (int P = 1; P < S; ++P) {
+            if ((P & S) != P || !(P & low)) continue;
+            const float c = copt[P] + copt[S ^ P];
+            if (c < best) { best = c; bp = P; }
+          }
+          copt[S] = box_area3(ulo, uhi) * kTreeletCi + best;
+          part[S] = (unsigned char)bp;
+        }
+        if (copt[full] < cp * 0.9999f) {       // rewire the treelet's internal nodes
+          int st[DT_TREELET_N], sn[DT_TREELET_N], sp = 0, pool = 1;
+          st[sp] = full; sn[sp++] = p;
+          while (sp > 0) {
+            const int S = st[--sp], nd = sn[sp];
+            const int P = part[S], Q = S ^ P;
+            int kid[2];
+            const int sub[2] = {P, Q};
+            for (int q = 0; q < 2; ++q) {
+              if ((sub[q] & (sub[q] - 1)) == 0) {
+                kid[q] = L[__ffs(sub[q]) - 1];
+              } else {
+                kid[q] = I[pool++];
+                st[sp] = sub[q]; sn[sp++] = kid[q];
+              }
+              if (kid[q] < 0) parent_leaf[~kid[q]] = nd; else parent_int[kid[q]] = nd;
+            }
+            __stcg(children + nd, make_int2(kid[0], kid[1]));
+            float3 ulo = f3(kInf, kInf, kInf), uhi = f3(-kInf, -kInf, -kInf);
+            int c = 0;
+            for (int i = 0; i < nl; ++i)
+              if (S >> i & 1) { ulo = fminf3(ulo, lo[i]); uhi = fmaxf3(uhi, hi[i]); c += cn[i]; }
+            __stcg(nodebox + 2 * (size_t)nd, f4(ulo, 0.f));
+            __stcg(nodebox + 2 * (size_t)nd + 1, f4(uhi, 0.f));
+            __stcg(cost + nd, copt[S]);
+            __stcg(ranges + nd, make_int2(0, c - 1));
+            __stcg(narea + nd, box_area3(ulo, uhi));
+          }
+          cp = copt[full];
+        }
+      }
+      __stcg(cost + p, cp);
+      __stcg(ranges + p, make_int2(0, cnt - 1));
+      __stcg(narea + p, ap);
+      p = __ldcg(parent_int + p);
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- 4-wide collapse
 // The binary Karras tree is collapsed into a 4-wide BVH by keeping the binary nodes at even
 // depth: a wide node's children are its binary grandchildren (a binary child that is a leaf,
@@ -818,6 +956,16 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
   }
   k_refit<<<gf, T, 0, st>>>(c->V, c->F, sv, nf, c->children, c->parent_int, c->parent_leaf, c->rflags, c->leafbox,
                             c->nodebox);
+  if (nf >= DT_TREELET_N) {                             // treelet restructuring (cost in key scratch)
+    float* tcost = reinterpret_cast<float*>(c->keys);
+    float* narea = tcost + nf;                          // (keys hold 6 nf words)
+    for (int pass = 0; pass < c->treelet_passes; ++pass) {
+      cudaMemsetAsync(c->rflags, 0, (size_t)(nf - 1) * sizeof(int), st);
+      k_treelet<<<gf, T, 0, st>>>(c->children, c->parent_int, c->parent_leaf, c->rflags, c->nodebox, c->leafbox, tcost,
+                                  c->ranges, narea, nf);
+      ++launches;
+    }
+  }
   // collapse to the quantised 4-wide BVH
   if (nf > 1) {                                         // surface-area greedy, top down
     if (!c->wqueue || c->wqueue_cap < nf) {

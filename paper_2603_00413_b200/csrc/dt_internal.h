@@ -156,6 +156,7 @@ struct dt_ctx {
   float* gior = nullptr;
   size_t gsig_cap = 0;
   int leaf_max = 1;           // triangles per wide-BVH leaf (r01 sweep of 1..4: 1 is fastest)
+  int treelet_passes = 2;     // treelet restructuring passes per build (dt_set_bvh_quality)
   int grid_cache[dt::kGridCount] = {};    // persistent-kernel grid sizes of this device (occupancy x SMs), by kGrid*
   // profiling (dt_set_profiling / dt_get_profile)
   bool prof = false;

@@ -172,6 +172,10 @@ class Tracer:
             raise N.DiffTransError(f"{N.STATUS.get(rc, rc)}: {msg}", rc)
 
     # ------------------------------------------------------------------ path
+    def set_bvh_quality(self, treelet_passes: int):
+        """Treelet-restructuring passes of the following builds (0..4, default 2)."""
+        self._check(self._lib.dt_set_bvh_quality(self.h, int(treelet_passes)), self.h)
+
     def build_bvh(self, V: torch.Tensor, F: torch.Tensor, stream=None):
         assert V.is_cuda and V.dtype == torch.float32 and V.is_contiguous() and V.shape[-1] == 3
         assert F.is_cuda and F.dtype == torch.int32 and F.is_contiguous() and F.shape[-1] == 3

@@ -509,3 +509,26 @@ def test_degenerate_method_cases(tracer):
     V, F = S.icosphere(2)
     sc = T.scene(V, F, T.one_view(20, 16, (0.0, 0.0, 0.3), fov_deg=70.0, target=(1.0, 0.2, 0.3)), env=T.lobe_env(), D=4)
     parity_case(tracer, sc, np.arange(sc.n_pixels), "camera-inside")
+
+
+@pytest.mark.parametrize("quality", [0, 1, 4])
+def test_bvh_quality_levels_same_hits(tracer, quality):
+    """dt_set_bvh_quality: every treelet-restructuring level gives a valid tree (boxes contain
+    their children, every face reached once) and closest hits bit-identical to brute force."""
+    from paper_2603_00413_b200.tracer import DeviceScene
+    sc = S.config_c2()
+    ds = DeviceScene(sc, torch.device("cuda:0"))
+    tracer.set_bvh_quality(quality)
+    try:
+        tracer.build_bvh(ds.V, ds.F)
+        chk = tracer.bvh_check()
+        assert chk["bad_boxes"] == 0 and chk["leaves"] == sc.F.shape[0] and chk["distinct_faces"] == sc.F.shape[0]
+        g = torch.Generator(device="cuda:0")
+        g.manual_seed(quality + 5)
+        rays = torch.randn(20000, 6, device="cuda:0", generator=g)
+        rays[:, :3] *= 0.4
+        f1, t1 = tracer.closest_hit(rays, 1e-4, brute_force=False)
+        f2, t2 = tracer.closest_hit(rays, 1e-4, brute_force=True)
+        assert torch.equal(f1, f2) and torch.equal(t1, t2)
+    finally:
+        tracer.set_bvh_quality(2)
