@@ -359,7 +359,10 @@ __global__ void k_refit(const float4* __restrict__ V, const int* __restrict__ F,
 #ifndef DT_TREELET_N
 #define DT_TREELET_N 5                 // treelet leaves (DP over 2^N - 1 subsets)
 #endif
-constexpr float kTreeletCi = 1.2f, kTreeletCt = 1.0f;
+#ifndef DT_TREELET_CI
+#define DT_TREELET_CI 1.2f
+#endif
+constexpr float kTreeletCi = DT_TREELET_CI, kTreeletCt = 1.0f;
 
 DT_D float box_area3(float3 lo, float3 hi) {
   const float dx = hi.x - lo.x, dy = hi.y - lo.y, dz = hi.z - lo.z;
