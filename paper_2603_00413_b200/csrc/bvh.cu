@@ -369,7 +369,10 @@ DT_D float box_area3(float3 lo, float3 hi) {
   return dx * dy + dy * dz + dz * dx;
 }
 
-__global__ void k_treelet(int2* children, int* parent_int, int* parent_leaf, int* flags, float4* nodebox,
+#ifndef DT_TREELET_MINB
+#define DT_TREELET_MINB 3
+#endif
+__global__ void __launch_bounds__(256, DT_TREELET_MINB) k_treelet(int2* children, int* parent_int, int* parent_leaf, int* flags, float4* nodebox,
                           const float4* __restrict__ leafbox, float* cost, int2* ranges, float* narea, int n) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     int p = parent_leaf[j];
