@@ -42,10 +42,10 @@ constexpr int kBwdThreads = 128;
 #else
 #define DT_TRAV_LB __launch_bounds__(kTraceThreads)
 #endif
-// camera-ray kernel: capped at 64 registers (8 blocks / SM; the float64 camera ray and env
-// lookup need ~64 without spilling)
+// camera-ray kernel: 12 blocks / SM (r02 sweep, C3 trace0 ms: 8 / 9 / 10 / 12 blocks: 8.20 /
+// 8.13 / 8.08 / 7.99; occupancy beats the spills of the float64 camera ray and env lookup)
 #ifndef DT_PRIM_MINB
-#define DT_PRIM_MINB 8
+#define DT_PRIM_MINB 12
 #endif
 #define DT_PRIM_LB __launch_bounds__(kTraceThreads, DT_PRIM_MINB)
 #if DT_SHADE_MINB > 1
