@@ -47,7 +47,10 @@ constexpr int kBwdThreads = 128;
 #ifndef DT_PRIM_MINB
 #define DT_PRIM_MINB 12
 #endif
-#define DT_PRIM_LB __launch_bounds__(kTraceThreads, DT_PRIM_MINB)
+#ifndef DT_PRIM_VOL_MINB
+#define DT_PRIM_VOL_MINB 8             // the volumetric-env variant (32-sample env integral) spills below 64
+#endif
+#define DT_PRIM_LB __launch_bounds__(kTraceThreads, VOL ? DT_PRIM_VOL_MINB : DT_PRIM_MINB)
 #if DT_SHADE_MINB > 1
 #define DT_SHADE_LB __launch_bounds__(kTraceThreads, DT_SHADE_MINB)
 #else
