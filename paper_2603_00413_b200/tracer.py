@@ -100,7 +100,10 @@ class DeviceScene:
             c.tile, c.shard_rank, c.shard_count = sh.tile, sh.rank, sh.count
             if sh.tile_ids is not None:
                 assert sh.tile_ids.is_cuda and sh.tile_ids.dtype == torch.int32 and sh.tile_ids.is_contiguous()
-                c.tile_ids, c.n_tiles = _ptr(sh.tile_ids), sh.tile_ids.numel()
+                ids = sh.tile_ids
+                if ids.numel() == 0:         # an empty list is not "the cyclic rule" (NULL)
+                    self._empty_tiles = ids = torch.zeros(1, dtype=torch.int32, device=ids.device)
+                c.tile_ids, c.n_tiles = _ptr(ids), sh.tile_ids.numel()
             c.n_rays = sh.n_rays(self.n_views, self.width, self.height)
             return c
         if pixel_ids is not None:

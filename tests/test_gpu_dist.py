@@ -142,3 +142,20 @@ def test_tile_shard_equals_pixel_list():
             gB = tr.trace_backward(g)
             assert rel_l2(gB[0].cpu().numpy(), gA[0].cpu().numpy()) < 1e-5
             assert abs(float(gB[1]) - float(gA[1])) <= 1e-5 * abs(float(gA[1])) + 1e-7
+
+
+def test_empty_tile_shard():
+    """A rank with no tiles (more ranks than tiles, or an empty LPT list) traces zero rays and
+    its backward contributes zero gradients."""
+    from paper_2603_00413_b200 import scenes as S
+    from paper_2603_00413_b200.tracer import DeviceScene, TileShard, Tracer
+    dev = torch.device("cuda:0")
+    sc = S.config_c2(n_views=1, res=64)               # 4 tiles of 32 x 32
+    ds = DeviceScene(sc, dev)
+    tr = Tracer(dev)
+    tr.build_bvh(ds.V, ds.F)
+    for sh in (TileShard(32, 5, 8), TileShard(32, tile_ids=torch.zeros(0, dtype=torch.int32, device=dev))):
+        out = tr.trace_forward(ds, sh)
+        assert out.rgb.shape == (0, 3)
+        gV, gI, gS = tr.trace_backward(torch.zeros((0, 3), device=dev))
+        assert float(gV.abs().sum()) == 0.0 and float(gI.abs().sum()) == 0.0
