@@ -85,28 +85,43 @@ DT_D int fetch_work(int* counter, int chunk = 32) {
   return __shfl_sync(~0u, base, 0);
 }
 
-// Hit-first lane order over a warp's window of 64 records (2 rounds of 32): records of class
-// 0 (a traced hit: interface path) first, then class 1 (a miss: environment path), then class 2
-// (nothing to do).  The per-record code has two long, disjoint paths, so warps that mix them
-// run both at half width; sorted, round 0 and round 1 are (nearly) uniform.  cA / cB: class of
-// window offsets lane and 32 + lane; returns the offsets this lane processes in the two rounds.
-// slot: the warp's 64 bytes of shared memory.
-DT_D void hit_first_order(int cA, int cB, unsigned char* slot, int& r0, int& r1) {
+
+// Hit-first lane order over a warp's window of 32 R records (R rounds of 32, R = DT_WIN_ROUNDS):
+// records of class 0 (a traced hit: interface path) first, then class 1 (a miss: environment
+// path), then class 2 (nothing to do).  The per-record code has two long, disjoint paths, so
+// warps that mix them run both at half width; sorted, each round is (nearly) uniform.
+// c[h]: class of window offset 32 h + lane; ord[h]: the offset this lane processes in round h.
+// slot: the warp's 32 R bytes of shared memory.  R = 2 measured best (R = 4: C4 -0.8 %, C3 +1.6 %,
+// C4H +1.5 % ms/step; R = 1: C3 +9.6 %; profiles/r02_traversal_sweep.txt).
+#ifndef DT_WIN_ROUNDS
+#define DT_WIN_ROUNDS 2
+#endif
+template <int R>
+DT_D void hit_first_order_r(const int (&c)[R], unsigned char* slot, int (&ord)[R]) {
   const unsigned lt = lanemask_lt();
-  const unsigned a0 = __ballot_sync(~0u, cA == 0), b0 = __ballot_sync(~0u, cB == 0);
-  const unsigned a1 = __ballot_sync(~0u, cA == 1), b1 = __ballot_sync(~0u, cB == 1);
-  const unsigned a2 = __ballot_sync(~0u, cA == 2), b2 = __ballot_sync(~0u, cB == 2);
-  const int n0 = __popc(a0) + __popc(b0), n1 = __popc(a1) + __popc(b1);
-  const int rA = cA == 0 ? __popc(a0 & lt) : cA == 1 ? n0 + __popc(a1 & lt) : n0 + n1 + __popc(a2 & lt);
-  const int rB = cB == 0 ? __popc(a0) + __popc(b0 & lt)
-               : cB == 1 ? n0 + __popc(a1) + __popc(b1 & lt)
-                         : n0 + n1 + __popc(a2) + __popc(b2 & lt);
-  DT_CHECK(rA >= 0 && rA < 64 && rB >= 0 && rB < 64);
-  slot[rA] = (unsigned char)lane_id();
-  slot[rB] = (unsigned char)(32 + lane_id());
+  unsigned b[3][R];
+  int n[3] = {0, 0, 0};
+#pragma unroll
+  for (int h = 0; h < R; ++h)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      b[q][h] = __ballot_sync(~0u, c[h] == q);
+      n[q] += __popc(b[q][h]);
+    }
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int q = c[h];
+    int r = q == 0 ? 0 : q == 1 ? n[0] : n[0] + n[1];
+#pragma unroll
+    for (int g = 0; g < R; ++g)
+      if (g < h) r += __popc(q == 0 ? b[0][g] : q == 1 ? b[1][g] : b[2][g]);
+    r += __popc((q == 0 ? b[0][h] : q == 1 ? b[1][h] : b[2][h]) & lt);
+    DT_CHECK(r >= 0 && r < 32 * R);
+    slot[r] = (unsigned char)(32 * h + lane_id());
+  }
   __syncwarp();
-  r0 = slot[lane_id()];
-  r1 = slot[32 + lane_id()];
+#pragma unroll
+  for (int h = 0; h < R; ++h) ord[h] = slot[32 * h + lane_id()];
   __syncwarp();
 }
 
@@ -383,22 +398,28 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
 #endif
   constexpr bool kDyn = ABS != 0 || VOL || DT_SHADE_DYN;
   int* const ctr = a.lvl + LV_WORK_SHADE + k;
-  __shared__ unsigned char sslot[kTraceThreads * 2];
-  int64_t wbase = kDyn ? (int64_t)fetch_work(ctr, 64) : (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 2;
-  int round = 0, ord0 = 0, ord1 = 0, next = 0;
+  constexpr int RW = DT_WIN_ROUNDS, WIN = 32 * RW;
+  __shared__ unsigned char sslot[kTraceThreads * RW];
+  int64_t wbase = kDyn ? (int64_t)fetch_work(ctr, WIN) : (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * RW;
+  int round = 0, next = 0;
+  int ord[RW];
   while (wbase < n) {
-    if (round == 0 && kDyn && lane_id() == 0) next = atomicAdd(ctr, 64);
+    if (round == 0 && kDyn && lane_id() == 0) next = atomicAdd(ctr, WIN);
     if (round == 0) {
-      int c[2];
+      int c[RW];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < RW; ++h) {
         const int64_t it = wbase + 32 * h + lane_id();
         c[h] = 2;
         if (it < n) c[h] = __float_as_int(a.r.hit[k == 0 ? a.cap - 1 - it : off + it].x) >= 0 ? 0 : 1;
       }
-      hit_first_order(c[0], c[1], sslot + 2 * (threadIdx.x & ~31), ord0, ord1);
+      hit_first_order_r<RW>(c, sslot + RW * (threadIdx.x & ~31), ord);
     }
-    const int64_t item = wbase + (round == 0 ? ord0 : ord1);
+    int my = ord[0];
+#pragma unroll
+    for (int h = 1; h < RW; ++h)
+      if (round == h) my = ord[h];
+    const int64_t item = wbase + my;
     const bool valid = item < n;
     const int64_t idx = k == 0 ? a.cap - 1 - item : off + item;
     double3 o = d3(0, 0, 0), d = d3(0, 0, 1);
@@ -420,11 +441,9 @@ DT_D void shade_level_body(const FwdLaunch& a, int k, int max_depth) {
     if (valid && k > 0 && a.segc) atomicAdd(a.segc + ray, 1);
     shade_and_spawn<ABS, VOL>(a, ior, child_off, lim, k, max_depth, valid, idx, o, d, ray, pos, thr, w, face, i0, i1,
                               i2);
-    if (round == 0) {
-      round = 1;
-    } else {
+    if (++round == RW) {
       round = 0;
-      wbase = kDyn ? (int64_t)__shfl_sync(~0u, next, 0) : wbase + 2 * stride;
+      wbase = kDyn ? (int64_t)__shfl_sync(~0u, next, 0) : wbase + RW * stride;
     }
   }
 }
@@ -574,20 +593,21 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
   const int64_t off = k == 0 ? 0 : level_base(a.lvl, k);
   float gior = 0.0f;
   float3 gsc = f3(0, 0, 0);
-  __shared__ unsigned char sslot[kBwdThreads * 2];
+  constexpr int RW = DT_WIN_ROUNDS, WIN = 32 * RW;
+  __shared__ unsigned char sslot[kBwdThreads * RW];
   // 64-record windows taken from the level's counter (the next window's atomic in flight while
   // this one is replayed): window costs vary with the hit / miss mix, so a static stride leaves
   // a tail
   int* const ctr = a.lvl + LV_WORK_BWD + k;
-  int64_t wb = fetch_work(ctr, 64);
+  int64_t wb = fetch_work(ctr, WIN);
   int nx = 0;
-  if (lane_id() == 0) nx = atomicAdd(ctr, 64);
+  if (lane_id() == 0) nx = atomicAdd(ctr, WIN);
   while (wb < n) {
-  int o0, o1;
+  int ord[RW];
   {
-    int c[2];
+    int c[RW];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < RW; ++h) {
       const int64_t it = wb + 32 * h + lane_id();
       c[h] = 2;
       if (it < n) {
@@ -595,10 +615,15 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
         c[h] = (f & RF_MISS) ? 1 : ((f & RF_CAPPED) && s.cap_policy == 0 && !VOL) ? 2 : 0;
       }
     }
-    hit_first_order(c[0], c[1], sslot + 2 * (threadIdx.x & ~31), o0, o1);
+    hit_first_order_r<RW>(c, sslot + RW * (threadIdx.x & ~31), ord);
   }
-  for (int round = 0; round < 2; ++round) {
-    const int64_t item = wb + (round == 0 ? o0 : o1);
+#pragma unroll 1
+  for (int round = 0; round < RW; ++round) {
+    int my = ord[0];
+#pragma unroll
+    for (int h = 1; h < RW; ++h)
+      if (round == h) my = ord[h];
+    const int64_t item = wb + my;
     const bool valid = item < n;
     int64_t idx = 0;
     float3 go = f3(0, 0, 0), gd = go, gx = go, gS = go, gNk[3];
@@ -724,7 +749,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
     }
   }
   wb = __shfl_sync(~0u, nx, 0);
-  if (lane_id() == 0) nx = atomicAdd(ctr, 64);
+  if (lane_id() == 0) nx = atomicAdd(ctr, WIN);
   }
   // warp reductions of the scalar adjoints
   for (int o = 16; o > 0; o >>= 1) {
