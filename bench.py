@@ -185,6 +185,16 @@ def algorithmic_bytes(stats, prof, steps: int):
 OPS_PER_VISIT, OPS_PER_TEST = 130, 37
 
 
+def walk_peaks():
+    """Scattered float4 gather / atomic rates (tools/microbench/l2_gather.cu, measured on the
+    GPU box): the texture walks' roofline peaks; None if the measurement is absent."""
+    f = os.path.join(ROOT, "profiles", "r02_l2_gather.json")
+    try:
+        return json.load(open(f)), "measured (profiles/r02_l2_gather.json)"
+    except Exception:
+        return None
+
+
 def alu_peak(sm_count: int):
     """SIMT lane-operation issue peak (B200_PROFILING.md / B300_MICROARCH.md unit counts): 4
     schedulers x 32 lanes per SM issue one operation per clock at the max SM clock."""
@@ -475,6 +485,36 @@ def run_ours(args, rank, world, local_rank):
                     "peak_source": apk_src, "unit": "Tlane-op/s", "frac": round(a_ops / apk, 4),
                     "ops_per_node_visit": OPS_PER_VISIT, "ops_per_triangle_test": OPS_PER_TEST,
                     "ops_per_launch": int(ops_launch)}
+    elif cls == "bwd" and prof.get("walk_cells_bwd", 0) > 0 and walk_peaks() is not None:
+        # texture walks (sigma grid C4 / hash texture C4H): the backward is bound by the L2
+        # serving its corner fetches and float4 adjoint atomics, counted on the device per cell
+        # visit (grid: 4 x-pair loads; hash: 8 entry loads; both: 8 atomics).  Peak: the time
+        # those operations take at the L2's measured ceilings for the same operations
+        # (coalesced float4 loads / REDs, tools/microbench/l2_gather.cu); the same at the
+        # measured rates of fully scattered accesses (the walks sit in between: neighbouring
+        # rays and samples share cells) and the record-bytes view are kept alongside
+        wp, wp_src = walk_peaks()
+        hashed = sc.absorption.kind == 2
+        cells = prof["walk_cells_bwd"] / max(launches, 1)
+        g_ops, r_ops = cells * (8 if hashed else 4), cells * 8
+        t = ms_per_launch / 1e3
+        achieved = (g_ops + r_ops) / t / 1e9
+
+        def peak_of(g, r):
+            return (g_ops + r_ops) / (g_ops / (g * 1e9) + r_ops / (r * 1e9)) / 1e9
+        pk = peak_of(wp["gather_coalesced_gops"], wp["red_coalesced_gops"])
+        size = "128mb" if hashed else "8mb"
+        pk_s = peak_of(wp[f"gather_{size}_gops"], wp[f"red_{size}_gops"])
+        roofline = {"bound": "l2", "kernel": kname + ("_hash" if hashed else "_grid"), "achieved": round(achieved, 2),
+                    "peak": round(pk, 2), "peak_source": wp_src + ": coalesced float4 load / RED ceilings",
+                    "unit": "Gop/s", "frac": round(achieved / pk, 4),
+                    "ops": "L2 accesses of the walk: corner fetches + float4 adjoint atomics",
+                    "cell_visits_per_launch": int(cells), "gathers_per_launch": int(g_ops),
+                    "atomics_per_launch": int(r_ops), "gather_gops": round(g_ops / t / 1e9, 2),
+                    "atomic_gops": round(r_ops / t / 1e9, 2),
+                    "scattered_view": {"peak": round(pk_s, 2), "frac": round(achieved / pk_s, 4),
+                                       "table": size, "source": wp_src + ": hashed-index float4 load / RED rates"},
+                    "hbm_view": hbm_view}
     else:
         roofline = {"bound": "hbm", "kernel": kname, **{k: v for k, v in hbm_view.items() if k != "bytes_per_launch"},
                     "bytes_per_launch": int(bytes_per_launch)}
@@ -513,7 +553,9 @@ def run_ours(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "phase_ms_per_step": {k: round(v / args.steps, 3) for k, v in ph.items()},
         "counters_per_step": {"node_visits": prof["node_visits"] // args.steps,
-                              "tri_tests": prof["tri_tests"] // args.steps},
+                              "tri_tests": prof["tri_tests"] // args.steps,
+                              "walk_cells_fwd": prof["walk_cells_fwd"] // args.steps,
+                              "walk_cells_bwd": prof["walk_cells_bwd"] // args.steps},
     }
     return line
 

@@ -240,6 +240,10 @@ typedef struct {
   int64_t node_visits_primary;     /* the part of node_visits made by camera rays (depth 0)  */
   int64_t tri_tests_primary;       /* the part of tri_tests made by camera rays (depth 0)    */
   int64_t segments;                /* traced segments of all forwards since the reset        */
+  int64_t walk_cells_fwd;          /* cell visits of the sigma-grid / hash-texture walks of   *
+                                    * the forward (each: 8 corner fetches)                    */
+  int64_t walk_cells_bwd;          /* the same of the backward (each: 8 corner fetches and   *
+                                    * 8 float4 adjoint atomics)                               */
 } dt_profile;
 /* ---------------------------------------------------------------------------------------
  * The optimisation step around the tracer (PAPER P:176-194, P:439-443,

@@ -1051,6 +1051,7 @@ DevScene scene_from_ctx(const dt_ctx* c) {
   s.tris = c->tris;
   s.root = 0;
   s.scal = c->scal;
+  s.wcount = c->counters + 5;
   return s;
 }
 

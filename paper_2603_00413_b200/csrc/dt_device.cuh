@@ -76,6 +76,10 @@ struct DevScene {
   int far_field;
   // options
   int max_depth, cap_policy;
+  // walk counters (the texture walks' roofline, bench.py): [0] cell visits of the forward
+  // optical-depth walks, [1] cell visits of the backward walks (each: 8 corner fetches; in the
+  // backward also 8 float4 atomics)
+  unsigned long long* wcount;
 };
 
 // ----------------------------------------------------------------------------- camera (R19)
@@ -586,6 +590,12 @@ DT_D GridMap grid_map(const DevScene& s) {
 
 DT_D void corner_weights(const float f[3], float w[8]);
 
+// one 64-bit atomic per warp: the warp's cell visits of one walk call (all 32 lanes call it)
+DT_D void flush_walk_count(unsigned long long* c, int cells) {
+  const unsigned tot = __reduce_add_sync(~0u, (unsigned)cells);
+  if (c && lane_id() == 0 && tot) atomicAdd(c, (unsigned long long)tot);
+}
+
 // ---- hash texture (ABS = DT_ABS_HASH, R29): mu(p) = sum_l trilinear lookup of level l
 // Table entry of corner (x, y, z) at level l (N cells per axis, T = 2^hlog2 entries).
 DT_D uint32_t hash_index(const DevScene& s, int l, int N, int x, int y, int z) {
@@ -677,6 +687,7 @@ template <int G, int ABS>
 DT_D float3 group_optical_depth(const DevScene& s, const GridMap& m, float3 o, float3 x, bool active) {
   const float3 dx = x - o;
   float3 S = f3(0, 0, 0);
+  int cells = 0;
   if (ABS == 2 && active) {            // hash texture: level by level, corners reused per cell run
     const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
     const size_t T = (size_t)1 << s.hlog2;
@@ -706,6 +717,7 @@ DT_D float3 group_optical_depth(const DevScene& s, const GridMap& m, float3 o, f
           for (int k = 0; k < 8; ++k)
             c[k] = f3(__ldg(tab + hash_index(s, l, N, i[0] + (k & 1), i[1] + ((k >> 1) & 1), i[2] + (k >> 2))));
           cur[0] = i[0]; cur[1] = i[1]; cur[2] = i[2];
+          ++cells;
         }
         corner_weights(f, w);
 #pragma unroll
@@ -737,6 +749,7 @@ DT_D float3 group_optical_depth(const DevScene& s, const GridMap& m, float3 o, f
         }
         grid_corners(s, m, base, c);   // consumed at the run's end: latency behind the run
         cur = base;
+        ++cells;
       }
       corner_weights(f, w);
 #pragma unroll
@@ -753,6 +766,7 @@ DT_D float3 group_optical_depth(const DevScene& s, const GridMap& m, float3 o, f
     S.y += __shfl_xor_sync(~0u, S.y, off);
     S.z += __shfl_xor_sync(~0u, S.z, off);
   }
+  flush_walk_count(s.wcount, cells);
   return S * (length(dx) / (float)m.N);
 }
 
@@ -769,6 +783,7 @@ DT_D void group_transmittance_backward(const DevScene& s, const GridMap& m, floa
   const float3 gSs = gS * sc;
   float gl = 0.f;
   float3 gsum = f3(0, 0, 0), gtsum = f3(0, 0, 0);
+  int cells = 0;
   if (ABS == 2 && active) {            // hash texture: level by level, merged per cell run
     const int P = (m.N + G - 1) / G, j0 = (lane_id() % G) * P, j1 = min(j0 + P, m.N);
     const size_t T = (size_t)1 << s.hlog2;
@@ -800,6 +815,7 @@ DT_D void group_transmittance_backward(const DevScene& s, const GridMap& m, floa
 #pragma unroll
           for (int k = 0; k < 8; ++k) gk[k] = dot(gS, f3(__ldg(s.sigma + lt + e[k])));
           cur[0] = i[0]; cur[1] = i[1]; cur[2] = i[2];
+          ++cells;
         }
         corner_weights(f, w);
         float gv = 0.f;
@@ -853,6 +869,7 @@ DT_D void group_transmittance_backward(const DevScene& s, const GridMap& m, floa
 #pragma unroll
         for (int k = 0; k < 8; ++k) gk[k] = dot(gS, c[k]);
         cur = base;
+        ++cells;
       }
       corner_weights(f, w);
       float gv = 0.f;
@@ -892,6 +909,7 @@ DT_D void group_transmittance_backward(const DevScene& s, const GridMap& m, floa
     gtsum.y += __shfl_xor_sync(~0u, gtsum.y, off);
     gtsum.z += __shfl_xor_sync(~0u, gtsum.z, off);
   }
+  flush_walk_count(s.wcount ? s.wcount + 1 : nullptr, cells);
   // grad_p mu = grad_g mu * scl; quadrature weight sc; x_j = o (1 - t_j) + x t_j
   const float3 k3 = m.scl * sc;
   const float3 gxt = f3(gtsum.x * k3.x, gtsum.y * k3.y, gtsum.z * k3.z);

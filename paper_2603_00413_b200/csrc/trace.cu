@@ -378,7 +378,7 @@ __global__ void DT_PRIM_LB k_trace_primary(FwdLaunch a, int max_depth) {
 // event and spawns the children into level k+1 (warp-ballot compaction).  Level 0 needs
 // the final level-0 count, so it always runs after the traversal pass.
 // Each warp takes a window of 64 records and shades them in two rounds of 32 in hit-first
-// lane order (hit_first_order).  Work distribution: warps take 64-record windows from the
+// lane order (hit_first_order_r).  Work distribution: warps take 64-record windows from the
 // level's counter, the next window's atomic in flight while the current one is shaded -- a
 // window's cost varies with its hit / miss mix (and with the interior walks of a sigma grid,
 // a hash texture or a volumetric env), so a static stride left a tail (r02: constant-sigma C3

@@ -532,3 +532,26 @@ def test_bvh_quality_levels_same_hits(tracer, quality):
         assert torch.equal(f1, f2) and torch.equal(t1, t2)
     finally:
         tracer.set_bvh_quality(2)
+
+
+def test_walk_counters(tracer):
+    """Device walk counters behind the texture walks' roofline (bench.py): zero for a constant
+    sigma; for a sigma grid the backward replays the forward's walks with the same lane groups,
+    so both count the same cell visits, at most nsamp per traced segment."""
+    from paper_2603_00413_b200.tracer import DeviceScene
+    V, F = S.icosphere(2)
+    cams = T.one_view(40, 28, (0.6, -0.4, 2.6), fov_deg=55)
+    for ab, walks in ((None, False), (T.small_sigma_grid(V, 8), True)):
+        kw = {} if ab is None else {"absorption": ab}
+        sc = T.scene(V, F, cams, env=T.small_grid_env(far_field=1), D=4, **kw)
+        ds = DeviceScene(sc, torch.device("cuda:0"))
+        tracer.build_bvh(ds.V, ds.F)
+        tracer.profile(reset=True)
+        tracer.trace_forward(ds, None)
+        tracer.trace_backward(torch.ones((sc.n_pixels, 3), dtype=torch.float32, device="cuda:0"))
+        torch.cuda.synchronize()
+        p = tracer.profile(reset=True)
+        if not walks:
+            assert p["walk_cells_fwd"] == 0 and p["walk_cells_bwd"] == 0, p
+        else:
+            assert 0 < p["walk_cells_fwd"] == p["walk_cells_bwd"] <= p["segments"] * sc.absorption.n_samples, p
