@@ -506,7 +506,7 @@ DT_D bool wide_entry(const int2* __restrict__ ranges, int e, int leaf_max) {
 
 // Quantise and write wide node w: its entries ent[0..ne) (binary refs; internal entries carry
 // their own wide index in wref), boxes padded outward so the slab test stays conservative.
-DT_D void write_wide_node(int i, const int* ent, const int* wref, int ne, unsigned w, int wd, double pad,
+DT_D void write_wide_node(int i, const int ent[4], const int wref[4], int ne, unsigned w, int wd, double pad,
                           const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
                           const int2* __restrict__ ranges, int leaf_max, uint4* __restrict__ wnodes,
                           float4* __restrict__ wbox, int* __restrict__ wdepth) {
@@ -566,109 +566,6 @@ DT_D void write_wide_node(int i, const int* ent, const int* wref, int ne, unsign
   wdepth[w] = wd;
 }
 
-#if DT_BVH_WIDE == 8
-// The 8-wide node (layout: dt_device.cuh, node8_hits): the same conservative quantisation, and
-// the children placed in slots by octant -- slot bit a set means "toward -a from the node's
-// centre" -- greedily by the largest score sum_a (+-1) (c_a - centre_a), so that rays of
-// direction-sign octant oct meet them roughly front to back in the order slot ^ (~oct & 7).
-DT_D void write_wide_node8(int i, const int* ent, const int* wref, int ne, unsigned w, int wd, double pad,
-                           const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
-                           const int2* __restrict__ ranges, int leaf_max, uint4* __restrict__ wnodes,
-                           float4* __restrict__ wbox, int* __restrict__ wdepth) {
-  float3 ulo, uhi;
-  load_box(leafbox, nodebox, i, ulo, uhi);
-  double P[3] = {(double)__double2float_rd((double)ulo.x - pad), (double)__double2float_rd((double)ulo.y - pad),
-                 (double)__double2float_rd((double)ulo.z - pad)};
-  double hiU[3] = {(double)uhi.x + pad, (double)uhi.y + pad, (double)uhi.z + pad};
-  int ex[3];
-  double sc[3];
-  for (int a = 0; a < 3; ++a) {
-    double ext = hiU[a] - P[a];
-    int k = -126;
-    if (ext > 0.0) { frexp(ext / 255.0, &k); k = max(-126, min(127, k)); }
-    ex[a] = k + 127;
-    sc[a] = ldexp(1.0, k);
-  }
-  // octant slot assignment
-  const float3 ctr = (ulo + uhi) * 0.5f;
-  float3 cc[8];
-  for (int c = 0; c < ne; ++c) {
-    float3 lo, hi;
-    load_box(leafbox, nodebox, ent[c], lo, hi);
-    cc[c] = (lo + hi) * 0.5f - ctr;
-  }
-  int slot_of[8];
-  unsigned used = 0u, done = 0u;
-  for (int r = 0; r < ne; ++r) {
-    float bs = -kInf;
-    int bc = -1, bslot = -1;
-    for (int c = 0; c < ne; ++c) {
-      if (done >> c & 1u) continue;
-      for (int sl = 0; sl < 8; ++sl) {
-        if (used >> sl & 1u) continue;
-        const float sc3 = ((sl & 1) ? -cc[c].x : cc[c].x) + ((sl & 2) ? -cc[c].y : cc[c].y) + ((sl & 4) ? -cc[c].z : cc[c].z);
-        if (sc3 > bs || bc < 0) { bs = sc3; bc = c; bslot = sl; }
-      }
-    }
-    slot_of[bc] = bslot;
-    done |= 1u << bc;
-    used |= 1u << bslot;
-  }
-  unsigned u[32];
-  for (int q = 0; q < 32; ++q) u[q] = 0u;
-  for (int sl = 0; sl < 8; ++sl) {               // empty slots: qlo = 255 > qhi = 0, unoccupied
-    const int wd2 = sl >> 2, sh = 8 * (sl & 3);
-    for (int a = 0; a < 3; ++a) u[8 + 2 * a + wd2] |= 255u << sh;
-    u[20 + sl] = (unsigned)kEmptyRef;
-  }
-  unsigned occ = 0u, imask = 0u;
-  for (int c = 0; c < ne; ++c) {
-    const int e = ent[c], sl = slot_of[c], wd2 = sl >> 2, sh = 8 * (sl & 3);
-    float3 lo, hi;
-    load_box(leafbox, nodebox, e, lo, hi);
-    const float l3[3] = {lo.x, lo.y, lo.z}, h3[3] = {hi.x, hi.y, hi.z};
-    for (int a = 0; a < 3; ++a) {
-      const double fl = floor(((double)l3[a] - pad - P[a]) / sc[a]);
-      const double fh = ceil(((double)h3[a] + pad - P[a]) / sc[a]);
-      const unsigned ql = (unsigned)fmin(fmax(fl, 0.0), 255.0), qh = (unsigned)fmin(fmax(fh, 0.0), 255.0);
-      u[8 + 2 * a + wd2] = (u[8 + 2 * a + wd2] & ~(255u << sh)) | (ql << sh);
-      u[14 + 2 * a + wd2] |= qh << sh;
-    }
-    occ |= 1u << sl;
-    if (wide_entry(ranges, e, leaf_max)) {
-      u[20 + sl] = (unsigned)wref[c];
-      imask |= 1u << sl;
-    } else {
-      const int first = e < 0 ? ~e : ranges[e].x;
-      u[20 + sl] = (unsigned)(-1 - ((first << 2) | (bsize(ranges, e) - 1)));
-    }
-  }
-  u[0] = __float_as_uint((float)P[0]);
-  u[1] = __float_as_uint((float)P[1]);
-  u[2] = __float_as_uint((float)P[2]);
-  u[3] = (unsigned)ex[0] << 23;
-  u[4] = (unsigned)ex[1] << 23;
-  u[5] = (unsigned)ex[2] << 23;
-  u[6] = occ | imask << 8;
-  uint4* nd = wnodes + 8 * (size_t)w;
-  for (int q = 0; q < 8; ++q) nd[q] = make_uint4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
-  wbox[2 * (size_t)w] = f4(ulo, 0.f);
-  wbox[2 * (size_t)w + 1] = f4(uhi, 0.f);
-  wdepth[w] = wd;
-}
-#endif
-
-DT_D void write_node(int i, const int* ent, const int* wref, int ne, unsigned w, int wd, double pad,
-                     const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
-                     const int2* __restrict__ ranges, int leaf_max, uint4* __restrict__ wnodes,
-                     float4* __restrict__ wbox, int* __restrict__ wdepth) {
-#if DT_BVH_WIDE == 8
-  write_wide_node8(i, ent, wref, ne, w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
-#else
-  write_wide_node(i, ent, wref, ne, w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
-#endif
-}
-
 DT_D double wide_pad(const int* __restrict__ ibox) {
   float m = fmaxf(fmaxf(fmaxf(fabsf(ord2f(ibox[0])), fabsf(ord2f(ibox[1]))), fmaxf(fabsf(ord2f(ibox[2])), fabsf(ord2f(ibox[3])))),
                   fmaxf(fabsf(ord2f(ibox[4])), fabsf(ord2f(ibox[5]))));
@@ -679,9 +576,9 @@ DT_D double wide_pad(const int* __restrict__ ibox) {
 __global__ void k_wide_single(const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
                               const int2* __restrict__ ranges, const int* __restrict__ ibox, uint4* __restrict__ wnodes,
                               float4* __restrict__ wbox, int* __restrict__ wdepth, int* __restrict__ nwide, int leaf_max) {
-  const int ent[8] = {~0, 0, 0, 0, 0, 0, 0, 0}, wref[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int ent[4] = {~0, 0, 0, 0}, wref[4] = {0, 0, 0, 0};
   *nwide = 1;
-  write_node(~0, ent, wref, 1, 0u, 0, wide_pad(ibox), leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
+  write_wide_node(~0, ent, wref, 1, 0u, 0, wide_pad(ibox), leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
 }
 
 // Collapse to the 4-wide BVH (surface-area greedy): top down from the root, a wide node starts with
@@ -815,106 +712,8 @@ __global__ void k_wide_cost(const int2* __restrict__ children, const int2* __res
   }
 }
 
-#if DT_BVH_WIDE == 8
-// ---- the same DP at width 8.  Per internal node (went, 3 int4): C(n, 1..8) in the first two,
-// and in the third the decisions of i = 2..8, 4 bits each: the split a of best(i) (bits 0-2)
-// and whether n is opened at budget i (bit 3).  The entry lists are expanded top down
-// (sah_entries) instead of stored: up to 8 entries per list would not fit.
-#ifndef DT_COST_NODE8
-#define DT_COST_NODE8 (170.f / 37.f)
-#endif
-__global__ void k_wide_cost8(const int2* __restrict__ children, const int* __restrict__ parent_int,
-                             const int* __restrict__ parent_leaf, int* __restrict__ flags, const float4* __restrict__ leafbox,
-                             const float4* __restrict__ nodebox, int n, int4* __restrict__ went) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    int p = parent_leaf[j];
-    while (p >= 0) {
-      __threadfence();
-      if (atomicAdd(flags + p, 1) == 0) break;   // the second arrival evaluates the node
-      __threadfence();
-      const int2 ch = children[p];
-      float Cl[8], Cr[8];
-      const int cc[2] = {ch.x, ch.y};
-#pragma unroll
-      for (int s2 = 0; s2 < 2; ++s2) {
-        float* C = s2 == 0 ? Cl : Cr;
-        if (cc[s2] < 0) {
-          const float c = box_area2(leafbox, nodebox, cc[s2]) * kCostTri;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) C[q] = c;
-        } else {
-          const int4 a = __ldcg(went + 3 * (size_t)cc[s2]), b = __ldcg(went + 3 * (size_t)cc[s2] + 1);
-          C[0] = __int_as_float(a.x); C[1] = __int_as_float(a.y); C[2] = __int_as_float(a.z); C[3] = __int_as_float(a.w);
-          C[4] = __int_as_float(b.x); C[5] = __int_as_float(b.y); C[6] = __int_as_float(b.z); C[7] = __int_as_float(b.w);
-        }
-      }
-      float best[9];
-      int split[9];
-#pragma unroll
-      for (int i = 2; i <= 8; ++i) {
-        float bv = kInf;
-        int ba = 1;
-#pragma unroll
-        for (int a = 1; a < i; ++a) {
-          const float v = Cl[a - 1] + Cr[i - a - 1];
-          if (v < bv) { bv = v; ba = a; }
-        }
-        best[i] = bv;
-        split[i] = ba;
-      }
-      float C[8];
-      unsigned dec = 0u;
-      C[0] = box_area2(leafbox, nodebox, p) * DT_COST_NODE8 + best[8];
-#pragma unroll
-      for (int i = 2; i <= 8; ++i) {
-        const bool open = best[i] < C[i - 2];
-        C[i - 1] = open ? best[i] : C[i - 2];
-        dec |= ((unsigned)split[i] | (open ? 8u : 0u)) << (4 * (i - 2));
-      }
-      __stcg(went + 3 * (size_t)p, make_int4(__float_as_int(C[0]), __float_as_int(C[1]), __float_as_int(C[2]),
-                                             __float_as_int(C[3])));
-      __stcg(went + 3 * (size_t)p + 1, make_int4(__float_as_int(C[4]), __float_as_int(C[5]), __float_as_int(C[6]),
-                                                 __float_as_int(C[7])));
-      __stcg(went + 3 * (size_t)p + 2, make_int4((int)dec, 0, 0, 0));
-      p = parent_int[p];
-    }
-  }
-}
-
-// Entries of the wide node made of binary node b: its children split by best(8), each
-// expanded by its own decisions (E(x, k): x itself if k = 1 or x is a leaf; E(x, k - 1) if x
-// is not opened at k; else E(left, a) ++ E(right, k - a)).
-DT_D int sah_entries(const int2* __restrict__ children, const int4* __restrict__ went, int b, int* ent) {
-  int sx[8], sk[8], sp = 0, ne = 0;
-  const unsigned d8 = (unsigned)__ldcg(went + 3 * (size_t)b + 2).x;
-  const int a8 = (int)((d8 >> 24) & 7u);
-  const int2 c0 = children[b];
-  sx[sp] = c0.y; sk[sp++] = 8 - a8;
-  sx[sp] = c0.x; sk[sp++] = a8;
-  while (sp > 0) {
-    const int x = sx[--sp];
-    int k = sk[sp];
-    unsigned dec = 0u;
-    if (x >= 0 && k > 1) {
-      dec = (unsigned)__ldcg(went + 3 * (size_t)x + 2).x;
-      while (k > 1 && !((dec >> (4 * (k - 2) + 3)) & 1u)) --k;
-    }
-    if (x < 0 || k <= 1) {
-      DT_CHECK(ne < 8);
-      ent[ne++] = x;
-      continue;
-    }
-    const int a = (int)((dec >> (4 * (k - 2))) & 7u);
-    const int2 ch = children[x];
-    DT_CHECK(sp + 2 <= 8 && a >= 1 && a < k);
-    sx[sp] = ch.y; sk[sp++] = k - a;
-    sx[sp] = ch.x; sk[sp++] = a;
-  }
-  return ne;
-}
-#else
 // Entries of the wide node made of binary node b (at most 4): W(b) from the DP.
-DT_D int sah_entries(const int2* __restrict__, const int4* __restrict__ went, int b, int* ent) {
+DT_D int sah_entries(const int4* __restrict__ went, int b, int ent[4]) {
   const int4 w1 = __ldcg(went + 3 * (size_t)b + 1), w2 = __ldcg(went + 3 * (size_t)b + 2);
   const int e[4] = {w1.y, w1.z, w1.w, w2.x};
   int ne = 0;
@@ -923,7 +722,6 @@ DT_D int sah_entries(const int2* __restrict__, const int4* __restrict__ went, in
     if (e[q] != kEmptyRef) ent[ne++] = e[q];
   return ne;
 }
-#endif
 
 __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __restrict__ ranges,
                                const float4* __restrict__ leafbox, const float4* __restrict__ nodebox,
@@ -945,13 +743,12 @@ __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __
     __threadfence();                                   // acquire: the parent's writes before publishing
     const int b = (int)(item & 0xffffffffu), w = (int)(item >> 32);
     DT_CHECK(b >= 0 && w >= 0 && w < cap);
-    int ent[kWide], wref[kWide], ne = 2;
-    for (int q = 0; q < kWide; ++q) wref[q] = 0;
+    int ent[4], wref[4] = {0, 0, 0, 0}, ne = 2;
     const int2 ch = children[b];
     ent[0] = ch.x;
     ent[1] = ch.y;
-    if (went) ne = sah_entries(children, went, b, ent);
-    while (!went && ne < kWide) {
+    if (went) ne = sah_entries(went, b, ent);
+    while (!went && ne < 4) {
       int best = -1;
       float ba = -1.f;
       for (int c = 0; c < ne; ++c) {
@@ -973,7 +770,7 @@ __global__ void k_wide_topdown(const int2* __restrict__ children, const int2* __
     for (int c = 0, k = 0; c < ne; ++c)
       if (wide_entry(ranges, ent[c], leaf_max)) wref[c] = base + k++;
     DT_CHECK(base + nin <= cap);
-    write_node(b, ent, wref, ne, (unsigned)w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
+    write_wide_node(b, ent, wref, ne, (unsigned)w, wd, pad, leafbox, nodebox, ranges, leaf_max, wnodes, wbox, wdepth);
     for (int c = 0; c < ne; ++c) {
       if (!wide_entry(ranges, ent[c], leaf_max)) continue;
       wdepth[wref[c]] = wd + 1;
@@ -1032,27 +829,14 @@ __global__ void k_bvh_check(const uint4* __restrict__ wnodes, const float4* __re
                             int* __restrict__ wref) {
   int nw = *nwide_p;
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
-    const uint4* nd = wnodes + (kNodeWords / 4) * (size_t)w;
+    const uint4* nd = wnodes + 4 * (size_t)w;
+    uint4 n0 = nd[0], n1 = nd[1], n2 = nd[2], n3 = nd[3];
     unsigned long long bad = 0, leaves = 0;
-#if DT_BVH_WIDE == 8
-    const unsigned masks = reinterpret_cast<const unsigned*>(nd)[6];
-#endif
-    for (int c = 0; c < kWide; ++c) {
-#if DT_BVH_WIDE == 8
-      const int ref = wide_ref(nd, c);
-      if (ref == kEmptyRef) {
-        if (masks >> c & 1u) bad++;              // an occupied slot without a child
-        continue;
-      }
-      if (!(masks >> c & 1u) || ((masks >> (8 + c)) & 1u) != (ref >= 0 ? 1u : 0u)) bad++;
-      float3 lo, hi;
-      decode_wide_child(nd, c, lo, hi);
-#else
-      int ref = wide_ref(nd[2], nd[3], c);
+    for (int c = 0; c < 4; ++c) {
+      int ref = wide_ref(n2, n3, c);
       if (ref == kEmptyRef) continue;
       float3 lo, hi;
-      decode_wide_child(nd[0], nd[1], nd[2], nd[3], c, lo, hi);
-#endif
+      decode_wide_child(n0, n1, n2, n3, c, lo, hi);
       float3 clo, chi;
       if (ref >= 0) {
         atomicAdd(wref + ref, 1);
@@ -1125,7 +909,7 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
       if (p) cudaFree(p);
     size_t ks = 2 * 3 * cap;   // keys/vals ping-pong sized for the 3*nf corner sort
     if ((e = cudaMalloc(&c->F, cap * 3 * sizeof(int))) || (e = cudaMalloc(&c->fnrm, cap * sizeof(D4))) ||
-        (e = cudaMalloc(&c->nodes, cap * kNodeWords * 4)) || (e = cudaMalloc(&c->tris, cap * 48)) ||
+        (e = cudaMalloc(&c->nodes, cap * 64)) || (e = cudaMalloc(&c->tris, cap * 48)) ||
         (e = cudaMalloc(&c->keys, ks * sizeof(unsigned))) || (e = cudaMalloc(&c->vals, ks * sizeof(unsigned))) ||
         (e = cudaMalloc(&c->children, cap * sizeof(int2))) || (e = cudaMalloc(&c->parent_int, cap * sizeof(int))) ||
         (e = cudaMalloc(&c->parent_leaf, cap * sizeof(int))) || (e = cudaMalloc(&c->rflags, cap * sizeof(int))) ||
@@ -1210,16 +994,11 @@ cudaError_t build_bvh(dt_ctx* c, const float* Vin, int nv, const int* Fin, int n
 #if DT_WIDE_SAH
     // the DP's per-node costs live in scratch the collapse does not otherwise use at this
     // point (the sort keys: 4 words per node of the 6 nf available); its entry lists in went
+    float4* cost = reinterpret_cast<float4*>(c->keys);
     went = c->went;
     cudaMemsetAsync(c->rflags, 0, (size_t)(nf - 1) * sizeof(int), st);
-#if DT_BVH_WIDE == 8
-    k_wide_cost8<<<gf, T, 0, st>>>(c->children, c->parent_int, c->parent_leaf, c->rflags, c->leafbox, c->nodebox, nf,
-                                   went);
-#else
-    float4* cost = reinterpret_cast<float4*>(c->keys);
     k_wide_cost<<<gf, T, 0, st>>>(c->children, c->ranges, c->parent_int, c->parent_leaf, c->rflags, c->leafbox,
                                   c->nodebox, nf, cost, went);
-#endif
     launches += 1;
 #endif
     cudaMemsetAsync(c->wqueue, 0xff, (size_t)nf * sizeof(unsigned long long), st);

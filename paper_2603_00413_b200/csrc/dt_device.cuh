@@ -29,13 +29,6 @@ constexpr int kStackShared = 16;   // short stack entries per thread in shared m
 constexpr int kStackLocal = 112;   // spill entries per thread (local memory, L1-cached)
 constexpr int kLeafMax = 3;        // triangles per wide-BVH leaf (a contiguous leaf-order range)
 constexpr int kEmptyRef = 0x7fffffff;
-// width of the quantised wide BVH: 4 (64-B nodes, sorted child keys) or 8 (128-B nodes,
-// octant-ordered child slots, node-group stack; profiles/r02_traversal_sweep.txt)
-#ifndef DT_BVH_WIDE
-#define DT_BVH_WIDE 4
-#endif
-constexpr int kWide = DT_BVH_WIDE;
-constexpr int kNodeWords = kWide == 8 ? 32 : 16;   // 32-bit words per wide node
 
 // per-record event codes (the protocol numbering, shared only as a spec)
 enum { EV_MISS = 0, EV_HIT_OUT = 1, EV_HIT_IN = 2, EV_HIT_OUT_TIR = 3, EV_HIT_IN_TIR = 4, EV_CAP_OUT = 5, EV_CAP_IN = 6,
@@ -220,176 +213,6 @@ DT_D bool slab(float lx, float hx, float ly, float hy, float lz, float hz, float
   return tmin * 0.99999f <= tmax * 1.00001f;
 }
 
-
-// quantised plane byte c of word w as a float (exact, 0..255).  DT_QBYTE_PRMT = 1: the byte is
-// placed under the exponent of 2^23 (one PRMT) and 2^23 subtracted (one exact FADD), both
-// full-rate pipes, instead of an I2F.U8 conversion
-#ifndef DT_QBYTE_PRMT
-#define DT_QBYTE_PRMT 0
-#endif
-DT_D float qbyte(unsigned w, int c) {
-#if DT_QBYTE_PRMT
-  return __uint_as_float(__byte_perm(w, 0x4B000000u, (unsigned)c | 0x7650u)) - 8388608.0f;
-#else
-  return (float)((w >> (8 * c)) & 0xff);
-#endif
-}
-
-#if DT_BVH_WIDE == 8
-// ----------------------------------------------------------------------------- 8-wide nodes
-// 128-B node (bvh.cu, write_wide_node8): words
-//   0-3  p.x p.y p.z s.x        4-7  s.y s.z masks -      (masks: occupied | internal << 8)
-//   8-19 qlo_x[8] qlo_y[8] qlo_z[8] qhi_x[8] qhi_y[8] qhi_z[8]   (one byte per slot, 2 words each)
-//   20-27 ref[8]                28-31 -
-// Slots are assigned at build by octant (slot bit a set: the child lies toward -a from the node
-// centre), so a ray whose direction has sign bits `oct` meets the slots approximately in the
-// order slot ^ flip, flip = ~oct & 7 (Ylitie, Karras & Laine 2017).  A node visit keeps the
-// hit children as two 8-bit masks over those order positions (internal children; leaves), and
-// the stack holds node groups (node << 8 | remaining internal mask): no per-visit sort and at
-// most one push per descent.
-struct Trav {
-  unsigned ngrp, tgrp;   // node << 8 | mask over order positions: internal / leaf children left
-  int cur, sp, best;     // cur: node to visit next (the root at the start), -1: none
-  float bt, bu, bv;
-};
-
-DT_D void trav_init(Trav& T) {
-  T.ngrp = T.tgrp = 0u;
-  T.cur = 0;
-  T.sp = 0;
-  T.best = -1;
-  T.bt = kInf;
-  T.bu = T.bv = 0.0f;
-}
-
-
-#ifndef DT_TLO_CULL
-#define DT_TLO_CULL 1
-#endif
-
-// bit p of each byte -> bit p ^ f (the slot <-> order-position map)
-DT_D unsigned xor_bits(unsigned m, int f) {
-  if (f & 1) m = ((m & 0x5555u) << 1) | ((m >> 1) & 0x5555u);
-  if (f & 2) m = ((m & 0x3333u) << 2) | ((m >> 2) & 0x3333u);
-  if (f & 4) m = ((m & 0x0f0fu) << 4) | ((m >> 4) & 0x0f0fu);
-  return m;
-}
-
-DT_D const int* node_refs(const DevScene& s, unsigned node) {
-  return reinterpret_cast<const int*>(s.nodes) + (size_t)node * kNodeWords + 20;
-}
-
-// Visit node: slab-test its 8 child boxes (the 4-wide rule: one FMA per plane, near / far
-// planes by direction sign, tmin <= tmax * 1.000021, entry clamped at tlo); returns the hit
-// internal / leaf children as masks over order positions.
-DT_D void node8_hits(const DevScene& s, unsigned node, float3 o, float3 inv, float bt, float tlo, int flip,
-                     unsigned& ih, unsigned& th) {
-  const uint4* nd = reinterpret_cast<const uint4*>(s.nodes) + (size_t)node * (kNodeWords / 4);
-  uint4 a0, a1, b0, b1;
-  ldg256(nd, a0, a1);
-  ldg256(nd + 2, b0, b1);
-  const uint4 c0 = __ldg(nd + 4);
-  const float3 A = f3(__uint_as_float(a0.w) * inv.x, __uint_as_float(a1.x) * inv.y, __uint_as_float(a1.y) * inv.z);
-  const float3 B = f3((__uint_as_float(a0.x) - o.x) * inv.x, (__uint_as_float(a0.y) - o.y) * inv.y,
-                      (__uint_as_float(a0.z) - o.z) * inv.z);
-  const bool sx = inv.x < 0.0f, sy = inv.y < 0.0f, sz = inv.z < 0.0f;
-  // lo words: x b0.x b0.y, y b0.z b0.w, z b1.x b1.y; hi words: x b1.z b1.w, y c0.x c0.y, z c0.z c0.w
-  const unsigned xn0 = sx ? b1.z : b0.x, xn1 = sx ? b1.w : b0.y, xf0 = sx ? b0.x : b1.z, xf1 = sx ? b0.y : b1.w;
-  const unsigned yn0 = sy ? c0.x : b0.z, yn1 = sy ? c0.y : b0.w, yf0 = sy ? b0.z : c0.x, yf1 = sy ? b0.w : c0.y;
-  const unsigned zn0 = sz ? c0.z : b1.x, zn1 = sz ? c0.w : b1.y, zf0 = sz ? b1.x : c0.z, zf1 = sz ? b1.y : c0.w;
-  unsigned hit = 0u;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int b = c & 3;
-    const unsigned xn = c < 4 ? xn0 : xn1, yn = c < 4 ? yn0 : yn1, zn = c < 4 ? zn0 : zn1;
-    const unsigned xf = c < 4 ? xf0 : xf1, yf = c < 4 ? yf0 : yf1, zf = c < 4 ? zf0 : zf1;
-    const float tmin = fmaxf(fmaxf(fmaf(qbyte(xn, b), A.x, B.x), fmaf(qbyte(yn, b), A.y, B.y)),
-                             fmaxf(fmaf(qbyte(zn, b), A.z, B.z), tlo));
-    const float tmax = fminf(fminf(fmaf(qbyte(xf, b), A.x, B.x), fmaf(qbyte(yf, b), A.y, B.y)),
-                             fminf(fmaf(qbyte(zf, b), A.z, B.z), bt));
-    hit |= (tmin <= tmax * 1.000021f ? 1u : 0u) << c;
-  }
-  const unsigned masks = a1.z;                                   // occupied | internal << 8
-  const unsigned m = xor_bits((hit & masks & 0xffu) | (masks & 0xff00u), flip);
-  ih = m & (m >> 8) & 0xffu;
-  th = m & ~(m >> 8) & 0xffu;
-}
-
-DT_D void stack_push(Trav& T, int* sstack, int stride, int* lstack, unsigned g, int& err) {
-  if (T.sp < kStackShared) sstack[T.sp * stride] = (int)g;
-  else if (T.sp < kStackShared + kStackLocal) lstack[T.sp - kStackShared] = (int)g;
-  else err = 1;
-  ++T.sp;
-}
-DT_D bool stack_pop(Trav& T, const int* sstack, int stride, const int* lstack, unsigned& g) {
-  if (T.sp == 0) return false;
-  --T.sp;
-  g = (unsigned)(T.sp < kStackShared ? sstack[T.sp * stride] : lstack[T.sp - kStackShared]);
-  return true;
-}
-
-// Tests the triangles of leaf ref, keeping the closest hit (R18 ties).
-DT_D void leaf_test(const DevScene& s, float3 o, float3 d, float t_lo, int ref, Trav& T, int& tests) {
-  int first, cnt;
-  leaf_range(ref, first, cnt);
-  DT_CHECK(first >= 0 && first + cnt <= s.nf);
-  const float4* tr = s.tris + 3 * (size_t)first;
-  do {
-    float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
-    float t, u, v;
-    ++tests;
-    if (intersect_tri(o, d, f3(a), f3(b), f3(c), t_lo, t, u, v)) {
-      int id = __float_as_int(a.w);
-      if (t < T.bt || (t == T.bt && id < T.best)) { T.bt = t; T.bu = u; T.bv = v; T.best = id; }
-    }
-    tr += 3;
-  } while (--cnt > 0);
-}
-
-// One traversal step: with no leaf of the current node left to test, take the next internal
-// child (of the current group, else of the group popped from the stack), push the group's
-// remainder and visit the child; then test the next leaf child of the visited node.  Returns
-// true when the ray is finished.
-DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_lo, Trav& T, int* sstack, int stride,
-                    int* lstack, int& err, int& visits, int& tests) {
-  const int flip = (inv.x >= 0.0f ? 1 : 0) | (inv.y >= 0.0f ? 2 : 0) | (inv.z >= 0.0f ? 4 : 0);
-  if ((T.tgrp & 0xffu) == 0u) {
-    int node = T.cur;
-    if (node < 0) {
-      if ((T.ngrp & 0xffu) == 0u && (err || !stack_pop(T, sstack, stride, lstack, T.ngrp))) return true;
-      const unsigned g = T.ngrp;
-      const int pos = __ffs(g & 0xffu) - 1;
-      T.ngrp = g & (g - 1u);
-      node = __ldg(node_refs(s, g >> 8) + (pos ^ flip));
-      if (T.ngrp & 0xffu) stack_push(T, sstack, stride, lstack, T.ngrp, err);
-    }
-    DT_CHECK(node >= 0 && node < max(s.nf - 1, 1));
-    T.cur = -1;
-    ++visits;
-    unsigned ih, th;
-    node8_hits(s, (unsigned)node, o, inv, T.bt, DT_TLO_CULL ? t_lo : 0.0f, flip, ih, th);
-    T.ngrp = ((unsigned)node << 8) | ih;
-    T.tgrp = ((unsigned)node << 8) | th;
-  }
-  if (T.tgrp & 0xffu) {
-    const unsigned g = T.tgrp;
-    const int pos = __ffs(g & 0xffu) - 1;
-    T.tgrp = g & (g - 1u);
-    leaf_test(s, o, d, t_lo, __ldg(node_refs(s, g >> 8) + (pos ^ flip)), T, tests);
-  }
-  return false;
-}
-
-DT_D int wide_ref(const uint4* w, int c) { return (int)reinterpret_cast<const unsigned*>(w)[20 + c]; }
-DT_D void decode_wide_child(const uint4* w, int c, float3& lo, float3& hi) {
-  const unsigned* u = reinterpret_cast<const unsigned*>(w);
-  const float3 p = f3(__uint_as_float(u[0]), __uint_as_float(u[1]), __uint_as_float(u[2]));
-  const float3 sc = f3(__uint_as_float(u[3]), __uint_as_float(u[4]), __uint_as_float(u[5]));
-  const int wd = c >> 2, b = c & 3;
-  lo = f3(fmaf(qbyte(u[8 + wd], b), sc.x, p.x), fmaf(qbyte(u[10 + wd], b), sc.y, p.y), fmaf(qbyte(u[12 + wd], b), sc.z, p.z));
-  hi = f3(fmaf(qbyte(u[14 + wd], b), sc.x, p.x), fmaf(qbyte(u[16 + wd], b), sc.y, p.y), fmaf(qbyte(u[18 + wd], b), sc.z, p.z));
-}
-#else
 // Closest-hit traversal state of one ray through the 4-wide BVH.  Ties in t resolve to the
 // lowest ORIGINAL face id (R18), so the answer does not depend on the visiting order.
 struct Trav {
@@ -411,6 +234,8 @@ DT_D void trav_init(Trav& T) {
     int tr = r##a; r##a = r##b; r##b = tr;                       \
   }
 
+// quantised plane byte c of word w as a float (exact, 0..255; I2F.U8 with a byte select)
+DT_D float qbyte(unsigned w, int c) { return (float)((w >> (8 * c)) & 0xff); }
 
 // DT_TLO_CULL = 1: a child box the ray leaves before t_lo (R17) cannot hold a hit: its entry
 // distance is clamped at t_lo instead of 0 (secondary rays skip the thin boxes of the surface
@@ -528,7 +353,6 @@ DT_D bool trav_step(const DevScene& s, float3 o, float3 d, float3 inv, float t_l
 }
 
 #undef DT_CX
-#endif  // DT_BVH_WIDE
 
 // Closest hit (whole traversal).  Returns the original face id or -1.
 DT_D int traverse(const DevScene& s, float3 o, float3 d, float t_lo, float& bt, float& bu, float& bv, int* sstack,
