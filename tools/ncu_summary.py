@@ -11,7 +11,13 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
            "sm__maximum_warps_per_active_cycle_pct", "launch__registers_per_thread",
            "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__inst_executed.avg.per_cycle_active",
-           "launch__grid_size", "launch__block_size"]
+           "launch__grid_size", "launch__block_size",
+           # L2 operation counts (the texture walks' roofline: corner fetches and adjoint REDs)
+           "lts__t_requests_srcunit_tex_op_red.sum", "lts__t_sectors_srcunit_tex_op_red.sum",
+           "lts__t_requests_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
+           "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+           "l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct",
+           "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"]
 
 
 def launches(path):
