@@ -515,6 +515,23 @@ def run_ours(args, rank, world, local_rank):
                     "scattered_view": {"peak": round(pk_s, 2), "frac": round(achieved / pk_s, 4),
                                        "table": size, "source": wp_src + ": hashed-index float4 load / RED rates"},
                     "hbm_view": hbm_view}
+    elif cls == "bwd" and prof.get("env_samples_bwd", 0) > 0 and walk_peaks() is not None:
+        # volumetric env (C3V): the backward replays every exterior segment's env-volume samples,
+        # each 8 voxel + 12 plane float4 texel fetches (frozen env: no atomics), counted on the
+        # device; peak: the L2's coalesced float4 load ceiling (scattered view beside it)
+        wp, wp_src = walk_peaks()
+        samp = prof["env_samples_bwd"] / max(launches, 1)
+        g_ops = samp * 20
+        t = ms_per_launch / 1e3
+        achieved = g_ops / t / 1e9
+        pk, pk_s = wp["gather_coalesced_gops"], wp["gather_128mb_gops"]
+        roofline = {"bound": "l2", "kernel": kname + "_vol", "achieved": round(achieved, 2), "peak": round(pk, 2),
+                    "peak_source": wp_src + ": coalesced float4 load ceiling", "unit": "Gop/s",
+                    "frac": round(achieved / pk, 4), "ops": "env-volume texel fetches (8 voxel + 12 plane per sample)",
+                    "samples_per_launch": int(samp), "fetches_per_launch": int(g_ops),
+                    "scattered_view": {"peak": round(pk_s, 2), "frac": round(achieved / pk_s, 4), "table": "128mb",
+                                       "source": wp_src + ": hashed-index float4 load rate"},
+                    "hbm_view": hbm_view}
     else:
         roofline = {"bound": "hbm", "kernel": kname, **{k: v for k, v in hbm_view.items() if k != "bytes_per_launch"},
                     "bytes_per_launch": int(bytes_per_launch)}
@@ -555,7 +572,8 @@ def run_ours(args, rank, world, local_rank):
         "counters_per_step": {"node_visits": prof["node_visits"] // args.steps,
                               "tri_tests": prof["tri_tests"] // args.steps,
                               "walk_cells_fwd": prof["walk_cells_fwd"] // args.steps,
-                              "walk_cells_bwd": prof["walk_cells_bwd"] // args.steps},
+                              "walk_cells_bwd": prof["walk_cells_bwd"] // args.steps,
+                              "env_samples_bwd": prof["env_samples_bwd"] // args.steps},
     }
     return line
 

@@ -244,6 +244,8 @@ typedef struct {
                                     * the forward (each: 8 corner fetches)                    */
   int64_t walk_cells_bwd;          /* the same of the backward (each: 8 corner fetches and   *
                                     * 8 float4 adjoint atomics)                               */
+  int64_t env_samples_bwd;         /* volumetric-env samples replayed by the backward (each:   *
+                                    * 8 voxel + 12 plane texel fetches)                       */
 } dt_profile;
 /* ---------------------------------------------------------------------------------------
  * The optimisation step around the tracer (PAPER P:176-194, P:439-443,

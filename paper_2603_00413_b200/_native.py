@@ -69,7 +69,7 @@ class Profile(C.Structure):
     _fields_ = [("ms", C.c_double * len(PHASES)), ("launches", C.c_int64 * len(PHASES)),
                 ("kernel_launches", C.c_int64), ("node_visits", C.c_int64), ("tri_tests", C.c_int64),
                 ("node_visits_primary", C.c_int64), ("tri_tests_primary", C.c_int64), ("segments", C.c_int64),
-                ("walk_cells_fwd", C.c_int64), ("walk_cells_bwd", C.c_int64)]
+                ("walk_cells_fwd", C.c_int64), ("walk_cells_bwd", C.c_int64), ("env_samples_bwd", C.c_int64)]
 
     def as_dict(self):
         return dict(ms={p: float(self.ms[i]) for i, p in enumerate(PHASES)},
@@ -77,7 +77,8 @@ class Profile(C.Structure):
                     kernel_launches=int(self.kernel_launches), node_visits=int(self.node_visits),
                     tri_tests=int(self.tri_tests), node_visits_primary=int(self.node_visits_primary),
                     tri_tests_primary=int(self.tri_tests_primary), segments=int(self.segments),
-                    walk_cells_fwd=int(self.walk_cells_fwd), walk_cells_bwd=int(self.walk_cells_bwd))
+                    walk_cells_fwd=int(self.walk_cells_fwd), walk_cells_bwd=int(self.walk_cells_bwd),
+                    env_samples_bwd=int(self.env_samples_bwd))
 
 
 _P = C.c_void_p

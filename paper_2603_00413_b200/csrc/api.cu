@@ -597,6 +597,7 @@ dt_status dt_get_profile(dt_ctx* c, dt_profile* out, int32_t reset) {
   out->segments = (int64_t)cnt[4];
   out->walk_cells_fwd = (int64_t)cnt[5];
   out->walk_cells_bwd = (int64_t)cnt[6];
+  out->env_samples_bwd = (int64_t)cnt[7];
   if (reset) {
     for (int i = 0; i < DT_PH_COUNT; ++i) { c->ph_ms[i] = 0.0; c->ph_launches[i] = 0; }
     c->kernel_launches = 0;

@@ -78,7 +78,8 @@ struct DevScene {
   int max_depth, cap_policy;
   // walk counters (the texture walks' roofline, bench.py): [0] cell visits of the forward
   // optical-depth walks, [1] cell visits of the backward walks (each: 8 corner fetches; in the
-  // backward also 8 float4 atomics)
+  // backward also 8 float4 atomics), [2] volumetric-env samples replayed by the backward
+  // (each: 8 voxel + 12 plane texels)
   unsigned long long* wcount;
 };
 

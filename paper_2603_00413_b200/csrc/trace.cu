@@ -593,6 +593,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
   const int64_t off = k == 0 ? 0 : level_base(a.lvl, k);
   float gior = 0.0f;
   float3 gsc = f3(0, 0, 0);
+  int vsamp = 0;                       // volumetric-env samples replayed (the bench's roofline)
   constexpr int RW = DT_WIN_ROUNDS, WIN = 32 * RW;
   __shared__ unsigned char sslot[kBwdThreads * RW];
   // 64-record windows taken from the level's counter (the next window's atomic in flight while
@@ -653,6 +654,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
       if (fl & RF_MISS) {
         float Tm = a.r.tau[idx].x;
         env_escape<VOL>(s, o, d, adj, &go, &gd, &Tm, &mom);
+        if (VOL) vsamp += s.env_nsamp;
       } else if ((fl & RF_CAPPED) && s.cap_policy == 0 && !volx) {
         // capped branches return 0: no dependence
       } else {
@@ -675,6 +677,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
             float aT = 0.f;
             if (s.cap_policy == 1) aT = dot(adj, env_eval(s, o, d, adj * tau, &go, &gd));
             env_volume_bwd(s, of, xf, adj, aT, tau.x, mom, go, gx);
+            vsamp += s.env_nsamp;
           } else {
             const float3 E = env_eval(s, o, d, adj * tau, &go, &gd);
             if (inside) { walk = true; gS = -(adj * E * tau); }
@@ -701,6 +704,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
           if (inside) { walk = true; gS = -(adj * Lc * tau); }
           if (volx) {                                                         // V + Tn * Lc (R30)
             env_volume_bwd(s, of, xf, adj, dot(adj, Lc), tau.x, mom, go, gx);
+            vsamp += s.env_nsamp;
           }
           float3 gd_s;
           float gi;
@@ -758,6 +762,7 @@ DT_D void backward_level_body(const BwdLaunch& a, int k, int max_depth, int64_t 
     gsc.y += __shfl_xor_sync(~0u, gsc.y, o);
     gsc.z += __shfl_xor_sync(~0u, gsc.z, o);
   }
+  if (VOL) flush_walk_count(s.wcount ? s.wcount + 2 : nullptr, vsamp);
   if (lane_id() == 0) {
     if (gior != 0.0f) atomicAdd(a.dior, gior);
     if (ABS == 0 && (gsc.x != 0.0f || gsc.y != 0.0f || gsc.z != 0.0f)) {

@@ -555,3 +555,26 @@ def test_walk_counters(tracer):
             assert p["walk_cells_fwd"] == 0 and p["walk_cells_bwd"] == 0, p
         else:
             assert 0 < p["walk_cells_fwd"] == p["walk_cells_bwd"] <= p["segments"] * sc.absorption.n_samples, p
+
+
+def test_env_volume_sample_counter(tracer):
+    """The volumetric env's backward sample counter (bench.py roofline): every exterior segment
+    replays env_nsamp samples, so the count is a positive multiple of env_nsamp, at most
+    segments * env_nsamp; zero for the shell env."""
+    from paper_2603_00413_b200.tracer import DeviceScene
+    V, F = S.icosphere(2)
+    cams = T.one_view(40, 28, (0.6, -0.4, 2.6), fov_deg=55)
+    for env, vol in ((T.small_grid_env(far_field=1), False), (T.small_volume_env(), True)):
+        sc = T.scene(V, F, cams, env=env, D=3)
+        ds = DeviceScene(sc, torch.device("cuda:0"))
+        tracer.build_bvh(ds.V, ds.F)
+        tracer.profile(reset=True)
+        tracer.trace_forward(ds, None)
+        tracer.trace_backward(torch.ones((sc.n_pixels, 3), dtype=torch.float32, device="cuda:0"))
+        torch.cuda.synchronize()
+        p = tracer.profile(reset=True)
+        if not vol:
+            assert p["env_samples_bwd"] == 0, p
+        else:
+            m = sc.env.n_samples
+            assert 0 < p["env_samples_bwd"] <= p["segments"] * m and p["env_samples_bwd"] % m == 0, p
